@@ -1,0 +1,178 @@
+"""Pin the CPU oracle against the golden fixtures made by the real reference.
+
+The fixtures (tests/golden/*.npz) were produced by tests/golden/make_golden.py
+running ``normint.run_pipeline`` (/root/reference/pkg/src/normint) in the
+build container.  Nothing here reads /root/reference.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import normint_oracle as O
+from tests.parity import assert_depth_close
+
+from tests.conftest import GOLDEN
+
+PIPE_CASES = sorted(
+    os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if "seam_" not in p
+)
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False))
+
+
+def reference_drifted(d):
+    """True when the reference hit the CG cap in a scale step (the null-space
+    drift documented in oracle.normint_oracle.project_range)."""
+    text = json.loads(str(d["warning_text"])) if "warning_text" in d else []
+    return any(w.startswith("iteration") for w in text)
+
+
+def run_oracle(d):
+    opts = json.loads(str(d["options"]))
+    theta = opts.get("theta_c_deg", 3.5)
+    st = O.Settings(freq_merging=opts.get("merge_freq"), reweighting_mode=opts.get("reweighting", "soft"))
+    return O.run_pipeline(
+        d["normals"].astype(np.float64), d["mask"], tuple(d["intr"]),
+        None if theta is None else float(np.deg2rad(theta)), st,
+        opts.get("connectivity", 8), opts.get("model", "milano"), opts.get("gauge_depth"))
+
+
+@pytest.mark.parametrize("name", PIPE_CASES)
+def test_oracle_matches_reference_pipeline(name):
+    d = load(name)
+    r = run_oracle(d)
+    mask = d["mask"]
+    # labels: bit-exact, both canonical
+    assert r.count0 == int(d["count0"])
+    assert np.array_equal(r.labels0, d["labels0"].astype(np.int64))
+    assert np.max(np.abs(r.filled - d["filled"])[mask]) < 1e-6
+    if reference_drifted(d):
+        # The reference's second alignment solve ran CG to its cap on a
+        # roundoff right-hand side and drifted along the null space (scales
+        # ~1e12, E_1 != E_0); from there its trajectory is roundoff-driven.
+        # The oracle (and the GPU path) project the RHS onto range(M) and keep
+        # the designed invariant E_1 == E_0 (pipeline.py:72-74).
+        assert abs(r.energies[1] - r.energies[0]) <= 1e-9 * r.energies[0]
+        assert np.isclose(r.energies[0], d["energies"][0], rtol=1e-9)
+        return
+    assert r.count == int(d["count"])
+    assert np.array_equal(r.labels, d["labels"].astype(np.int64))
+    # discrete trajectory: same number of outer iterations
+    assert r.iterations == int(d["iterations"])
+    # depth within the north-star tolerance, and in fact far tighter
+    fx = float(d["intr"][0])
+    assert_depth_close(r.log_depth, d["log_depth"], mask, fx)
+    assert np.max(np.abs(r.filled - d["filled"])[mask]) < 1e-6
+    e_ref = d["energies"]
+    if r.iterations < 150:
+        # converged runs: the trajectories agree to solver precision
+        assert np.max(np.abs(r.log_depth - d["log_depth"])[mask]) < 1e-6
+        assert np.allclose(r.energies, e_ref, rtol=1e-5, atol=1e-12)
+    else:
+        # a run that never meets the energy test (c1_hemi64 oscillates for
+        # all 150 iterations) amplifies 1e-10 differences; only the first
+        # iterations and the tolerance-level depth are comparable
+        assert np.allclose(r.energies[:4], e_ref[:4], rtol=1e-5, atol=1e-12)
+    # records: same stage sequence and keys
+    rec = json.loads(str(d["records"]))
+    assert len(rec) == len(r.records)
+    for a, b in zip(r.records, rec):
+        assert set(a) == set(b) | {"wall_ms"}
+        for k in ("stage", "vertices", "edges", "component_count", "degenerate_edges",
+                  "t", "merge_performed", "components_before", "components_after", "iterations"):
+            if k in b:
+                assert a[k] == b[k], (k, a[k], b[k])
+
+
+def test_oracle_seams():
+    d = load("seam_voronoi32")
+    n64, m = O.normalize_normals(d["normals"].astype(np.float64), d["mask"])
+    edges, _ = O.pixel_edges(m, 8)
+    assert np.array_equal(edges, d["edges"].astype(np.int64))
+    labels, count = O.components(n64, m, edges, float(np.deg2rad(3.5)))
+    assert count == int(d["count0"]) and np.array_equal(labels, d["labels0"])
+    co = O.edge_coefficients(n64, m, edges, tuple(d["intr"]), "milano")
+    assert np.array_equal(co.valid, d["valid"])
+    assert np.array_equal(co.opp_a, d["opp_a"]) and np.array_equal(co.opp_b, d["opp_b"])
+    for k, ref in (("omega_a", "omega_a"), ("omega_b", "omega_b"), ("gamma_a", "gamma_a"), ("gamma_b", "gamma_b")):
+        np.testing.assert_allclose(getattr(co, k), d[ref], rtol=1e-12, atol=1e-15)
+    st = O.Settings()
+    z, _, _ = O.fill(labels, count, edges, co, st)
+    assert np.max(np.abs(z - d["filled"])) < 1e-9
+    eids = O.inter_edge_ids(labels, edges)
+    assert np.array_equal(eids, d["inter_edge_ids"])
+    zc = z.copy()
+    steps = {}
+    for t in (0, 2):
+        s = O.scale_step(labels, count, edges, eids, co, zc, t, st)
+        steps[t] = s
+        zc[labels >= 0] += s.scales[labels[labels >= 0]]
+    np.testing.assert_allclose(steps[0].scales, d["scales_t0"], atol=1e-9)
+    np.testing.assert_allclose(steps[2].scales, d["scales_t2"], atol=1e-9)
+    np.testing.assert_allclose(steps[0].weights, d["weights_t0"], rtol=1e-12)
+    np.testing.assert_allclose(steps[2].weights, d["weights_t2"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(steps[2].energy, float(d["energy_t2"]), rtol=1e-6)
+    pairs = np.stack([labels[edges[eids, 0]], labels[edges[eids, 1]]], axis=1)
+    ml, mc = O.merge(labels, count, pairs, np.abs(steps[2].residual[0::2]))
+    assert mc == int(d["merged_count"]) and np.array_equal(ml, d["merged_labels"])
+
+
+def test_dot_cutoff_matches_arccos_lattice():
+    for deg in (1.0, 2.0, 3.5, 5.0, 10.0, 45.0):
+        th = float(np.deg2rad(deg))
+        d = O.dot_cutoff(th)
+        lat = d + np.arange(-4096, 4097) * np.spacing(d)
+        lat = np.concatenate([lat, np.nextafter(d, -2.0) - np.arange(0, 64) * np.spacing(d)])
+        keep_ref = np.arccos(np.clip(lat, -1.0, 1.0)) < th
+        assert np.array_equal(keep_ref, lat >= d), deg
+
+
+def test_union_find_matches_flood_fill():
+    rng = np.random.default_rng(7)
+    n = 300
+    ea = rng.integers(0, n, 280)
+    eb = rng.integers(0, n, 280)
+    roots = O._union_find_roots(n, ea, eb)
+    # brute force: flood fill
+    adj = [[] for _ in range(n)]
+    for a, b in zip(ea, eb):
+        adj[a].append(b)
+        adj[b].append(a)
+    seen = -np.ones(n, int)
+    for s in range(n):
+        if seen[s] >= 0:
+            continue
+        stack = [s]
+        seen[s] = s
+        while stack:
+            x = stack.pop()
+            for y in adj[x]:
+                if seen[y] < 0:
+                    seen[y] = s
+                    stack.append(y)
+    assert np.array_equal(roots, seen)
+
+
+def test_cg_two_pixel_known_answer():
+    # test_solver.py:108-115 -- two pixels, omega 0.7 -> (0.35, -0.35)
+    m, rhs = O.pair_normal_system(np.array([0]), np.array([1]), np.array([0.7]), np.array([-0.7]),
+                                  np.array([1.0]), np.array([1.0]), 2)
+    x, ok, _ = O.conjugate_gradient(m.dot, rhs, 1e-6, 5000)
+    assert ok
+    np.testing.assert_allclose(x, [0.35, -0.35], atol=1e-12)
+
+
+def test_normalize_rejects_non_unit():
+    n = np.zeros((2, 2, 3))
+    n[..., 2] = -1.0
+    n[0, 0, 2] = -1.01
+    with pytest.raises(ValueError):
+        O.normalize_normals(n)
+    with pytest.raises(O.EmptyMaskError):
+        O.pixel_edges(np.zeros((3, 3), bool))
