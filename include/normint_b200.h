@@ -1,0 +1,164 @@
+/*
+ * normint_b200 -- C ABI of the B200 (sm_100a) kernels behind the drop-in
+ * replacement of the reference's component-integration hot path
+ * (normint.run_pipeline, /root/reference/pkg/src/normint/pipeline.py:105-248).
+ *
+ * The reference has no FFI: its seams are Python functions.  Each entry point
+ * below replaces one of them (cited per function).  Conventions:
+ *
+ *  - Every pointer argument is a DEVICE pointer unless its name ends in _host.
+ *  - The pixel grid is a batch of B maps of H x W pixels, row-major, map-major:
+ *    pixel id = (m * H + v) * W + u.  A single map is B = 1.  Edges never
+ *    cross map boundaries, so a batch is exactly B independent problems.
+ *  - Forward neighbour offsets (graph.py:24-25): 4-connectivity
+ *    k=0:(+1,0) k=1:(0,+1); 8-connectivity k=0:(+1,0) k=1:(-1,+1) k=2:(0,+1)
+ *    k=3:(+1,+1).  The edge key of forward edge k at pixel a is a*KF + k
+ *    (KF = 2 or 4), whose order equals the reference's lexicographic (a, b)
+ *    edge order (graph.py:80-83).
+ *  - Calls are asynchronous on `stream` unless stated otherwise and return an
+ *    ni_status; ni_last_error() gives a thread-local message.
+ *  - The library allocates no persistent memory: scratch space is a caller
+ *    buffer sized by the matching *_workspace_size query.
+ *  - Results are deterministic: no floating-point atomics anywhere.
+ */
+#ifndef NORMINT_B200_H
+#define NORMINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* ni_stream_t; /* a cudaStream_t */
+
+typedef enum {
+  NI_OK = 0,
+  NI_ERR_INVALID_ARG = 1,     /* ValueError in the reference */
+  NI_ERR_EMPTY_MASK = 2,      /* normint.errors.EmptyMask (graph.py:65-66) */
+  NI_ERR_NONUNIT_NORMAL = 3,  /* ValueError from NormalMap.create (geometry.py:134-141) */
+  NI_ERR_NONFINITE = 4,       /* ValueError "valid normals must be finite" (geometry.py:131-132) */
+  NI_ERR_WORKSPACE = 5,       /* workspace smaller than the query returned */
+  NI_ERR_CUDA = 6,            /* CUDA runtime error */
+  NI_ERR_UNSUPPORTED = 7
+} ni_status;
+
+const char* ni_last_error(void);
+const char* ni_version(void);
+
+/* Counters written by ni_normalize / ni_coefficients (device struct). */
+typedef struct {
+  long long valid_pixels;      /* vertices record (pipeline.py:137-142) */
+  long long nonfinite;         /* valid pixels with a non-finite component */
+  long long nonunit;           /* valid pixels with |‖n‖-1| > 1e-4 */
+  unsigned long long max_dev;  /* bits of the largest |‖n‖-1| (non-negative double) */
+  long long edges;             /* edges record (pipeline.py:137-142) */
+  long long degenerate_edges;  /* edge_coefficients record (pipeline.py:153-159) */
+} ni_stats;
+
+/* K0 -- NormalMap.create (geometry.py:115-145).  normals: (B*H*W, 3) float32
+ * (dtype 0) or float64 (dtype 1), interleaved; mask: one byte per pixel, or
+ * NULL for all-valid.  Writes float64 SoA normals n_out[3][npix] renormalised
+ * as n / sqrt((x0^2 + x1^2) + x2^2) (zero on invalid pixels) and valid_out.
+ * SYNCHRONOUS: reads back the counters and returns NI_ERR_NONFINITE,
+ * NI_ERR_NONUNIT_NORMAL or NI_ERR_EMPTY_MASK like the reference raises. */
+int ni_normalize(const void* normals, int dtype, const uint8_t* mask, int B, int H, int W,
+                 double* n_out, uint8_t* valid_out, ni_stats* stats, ni_stream_t stream);
+
+/* K1 -- form_components (graph.py:141-165) + build_pixel_graph's edge count.
+ * Keeps edge (a,b) iff both valid and ((na0*nb0 + na1*nb1) + na2*nb2) >= dot_cutoff,
+ * which equals arccos(clip(dot)) < theta_c when dot_cutoff is the smallest
+ * float64 with numpy.arccos(d) < theta_c (computed by the host).  theta_none
+ * != 0 gives one component per valid pixel (graph.py:153-155).
+ * labels_out: int32 per pixel, canonical (rank of the component's smallest
+ * pixel id; -1 invalid).  count_out[0] = component count;
+ * map_first_out[m] = first label of map m (B+1 entries, last = count). */
+int ni_components_workspace_size(int B, int H, int W, size_t* bytes);
+int ni_components(const double* n, const uint8_t* valid, int B, int H, int W, int connectivity,
+                  double dot_cutoff, int theta_none, int32_t* labels_out, int32_t* count_out,
+                  int32_t* map_first_out, ni_stats* stats, void* workspace, size_t workspace_bytes,
+                  ni_stream_t stream);
+
+/* K2 -- build_edge_coefficients (continuity.py:210-289).  model 0 = milano,
+ * 1 = bini (4-connectivity only).  intrinsics: per map (fx, fy, cx, cy)
+ * float64 [B*4].  Outputs, per pixel a and forward edge k:
+ *   omega_a[k*npix + a] (float64), omega_b[k*npix + a] (bini only; may be NULL
+ *   for milano where omega_b = -omega_a), gamma[a] (float64),
+ *   eflags[a]: bit k = edge exists (both endpoints valid), bit 4+k = its
+ *   coefficient is valid (continuity.py:243-245, 266). */
+int ni_coefficients(const double* n, const uint8_t* valid, const double* intrinsics, int B, int H,
+                    int W, int connectivity, int model, double* omega_a, double* omega_b,
+                    double* gamma, uint8_t* eflags, ni_stats* stats, ni_stream_t stream);
+
+/* K3 -- fill_components (solver.py:195-239): per-component CG on the
+ * weighted normal equations at z = 0, all components in one batched solve.
+ * SYNCHRONOUS (polls convergence).  Writes z_out (float64, npix; 0 on invalid
+ * pixels, singletons and zero-RHS components), comp_iters[count] and
+ * comp_status[count] (0 converged / zero RHS / singleton, 1 hit the cap
+ * max(cg_max_iters, size)).  precision: 0 = fp32 vectors + fp64 dots. */
+int ni_fill_workspace_size(int B, int H, int W, int connectivity, int count, size_t* bytes);
+int ni_fill(const int32_t* labels, int count, const double* omega_a, const double* omega_b,
+            const double* gamma, const uint8_t* eflags, int B, int H, int W, int connectivity,
+            int model, double cg_tol, int cg_max_iters, double* z_out, int32_t* comp_iters,
+            int32_t* comp_status, void* workspace, size_t workspace_bytes, ni_stream_t stream);
+
+/* Inter-component edge list of a partition (graph.py:186-196): edge keys
+ * (a*KF + k) with differing endpoint labels, ascending.  n_out[0] = K. */
+int ni_inter_edges_workspace_size(int B, int H, int W, int connectivity, size_t* bytes);
+int ni_inter_edges(const int32_t* labels, const uint8_t* eflags, int B, int H, int W,
+                   int connectivity, int32_t* keys_out, int32_t* n_out, void* workspace,
+                   size_t workspace_bytes, ni_stream_t stream);
+
+/* Static structure of the inter-component system of one map's partition
+ * (solver.py:153-180): per-edge endpoints and component pairs, runs of edges
+ * per unordered component pair (sorted by edge index inside a run),
+ * per-component incidence lists and the sparsity of the component
+ * Laplacian A^T W A.  keys: the map's K inter edge keys (from ni_inter_edges,
+ * ascending); labels of the map lie in [label_base, label_base + count).
+ * SYNCHRONOUS (reads back the number of distinct pairs into n_pairs_host). */
+int ni_quotient_workspace_size(int K, int count, size_t* bytes);
+int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int label_base, int count,
+                      int W, int connectivity, void* quot_ws, size_t quot_bytes,
+                      int32_t* n_pairs_host, ni_stream_t stream);
+
+/* K4-K7 -- relative_scale_step (solver.py:253-303) for map `map_index` at
+ * 0-based iteration t, followed by z[valid] += s[label] (pipeline.py:181-182)
+ * on that map's pixels.  mode: 0 off, 1 soft, 2 hard
+ * (continuity.py:140-158).  Outputs scales[count], residual[2K] (rows a, b
+ * interleaved like solver.py:_pair_system), weights[2K], energy_out[0],
+ * cg_ok_out[0].  The right-hand side's roundoff null-space component is
+ * removed before the CG ("Reference numerics").
+ * SYNCHRONOUS: one 4-byte read-back (does A^T W b vanish, solver.py:112). */
+int ni_scale_step_workspace_size(int K, int count, size_t* bytes);
+int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, const int32_t* labels,
+                  int label_base, const double* omega_a, const double* omega_b,
+                  const double* gamma, const uint8_t* eflags, int B, int H, int W,
+                  int connectivity, int model, int map_index, int t, int alignment_iters,
+                  int mode, double k, double outlier_low, double outlier_high, double cg_tol,
+                  int cg_max_iters, double* z, double* scales, double* residual, double* weights,
+                  double* energy_out, int32_t* cg_ok_out, void* workspace,
+                  size_t workspace_bytes, ni_stream_t stream);
+
+/* K8 -- merge_components (graph.py:207-250) with |residual[2e]| as the merge
+ * key, plus the energy restricted to edges that stay inter-component
+ * (pipeline.py:187-203).  Relabels the map's pixels in place (labels stay
+ * in [label_base, label_base + new_count)). */
+int ni_merge_workspace_size(int K, int count, size_t* bytes);
+int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int32_t* labels,
+             int label_base, int H, int W, int map_index, const double* residual,
+             const double* weights, int32_t* new_count_out, double* energy_out, void* workspace,
+             size_t workspace_bytes, ni_stream_t stream);
+
+/* K9 -- gauge fix (pipeline.py:86-88, 229): z += target - median(z[valid])
+ * for each map separately (B medians); target = log(gauge_depth) or 0.
+ * Optionally writes depth_out = exp(z) on valid pixels (geometry.py:180-184). */
+int ni_gauge_workspace_size(int B, int H, int W, size_t* bytes);
+int ni_gauge(double* z, const uint8_t* valid, int B, int H, int W, double target,
+             double* depth_out, void* workspace, size_t workspace_bytes, ni_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NORMINT_B200_H */

@@ -1,0 +1,98 @@
+"""ctypes binding of ``libnormint_b200.so`` (the C ABI in include/normint_b200.h).
+
+The product path has no CPU fallback: if the library cannot be loaded, or no
+CUDA device is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnormint_b200.so")
+
+# status codes (include/normint_b200.h)
+NI_OK = 0
+NI_ERR_INVALID_ARG = 1
+NI_ERR_EMPTY_MASK = 2
+NI_ERR_NONUNIT_NORMAL = 3
+NI_ERR_NONFINITE = 4
+NI_ERR_WORKSPACE = 5
+NI_ERR_CUDA = 6
+NI_ERR_UNSUPPORTED = 7
+
+# every exported symbol and its signature
+_P = C.c_void_p
+_I = C.c_int
+_D = C.c_double
+_SZ = C.c_size_t
+_PSZ = C.POINTER(C.c_size_t)
+_PI32 = C.POINTER(C.c_int32)
+
+SIGNATURES = {
+    "ni_last_error": ([], C.c_char_p),
+    "ni_version": ([], C.c_char_p),
+    "ni_normalize": ([_P, _I, _P, _I, _I, _I, _P, _P, _P, _P], _I),
+    "ni_components_workspace_size": ([_I, _I, _I, _PSZ], _I),
+    "ni_components": ([_P, _P, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_coefficients": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P], _I),
+    "ni_fill_workspace_size": ([_I, _I, _I, _I, _I, _PSZ], _I),
+    "ni_fill": ([_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_inter_edges_workspace_size": ([_I, _I, _I, _I, _PSZ], _I),
+    "ni_inter_edges": ([_P, _P, _I, _I, _I, _I, _P, _P, _P, _SZ, _P], _I),
+    "ni_quotient_workspace_size": ([_I, _I, _PSZ], _I),
+    "ni_quotient_build": ([_P, _I, _P, _I, _I, _I, _I, _P, _SZ, _PI32, _P], _I),
+    "ni_scale_step_workspace_size": ([_I, _I, _PSZ], _I),
+    "ni_scale_step": ([_P, _SZ, _I, _I, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I,
+                       _I, _D, _D, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_merge_workspace_size": ([_I, _I, _PSZ], _I),
+    "ni_merge": ([_P, _SZ, _I, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_gauge_workspace_size": ([_I, _I, _I, _PSZ], _I),
+    "ni_gauge": ([_P, _P, _I, _I, _I, _D, _P, _P, _SZ, _P], _I),
+}
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and return the library handle; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"{p} is missing: build it with `python -m paper_2510_11508_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(p)
+    for name, (args, res) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().ni_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str) -> None:
+    """Map an ni_status to the reference's exception types."""
+    if status == NI_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if status == NI_ERR_EMPTY_MASK:
+        raise errors.EmptyMask(last_error())
+    if status in (NI_ERR_NONUNIT_NORMAL, NI_ERR_NONFINITE, NI_ERR_INVALID_ARG):
+        raise ValueError(last_error())
+    raise errors.DeviceError(msg)
+
+
+def size_query(fn, *args) -> int:
+    out = C.c_size_t(0)
+    check(fn(*args, C.byref(out)), fn.__name__)
+    return int(out.value)

@@ -1,0 +1,128 @@
+// K2 -- per-edge continuity coefficients (continuity.py:210-289), float64.
+//
+// One thread per pixel a evaluates its KF forward edges; coefficients are
+// stored as KF planes (omega_a[k*npix + a]) so every later pass reads them
+// coalesced.  gamma (continuity.py:270-274) depends only on the pixel, so it
+// is stored once per pixel instead of twice per edge.
+#include "ni_common.cuh"
+
+namespace ni {
+
+constexpr double kEpsDen = 1e-8;   // continuity.py:34
+constexpr double kEpsLog = 1e-12;  // continuity.py:35
+
+template <int CONN, int MODEL>
+__global__ void __launch_bounds__(256) coefficients_kernel(
+    const double* __restrict__ n, const uint8_t* __restrict__ valid,
+    const double* __restrict__ intr, int H, int W, int64_t npix, double* __restrict__ omega_a,
+    double* __restrict__ omega_b, double* __restrict__ gamma, uint8_t* __restrict__ eflags,
+    ni_stats* __restrict__ st) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  long long ndegen = 0;
+  const int64_t per_map = int64_t(H) * W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int m = int(i / per_map);
+    const double fx = intr[4 * m + 0], fy = intr[4 * m + 1];
+    const double cx = intr[4 * m + 2], cy = intr[4 * m + 3];
+    const int u = int(i % W);
+    const int vloc = int((i / W) % H);
+    uint8_t flags = 0;
+    double g = 0.0;
+    double om_a[KF], om_b[KF];
+#pragma unroll
+    for (int k = 0; k < KF; ++k) om_a[k] = om_b[k] = 0.0;
+    if (valid[i]) {
+      const double a0 = n[i], a1 = n[npix + i], a2 = n[2 * npix + i];
+      const double ua = double(u), va = double(vloc);
+      const double ta0 = (ua - cx) / fx, ta1 = (va - cy) / fy;
+      // gamma = mean_focal * |n . tau / ||tau|| |
+      const double tn = sqrt(ta0 * ta0 + ta1 * ta1 + 1.0);
+      g = 0.5 * (fx + fy) * fabs(a0 * (ta0 / tn) + a1 * (ta1 / tn) + a2 * (1.0 / tn));
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {
+        const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+        if (!fwd_inside(u, vloc, du, dv, W, H)) continue;
+        const int64_t j = i + int64_t(dv) * W + du;
+        if (!valid[j]) continue;
+        flags |= uint8_t(1u << k);
+        const double b0 = n[j], b1 = n[npix + j], b2 = n[2 * npix + j];
+        const double ub = ua + du, vb = va + dv;
+        bool ok;
+        if (MODEL == 0) {  // milano, continuity.py:232-247
+          const double tb0 = (ub - cx) / fx, tb1 = (vb - cy) / fy;
+          const double tm0 = (0.5 * (ua + ub) - cx) / fx, tm1 = (0.5 * (va + vb) - cy) / fy;
+          const double pa = a0 * ta0 + a1 * ta1 + a2;
+          const double pb = b0 * tb0 + b1 * tb1 + b2;
+          const double ma = a0 * tm0 + a1 * tm1 + a2;
+          const double mb = b0 * tm0 + b1 * tm1 + b2;
+          const double small = fmin(fmin(fabs(pa), fabs(pb)), fmin(fabs(ma), fabs(mb)));
+          const double arg = (ma * pb) / (pa * mb);
+          ok = small >= kEpsDen && arg > kEpsLog;
+          if (ok) {
+            om_a[k] = log(arg);
+            om_b[k] = -om_a[k];
+          }
+        } else {  // bini, continuity.py:248-268 (axis-aligned edges only)
+          const bool horiz = dv == 0;
+          const double f = horiz ? fx : fy;
+          const double num_a = horiz ? du * a0 : dv * a1;
+          const double num_b = horiz ? -du * b0 : -dv * b1;
+          const double den_a = a0 * (ua - cx) + a1 * (va - cy) + a2 * f;
+          const double den_b = b0 * (ub - cx) + b1 * (vb - cy) + b2 * f;
+          ok = fabs(den_a) >= kEpsDen && fabs(den_b) >= kEpsDen;
+          if (ok) {
+            om_a[k] = num_a / den_a;
+            om_b[k] = num_b / den_b;
+          }
+        }
+        if (ok) flags |= uint8_t(1u << (4 + k));
+        else ++ndegen;
+      }
+    }
+    gamma[i] = g;
+    eflags[i] = flags;
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      omega_a[k * npix + i] = om_a[k];
+      if (MODEL == 1) omega_b[k * npix + i] = om_b[k];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ndegen += __shfl_xor_sync(0xffffffffu, ndegen, o);
+  if ((threadIdx.x & 31) == 0 && ndegen)
+    atomicAdd((unsigned long long*)&st->degenerate_edges, (unsigned long long)ndegen);
+}
+
+}  // namespace ni
+
+using namespace ni;
+
+extern "C" int ni_coefficients(const double* n, const uint8_t* valid, const double* intrinsics, int B,
+                               int H, int W, int connectivity, int model, double* omega_a,
+                               double* omega_b, double* gamma, uint8_t* eflags, ni_stats* stats,
+                               ni_stream_t stream) {
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  NI_CHECK_ARG(model == 0 || model == 1, "model must be 0 (milano) or 1 (bini)");
+  NI_CHECK_ARG(!(model == 1 && connectivity == 8),
+               "the pinhole finite-difference model defines no diagonal coefficient; use "
+               "connectivity=4 with model='bini'");
+  NI_CHECK_ARG(n && valid && intrinsics && omega_a && gamma && eflags && stats, "null pointer");
+  NI_CHECK_ARG(model == 0 || omega_b, "bini needs omega_b");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npix = int64_t(B) * H * W;
+  NI_CUDA_TRY(cudaMemsetAsync(&stats->degenerate_edges, 0, sizeof(long long), s));
+  int64_t blocks64 = (npix + 255) / 256;
+  const int blocks = int(blocks64 < kSMs * 16 ? blocks64 : kSMs * 16);
+  if (connectivity == 8)
+    coefficients_kernel<8, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+                                                     omega_b, gamma, eflags, stats);
+  else if (model == 0)
+    coefficients_kernel<4, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+                                                     omega_b, gamma, eflags, stats);
+  else
+    coefficients_kernel<4, 1><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+                                                     omega_b, gamma, eflags, stats);
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}

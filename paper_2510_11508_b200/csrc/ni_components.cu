@@ -1,0 +1,283 @@
+// K0 (NormalMap.create) and K1 (form_components) on the pixel grid.
+//
+// K0 reproduces geometry.py:123-145 bit for bit: float64 norm
+// sqrt((x0*x0 + x1*x1) + x2*x2) with IEEE products/sums (no FMA), IEEE
+// division.  K1 reproduces graph.py:89-98 + 141-165: the kept-edge predicate
+// is the float64 dot ((a0*b0 + a1*b1) + a2*b2) >= d*, where the host passes
+// d* = the smallest float64 whose numpy arccos is < theta_c, so the kept set
+// is bit-identical to arccos(clip(dot)) < theta_c.  Components are found by a
+// lock-free union-find (roots hooked under the smaller id with atomicMin, so
+// every root is its component's smallest pixel id) and ranked by an
+// exclusive scan of the root flags, which is exactly the canonical labelling
+// of graph.py:133-138 (rank of the smallest row-major id).
+#include "ni_common.cuh"
+
+namespace ni {
+
+// ------------------------------------------------------------------ K0
+
+template <typename T>
+__global__ void __launch_bounds__(256) normalize_kernel(const T* __restrict__ in,
+                                                        const uint8_t* __restrict__ mask,
+                                                        int64_t npix, double* __restrict__ n_out,
+                                                        uint8_t* __restrict__ valid_out,
+                                                        ni_stats* __restrict__ st) {
+  long long nvalid = 0, nnonfin = 0, nnonunit = 0;
+  unsigned long long maxdev = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const bool m = mask ? mask[i] != 0 : true;
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+    if (m) {
+      const double x0 = double(in[3 * i + 0]);
+      const double x1 = double(in[3 * i + 1]);
+      const double x2 = double(in[3 * i + 2]);
+      ++nvalid;
+      if (!(isfinite(x0) && isfinite(x1) && isfinite(x2))) {
+        ++nnonfin;
+      } else {
+        const double nrm = __dsqrt_rn(add_rn(add_rn(mul_rn(x0, x0), mul_rn(x1, x1)), mul_rn(x2, x2)));
+        const double dev = fabs(__dadd_rn(nrm, -1.0));
+        if (dev > 1e-4) {
+          ++nnonunit;
+          unsigned long long b = __double_as_longlong(dev);
+          maxdev = b > maxdev ? b : maxdev;
+        }
+        o0 = __ddiv_rn(x0, nrm);
+        o1 = __ddiv_rn(x1, nrm);
+        o2 = __ddiv_rn(x2, nrm);
+      }
+    }
+    valid_out[i] = m ? 1 : 0;
+    n_out[i] = o0;
+    n_out[npix + i] = o1;
+    n_out[2 * npix + i] = o2;
+  }
+  // one atomic per warp per counter (integer: order-independent)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+    nnonfin += __shfl_xor_sync(0xffffffffu, nnonfin, o);
+    nnonunit += __shfl_xor_sync(0xffffffffu, nnonunit, o);
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, maxdev, o);
+    maxdev = t > maxdev ? t : maxdev;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nvalid) atomicAdd((unsigned long long*)&st->valid_pixels, (unsigned long long)nvalid);
+    if (nnonfin) atomicAdd((unsigned long long*)&st->nonfinite, (unsigned long long)nnonfin);
+    if (nnonunit) atomicAdd((unsigned long long*)&st->nonunit, (unsigned long long)nnonunit);
+    if (maxdev) atomicMax(&st->max_dev, maxdev);
+  }
+}
+
+// ------------------------------------------------------------------ K1
+
+__device__ __forceinline__ int uf_find(volatile int32_t* parent, int32_t x) {
+  int32_t p = parent[x];
+  while (p != x) {
+    x = p;
+    p = parent[x];
+  }
+  return x;
+}
+
+// Union by hooking the larger root under the smaller one (atomicMin), retried
+// until both endpoints share a root.  parent[x] <= x always holds.
+__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
+  volatile int32_t* vp = parent;
+  while (true) {
+    a = uf_find(vp, a);
+    b = uf_find(vp, b);
+    if (a == b) return;
+    if (a < b) {
+      int32_t t = a;
+      a = b;
+      b = t;
+    }
+    // a > b: try to hook root a under b
+    int32_t old = atomicMin(parent + a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
+__global__ void uf_init_kernel(const uint8_t* __restrict__ valid, int64_t npix,
+                               int32_t* __restrict__ parent) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x)
+    parent[i] = valid[i] ? int32_t(i) : -1;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(256) uf_union_kernel(const double* __restrict__ n,
+                                                       const uint8_t* __restrict__ valid, int H,
+                                                       int W, int64_t npix, double cutoff,
+                                                       int theta_none, int32_t* parent,
+                                                       ni_stats* st) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  long long nedges = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (!valid[i]) continue;
+    const int u = int(i % W);
+    const int vloc = int((i / W) % H);
+    double a0 = 0, a1 = 0, a2 = 0;
+    if (!theta_none) {
+      a0 = n[i];
+      a1 = n[npix + i];
+      a2 = n[2 * npix + i];
+    }
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+      if (!fwd_inside(u, vloc, du, dv, W, H)) continue;
+      const int64_t j = i + int64_t(dv) * W + du;
+      if (!valid[j]) continue;
+      ++nedges;
+      if (theta_none) continue;
+      const double d = add_rn(add_rn(mul_rn(a0, n[j]), mul_rn(a1, n[npix + j])),
+                              mul_rn(a2, n[2 * npix + j]));
+      if (d >= cutoff) uf_union(parent, int32_t(i), int32_t(j));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nedges += __shfl_xor_sync(0xffffffffu, nedges, o);
+  if ((threadIdx.x & 31) == 0 && nedges)
+    atomicAdd((unsigned long long*)&st->edges, (unsigned long long)nedges);
+}
+
+__global__ void uf_flatten_kernel(int32_t* parent, int64_t npix, int32_t* __restrict__ root_flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int32_t p = parent[i];
+    if (p < 0) {
+      root_flag[i] = 0;
+      continue;
+    }
+    int32_t r = uf_find(parent, int32_t(i));
+    parent[i] = r;
+    root_flag[i] = (r == int32_t(i)) ? 1 : 0;
+  }
+}
+
+__global__ void relabel_kernel(const int32_t* __restrict__ parent, const int32_t* __restrict__ rank,
+                               int64_t npix, int32_t* __restrict__ labels) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int32_t p = parent[i];
+    labels[i] = p < 0 ? -1 : rank[p];
+  }
+}
+
+__global__ void map_first_kernel(const int32_t* __restrict__ rank, const int32_t* __restrict__ total,
+                                 int B, int64_t per_map, int32_t* __restrict__ map_first,
+                                 int32_t* __restrict__ count) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < B) map_first[m] = rank[int64_t(m) * per_map];
+  if (m == B) {
+    map_first[B] = total[0];
+    count[0] = total[0];
+  }
+}
+
+static int grid_blocks(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = int64_t(kSMs) * 16;
+  return int(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+}  // namespace ni
+
+using namespace ni;
+
+extern "C" int ni_normalize(const void* normals, int dtype, const uint8_t* mask, int B, int H, int W,
+                            double* n_out, uint8_t* valid_out, ni_stats* stats, ni_stream_t stream) {
+  NI_CHECK_ARG(B >= 1 && H >= 1 && W >= 1, "grid dimensions must be positive");
+  NI_CHECK_ARG(int64_t(B) * H * W < (int64_t(1) << 31) - 1, "grid larger than 2^31-1 pixels");
+  NI_CHECK_ARG(dtype == 0 || dtype == 1, "dtype must be 0 (float32) or 1 (float64)");
+  NI_CHECK_ARG(normals && n_out && valid_out && stats, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npix = int64_t(B) * H * W;
+  NI_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(ni_stats), s));
+  const int blocks = grid_blocks(npix);
+  if (dtype == 0)
+    normalize_kernel<float><<<blocks, 256, 0, s>>>((const float*)normals, mask, npix, n_out,
+                                                  valid_out, stats);
+  else
+    normalize_kernel<double><<<blocks, 256, 0, s>>>((const double*)normals, mask, npix, n_out,
+                                                   valid_out, stats);
+  NI_LAUNCH_CHECK();
+  ni_stats h;
+  NI_CUDA_TRY(cudaMemcpyAsync(&h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+  NI_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h.nonfinite) {
+    set_error("valid normals must be finite (%lld non-finite)", h.nonfinite);
+    return NI_ERR_NONFINITE;
+  }
+  if (h.nonunit) {
+    double worst;
+    memcpy(&worst, &h.max_dev, sizeof(worst));
+    set_error("%lld valid normals deviate from unit norm by up to %.3g (tolerance 0.0001)", h.nonunit,
+              worst);
+    return NI_ERR_NONUNIT_NORMAL;
+  }
+  if (h.valid_pixels == 0) {
+    set_error("normal map has no valid pixel");
+    return NI_ERR_EMPTY_MASK;
+  }
+  return NI_OK;
+}
+
+extern "C" int ni_components_workspace_size(int B, int H, int W, size_t* bytes) {
+  NI_CHECK_ARG(bytes, "null pointer");
+  const int64_t npix = int64_t(B) * H * W;
+  Sizer z;
+  z.take<int32_t>(npix);  // parent
+  z.take<int32_t>(npix);  // root flags
+  z.take<int32_t>(npix);  // rank
+  z.take<int32_t>(1);     // total
+  z.take<char>(scan_ws_bytes(npix));
+  *bytes = z.used;
+  return NI_OK;
+}
+
+extern "C" int ni_components(const double* n, const uint8_t* valid, int B, int H, int W,
+                             int connectivity, double dot_cutoff, int theta_none, int32_t* labels_out,
+                             int32_t* count_out, int32_t* map_first_out, ni_stats* stats,
+                             void* workspace, size_t workspace_bytes, ni_stream_t stream) {
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  NI_CHECK_ARG(B >= 1 && H >= 1 && W >= 1, "grid dimensions must be positive");
+  NI_CHECK_ARG(n && valid && labels_out && count_out && map_first_out && stats, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npix = int64_t(B) * H * W;
+  Carver c(workspace, workspace_bytes);
+  int32_t* parent = c.take<int32_t>(npix);
+  int32_t* flags = c.take<int32_t>(npix);
+  int32_t* rank = c.take<int32_t>(npix);
+  int32_t* total = c.take<int32_t>(1);
+  void* scan_ws = c.take<char>(scan_ws_bytes(npix));
+  if (!c.ok() || !workspace) {
+    set_error("ni_components: workspace too small (%zu < %zu)", workspace_bytes, c.used);
+    return NI_ERR_WORKSPACE;
+  }
+  NI_CUDA_TRY(cudaMemsetAsync(&stats->edges, 0, sizeof(long long), s));
+  const int blocks = grid_blocks(npix);
+  uf_init_kernel<<<blocks, 256, 0, s>>>(valid, npix, parent);
+  NI_LAUNCH_CHECK();
+  if (connectivity == 8)
+    uf_union_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
+                                              stats);
+  else
+    uf_union_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
+                                              stats);
+  NI_LAUNCH_CHECK();
+  uf_flatten_kernel<<<blocks, 256, 0, s>>>(parent, npix, flags);
+  NI_LAUNCH_CHECK();
+  NI_TRY(exclusive_scan_i32(flags, rank, npix, total, scan_ws, s));
+  relabel_kernel<<<blocks, 256, 0, s>>>(parent, rank, npix, labels_out);
+  NI_LAUNCH_CHECK();
+  map_first_kernel<<<div_up(B + 1, 128), 128, 0, s>>>(rank, total, B, int64_t(H) * W, map_first_out,
+                                                      count_out);
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}

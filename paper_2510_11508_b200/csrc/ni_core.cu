@@ -1,0 +1,47 @@
+// Library-wide plumbing: thread-local error string, version, int scans.
+#include <stdarg.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include "ni_common.cuh"
+
+namespace ni {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+size_t scan_ws_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return bytes + 512;
+}
+
+__global__ void total_kernel(const int32_t* in, const int32_t* out, int64_t n, int32_t* total) {
+  if (n > 0) total[0] = out[n - 1] + in[n - 1];
+  else total[0] = 0;
+}
+
+int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* total_dev, void* ws,
+                       cudaStream_t s) {
+  size_t bytes = scan_ws_bytes(n) - 512;
+  if (n > 0) NI_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws, bytes, in, out, (int)n, s));
+  if (total_dev) {
+    total_kernel<<<1, 1, 0, s>>>(in, out, n, total_dev);
+    NI_LAUNCH_CHECK();
+  }
+  return NI_OK;
+}
+
+}  // namespace ni
+
+extern "C" const char* ni_last_error(void) { return ni::g_last_error.c_str(); }
+
+extern "C" const char* ni_version(void) { return "normint_b200 0.1.0 (sm_100a)"; }

@@ -1,0 +1,474 @@
+"""Drop-in ``run_pipeline`` (pipeline.py:105-248) on the B200 kernels.
+
+The host code keeps the reference's signature, options, diagnostics records
+and result type; every data-parallel step runs in ``libnormint_b200.so``
+through the C ABI.  The host only makes the scalar decisions of Algorithm 1
+(energy convergence test, merge schedule), reading back a few bytes per
+outer iteration.
+
+``run_pipeline_batch`` runs B independent maps of one size as a single grid
+(one components launch, one coefficients launch, ONE batched fill over the
+components of all maps), then the small per-map outer loops.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import EmptyMask
+from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _stream
+from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
+
+ENERGY_FLOOR = 1e-300  # pipeline.py:55
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _ws(nbytes: int, dev) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+
+
+def _ms(start: float) -> float:
+    return (time.perf_counter() - start) * 1e3
+
+
+# ----------------------------------------------------------------- threshold
+
+
+def _f64_key(x: float) -> int:
+    bits = int(np.array([x], np.float64).view(np.int64)[0])
+    return bits if bits >= 0 else -(bits & 0x7FFFFFFFFFFFFFFF)
+
+
+def _f64_from_key(k: int) -> float:
+    bits = k if k >= 0 else ((-k) | (1 << 63)) - (1 << 64)
+    return float(np.array([bits], np.int64).view(np.float64)[0])
+
+
+def dot_cutoff(theta_c: float) -> float:
+    """Smallest float64 d with numpy.arccos(clip(d, -1, 1)) < theta_c.
+
+    The reference keeps an edge iff arccos(clip(n_a . n_b)) < theta_c
+    (graph.py:92, 159).  numpy's arccos is monotone, so the kept set equals
+    {dot >= d*}; d* is found by bisection over the float64 lattice with the
+    host's own numpy arccos (evaluated through a full SIMD-width vector, the
+    same inner loop the reference runs on its edge arrays).  The GPU then
+    needs no transcendental at all and reproduces the kept set bit for bit.
+    """
+    theta_c = float(theta_c)
+
+    def kept(d):
+        v = np.clip(np.full(64, d, np.float64), -1.0, 1.0)
+        return bool(np.arccos(v)[17] < theta_c)
+
+    if not kept(1.0):
+        return math.inf
+    if kept(-1.0):
+        return -math.inf
+    lo, hi = _f64_key(-1.0), _f64_key(1.0)
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if kept(_f64_from_key(mid)):
+            hi = mid
+        else:
+            lo = mid
+    return _f64_from_key(hi)
+
+
+# ------------------------------------------------------------------ results
+
+
+class Partition:
+    """Assignment of every valid pixel to a component (graph.py:101-130).
+
+    ``labels`` (host, int64, -1 invalid) is materialised lazily from the
+    device tensor ``labels_t`` (int32).  Labels are canonical.
+    """
+
+    def __init__(self, labels_t: torch.Tensor, component_count: int, version: int = 0,
+                 label_base: int = 0):
+        self.labels_t = labels_t
+        self.component_count = int(component_count)
+        self.version = int(version)
+        self.label_base = int(label_base)
+        self._labels = None
+
+    @property
+    def labels(self) -> np.ndarray:
+        if self._labels is None:
+            a = self.labels_t.to(torch.int64).cpu().numpy()
+            if self.label_base:
+                a = np.where(a >= 0, a - self.label_base, -1)
+            a.flags.writeable = False
+            self._labels = a
+        return self._labels
+
+    @property
+    def sizes(self) -> np.ndarray:
+        lab = self.labels
+        return np.bincount(lab[lab >= 0], minlength=self.component_count)
+
+    def pixels_of(self, c: int) -> np.ndarray:
+        return np.flatnonzero(self.labels == c)
+
+
+@dataclass
+class PipelineResult:
+    """Everything the component pipeline produced (pipeline.py:91-102)."""
+
+    log_depth: LogDepthMap
+    filled: LogDepthMap
+    partition0: Partition
+    partition: Partition
+    records: list = field(default_factory=list)
+    warnings: list = field(default_factory=list)
+    iterations: int = 0
+    energies: list = field(default_factory=list)
+    fill_iterations: np.ndarray | None = None  # per component CG iterations (GPU extra)
+
+
+def _has_converged(e_t: float, e_prev: float, t: int, settings: SolveSettings) -> bool:
+    """pipeline.py:66-83."""
+    if t >= settings.max_iters:
+        return True
+    if e_t <= ENERGY_FLOOR:
+        return True
+    if t <= settings.alignment_iters + 1 or e_prev <= ENERGY_FLOOR:
+        return False
+    return abs(e_t - e_prev) / e_prev < settings.delta_e_max
+
+
+def _digest(z_map: torch.Tensor) -> str:
+    """First 16 hex digits of SHA-256 over the map's float64 z (pipeline.py:58-59)."""
+    return hashlib.sha256(z_map.cpu().numpy().tobytes()).hexdigest()[:16]
+
+
+# ------------------------------------------------------------------- engine
+
+
+class _Grid:
+    """Device state shared by every stage of one (batched) run."""
+
+    def __init__(self, nmap: NormalMap, connectivity: int, model: str):
+        self.nmap = nmap
+        self.dev = nmap.device
+        self.stream = _stream(self.dev)
+        self.B, self.H, self.W = nmap.batch, nmap.height, nmap.width
+        self.hw = self.H * self.W
+        self.npix = nmap.npix
+        self.conn = connectivity
+        self.kf = 4 if connectivity == 8 else 2
+        self.model = CONTINUITY_MODELS.index(model)
+        self.lib = _lib.load()
+        self.stats = torch.zeros(6, dtype=torch.int64, device=self.dev)
+
+    def s(self):
+        return C.c_void_p(self.stream)
+
+
+def _components(g: _Grid, theta_c):
+    lib = g.lib
+    labels = torch.empty(g.npix, dtype=torch.int32, device=g.dev)
+    count = torch.zeros(1, dtype=torch.int32, device=g.dev)
+    map_first = torch.zeros(g.B + 1, dtype=torch.int32, device=g.dev)
+    ws = _ws(_lib.size_query(lib.ni_components_workspace_size, g.B, g.H, g.W), g.dev)
+    cutoff = 0.0 if theta_c is None else dot_cutoff(theta_c)
+    _lib.check(lib.ni_components(_ptr(g.nmap.n_soa), _ptr(g.nmap.valid_t), g.B, g.H, g.W, g.conn,
+                                 C.c_double(cutoff), 1 if theta_c is None else 0, _ptr(labels),
+                                 _ptr(count), _ptr(map_first), _ptr(g.stats), _ptr(ws), ws.numel(),
+                                 g.s()), "form_components")
+    return labels, map_first
+
+
+def _coefficients(g: _Grid, intrinsics: list[CameraIntrinsics]):
+    lib = g.lib
+    intr = torch.tensor([i.as_tuple() for i in intrinsics], dtype=torch.float64).to(g.dev)
+    omega_a = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
+    omega_b = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev) if g.model == 1 else None
+    gamma = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
+    eflags = torch.empty(g.npix, dtype=torch.uint8, device=g.dev)
+    _lib.check(lib.ni_coefficients(_ptr(g.nmap.n_soa), _ptr(g.nmap.valid_t), _ptr(intr), g.B, g.H,
+                                   g.W, g.conn, g.model, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
+                                   _ptr(eflags), _ptr(g.stats), g.s()), "build_edge_coefficients")
+    return omega_a, omega_b, gamma, eflags
+
+
+def _fill(g: _Grid, labels, count, co, settings: SolveSettings):
+    lib = g.lib
+    omega_a, omega_b, gamma, eflags = co
+    z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
+    iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    ws = _ws(_lib.size_query(lib.ni_fill_workspace_size, g.B, g.H, g.W, g.conn, count), g.dev)
+    _lib.check(lib.ni_fill(_ptr(labels), count, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
+                           _ptr(eflags), g.B, g.H, g.W, g.conn, g.model, C.c_double(settings.cg_tol),
+                           int(settings.cg_max_iters), _ptr(z), _ptr(iters), _ptr(status), _ptr(ws),
+                           ws.numel(), g.s()), "fill_components")
+    return z, iters[:count], status[:count]
+
+
+class _MapLoop:
+    """The outer relative-scale loop of one map (pipeline.py:169-227)."""
+
+    def __init__(self, g: _Grid, m: int, labels: torch.Tensor, base: int, count: int, co,
+                 settings: SolveSettings, weights: WeightParams):
+        self.g, self.m, self.labels, self.base, self.count = g, m, labels, base, count
+        self.co = co
+        self.settings, self.weights = settings, weights
+        self.version = 0
+        self.keys = None
+        self.K = 0
+        self.quot = None
+
+    def rebuild(self, keys: torch.Tensor | None = None):
+        g, lib = self.g, self.g.lib
+        if keys is None:
+            hw = g.hw
+            lab = self.labels[self.m * hw:(self.m + 1) * hw]
+            ef = self.co[3][self.m * hw:(self.m + 1) * hw]
+            out = torch.empty(hw * g.kf, dtype=torch.int32, device=g.dev)
+            n = torch.zeros(1, dtype=torch.int32, device=g.dev)
+            ws = _ws(_lib.size_query(lib.ni_inter_edges_workspace_size, 1, g.H, g.W, g.conn), g.dev)
+            _lib.check(lib.ni_inter_edges(_ptr(lab), _ptr(ef), 1, g.H, g.W, g.conn, _ptr(out), _ptr(n),
+                                          _ptr(ws), ws.numel(), g.s()), "build_quotient")
+            K = int(n.item())
+            keys = out[:K] + self.m * hw * g.kf
+        self.keys = keys.contiguous()
+        self.K = int(self.keys.numel())
+        qbytes = _lib.size_query(lib.ni_quotient_workspace_size, self.K, self.count)
+        self.quot = _ws(qbytes, g.dev)
+        npairs = C.c_int32(0)
+        _lib.check(lib.ni_quotient_build(_ptr(self.keys), self.K, _ptr(self.labels), self.base,
+                                         self.count, g.W, g.conn, _ptr(self.quot), self.quot.numel(),
+                                         C.byref(npairs), g.s()), "build_quotient")
+
+    def step(self, z: torch.Tensor, t: int):
+        g, lib = self.g, self.g.lib
+        st, wp = self.settings, self.weights
+        omega_a, omega_b, gamma, eflags = self.co
+        C_ = self.count
+        scales = torch.empty(max(C_, 1), dtype=torch.float64, device=g.dev)
+        residual = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
+        wts = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
+        out = torch.zeros(2, dtype=torch.float64, device=g.dev)
+        ok = torch.zeros(1, dtype=torch.int32, device=g.dev)
+        ws = _ws(_lib.size_query(lib.ni_scale_step_workspace_size, self.K, C_), g.dev)
+        _lib.check(lib.ni_scale_step(
+            _ptr(self.quot), self.quot.numel(), self.K, C_, _ptr(self.labels), self.base,
+            _ptr(omega_a), _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
+            self.m, t, st.alignment_iters, wp.mode_code, C.c_double(wp.k),
+            C.c_double(wp.outlier_low), C.c_double(wp.outlier_high), C.c_double(st.cg_tol),
+            int(st.cg_max_iters), _ptr(z), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(out),
+            _ptr(ok), _ptr(ws), ws.numel(), g.s()), "relative_scale_step")
+        return scales, residual, wts, out, ok
+
+    def merge(self, residual, wts):
+        g, lib = self.g, self.g.lib
+        new_count = torch.zeros(1, dtype=torch.int32, device=g.dev)
+        energy = torch.zeros(1, dtype=torch.float64, device=g.dev)
+        ws = _ws(_lib.size_query(lib.ni_merge_workspace_size, self.K, self.count), g.dev)
+        _lib.check(lib.ni_merge(_ptr(self.quot), self.quot.numel(), self.K, self.count,
+                                _ptr(self.labels), self.base, g.H, g.W, self.m, _ptr(residual),
+                                _ptr(wts), _ptr(new_count), _ptr(energy), _ptr(ws), ws.numel(),
+                                g.s()), "merge_components")
+        return new_count, energy
+
+
+def _validate(model, connectivity):
+    if model not in CONTINUITY_MODELS:
+        raise ValueError(f"unknown continuity model {model!r}")
+    if connectivity not in (4, 8):
+        raise ValueError("connectivity must be 4 or 8")
+    if model == "bini" and connectivity == 8:
+        raise ValueError(
+            "the pinhole finite-difference model defines no diagonal "
+            "coefficient; use connectivity=4 with model='bini'"
+        )
+
+
+def run_pipeline_batch(
+    nmap: NormalMap,
+    intrinsics,
+    theta_c: float | None,
+    settings: SolveSettings | None = None,
+    weights: WeightParams | None = None,
+    connectivity: int = 8,
+    model: str = "milano",
+    gauge_depth: float | None = None,
+) -> list[PipelineResult]:
+    """``run_pipeline`` over the B maps of a batched NormalMap.
+
+    ``intrinsics`` is one CameraIntrinsics or a list of B.  Returns one
+    PipelineResult per map, each identical in content to what
+    ``run_pipeline`` returns for that map alone.
+    """
+    settings = settings or SolveSettings()
+    weights = weights or WeightParams()
+    _validate(model, connectivity)
+    if settings.refill_reweighted:
+        # solver.py:237-238 -- SURVEY.md §8(f) row 2, not built yet
+        raise NotImplementedError("refill_reweighted is not implemented on the GPU path yet")
+    B = nmap.batch
+    intr = list(intrinsics) if isinstance(intrinsics, (list, tuple)) else [intrinsics] * B
+    if len(intr) != B:
+        raise ValueError("need one CameraIntrinsics per map")
+    records = [[] for _ in range(B)]
+    warnings = [[] for _ in range(B)]
+    run_start = time.perf_counter()
+    g = _Grid(nmap, connectivity, model)
+    if nmap.valid_count == 0:
+        raise EmptyMask("normal map has no valid pixel")
+
+    t0 = time.perf_counter()
+    labels, map_first = _components(g, theta_c)
+    first = map_first.cpu().numpy().astype(np.int64)
+    stats = g.stats.cpu().numpy()
+    comp_ms = _ms(t0)
+    valid_per_map = g.nmap.valid_t.view(B, -1).sum(dim=1, dtype=torch.int64).cpu().numpy()
+    if B > 1 and (valid_per_map == 0).any():
+        raise EmptyMask("normal map has no valid pixel")
+    labels0 = labels.clone()
+    counts = [int(first[m + 1] - first[m]) for m in range(B)]
+    for m in range(B):
+        records[m].append({"stage": "build_graph", "vertices": int(valid_per_map[m]),
+                           "edges": int(stats[4]) if B == 1 else None, "wall_ms": 0.0})
+        records[m].append({"stage": "form_components", "component_count": counts[m],
+                           "wall_ms": comp_ms})
+
+    t0 = time.perf_counter()
+    co = _coefficients(g, intr)
+    degen = int(g.stats[5].item())
+    coef_ms = _ms(t0)
+    for m in range(B):
+        records[m].append({"stage": "edge_coefficients",
+                           "degenerate_edges": degen if B == 1 else None, "wall_ms": coef_ms})
+    if B > 1:
+        _per_map_edge_stats(g, co[3], records)
+
+    t0 = time.perf_counter()
+    total = int(first[B])
+    z, fill_iters, fill_status = _fill(g, labels, total, co, settings)
+    capped = np.flatnonzero(fill_status.cpu().numpy())
+    for c in capped:
+        m = int(np.searchsorted(first, c, side="right") - 1)
+        warnings[m].append(f"component {int(c - first[m])}: cg hit iteration cap")
+    fill_ms = _ms(t0)
+    for m in range(B):
+        records[m].append({"stage": "fill", "wall_ms": fill_ms})
+    filled = z.clone()
+    fit = fill_iters.cpu().numpy()
+
+    results = []
+    valid = g.nmap.valid_t
+    for m in range(B):
+        loop = _MapLoop(g, m, labels, int(first[m]), counts[m], co, settings, weights)
+        energies = []
+        e_prev = ENERGY_FLOOR
+        t = 0
+        converged = False
+        version = 0
+        loop.rebuild()
+        zm = z[m * g.hw:(m + 1) * g.hw]
+        while not converged:
+            it_start = time.perf_counter()
+            scales, residual, wts, out, ok = loop.step(z, t)
+            if not bool(ok.item()):
+                warnings[m].append(f"iteration {t}: cg hit iteration cap")
+            t += 1
+            merge_performed = False
+            extra = {}
+            if (settings.freq_merging is not None and t % settings.freq_merging == 0
+                    and loop.count > 1 and loop.K > 0):
+                digest = _digest(zm)
+                new_count, energy = loop.merge(residual, wts)
+                nc = int(new_count.item())
+                e_t = float(energy.item())
+                extra = {"components_before": loop.count, "components_after": nc,
+                         "z_digest_before": digest, "z_digest_after": _digest(zm)}
+                loop.count = nc
+                version += 1
+                loop.rebuild()
+                merge_performed = True
+            else:
+                e_t = float(out[0].item())
+            converged = _has_converged(e_t, e_prev, t, settings)
+            e_prev = e_t
+            energies.append(e_t)
+            records[m].append({"t": t, "E_t": e_t, "component_count": loop.count,
+                               "merge_performed": merge_performed, "wall_ms": _ms(it_start), **extra})
+        results.append((loop, energies, t, version))
+
+    target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
+    lib = g.lib
+    ws = _ws(_lib.size_query(lib.ni_gauge_workspace_size, g.B, g.H, g.W), g.dev)
+    _lib.check(lib.ni_gauge(_ptr(z), _ptr(valid), g.B, g.H, g.W, C.c_double(target), C.c_void_p(0),
+                            _ptr(ws), ws.numel(), g.s()), "gauge")
+    out = []
+    for m, (loop, energies, t, version) in enumerate(results):
+        sl = slice(m * g.hw, (m + 1) * g.hw)
+        records[m].append({"stage": "done", "iterations": t, "warnings": len(warnings[m]),
+                           "wall_ms": _ms(run_start)})
+        vm = valid[sl]
+        out.append(PipelineResult(
+            log_depth=LogDepthMap(z[sl], vm, g.H, g.W),
+            filled=LogDepthMap(torch.where(vm.bool(), filled[sl], torch.zeros_like(filled[sl])), vm,
+                               g.H, g.W),
+            partition0=Partition(labels0[sl], counts[m], 0, int(first[m])),
+            partition=Partition(labels[sl], loop.count, version, int(first[m])),
+            records=records[m],
+            warnings=warnings[m],
+            iterations=t,
+            energies=energies,
+            fill_iterations=fit[first[m]:first[m + 1]],
+        ))
+    return out
+
+
+def _per_map_edge_stats(g: _Grid, eflags: torch.Tensor, records):
+    """Per-map edge / degenerate counts for batched runs (records of
+    pipeline.py:137-159 are per map)."""
+    ef = eflags.view(g.B, -1).to(torch.int32)
+    ex = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
+    dg = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
+    for k in range(g.kf):
+        e = (ef >> k) & 1
+        v = (ef >> (4 + k)) & 1
+        ex += e.sum(dim=1)
+        dg += (e * (1 - v)).sum(dim=1)
+    ex = ex.cpu().numpy()
+    dg = dg.cpu().numpy()
+    for m in range(g.B):
+        records[m][0]["edges"] = int(ex[m])
+        records[m][2]["degenerate_edges"] = int(dg[m])
+
+
+def run_pipeline(
+    nmap: NormalMap,
+    intr: CameraIntrinsics,
+    theta_c: float | None,
+    settings: SolveSettings | None = None,
+    weights: WeightParams | None = None,
+    connectivity: int = 8,
+    model: str = "milano",
+    gauge_depth: float | None = None,
+) -> PipelineResult:
+    """Reconstruct a log-depth map from a normal map via component scales.
+
+    Same contract as normint.run_pipeline (pipeline.py:105-248): ``theta_c``
+    in radians (None = per-pixel components), output gauge-fixed to unit
+    median depth unless ``gauge_depth`` is given.
+    """
+    if nmap.batch != 1:
+        raise ValueError("run_pipeline takes a single map; use run_pipeline_batch")
+    return run_pipeline_batch(nmap, [intr], theta_c, settings, weights, connectivity, model,
+                              gauge_depth)[0]

@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden fixtures
+produced by the reference and against the CPU oracle on the same inputs.
+
+Bars (BASELINE.json north star):
+* component labels bit-exact (canonical: rank of smallest pixel id);
+* depth after the reference's own median gauge within
+  mean|d_gpu - d_ref| <= 1e-4 * mean|d_ref| + 1e-3 px  (tests/parity.py);
+* per-component scales (final z - filled z) within the same tolerance.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import GOLDEN
+from tests.parity import assert_depth_close, depth_error
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2510_11508_b200 as nb  # noqa: E402
+from paper_2510_11508_b200 import scenes  # noqa: E402
+from oracle import normint_oracle as O  # noqa: E402
+
+PIPE_CASES = sorted(
+    os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if "seam_" not in p
+)
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False))
+
+
+def opts_of(d):
+    return json.loads(str(d["options"]))
+
+
+def run_gpu(normals, mask, intr, opts):
+    theta = opts.get("theta_c_deg", 3.5)
+    nm = nb.NormalMap.create(normals, mask)
+    st = nb.SolveSettings(freq_merging=opts.get("merge_freq"))
+    wp = nb.WeightParams(reweighting_mode=opts.get("reweighting", "soft"))
+    return nb.run_pipeline(nm, nb.CameraIntrinsics(*intr),
+                           None if theta is None else float(np.deg2rad(theta)), st, wp,
+                           opts.get("connectivity", 8), opts.get("model", "milano"),
+                           opts.get("gauge_depth"))
+
+
+def reference_drifted(d):
+    text = json.loads(str(d["warning_text"])) if "warning_text" in d else []
+    return any(w.startswith("iteration") for w in text)
+
+
+@pytest.mark.parametrize("name", PIPE_CASES)
+def test_labels_bit_exact_vs_reference(name):
+    d = load(name)
+    r = run_gpu(d["normals"], d["mask"], tuple(d["intr"]), opts_of(d))
+    assert r.partition0.component_count == int(d["count0"])
+    assert np.array_equal(r.partition0.labels, d["labels0"].astype(np.int64))
+
+
+@pytest.mark.parametrize("name", PIPE_CASES)
+def test_pipeline_vs_reference(name):
+    d = load(name)
+    mask = d["mask"]
+    r = run_gpu(d["normals"], mask, tuple(d["intr"]), opts_of(d))
+    fx = float(d["intr"][0])
+    # fill: the per-component solution (fp32 CG vs scipy fp64 CG)
+    fill_err = np.abs(r.filled.values - d["filled"])[mask]
+    assert fill_err.max() < 2e-5, fill_err.max()
+    if reference_drifted(d):
+        # reference trajectory is roundoff-driven (see oracle.project_range);
+        # compare with the oracle instead (test_pipeline_vs_oracle)
+        return
+    assert r.iterations == int(d["iterations"])
+    assert r.partition.component_count == int(d["count"])
+    assert np.array_equal(r.partition.labels, d["labels"].astype(np.int64))
+    assert_depth_close(r.log_depth.values, d["log_depth"], mask, fx)
+    np.testing.assert_allclose(r.energies, d["energies"], rtol=2e-3, atol=1e-9)
+    rec = json.loads(str(d["records"]))
+    assert [x.get("stage") for x in r.records] == [x.get("stage") for x in rec]
+    for a, b in zip(r.records, rec):
+        assert set(a) == set(b) | {"wall_ms"}
+        for k in ("vertices", "edges", "component_count", "degenerate_edges", "t",
+                  "merge_performed", "components_before", "components_after", "iterations"):
+            if k in b:
+                assert a[k] == b[k], (k, a[k], b[k])
+
+
+@pytest.mark.parametrize("name", PIPE_CASES)
+def test_pipeline_vs_oracle(name):
+    d = load(name)
+    mask = d["mask"]
+    o = opts_of(d)
+    r = run_gpu(d["normals"], mask, tuple(d["intr"]), o)
+    theta = o.get("theta_c_deg", 3.5)
+    ref = O.run_pipeline(d["normals"].astype(np.float64), mask, tuple(d["intr"]),
+                         None if theta is None else float(np.deg2rad(theta)),
+                         O.Settings(freq_merging=o.get("merge_freq"),
+                                    reweighting_mode=o.get("reweighting", "soft")),
+                         o.get("connectivity", 8), o.get("model", "milano"), o.get("gauge_depth"))
+    assert np.array_equal(r.partition0.labels, ref.labels0)
+    if ref.iterations < 150:
+        assert r.iterations == ref.iterations
+        assert np.array_equal(r.partition.labels, ref.labels)
+    assert_depth_close(r.log_depth.values, ref.log_depth, mask, float(d["intr"][0]))
+
+
+def test_deterministic_reruns():
+    sc = scenes.config4(3, size=96, cells=14)
+    a = run_gpu(sc.normals, sc.mask, sc.intrinsics(), {"merge_freq": 5})
+    b = run_gpu(sc.normals, sc.mask, sc.intrinsics(), {"merge_freq": 5})
+    assert np.array_equal(a.log_depth.values, b.log_depth.values)
+    assert np.array_equal(a.filled.values, b.filled.values)
+    assert a.energies == b.energies
+
+    def strip(rs):
+        return [{k: v for k, v in x.items() if k != "wall_ms"} for x in rs]
+
+    assert strip(a.records) == strip(b.records)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_size_configs_vs_oracle(cfg):
+    sc = scenes.CONFIGS[cfg]()
+    theta = float(np.deg2rad(3.5))
+    nm = nb.NormalMap.create(sc.normals, sc.mask)
+    r = nb.run_pipeline(nm, nb.CameraIntrinsics(*sc.intrinsics()), theta)
+    ref = O.run_pipeline(sc.normals.astype(np.float64), sc.mask, sc.intrinsics(), theta)
+    assert np.array_equal(r.partition0.labels, ref.labels0)
+    err, bound = depth_error(r.log_depth.values, ref.log_depth, sc.mask, sc.fx)
+    print(f"{cfg}: iters gpu={r.iterations} oracle={ref.iterations} depth err {err:.3e} bound {bound:.3e}")
+    assert err <= bound
+
+
+def test_batch_equals_single_maps():
+    maps = [scenes.config5_map(i, size=64, cells=5) for i in range(3)]
+    nms = [nb.NormalMap.create(m.normals, m.mask) for m in maps]
+    intr = [nb.CameraIntrinsics(*m.intrinsics()) for m in maps]
+    theta = float(np.deg2rad(3.5))
+    batch = nb.run_pipeline_batch(nb.stack(nms), intr, theta)
+    for i, m in enumerate(maps):
+        single = nb.run_pipeline(nms[i], intr[i], theta)
+        assert np.array_equal(batch[i].partition0.labels, single.partition0.labels)
+        assert batch[i].iterations == single.iterations
+        assert_depth_close(batch[i].log_depth.values, single.log_depth.values, m.mask, m.fx)
+
+
+def test_errors_like_reference():
+    n = np.zeros((4, 4, 3), np.float32)
+    n[..., 2] = -1
+    with pytest.raises(nb.EmptyMask):
+        nm = nb.NormalMap.create(n, np.zeros((4, 4), bool))
+        nb.run_pipeline(nm, nb.CameraIntrinsics(1, 1, 0, 0), 0.1)
+    bad = n.copy()
+    bad[1, 1, 2] = -1.01
+    with pytest.raises(ValueError):
+        nb.NormalMap.create(bad)
+    nm = nb.NormalMap.create(n)
+    with pytest.raises(ValueError):
+        nb.run_pipeline(nm, nb.CameraIntrinsics(1, 1, 0, 0), 0.1, connectivity=8, model="bini")
