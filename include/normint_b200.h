@@ -46,6 +46,14 @@ typedef enum {
 
 const char* ni_last_error(void);
 const char* ni_version(void);
+/* Host-side count of kernels this library launched (all threads). */
+long long ni_launch_count(void);
+/* Diagnostics of the last ni_fill on the calling thread: device time of the
+ * persistent CG kernel (CUDA events on `stream`), sum over components of
+ * size * CG iterations, largest iteration count, cooperative grid size,
+ * number of 32x32 tiles and of (tile, component) partial slots. */
+int ni_fill_last_report(double* cg_ms, long long* px_iters, int* max_iters, int* grid,
+                        int* ntiles, int* npartials);
 
 /* Counters written by ni_normalize / ni_coefficients (device struct). */
 typedef struct {

@@ -35,6 +35,9 @@ _PI32 = C.POINTER(C.c_int32)
 SIGNATURES = {
     "ni_last_error": ([], C.c_char_p),
     "ni_version": ([], C.c_char_p),
+    "ni_launch_count": ([], C.c_longlong),
+    "ni_fill_last_report": ([C.POINTER(C.c_double), C.POINTER(C.c_longlong), _PI32, _PI32, _PI32,
+                             _PI32], _I),
     "ni_normalize": ([_P, _I, _P, _I, _I, _I, _P, _P, _P, _P], _I),
     "ni_components_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_components": ([_P, _P, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
@@ -96,3 +99,18 @@ def size_query(fn, *args) -> int:
     out = C.c_size_t(0)
     check(fn(*args, C.byref(out)), fn.__name__)
     return int(out.value)
+
+
+def launch_count() -> int:
+    """Kernels this library has launched so far (host-side counter)."""
+    return int(load().ni_launch_count())
+
+
+def fill_report() -> dict:
+    """Diagnostics of the last fill on this thread (see ni_fill_last_report)."""
+    ms, pxi = C.c_double(0), C.c_longlong(0)
+    mx, g, nt, npart = C.c_int32(0), C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    load().ni_fill_last_report(C.byref(ms), C.byref(pxi), C.byref(mx), C.byref(g), C.byref(nt),
+                               C.byref(npart))
+    return {"cg_ms": ms.value, "px_iters": pxi.value, "max_iters": mx.value, "grid": g.value,
+            "ntiles": nt.value, "npartials": npart.value}

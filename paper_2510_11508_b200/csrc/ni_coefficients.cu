@@ -115,13 +115,13 @@ extern "C" int ni_coefficients(const double* n, const uint8_t* valid, const doub
   int64_t blocks64 = (npix + 255) / 256;
   const int blocks = int(blocks64 < kSMs * 16 ? blocks64 : kSMs * 16);
   if (connectivity == 8)
-    coefficients_kernel<8, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<8, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   else if (model == 0)
-    coefficients_kernel<4, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<4, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   else
-    coefficients_kernel<4, 1><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<4, 1><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   NI_LAUNCH_CHECK();
   return NI_OK;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/normint_b200.h"
@@ -14,6 +15,21 @@ namespace ni {
 // ---------------------------------------------------------------- errors
 
 void set_error(const char* fmt, ...);
+
+// Host-side count of this library's kernel launches (ni_launch_count()).
+extern std::atomic<long long> g_launches;
+#define NI_COUNT_LAUNCH() (::ni::g_launches.fetch_add(1, std::memory_order_relaxed))
+
+// Diagnostics of the last ni_fill on this thread (ni_fill_last_report()).
+struct FillReport {
+  double cg_ms;        // device time of the persistent CG kernel (CUDA events)
+  long long px_iters;  // sum over components of size * CG iterations
+  int max_iters;       // largest per-component iteration count
+  int grid;            // CTAs of the cooperative launch
+  int ntiles;          // 32x32 tiles of the grid
+  int npartials;       // (tile, component) partial slots
+};
+extern thread_local FillReport g_fill_report;
 
 #define NI_CUDA_TRY(expr)                                                              \
   do {                                                                                 \

@@ -201,10 +201,10 @@ extern "C" int ni_normalize(const void* normals, int dtype, const uint8_t* mask,
   NI_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(ni_stats), s));
   const int blocks = grid_blocks(npix);
   if (dtype == 0)
-    normalize_kernel<float><<<blocks, 256, 0, s>>>((const float*)normals, mask, npix, n_out,
+    NI_COUNT_LAUNCH(), normalize_kernel<float><<<blocks, 256, 0, s>>>((const float*)normals, mask, npix, n_out,
                                                   valid_out, stats);
   else
-    normalize_kernel<double><<<blocks, 256, 0, s>>>((const double*)normals, mask, npix, n_out,
+    NI_COUNT_LAUNCH(), normalize_kernel<double><<<blocks, 256, 0, s>>>((const double*)normals, mask, npix, n_out,
                                                    valid_out, stats);
   NI_LAUNCH_CHECK();
   ni_stats h;
@@ -262,21 +262,21 @@ extern "C" int ni_components(const double* n, const uint8_t* valid, int B, int H
   }
   NI_CUDA_TRY(cudaMemsetAsync(&stats->edges, 0, sizeof(long long), s));
   const int blocks = grid_blocks(npix);
-  uf_init_kernel<<<blocks, 256, 0, s>>>(valid, npix, parent);
+  NI_COUNT_LAUNCH(), uf_init_kernel<<<blocks, 256, 0, s>>>(valid, npix, parent);
   NI_LAUNCH_CHECK();
   if (connectivity == 8)
-    uf_union_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
+    NI_COUNT_LAUNCH(), uf_union_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
                                               stats);
   else
-    uf_union_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
+    NI_COUNT_LAUNCH(), uf_union_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
                                               stats);
   NI_LAUNCH_CHECK();
-  uf_flatten_kernel<<<blocks, 256, 0, s>>>(parent, npix, flags);
+  NI_COUNT_LAUNCH(), uf_flatten_kernel<<<blocks, 256, 0, s>>>(parent, npix, flags);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(flags, rank, npix, total, scan_ws, s));
-  relabel_kernel<<<blocks, 256, 0, s>>>(parent, rank, npix, labels_out);
+  NI_COUNT_LAUNCH(), relabel_kernel<<<blocks, 256, 0, s>>>(parent, rank, npix, labels_out);
   NI_LAUNCH_CHECK();
-  map_first_kernel<<<div_up(B + 1, 128), 128, 0, s>>>(rank, total, B, int64_t(H) * W, map_first_out,
+  NI_COUNT_LAUNCH(), map_first_kernel<<<div_up(B + 1, 128), 128, 0, s>>>(rank, total, B, int64_t(H) * W, map_first_out,
                                                       count_out);
   NI_LAUNCH_CHECK();
   return NI_OK;

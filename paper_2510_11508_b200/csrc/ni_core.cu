@@ -8,6 +8,8 @@
 namespace ni {
 
 static thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+thread_local FillReport g_fill_report{};
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -34,7 +36,7 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* tota
   size_t bytes = scan_ws_bytes(n) - 512;
   if (n > 0) NI_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws, bytes, in, out, (int)n, s));
   if (total_dev) {
-    total_kernel<<<1, 1, 0, s>>>(in, out, n, total_dev);
+    NI_COUNT_LAUNCH(), total_kernel<<<1, 1, 0, s>>>(in, out, n, total_dev);
     NI_LAUNCH_CHECK();
   }
   return NI_OK;
@@ -45,3 +47,17 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* tota
 extern "C" const char* ni_last_error(void) { return ni::g_last_error.c_str(); }
 
 extern "C" const char* ni_version(void) { return "normint_b200 0.1.0 (sm_100a)"; }
+
+extern "C" long long ni_launch_count(void) { return ni::g_launches.load(); }
+
+extern "C" int ni_fill_last_report(double* cg_ms, long long* px_iters, int* max_iters, int* grid,
+                                   int* ntiles, int* npartials) {
+  const ni::FillReport& r = ni::g_fill_report;
+  if (cg_ms) *cg_ms = r.cg_ms;
+  if (px_iters) *px_iters = r.px_iters;
+  if (max_iters) *max_iters = r.max_iters;
+  if (grid) *grid = r.grid;
+  if (ntiles) *ntiles = r.ntiles;
+  if (npartials) *npartials = r.npartials;
+  return NI_OK;
+}

@@ -131,11 +131,11 @@ extern "C" int ni_gauge(double* z, const uint8_t* valid, int B, int H, int W, do
   int bx = int(std::min<int64_t>((per_map + 255) / 256, std::max<int64_t>(1, 4 * kSMs / B)));
   if (bx < 1) bx = 1;
   for (int shift = 56; shift >= 0; shift -= 8) {
-    select_hist_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, shift, st, hist);
-    select_pick_kernel<<<div_up(B, 64), 64, 0, s>>>(hist, st, shift, B);
+    NI_COUNT_LAUNCH(), select_hist_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, shift, st, hist);
+    NI_COUNT_LAUNCH(), select_pick_kernel<<<div_up(B, 64), 64, 0, s>>>(hist, st, shift, B);
   }
   NI_LAUNCH_CHECK();
-  gauge_apply_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, st, target, depth_out, med);
+  NI_COUNT_LAUNCH(), gauge_apply_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, st, target, depth_out, med);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }

@@ -693,12 +693,12 @@ extern "C" int ni_inter_edges(const int32_t* labels, const uint8_t* eflags, int 
     return NI_ERR_WORKSPACE;
   }
   if (connectivity == 8)
-    inter_flags_kernel<8><<<blocks_for(npix), 256, 0, s>>>(labels, eflags, W, npix, flag);
+    NI_COUNT_LAUNCH(), inter_flags_kernel<8><<<blocks_for(npix), 256, 0, s>>>(labels, eflags, W, npix, flag);
   else
-    inter_flags_kernel<4><<<blocks_for(npix), 256, 0, s>>>(labels, eflags, W, npix, flag);
+    NI_COUNT_LAUNCH(), inter_flags_kernel<4><<<blocks_for(npix), 256, 0, s>>>(labels, eflags, W, npix, flag);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(flag, pos, ne, n_out, sws, s));
-  compact_kernel<<<blocks_for(ne), 256, 0, s>>>(flag, pos, ne, keys_out);
+  NI_COUNT_LAUNCH(), compact_kernel<<<blocks_for(ne), 256, 0, s>>>(flag, pos, ne, keys_out);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }
@@ -737,37 +737,37 @@ extern "C" int ni_quotient_build(const int32_t* keys, int K, const int32_t* labe
     return NI_OK;
   }
   if (connectivity == 8)
-    quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+    NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
   else
-    quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+    NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
   NI_LAUNCH_CHECK();
   const int pbits = end_bits_for((int64_t)C * C);
   size_t sb = q.sort_bytes;
   // (1) edges sorted by component pair (stable => edge order within a run)
   NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.order, K, 0,
                                               pbits, s));
-  run_flags_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, q.flag);
+  NI_COUNT_LAUNCH(), run_flags_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, q.flag);
   NI_LAUNCH_CHECK();
   // q.v32b holds incidence values; use q.lcol as scratch for run positions
   NI_TRY(exclusive_scan_i32(q.flag, q.lcol, K, q.nU, q.scan_ws, s));
-  pair_runs_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, C, q.lcol, q);
+  NI_COUNT_LAUNCH(), pair_runs_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, C, q.lcol, q);
   NI_LAUNCH_CHECK();
-  set_tail_kernel<<<1, 1, 0, s>>>(q.pstart, q.nU, K);
+  NI_COUNT_LAUNCH(), set_tail_kernel<<<1, 1, 0, s>>>(q.pstart, q.nU, K);
   NI_LAUNCH_CHECK();
   // (2) incidence lists: (component, 2e+side) sorted by component, stable
   // keys are in q.flag? rebuild them (flag was overwritten by run flags)
   {
     if (connectivity == 8)
-      quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+      NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
     else
-      quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+      NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
     NI_LAUNCH_CHECK();
     const int cbits = end_bits_for(C);
     sb = q.sort_bytes;
     NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.flag, q.v32a, q.v32b, q.cent,
                                                 2 * K, 0, cbits, s));
     NI_CUDA_TRY(cudaMemsetAsync(q.hist, 0, sizeof(int32_t) * (C + 1), s));
-    hist_kernel<<<blocks_for(2 * int64_t(K)), 256, 0, s>>>(q.flag, 2 * K, q.hist);
+    NI_COUNT_LAUNCH(), hist_kernel<<<blocks_for(2 * int64_t(K)), 256, 0, s>>>(q.flag, 2 * K, q.hist);
     NI_LAUNCH_CHECK();
     NI_TRY(exclusive_scan_i32(q.hist, q.cstart, C + 1, nullptr, q.scan_ws, s));
   }
@@ -775,15 +775,15 @@ extern "C" int ni_quotient_build(const int32_t* keys, int K, const int32_t* labe
   NI_CUDA_TRY(cudaMemcpyAsync(&U, q.nU, sizeof(U), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaStreamSynchronize(s));
   // (3) Laplacian sparsity: entries (row, col) for both directions of a pair
-  lap_entries_kernel<<<blocks_for(U), 256, 0, s>>>(q, q.nU);
+  NI_COUNT_LAUNCH(), lap_entries_kernel<<<blocks_for(U), 256, 0, s>>>(q, q.nU);
   NI_LAUNCH_CHECK();
   sb = q.sort_bytes;
   NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.lpair, 2 * U,
                                               0, pbits, s));
-  lap_cols_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q, q.k64b, 2 * U);
+  NI_COUNT_LAUNCH(), lap_cols_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q, q.k64b, 2 * U);
   NI_LAUNCH_CHECK();
   NI_CUDA_TRY(cudaMemsetAsync(q.hist, 0, sizeof(int32_t) * (C + 1), s));
-  hist_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q.flag, 2 * U, q.hist);
+  NI_COUNT_LAUNCH(), hist_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q.flag, 2 * U, q.hist);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(q.hist, q.lstart, C + 1, nullptr, q.scan_ws, s));
   if (n_pairs_host) *n_pairs_host = U;
@@ -824,47 +824,47 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   const int C = count;
   const int64_t npix = int64_t(B) * H * W;
   if (K == 0) {  // solver.py:293-295
-    zero_kernel<<<blocks_for(C), 256, 0, s>>>(scales, C);
+    NI_COUNT_LAUNCH(), zero_kernel<<<blocks_for(C), 256, 0, s>>>(scales, C);
     NI_LAUNCH_CHECK();
     NI_CUDA_TRY(cudaMemsetAsync(energy_out, 0, sizeof(double), s));
-    set_int_kernel<<<1, 1, 0, s>>>(cg_ok_out, 1);
+    NI_COUNT_LAUNCH(), set_int_kernel<<<1, 1, 0, s>>>(cg_ok_out, 1);
     NI_LAUNCH_CHECK();
     return NI_OK;
   }
   const int uniform = t < alignment_iters;
   const double lt = log10(outlier_low), ut = log10(outlier_high);
   if (connectivity == 8)
-    weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
+    NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
                                                        npix, uniform, mode, k, lt, ut, outlier_high, w);
   else if (model == 0)
-    weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
+    NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
                                                        npix, uniform, mode, k, lt, ut, outlier_high, w);
   else
-    weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
+    NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
                                                        npix, uniform, mode, k, lt, ut, outlier_high, w);
   NI_LAUNCH_CHECK();
-  pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
+  NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
   NI_CUDA_TRY(cudaMemsetAsync(w.anyflag, 0, sizeof(int32_t), s));
-  comp_sum_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, w);
+  NI_COUNT_LAUNCH(), comp_sum_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, w);
   NI_LAUNCH_CHECK();
   int32_t any = 0;
   NI_CUDA_TRY(cudaMemcpyAsync(&any, w.anyflag, sizeof(any), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaStreamSynchronize(s));
   if (!any) {  // solver.py:112-113
-    zero_kernel<<<blocks_for(C), 256, 0, s>>>(w.s, C);
+    NI_COUNT_LAUNCH(), zero_kernel<<<blocks_for(C), 256, 0, s>>>(w.s, C);
     NI_LAUNCH_CHECK();
-    set_int_kernel<<<1, 1, 0, s>>>(w.okflag, 1);
+    NI_COUNT_LAUNCH(), set_int_kernel<<<1, 1, 0, s>>>(w.okflag, 1);
   } else {
     // remove the roundoff null-space component of A^T W b
-    part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
-    part_union_kernel<<<blocks_for(K), 256, 0, s>>>(q, w, q.nU);
-    part_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
+    NI_COUNT_LAUNCH(), part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
+    NI_COUNT_LAUNCH(), part_union_kernel<<<blocks_for(K), 256, 0, s>>>(q, w, q.nU);
+    NI_COUNT_LAUNCH(), part_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
     NI_LAUNCH_CHECK();
     size_t sb = w.sort_bytes;
     NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_ws, sb, w.pkey, w.pkey_s, w.pval, w.pval_s, C,
                                                 0, end_bits_for(C), s));
-    part_mean_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(w, C);
-    part_sub_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
+    NI_COUNT_LAUNCH(), part_mean_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(w, C);
+    NI_COUNT_LAUNCH(), part_sub_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
     NI_LAUNCH_CHECK();
     // K6
     int dev = 0;
@@ -881,15 +881,16 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     const int maxiter = cg_max_iters > C ? cg_max_iters : C;
     double rtol = cg_tol;
     void* args[] = {&q, &w, &rtol, (void*)&maxiter};
+    NI_COUNT_LAUNCH();
     NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(G), dim3(kCgThreads), args, 0,
                                             s));
   }
-  residual_kernel<<<kResBlocks, 256, 0, s>>>(q, w, scales, residual, weights);
+  NI_COUNT_LAUNCH(), residual_kernel<<<kResBlocks, 256, 0, s>>>(q, w, scales, residual, weights);
   NI_LAUNCH_CHECK();
-  energy_final_kernel<<<blocks_for(C), 256, 0, s>>>(w, kResBlocks, scales, C, energy_out, cg_ok_out);
+  NI_COUNT_LAUNCH(), energy_final_kernel<<<blocks_for(C), 256, 0, s>>>(w, kResBlocks, scales, C, energy_out, cg_ok_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  apply_kernel<<<blocks_for(per_map), 256, 0, s>>>(z, labels, w.s, label_base, map_index * per_map,
+  NI_COUNT_LAUNCH(), apply_kernel<<<blocks_for(per_map), 256, 0, s>>>(z, labels, w.s, label_base, map_index * per_map,
                                                    (map_index + 1) * per_map);
   NI_LAUNCH_CHECK();
   return NI_OK;
@@ -921,17 +922,17 @@ extern "C" int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count
     return NI_ERR_WORKSPACE;
   }
   const int C = count;
-  merge_select_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, residual, m);
-  merge_union_kernel<<<blocks_for(C), 256, 0, s>>>(q, m);
-  merge_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(m, C);
+  NI_COUNT_LAUNCH(), merge_select_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, residual, m);
+  NI_COUNT_LAUNCH(), merge_union_kernel<<<blocks_for(C), 256, 0, s>>>(q, m);
+  NI_COUNT_LAUNCH(), merge_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(m, C);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(m.flag, m.rank, C, m.total, m.scan_ws, s));
-  merge_energy_kernel<<<kResBlocks, 256, 0, s>>>(q, m, residual, weights);
+  NI_COUNT_LAUNCH(), merge_energy_kernel<<<kResBlocks, 256, 0, s>>>(q, m, residual, weights);
   NI_LAUNCH_CHECK();
-  merge_final_kernel<<<1, 1, 0, s>>>(m, kResBlocks, energy_out, new_count_out);
+  NI_COUNT_LAUNCH(), merge_final_kernel<<<1, 1, 0, s>>>(m, kResBlocks, energy_out, new_count_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  merge_relabel_kernel<<<blocks_for(per_map), 256, 0, s>>>(labels, m, label_base,
+  NI_COUNT_LAUNCH(), merge_relabel_kernel<<<blocks_for(per_map), 256, 0, s>>>(labels, m, label_base,
                                                            map_index * per_map,
                                                            (map_index + 1) * per_map);
   NI_LAUNCH_CHECK();

@@ -135,6 +135,7 @@ class PipelineResult:
     iterations: int = 0
     energies: list = field(default_factory=list)
     fill_iterations: np.ndarray | None = None  # per component CG iterations (GPU extra)
+    fill_report: dict | None = None  # device timing of the batched fill (GPU extra)
 
 
 def _has_converged(e_t: float, e_prev: float, t: int, settings: SolveSettings) -> bool:
@@ -358,6 +359,7 @@ def run_pipeline_batch(
     t0 = time.perf_counter()
     total = int(first[B])
     z, fill_iters, fill_status = _fill(g, labels, total, co, settings)
+    report = _lib.fill_report()
     capped = np.flatnonzero(fill_status.cpu().numpy())
     for c in capped:
         m = int(np.searchsorted(first, c, side="right") - 1)
@@ -430,6 +432,7 @@ def run_pipeline_batch(
             iterations=t,
             energies=energies,
             fill_iterations=fit[first[m]:first[m + 1]],
+            fill_report=report,
         ))
     return out
 

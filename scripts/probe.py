@@ -19,6 +19,7 @@ for cfg in cfgs:
     gen = time.time() - t
     theta = float(np.deg2rad(3.5))
     st = nb.SolveSettings(freq_merging=sc.options.get("merge_freq"))
+    prev = None
     for rep in range(2):
         torch.cuda.synchronize()
         t = time.time()
@@ -33,3 +34,7 @@ for cfg in cfgs:
               f"comps {r.partition0.component_count}->{r.partition.component_count} outer {r.iterations} "
               f"stages {stages} outer_ms {it_ms:.1f} fill_iters max {fi.max() if len(fi) else 0} "
               f"warnings {len(r.warnings)}", flush=True)
+        cur = r.log_depth.values.copy()
+        if prev is not None:
+            print(f"{cfg}: bit-identical rerun: {np.array_equal(prev, cur)}", flush=True)
+        prev = cur
