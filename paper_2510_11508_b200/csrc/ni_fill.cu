@@ -15,32 +15,41 @@
 // loses that and doubles the iteration count).
 //
 // Data layout in HBM (per pixel, npix = B*H*W, row-major):
-//   x, r, q, p[2] : float32 CG vectors (p double-buffered: sweep 1 reads the
-//                   neighbours' previous p while other warps write the new)
+//   x             : float32 solution
+//   r[2], q[2], p[2] : float32 CG vectors, double-buffered by iteration parity
+//                   (a sweep reads its neighbours' previous values while
+//                   other warps write the new ones)
 //   hw            : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
 //   imask         : uint8, bit k = forward edge k intra-component and valid,
 //                   bit 4+k = backward edge k (pixel - offset_k)
+//
+// ONE sweep and ONE grid sync per CG iteration.  scipy's iteration k
+//   p_k = r_k + beta p_{k-1};  q_k = A p_k;  alpha = rho_k / <p_k, q_k>;
+//   x_{k+1} = x_k + alpha p_k;  r_{k+1} = r_k - alpha q_k;  rho_{k+1} = <r_{k+1}, r_{k+1}>
+// is regrouped so that sweep k forms r_k = r_{k-1} - alpha_{k-1} q_{k-1} and
+// x_k = x_{k-1} + alpha_{k-1} p_{k-1} on the fly (also for the stencil halo),
+// then p_k and q_k, and reduces <p,q>, <r,q>, <q,q>, <r,r> in the same pass.
+// rho_k = <r_k, r_k> is exact; rho_{k+1}, needed for beta and for scipy's
+// stop test before r_{k+1} exists, is rho_k - 2 alpha <r,q> + alpha^2 <q,q>
+// (float64, no cancellation at CG's per-step contraction).  A component that
+// stops gets one last "flush" sweep that applies its pending x update.
 //
 // Work decomposition: the grid is cut into strips of 30 columns x 32 rows.
 // A warp processes a strip by marching down its rows with a register ring
 // of rows y-1, y, y+1 (+ prefetched rows); lanes 0 and 31 carry the left /
 // right halo columns, so horizontal neighbours are warp shuffles and there
 // is no block barrier anywhere in a sweep.  A strip touching several
-// multi-pixel components becomes ceil(n/4) "items" of <= 4 components that
+// multi-pixel components becomes ceil(n/2) "items" of <= 2 components that
 // read the int32 labels; a strip with one component (the common case) is a
 // "pure" item that needs no label at all (singletons / invalid pixels carry
-// r = p = 0 and stay 0 under any update).
+// r = q = p = 0 and stay 0 under any update).
 //
-// Reductions are deterministic: each item writes one float64 partial per
+// Reductions are deterministic: each item writes float64 partials per
 // component (lane-local sums over rows, fixed xor tree over lanes); the last
 // warp to arrive for a component (integer counter) sums the component's
-// partials in plan order and updates its scalars.  Two grid syncs per
-// iteration:
-//   sweep 1: p' = r + beta p ; q = A p' ; <p', q>   -> alpha
-//   sweep 2: x += alpha p' ; r -= alpha q ; <r, r>  -> stop test, beta
+// partials in plan order and updates its scalars.
 // Algorithmic bytes per active pixel and iteration (pure items):
-//   sweep 1: read r, p, hw, imask (13 B), write p', q (8 B)
-//   sweep 2: read x, r, p', q (16 B), write x, r (8 B)          => 45 B/px
+//   read r, q, p, x, hw (20 B) + imask (1 B); write r, q, p, x (16 B) => 37 B/px
 // (halo rows/columns are re-read from L2 and not counted).
 #include <cooperative_groups.h>
 #include <stdlib.h>
@@ -58,16 +67,17 @@ constexpr int SH = 32;     // strip height (rows per item)
 constexpr int SPX = 1024;  // padded pixels per strip (sort buffer)
 constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
-constexpr int SLOTS = 4;  // components per item
-constexpr int PF = 4;     // rows prefetched ahead in sweep 1
+constexpr int SLOTS = 2;  // components per item
+constexpr int PF = 3;     // rows prefetched ahead
+constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 
-enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3 };
+enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3, ST_FLUSH = 4 };
 
-// One work item: a strip and up to 4 of its components.
+// One work item: a strip and up to 2 of its components.
 struct __align__(16) Item {
   int32_t x0, y0;  // top-left pixel of the strip (column of lane 1)
   int32_t pbase;   // first partial slot of this item
-  int32_t flags;   // bits 0-7: components in the item (1..4); bit 8: pure strip
+  int32_t flags;   // bits 0-7: components in the item (1..2); bit 8: pure strip
   int32_t comp[SLOTS];
 };
 
@@ -77,10 +87,9 @@ __device__ __forceinline__ bool item_pure(const Item& it) { return (it.flags >> 
 struct FillArgs {
   int rows, W;
   float* x;
-  float* r;
-  float* q;
-  float* p0;
-  float* p1;
+  float* r[2];
+  float* q[2];
+  float* p[2];
   const float* hw;
   const uint8_t* imask;
   const int32_t* labels;
@@ -90,20 +99,20 @@ struct FillArgs {
   const int32_t* comp_pstart;  // [C+1] partial range per component
   const int32_t* comp_plist;   // [P] partial indices grouped by component
   int32_t* comp_cnt;           // [C] arrival counters (zero between sweeps)
-  double* partial;             // [P]
+  double* partial;             // [P][NDOT]
   int32_t* active_items;       // [2][nitems]
   int32_t* nactive_items;      // [2]
   // component state
-  double* rho;
-  double* alpha;
+  double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
+  double* alpha;   // alpha of the last completed sweep
   double* beta;
   double* tol;
   int32_t* iters;
   int32_t* cap;
   uint8_t* status;
-  uint8_t* brk;      // breakdown flag set in sweep 1, resolved in sweep 2
-  int32_t* active;   // number of active components
-  int32_t* changed;  // a component finished during the last sweep 2
+  uint8_t* final_status;  // status after the flush sweep
+  int32_t* active;   // components still ACTIVE or FLUSH
+  int32_t* changed;  // a component changed state during the last sweep
 };
 
 // ----------------------------------------------------------------- setup
@@ -114,16 +123,18 @@ __global__ void __launch_bounds__(256) prep_kernel(
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
     const uint8_t* __restrict__ eflags, int H, int W, int64_t npix, float* __restrict__ hw,
     uint8_t* __restrict__ imask, float* __restrict__ x, float* __restrict__ r,
-    float* __restrict__ p0, float* __restrict__ p1, float* __restrict__ q,
-    int32_t* __restrict__ comp_size) {
+    float* __restrict__ r1, float* __restrict__ q0, float* __restrict__ q1, float* __restrict__ p0,
+    float* __restrict__ p1, int32_t* __restrict__ comp_size) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t lab = labels[i];
     x[i] = 0.f;
+    r1[i] = 0.f;
+    q0[i] = 0.f;
+    q1[i] = 0.f;
     p0[i] = 0.f;
     p1[i] = 0.f;
-    q[i] = 0.f;
     if (lab < 0) {
       hw[i] = 0.f;
       imask[i] = 0;
@@ -274,28 +285,47 @@ __global__ void item_counts_kernel(const int32_t* __restrict__ nslots, int nstri
 
 // ------------------------------------------------------- warp machinery
 
-// Write the item's per-component partials, count arrivals, and let the last
-// arriving warp of a component reduce its partials in plan order.
+__device__ __forceinline__ int slot_of(const Item& it, int32_t lab) {
+  int s = -1;
+  const int n = item_n(it);
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j)
+    if (j < n && it.comp[j] == lab) s = j;
+  return s;
+}
+
+// Write the item's per-component partials (NDOT each), count arrivals, and
+// let the last arriving warp of a component reduce its partials in plan
+// order and call fin(c, dots).
 template <class Fin>
-__device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it, const double* acc,
-                                            Fin fin) {
+__device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
+                                            double (&acc)[SLOTS][NDOT], const bool* live, Fin fin) {
   const int lane = threadIdx.x & 31;
   const int n = item_n(it);
-  double tot[SLOTS];
+  double tot[SLOTS][NDOT];
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) tot[s] = warp_sum(acc[s]);
+  for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) tot[s][d] = warp_sum(acc[s][d]);
   unsigned last = 0;
   if (lane < n) {
-    double v = tot[0];
     int32_t c = it.comp[0];
+    bool lv = live[0];
+    double v[NDOT];
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) v[d] = tot[0][d];
 #pragma unroll
     for (int s = 1; s < SLOTS; ++s)
       if (lane == s) {
-        v = tot[s];
         c = it.comp[s];
+        lv = live[s];
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) v[d] = tot[s][d];
       }
-    if (__ldcg(a.status + c) == ST_ACTIVE) {
-      a.partial[it.pbase + lane] = v;
+    if (lv) {
+      double* dst = a.partial + size_t(it.pbase + lane) * NDOT;
+#pragma unroll
+      for (int d = 0; d < NDOT; ++d) dst[d] = v[d];
       __threadfence();
       const int32_t np = a.comp_pstart[c + 1] - a.comp_pstart[c];
       if (atomicAdd(a.comp_cnt + c, 1) == np - 1) last = 1;
@@ -311,9 +341,14 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it, c
       if (s == j) c = it.comp[j];
     __threadfence();
     const int32_t q0 = a.comp_pstart[c], q1 = a.comp_pstart[c + 1];
-    double sum = 0.0;
-    for (int j = q0 + lane; j < q1; j += 32) sum += __ldcg(a.partial + a.comp_plist[j]);
-    sum = warp_sum(sum);
+    double sum[NDOT] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = q0 + lane; j < q1; j += 32) {
+      const double* src = a.partial + size_t(a.comp_plist[j]) * NDOT;
+#pragma unroll
+      for (int d = 0; d < NDOT; ++d) sum[d] += __ldcg(src + d);
+    }
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) sum[d] = warp_sum(sum[d]);
     if (lane == 0) {
       fin(c, sum);
       a.comp_cnt[c] = 0;
@@ -322,29 +357,26 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it, c
   }
 }
 
-__device__ __forceinline__ int slot_of(const Item& it, int32_t lab) {
-  int s = -1;
-  const int n = item_n(it);
-#pragma unroll
-  for (int j = 0; j < SLOTS; ++j)
-    if (j < n && it.comp[j] == lab) s = j;
-  return s;
-}
+// Per-slot coefficients of the item for this sweep.
+struct Coefs {
+  float al[SLOTS], be[SLOTS];
+  uint8_t st[SLOTS];
+};
 
-// Item coefficients for one sweep: value (beta or alpha) and activity.
-__device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, int which,
-                                           float* coef, bool* act) {
+__device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, Coefs& k) {
   bool any = false;
   const int n = item_n(it);
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j) {
-    coef[j] = 0.f;
-    act[j] = false;
+    k.al[j] = 0.f;
+    k.be[j] = 0.f;
+    k.st[j] = ST_IDLE;
     if (j < n) {
       const int32_t c = it.comp[j];
-      act[j] = __ldcg(a.status + c) == ST_ACTIVE;
-      coef[j] = float(which == 0 ? __ldcg(a.beta + c) : __ldcg(a.alpha + c));
-      any |= act[j];
+      k.st[j] = __ldcg(a.status + c);
+      k.al[j] = float(__ldcg(a.alpha + c));
+      k.be[j] = float(__ldcg(a.beta + c));
+      any |= k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
     }
   }
   return any;
@@ -352,85 +384,101 @@ __device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, in
 
 // Raw values of one row for this lane (prefetch ring) ...
 struct Raw {
-  float r, p, h;
-  uint32_t m;    // imask
-  int32_t lab;   // label (mixed items only)
+  float r, q, p, h, x;
+  uint32_t m;   // imask
+  int32_t lab;  // label (mixed items only)
 };
 
-// ... and a row of the compute ring, with p' = r + beta p already formed
-// using the pixel's own component (only intra-component neighbours are ever
-// read, and those share the centre's component and beta).
+// ... and a row of the compute ring: r_k and p_k = r_k + beta p_{k-1}
+// formed with the pixel's own component (only intra-component neighbours
+// are ever read, and those share the centre's alpha and beta).
 struct Row {
-  float pn, h;
-  uint32_t m;  // imask | (slot + 1) << 8  (slot 0 for pure items)
+  float rn, pn, h, xn;
+  uint32_t m;  // imask | (slot + 1) << 8
 };
 
-__device__ __forceinline__ Raw load_raw(const FillArgs& a, const float* __restrict__ pin, int y,
-                                        int ylim, int x, bool pure) {
+template <bool PURE>
+__device__ __forceinline__ Raw load_raw(const FillArgs& a, int par, int y, int ylim, int x) {
   Raw w;
-  w.r = w.p = w.h = 0.f;
+  w.r = w.q = w.p = w.h = w.x = 0.f;
   w.m = 0;
   w.lab = -1;
   if (y >= 0 && y <= ylim && x >= 0 && x < a.W) {
     const int64_t i = int64_t(y) * a.W + x;
-    w.r = __ldcg(a.r + i);
-    w.p = __ldcg(pin + i);
+    w.r = __ldcg(a.r[par] + i);
+    w.q = __ldcg(a.q[par] + i);
+    w.p = __ldcg(a.p[par] + i);
+    w.x = __ldcg(a.x + i);
     w.h = __ldg(a.hw + i);
     w.m = __ldg(a.imask + i);
-    if (!pure) w.lab = __ldg(a.labels + i);
+    if (!PURE) w.lab = __ldg(a.labels + i);
   }
   return w;
 }
 
-__device__ __forceinline__ Row to_row(const Raw& w, const Item& it, const float* beta) {
+template <bool PURE>
+__device__ __forceinline__ Row to_row(const Raw& w, const Item& it, const Coefs& k) {
   Row o;
-  float b = beta[0];
+  float al = k.al[0], be = k.be[0];
   uint32_t m = w.m;
-  if (!item_pure(it)) {
+  if (!PURE) {
     const int s = slot_of(it, w.lab);
-    b = 0.f;
+    al = 0.f;
+    be = 0.f;
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j)
-      if (j == s) b = beta[j];
+      if (j == s) {
+        al = k.al[j];
+        be = k.be[j];
+      }
     m |= uint32_t(s + 1) << 8;
   } else {
     m |= 1u << 8;
   }
-  o.pn = fmaf(b, w.p, w.r);
+  o.rn = fmaf(-al, w.q, w.r);
+  o.pn = fmaf(be, w.p, o.rn);
+  o.xn = fmaf(al, w.p, w.x);
   o.h = w.h;
   o.m = m;
   return o;
 }
 
-// sweep 1 over one item
-template <int CONN>
-__device__ __forceinline__ void sweep1_item(const FillArgs& a, const Item& it,
-                                            const float* __restrict__ pin,
-                                            float* __restrict__ pout) {
+// One CG sweep over one item (see the header).
+template <int CONN, bool PURE>
+__device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, int par) {
   const int lane = threadIdx.x & 31;
-  float beta[SLOTS];
-  bool act[SLOTS];
-  if (!item_coefs(a, it, 0, beta, act)) return;
-  const bool pure = item_pure(it);
+  Coefs k;
+  if (!item_coefs(a, it, k)) return;
   const int x = it.x0 - 1 + lane;
   const bool center_lane = lane >= 1 && lane <= SW && x < a.W;
-  double acc[SLOTS] = {0.0, 0.0, 0.0, 0.0};
-  // compute ring U = y-1, C = y, D = y+1; raw prefetch ring F = y+2 .. y+1+PF
+  float* rout = a.r[par ^ 1];
+  float* qout = a.q[par ^ 1];
+  float* pout = a.p[par ^ 1];
+  double acc[SLOTS][NDOT];
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j)
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
   const int yend = min(it.y0 + SH, a.rows);
   const int ylim = min(yend, a.rows - 1);  // last row the stencil touches
   Raw F[PF];
 #pragma unroll
-  for (int k = 0; k < PF; ++k) F[k] = load_raw(a, pin, it.y0 + 2 + k, ylim, x, pure);
-  Row U = to_row(load_raw(a, pin, it.y0 - 1, ylim, x, pure), it, beta);
-  Row C = to_row(load_raw(a, pin, it.y0, ylim, x, pure), it, beta);
-  Row D = to_row(load_raw(a, pin, it.y0 + 1, ylim, x, pure), it, beta);
+  for (int t = 0; t < PF; ++t) F[t] = load_raw<PURE>(a, par, it.y0 + 2 + t, ylim, x);
+  Row U = to_row<PURE>(load_raw<PURE>(a, par, it.y0 - 1, ylim, x), it, k);
+  Row C = to_row<PURE>(load_raw<PURE>(a, par, it.y0, ylim, x), it, k);
+  Row D = to_row<PURE>(load_raw<PURE>(a, par, it.y0 + 1, ylim, x), it, k);
   for (int y = it.y0; y < yend; ++y) {
-    const Raw N = load_raw(a, pin, y + 2 + PF, ylim, x, pure);  // PF rows in flight
-    const int s = int(C.m >> 8) - 1;  // this pixel's slot, -1: not in the item
-    bool mine = center_lane && (C.m & 0xFF) != 0 && s >= 0;
+    const Raw N = load_raw<PURE>(a, par, y + 2 + PF, ylim, x);  // PF rows in flight
+    const int s = PURE ? 0 : int(C.m >> 8) - 1;  // this pixel's slot, -1: not in the item
+    uint8_t st = ST_IDLE;
+    if (PURE) {
+      st = k.st[0];
+    } else {
 #pragma unroll
-    for (int j = 0; j < SLOTS; ++j)
-      if (j == s) mine = mine && act[j];
+      for (int j = 0; j < SLOTS; ++j)
+        if (j == s) st = k.st[j];
+    }
+    const bool on = center_lane && (C.m & 0xFF) != 0;
     const float pa = C.pn;
     const float ha = C.h;
     const uint32_t m = C.m;
@@ -464,117 +512,75 @@ __device__ __forceinline__ void sweep1_item(const FillArgs& a, const Item& it,
 #undef NI_NB
 #undef NI_UP
 #undef NI_DN
-    if (mine) {
+    if (on && st == ST_ACTIVE) {
       const int64_t i = int64_t(y) * a.W + x;
+      __stcg(rout + i, C.rn);
       __stcg(pout + i, pa);
-      __stcg(a.q + i, q);
-      const double v = double(pa) * double(q);
+      __stcg(qout + i, q);
+      __stcg(a.x + i, C.xn);
+      const double dp = pa, dq = q, dr = C.rn;
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
-        if (j == s) acc[j] += v;
+        if (j == s) {
+          acc[j][0] = fma(dp, dq, acc[j][0]);
+          acc[j][1] = fma(dr, dq, acc[j][1]);
+          acc[j][2] = fma(dq, dq, acc[j][2]);
+          acc[j][3] = fma(dr, dr, acc[j][3]);
+        }
+    } else if (on && st == ST_FLUSH) {
+      __stcg(a.x + int64_t(y) * a.W + x, C.xn);  // the pending x_{k+1}
     }
     U = C;
     C = D;
-    D = to_row(F[0], it, beta);
+    D = to_row<PURE>(F[0], it, k);
 #pragma unroll
-    for (int k = 0; k < PF - 1; ++k) F[k] = F[k + 1];
+    for (int t = 0; t < PF - 1; ++t) F[t] = F[t + 1];
     F[PF - 1] = N;
   }
-  item_finish(a, it, acc, [&](int32_t c, double pq) {
-    if (pq > 0.0) {
-      a.alpha[c] = __ldcg(a.rho + c) / pq;
-    } else {  // breakdown (p' in the null space): resolved in sweep 2
-      a.alpha[c] = 0.0;
-      a.brk[c] = 1;
-    }
-  });
-}
-
-// sweep 2 over one item.  Pixels without intra edges (and singletons /
-// invalid pixels) have p' = q = 0, so x and r are unchanged there: pure items
-// need neither imask nor labels, and the stores are skipped.
-constexpr int U2 = 4;  // rows per batch of loads
-__device__ __forceinline__ void sweep2_item(const FillArgs& a, const Item& it,
-                                            const float* __restrict__ pnew) {
-  const int lane = threadIdx.x & 31;
-  float alpha[SLOTS];
-  bool act[SLOTS];
-  if (!item_coefs(a, it, 1, alpha, act)) return;
-  const bool pure = item_pure(it);
-  const int x = it.x0 - 1 + lane;
-  const bool on = lane >= 1 && lane <= SW && x < a.W;
-  double acc[SLOTS] = {0.0, 0.0, 0.0, 0.0};
-  const int yend = min(it.y0 + SH, a.rows);
-  for (int y0 = it.y0; y0 < yend; y0 += U2) {
-    float xv[U2], rv[U2], pv[U2], qv[U2];
-    int32_t lab[U2];
+  bool live[SLOTS];
 #pragma unroll
-    for (int k = 0; k < U2; ++k) {
-      const int y = y0 + k;
-      xv[k] = rv[k] = pv[k] = qv[k] = 0.f;
-      lab[k] = -1;
-      if (on && y < yend) {
-        const int64_t i = int64_t(y) * a.W + x;
-        pv[k] = __ldcg(pnew + i);
-        qv[k] = __ldcg(a.q + i);
-        rv[k] = __ldcg(a.r + i);
-        xv[k] = __ldcg(a.x + i);
-        if (!pure) lab[k] = __ldg(a.labels + i);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U2; ++k) {
-      const int y = y0 + k;
-      int s = 0;
-      float al = alpha[0];
-      bool mine = on && y < yend && act[0];
-      if (!pure) {
-        s = slot_of(it, lab[k]);
-        mine = on && y < yend && s >= 0;
-#pragma unroll
-        for (int j = 0; j < SLOTS; ++j)
-          if (j == s) {
-            al = alpha[j];
-            mine = mine && act[j];
-          }
-      }
-      if (!mine) continue;
-      const int64_t i = int64_t(y) * a.W + x;
-      if (pv[k] != 0.f) __stcg(a.x + i, fmaf(al, pv[k], xv[k]));
-      const float rn = fmaf(-al, qv[k], rv[k]);
-      if (qv[k] != 0.f) __stcg(a.r + i, rn);
-      const double v = double(rn) * double(rn);
-#pragma unroll
-      for (int j = 0; j < SLOTS; ++j)
-        if (j == s) acc[j] += v;
-    }
-  }
-  item_finish(a, it, acc, [&](int32_t c, double rr) {
-    const int itn = __ldcg(a.iters + c) + 1;
-    a.iters[c] = itn;
-    bool done = false;
-    if (__ldcg(a.brk + c)) {
-      a.status[c] = ST_CONVERGED;
-      done = true;
-    } else if (itn < __ldcg(a.cap + c) && sqrt(rr) < __ldcg(a.tol + c)) {  // scipy's top-of-loop test
-      a.status[c] = ST_CONVERGED;
-      done = true;
-    } else if (itn >= __ldcg(a.cap + c)) {  // loop exhausted: info = maxiter
-      a.status[c] = ST_CAPPED;
-      done = true;
-    } else {
-      a.beta[c] = rr / __ldcg(a.rho + c);
-      a.rho[c] = rr;
-    }
-    if (done) {
+  for (int j = 0; j < SLOTS; ++j) live[j] = k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
+  item_finish(a, it, acc, live, [&](int32_t c, const double* d) {
+    if (__ldcg(a.status + c) == ST_FLUSH) {  // the pending update is applied
+      a.status[c] = __ldcg(a.final_status + c);
       atomicSub(a.active, 1);
       atomicExch(a.changed, 1);
+      return;
+    }
+    const double pq = d[0], rq = d[1], qq = d[2], rr = d[3];
+    const int n = __ldcg(a.iters + c) + 1;  // updates once this sweep's alpha is applied
+    a.iters[c] = n;
+    a.rho[c] = rr;
+    double alpha = 0.0, rho1 = 0.0;
+    bool stop = false;
+    uint8_t fin = ST_CONVERGED;
+    if (pq > 0.0) {
+      alpha = rr / pq;
+      rho1 = rr - 2.0 * alpha * rq + alpha * alpha * qq;
+      if (rho1 < 0.0) rho1 = 0.0;
+      if (n < __ldcg(a.cap + c) && sqrt(rho1) < __ldcg(a.tol + c)) {
+        stop = true;  // scipy's top-of-loop test before iteration n
+      } else if (n >= __ldcg(a.cap + c)) {
+        stop = true;  // loop exhausted: info = maxiter
+        fin = ST_CAPPED;
+      }
+    } else {
+      stop = true;  // breakdown: p in the null space (only once r == 0)
+    }
+    a.alpha[c] = alpha;
+    if (stop) {
+      a.final_status[c] = fin;
+      a.status[c] = ST_FLUSH;
+      atomicExch(a.changed, 1);
+    } else {
+      a.beta[c] = rho1 / rr;
+      a.rho[c] = rho1;
     }
   });
 }
 
-// Rebuild the list of items with an active component (order irrelevant: the
-// partial slots are fixed per item).
+// Rebuild the list of items with an ACTIVE or FLUSH component (order is
+// irrelevant: the partial slots are fixed per item).
 __device__ void rebuild_items(const FillArgs& a, int dst, int gwarp, int nwarps) {
   const int lane = threadIdx.x & 31;
   for (int k0 = gwarp * 32; k0 < a.nitems; k0 += nwarps * 32) {
@@ -585,7 +591,10 @@ __device__ void rebuild_items(const FillArgs& a, int dst, int gwarp, int nwarps)
       const int n = item_n(it);
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
-        if (j < n && __ldcg(a.status + it.comp[j]) == ST_ACTIVE) act = true;
+        if (j < n) {
+          const uint8_t st = __ldcg(a.status + it.comp[j]);
+          if (st == ST_ACTIVE || st == ST_FLUSH) act = true;
+        }
     }
     const unsigned m = __ballot_sync(0xffffffffu, act);
     int base = 0;
@@ -610,17 +619,12 @@ __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   grid.sync();
   for (int it = 0;; ++it) {
     if (__ldcg(a.active) == 0) break;
-    const float* pin = (it & 1) ? a.p1 : a.p0;
-    float* pout = (it & 1) ? a.p0 : a.p1;
+    const int par = it & 1;
     const int n = __ldcg(a.nactive_items + cur);
     for (int k = gwarp; k < n; k += nwarps) {
       const Item item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
-      sweep1_item<CONN>(a, item, pin, pout);
-    }
-    grid.sync();
-    for (int k = gwarp; k < n; k += nwarps) {
-      const Item item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
-      sweep2_item(a, item, pout);
+      if (item_pure(item)) sweep_item<CONN, true>(a, item, par);
+      else sweep_item<CONN, false>(a, item, par);
     }
     grid.sync();
     if (__ldcg(a.changed)) {
@@ -646,27 +650,32 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
     const Item it = a.items[k];
     const int x = it.x0 - 1 + lane;
     const bool on = lane >= 1 && lane <= SW && x < a.W;
-    double acc[SLOTS] = {0.0, 0.0, 0.0, 0.0};
+    double acc[SLOTS][NDOT];
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j)
+#pragma unroll
+      for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
     const int yend = min(it.y0 + SH, a.rows);
     if (on) {
       for (int y = it.y0; y < yend; ++y) {
         const int64_t i = int64_t(y) * a.W + x;
         const int s = slot_of(it, a.labels[i]);
         if (s < 0) continue;
-        const double rv = a.r[i];
+        const double rv = a.r[0][i];
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j)
-          if (j == s) acc[j] += rv * rv;
+          if (j == s) acc[j][3] += rv * rv;
       }
     }
-    item_finish(a, it, acc, [&](int32_t c, double bb) {
+    bool live[SLOTS] = {true, true};
+    item_finish(a, it, acc, live, [&](int32_t c, const double* d) {
+      const double bb = d[3];
       a.rho[c] = bb;
       const double bn = sqrt(bb);
       a.tol[c] = rtol * bn;
       a.iters[c] = 0;
       a.alpha[c] = 0.0;
       a.beta[c] = 0.0;
-      a.brk[c] = 0;
       // scipy: bnrm2 == 0 -> x = 0; then the first top-of-loop test
       if (bb == 0.0 || bn < rtol * bn) {
         a.status[c] = ST_CONVERGED;
@@ -680,15 +689,14 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
   }
 }
 
-// status "active" only while the initial norm pass counts arrivals; the
-// finaliser of that pass sets the real state (ST_ACTIVE counts toward
-// a.active only there).
+// status ACTIVE only while the initial norm pass counts arrivals; its
+// finaliser sets the real state and the active count.
 __global__ void init_state_kernel(FillArgs a, const int32_t* __restrict__ comp_size, int C,
                                   int cg_max_iters) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
     a.status[c] = comp_size[c] >= 2 ? ST_ACTIVE : ST_IDLE;
+    a.final_status[c] = ST_CONVERGED;
     a.iters[c] = 0;
-    a.brk[c] = 0;
     const int n = comp_size[c];
     a.cap[c] = n > cg_max_iters ? n : cg_max_iters;
     a.rho[c] = 0.0;
@@ -726,7 +734,7 @@ __global__ void status_out_kernel(const FillArgs a, int C, const int32_t* __rest
 // ------------------------------------------------------------ workspace
 
 struct FillWs {
-  float *x, *r, *p0, *p1, *q, *hw;
+  float *x, *r0, *r1, *q0, *q1, *p0, *p1, *hw;
   uint8_t* imask;
   int32_t *slot_base, *nslots, *nitems_strip, *item_base, *strip_comps, *partial_comp,
       *partial_idx, *plist, *keys_sorted;
@@ -734,7 +742,7 @@ struct FillWs {
   int32_t *comp_size, *comp_nparts, *comp_pstart, *comp_cnt, *iters, *cap, *active, *changed,
       *total, *total_items, *active_items, *nactive_items;
   double *partial, *rho, *alpha, *beta, *tol;
-  uint8_t *status, *brk;
+  uint8_t *status, *final_status;
   unsigned long long* px_iters;
   int32_t* max_iters;
   void* sort_ws;
@@ -747,10 +755,12 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   const int64_t P = npix;
   const int64_t NI = nstrips + P / SLOTS + 1;  // items
   w.x = c.take<float>(npix);
-  w.r = c.take<float>(npix);
+  w.r0 = c.take<float>(npix);
+  w.r1 = c.take<float>(npix);
+  w.q0 = c.take<float>(npix);
+  w.q1 = c.take<float>(npix);
   w.p0 = c.take<float>(npix);
   w.p1 = c.take<float>(npix);
-  w.q = c.take<float>(npix);
   w.hw = c.take<float>(npix);
   w.imask = c.take<uint8_t>(npix);
   w.slot_base = c.take<int32_t>(nstrips + 1);
@@ -765,7 +775,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   w.partial_idx = c.take<int32_t>(P);
   w.plist = c.take<int32_t>(P);
   w.keys_sorted = c.take<int32_t>(P);
-  w.partial = c.take<double>(P);
+  w.partial = c.take<double>(P * NDOT);
   w.comp_size = c.take<int32_t>(C + 1);
   w.comp_nparts = c.take<int32_t>(C + 1);
   w.comp_pstart = c.take<int32_t>(C + 1);
@@ -777,7 +787,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   w.beta = c.take<double>(C + 1);
   w.tol = c.take<double>(C + 1);
   w.status = c.take<uint8_t>(C + 1);
-  w.brk = c.take<uint8_t>(C + 1);
+  w.final_status = c.take<uint8_t>(C + 1);
   w.active = c.take<int32_t>(1);
   w.changed = c.take<int32_t>(1);
   w.total = c.take<int32_t>(1);
@@ -845,7 +855,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
 #define NI_PREP(CONN, MODEL)                                                                   \
   NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<blocks, 256, 0, s>>>(                          \
                          labels, omega_a, omega_b, gamma, eflags, H, W, npix, w.hw, w.imask,   \
-                         w.x, w.r, w.p0, w.p1, w.q, w.comp_size)
+                         w.x, w.r0, w.r1, w.q0, w.q1, w.p0, w.p1, w.comp_size)
   if (connectivity == 8) NI_PREP(8, 0);
   else if (model == 0) NI_PREP(4, 0);
   else NI_PREP(4, 1);
@@ -880,10 +890,12 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.rows = rows;
   a.W = W;
   a.x = w.x;
-  a.r = w.r;
-  a.q = w.q;
-  a.p0 = w.p0;
-  a.p1 = w.p1;
+  a.r[0] = w.r0;
+  a.r[1] = w.r1;
+  a.q[0] = w.q0;
+  a.q[1] = w.q1;
+  a.p[0] = w.p0;
+  a.p[1] = w.p1;
   a.hw = w.hw;
   a.imask = w.imask;
   a.labels = labels;
@@ -902,7 +914,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.iters = w.iters;
   a.cap = w.cap;
   a.status = w.status;
-  a.brk = w.brk;
+  a.final_status = w.final_status;
   a.active = w.active;
   a.changed = w.changed;
   if (count > 0) {
@@ -916,11 +928,17 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   }
   // ---- the whole CG: one persistent cooperative launch
   {
-    // occupancy variant (experiments): NI_FILL_MINB=3 gives 85 registers
+    // occupancy variant (experiments): NI_FILL_MINB = CTAs/SM the register
+    // budget is sized for (2: 128 regs, 3: 80, 4: 64)
     const char* mb = getenv("NI_FILL_MINB");
-    const bool m3 = mb && atoi(mb) == 3;
-    void* kfn = connectivity == 8 ? (m3 ? (void*)fill_cg_kernel<8, 3> : (void*)fill_cg_kernel<8, 4>)
-                                  : (m3 ? (void*)fill_cg_kernel<4, 3> : (void*)fill_cg_kernel<4, 4>);
+    const int minb = mb ? atoi(mb) : 3;
+    void* kfn;
+    if (connectivity == 8)
+      kfn = minb == 2 ? (void*)fill_cg_kernel<8, 2>
+                      : (minb == 4 ? (void*)fill_cg_kernel<8, 4> : (void*)fill_cg_kernel<8, 3>);
+    else
+      kfn = minb == 2 ? (void*)fill_cg_kernel<4, 2>
+                      : (minb == 4 ? (void*)fill_cg_kernel<4, 4> : (void*)fill_cg_kernel<4, 3>);
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
