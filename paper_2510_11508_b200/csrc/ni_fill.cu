@@ -1,7 +1,6 @@
 // K3 -- fill_components (solver.py:195-239) as ONE batched CG over every
 // component of the partition, matrix-free on the pixel grid, run by ONE
-// persistent cooperative kernel whose workers are independent warps fed by
-// TMA (cp.async.bulk.tensor) through shared memory.
+// persistent cooperative kernel whose workers are independent warps.
 //
 // Per component c the reference solves (A^T W A) x = A^T W b with scipy's
 // unpreconditioned CG (x0 = 0, stop when ||r|| < rtol ||b|| at the top of an
@@ -15,20 +14,14 @@
 // constants stay an exact null vector in float32 (a rounded CSR Laplacian
 // loses that and doubles the iteration count).
 //
-// Data layout in HBM (rows = B*H; pixel (y, x) lives at padded index
-// (y + 1) * P + (x + XM), XM = 16, P = W + 32 rounded up to 16, with zeroed
-// margins: TMA boxes must start at non-negative, 16-byte-aligned columns):
-//   x                : float32 solution
+// Data layout in HBM (per pixel, npix = B*H*W, row-major):
+//   x             : float32 solution
 //   r[2], q[2], p[2] : float32 CG vectors, double-buffered by iteration parity
-//                      (a sweep reads its neighbours' previous values while
-//                      other warps write the new ones)
-//   hw               : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
-//   imask            : uint8, bit k = forward edge k intra-component and valid,
-//                      bit 4+k = backward edge k (pixel - offset_k)
-//   lab              : int32 labels (read by mixed items only)
-// The padded pitch makes every row 16-B aligned, as the TMA tensor maps need;
-// the margin and TMA's out-of-bounds zero fill provide the halo outside the
-// grid.
+//                   (a sweep reads its neighbours' previous values while
+//                   other warps write the new ones)
+//   hw            : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
+//   imask         : uint8, bit k = forward edge k intra-component and valid,
+//                   bit 4+k = backward edge k (pixel - offset_k)
 //
 // ONE sweep and ONE grid sync per CG iteration.  scipy's iteration k
 //   p_k = r_k + beta p_{k-1};  q_k = A p_k;  alpha = rho_k / <p_k, q_k>;
@@ -41,17 +34,15 @@
 // (float64, no cancellation at CG's per-step contraction).  A component that
 // stops gets one last "flush" sweep that applies its pending x update.
 //
-// Work decomposition: strips of 32 columns x 30 rows, one lane per column.
-// A warp processes a strip ("item") by streaming its window (rows y0-1 ..
-// y0+30; columns x0-4 .. x0+35 for the stencil inputs, x0 .. x0+31 for x and
-// imask) through shared memory in 4 TMA chunks of 8 rows, 3 chunks deep
-// (mbarrier complete_tx), and marching down the rows with the rows y-1, y in
-// registers; horizontal neighbours are warp shuffles, lanes 0 and 31 read
-// the halo columns from shared memory.  No block barrier anywhere in a sweep; items are drawn
-// dynamically from an atomic ticket.  A strip touching several multi-pixel
-// components becomes ceil(n/2) "mixed" items of <= 2 components that read the
-// labels; a strip with one component is a "pure" item (singleton / invalid
-// pixels carry r = q = p = 0 and stay 0 under any update).
+// Work decomposition: the grid is cut into strips of 30 columns x 32 rows.
+// A warp processes a strip by marching down its rows with a register ring
+// of rows y-1, y, y+1 (+ prefetched rows); lanes 0 and 31 carry the left /
+// right halo columns, so horizontal neighbours are warp shuffles and there
+// is no block barrier anywhere in a sweep.  A strip touching several
+// multi-pixel components becomes ceil(n/2) "items" of <= 2 components that
+// read the int32 labels; a strip with one component (the common case) is a
+// "pure" item that needs no label at all (singletons / invalid pixels carry
+// r = q = p = 0 and stay 0 under any update).
 //
 // Reductions are deterministic: each item writes float64 partials per
 // component (lane-local sums over rows, fixed xor tree over lanes); the last
@@ -61,8 +52,6 @@
 //   read r, q, p, x, hw (20 B) + imask (1 B); write r, q, p, x (16 B) => 37 B/px
 // (halo rows/columns are re-read from L2 and not counted).
 #include <cooperative_groups.h>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -73,59 +62,37 @@ namespace cg = cooperative_groups;
 
 namespace ni {
 
-constexpr int SW = 32;     // strip width (one lane per column)
-constexpr int SH = 30;     // strip height (rows per item)
+constexpr int SW = 30;     // strip width (lanes 1..30)
+constexpr int SH = 32;     // strip height (rows per item)
 constexpr int SPX = 1024;  // padded pixels per strip (sort buffer)
-constexpr int BOXW = 32;   // TMA box width of x / imask (columns x0 .. x0+31)
-constexpr int BOXH = 40;   // TMA box width of the stencil inputs (columns x0-4 .. x0+35)
-constexpr int XM = 16;     // left margin of the padded layout (keeps box starts 16-B aligned)
-constexpr int CH = 8;      // rows per TMA chunk
-constexpr int NCH = 4;     // chunks per item: rows y0-1 .. y0+30
-constexpr int NBUF = 3;    // chunk buffers per warp
-constexpr int NT = 256;    // threads per CTA (8 warps, 1 CTA per SM)
+constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
+constexpr int PF = 3;     // rows prefetched ahead
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 
 enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3, ST_FLUSH = 4 };
 
 // One work item: a strip and up to 2 of its components.
 struct __align__(16) Item {
-  int32_t x0, y0;  // top-left pixel of the strip (column of lane 0)
+  int32_t x0, y0;  // top-left pixel of the strip (column of lane 1)
   int32_t pbase;   // first partial slot of this item
   int32_t flags;   // bits 0-7: components in the item (1..2); bit 8: pure strip
   int32_t comp[SLOTS];
-  int32_t pad[2];
 };
 
 __device__ __forceinline__ int item_n(const Item& it) { return it.flags & 0xFF; }
 __device__ __forceinline__ bool item_pure(const Item& it) { return (it.flags >> 8) & 1; }
 
-// One TMA chunk (8 rows) of every array, 128-B aligned sub-arrays.
-struct __align__(128) Chunk {
-  float r[CH][BOXH];
-  float q[CH][BOXH];
-  float p[CH][BOXH];
-  float h[CH][BOXH];
-  int32_t lab[CH][BOXH];
-  float x[CH][BOXW];
-  uint8_t m[CH][BOXW];
-};
-constexpr uint32_t kChunkBytesPure = 4 * CH * BOXH * 4 + CH * BOXW * 4 + CH * BOXW;
-constexpr uint32_t kChunkBytesMixed = kChunkBytesPure + CH * BOXH * 4;
-constexpr size_t kSmemBytes = size_t(WPB) * NBUF * sizeof(Chunk) + WPB * NBUF * sizeof(uint64_t);
-
 struct FillArgs {
-  CUtensorMap tm_r[2], tm_q[2], tm_p[2], tm_h, tm_x, tm_m, tm_lab;
-  int rows, W, P;
-  int dbg;  // debug switches (NI_FILL_DEBUG), 0 in production
+  int rows, W;
   float* x;
   float* r[2];
   float* q[2];
   float* p[2];
   const float* hw;
   const uint8_t* imask;
-  const int32_t* lab;  // padded labels
+  const int32_t* labels;
   // plan
   const Item* items;
   int nitems;
@@ -135,7 +102,6 @@ struct FillArgs {
   double* partial;             // [P][NDOT]
   int32_t* active_items;       // [2][nitems]
   int32_t* nactive_items;      // [2]
-  int32_t* ticket;             // [2] dynamic item scheduling, by sweep parity
   // component state
   double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
   double* alpha;   // alpha of the last completed sweep
@@ -149,83 +115,37 @@ struct FillArgs {
   int32_t* changed;  // a component changed state during the last sweep
 };
 
-// ------------------------------------------------------------ PTX helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 // ----------------------------------------------------------------- setup
 
-// Padded-layout setup: hw, imask, RHS (= r_0) and the zeroed CG vectors.
 template <int CONN, int MODEL>
 __global__ void __launch_bounds__(256) prep_kernel(
     const int32_t* __restrict__ labels, const double* __restrict__ omega_a,
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
-    const uint8_t* __restrict__ eflags, int H, int W, int P, int64_t npix,
-    float* __restrict__ hw, uint8_t* __restrict__ imask, int32_t* __restrict__ lab_p,
-    float* __restrict__ x, float* __restrict__ r0, float* __restrict__ r1,
-    float* __restrict__ q0, float* __restrict__ q1, float* __restrict__ p0,
+    const uint8_t* __restrict__ eflags, int H, int W, int64_t npix, float* __restrict__ hw,
+    uint8_t* __restrict__ imask, float* __restrict__ x, float* __restrict__ r,
+    float* __restrict__ r1, float* __restrict__ q0, float* __restrict__ q1, float* __restrict__ p0,
     float* __restrict__ p1, int32_t* __restrict__ comp_size) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t lab = labels[i];
-    const int u = int(i % W);
-    const int64_t row = i / W;
-    const int vloc = int(row % H);
-    const int64_t o = (row + 1) * P + u + XM;  // padded index
-    x[o] = 0.f;
-    r1[o] = 0.f;
-    q0[o] = 0.f;
-    q1[o] = 0.f;
-    p0[o] = 0.f;
-    p1[o] = 0.f;
-    lab_p[o] = lab;
+    x[i] = 0.f;
+    r1[i] = 0.f;
+    q0[i] = 0.f;
+    q1[i] = 0.f;
+    p0[i] = 0.f;
+    p1[i] = 0.f;
     if (lab < 0) {
-      hw[o] = 0.f;
-      imask[o] = 0;
-      r0[o] = 0.f;
+      hw[i] = 0.f;
+      imask[i] = 0;
+      r[i] = 0.f;
       continue;
     }
     atomicAdd(comp_size + lab, 1);
     const double wa = 0.5 * (gamma[i] * gamma[i]);
-    hw[o] = float(wa);
+    hw[i] = float(wa);
+    const int u = int(i % W);
+    const int vloc = int((i / W) % H);
     const uint8_t ef = eflags[i];
     uint8_t m = 0;
     double b = 0.0;
@@ -257,8 +177,8 @@ __global__ void __launch_bounds__(256) prep_kernel(
         }
       }
     }
-    imask[o] = m;
-    r0[o] = float(b);
+    imask[i] = m;
+    r[i] = float(b);
   }
 }
 
@@ -346,7 +266,6 @@ __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
         it.comp[j] = j < n ? strip_comps[int64_t(s) * SPX + k * SLOTS + j] : -1;
-      it.pad[0] = it.pad[1] = 0;
       items[ib + k] = it;
     }
     for (int j = 0; j < ns; ++j) {
@@ -463,23 +382,47 @@ __device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, Co
   return any;
 }
 
-// A row of the compute ring: r_k, p_k = r_k + beta p_{k-1} and x_k formed
-// with the pixel's own component (only intra-component neighbours are ever
-// read, and those share the centre's alpha and beta).  Lane 0 also holds the
-// halo column on its left and lane 31 the one on its right (pe, he).
+// Raw values of one row for this lane (prefetch ring) ...
+struct Raw {
+  float r, q, p, h, x;
+  uint32_t m;   // imask
+  int32_t lab;  // label (mixed items only)
+};
+
+// ... and a row of the compute ring: r_k and p_k = r_k + beta p_{k-1}
+// formed with the pixel's own component (only intra-component neighbours
+// are ever read, and those share the centre's alpha and beta).
 struct Row {
-  float rn, pn, h, xn, pe, he;
+  float rn, pn, h, xn;
   uint32_t m;  // imask | (slot + 1) << 8
 };
 
 template <bool PURE>
-__device__ __forceinline__ float2 p_at(const Chunk& c, int rr, int col, const Item& it,
-                                       const Coefs& k, int* slot) {
-  const float r = c.r[rr][col], q = c.q[rr][col], p = c.p[rr][col];
+__device__ __forceinline__ Raw load_raw(const FillArgs& a, int par, int y, int ylim, int x) {
+  Raw w;
+  w.r = w.q = w.p = w.h = w.x = 0.f;
+  w.m = 0;
+  w.lab = -1;
+  if (y >= 0 && y <= ylim && x >= 0 && x < a.W) {
+    const int64_t i = int64_t(y) * a.W + x;
+    w.r = __ldcg(a.r[par] + i);
+    w.q = __ldcg(a.q[par] + i);
+    w.p = __ldcg(a.p[par] + i);
+    w.x = __ldcg(a.x + i);
+    w.h = __ldg(a.hw + i);
+    w.m = __ldg(a.imask + i);
+    if (!PURE) w.lab = __ldg(a.labels + i);
+  }
+  return w;
+}
+
+template <bool PURE>
+__device__ __forceinline__ Row to_row(const Raw& w, const Item& it, const Coefs& k) {
+  Row o;
   float al = k.al[0], be = k.be[0];
-  int s = 0;
+  uint32_t m = w.m;
   if (!PURE) {
-    s = slot_of(it, c.lab[rr][col]);
+    const int s = slot_of(it, w.lab);
     al = 0.f;
     be = 0.f;
 #pragma unroll
@@ -488,102 +431,26 @@ __device__ __forceinline__ float2 p_at(const Chunk& c, int rr, int col, const It
         al = k.al[j];
         be = k.be[j];
       }
+    m |= uint32_t(s + 1) << 8;
+  } else {
+    m |= 1u << 8;
   }
-  *slot = s;
-  const float rn = fmaf(-al, q, r);
-  return make_float2(rn, fmaf(be, p, rn));
-}
-
-template <bool PURE>
-__device__ __forceinline__ Row smem_row(const Chunk& c, int rr, int lane, const Item& it,
-                                        const Coefs& k) {
-  int s;
-  const float2 v = p_at<PURE>(c, rr, lane + 4, it, k, &s);
-  float al = k.al[0];
-  if (!PURE) {
-    al = 0.f;
-#pragma unroll
-    for (int j = 0; j < SLOTS; ++j)
-      if (j == s) al = k.al[j];
-  }
-  Row o;
-  o.rn = v.x;
-  o.pn = v.y;
-  o.h = c.h[rr][lane + 4];
-  o.xn = fmaf(al, c.p[rr][lane + 4], c.x[rr][lane]);
-  o.m = uint32_t(c.m[rr][lane]) | (uint32_t(s + 1) << 8);
-  o.pe = 0.f;
-  o.he = 0.f;
-  if (lane == 0 || lane == 31) {
-    const int col = lane == 0 ? 3 : 36;
-    int se;
-    o.pe = p_at<PURE>(c, rr, col, it, k, &se).y;
-    o.he = c.h[rr][col];
-  }
+  o.rn = fmaf(-al, w.q, w.r);
+  o.pn = fmaf(be, w.p, o.rn);
+  o.xn = fmaf(al, w.p, w.x);
+  o.h = w.h;
+  o.m = m;
   return o;
 }
 
-__device__ __forceinline__ float edge_sel(bool edge, float e, float v) { return edge ? e : v; }
-
-// Per-warp chunk stream: chunk number s lives in buffer s % NBUF and its
-// mbarrier completes for the (s / NBUF)-th time.
-struct Stream {
-  Chunk* buf;       // NBUF chunks of this warp
-  uint64_t* bar;    // NBUF mbarriers
-  uint32_t issued;  // chunks issued so far (this warp, whole kernel)
-  uint32_t used;    // chunks consumed so far
-};
-
-__device__ __forceinline__ void issue_chunk(const FillArgs& a, Stream& st, const Item& it, int j,
-                                            int par) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t s = st.issued++;
-  Chunk& c = st.buf[s % NBUF];
-  uint64_t* bar = st.bar + (s % NBUF);
-  __syncwarp();  // every lane finished reading this buffer's previous chunk
-  if (lane == 0) {
-    fence_proxy_async();
-    const bool pure = item_pure(it);
-    const int cx = it.x0 + XM - 4, cy = it.y0 + CH * j;  // padded (x0 - 4, y0 - 1 + 8j)
-    const int cxw = it.x0 + XM;                           // padded x0
-    // debug: bit 8+i skips TMA i (r, q, p, h, x, m, lab)
-    const int skip = a.dbg >> 8;
-    constexpr uint32_t FB = CH * BOXH * 4, XB = CH * BOXW * 4, MB = CH * BOXW;
-    uint32_t bytes = 0;
-    if (!(skip & 1)) bytes += FB;
-    if (!(skip & 2)) bytes += FB;
-    if (!(skip & 4)) bytes += FB;
-    if (!(skip & 8)) bytes += FB;
-    if (!(skip & 16)) bytes += XB;
-    if (!(skip & 32)) bytes += MB;
-    if (!pure && !(skip & 64)) bytes += FB;
-    mbar_expect_tx(bar, bytes);
-    if (!(skip & 1)) tma_load_2d(c.r, &a.tm_r[par], bar, cx, cy);
-    if (!(skip & 2)) tma_load_2d(c.q, &a.tm_q[par], bar, cx, cy);
-    if (!(skip & 4)) tma_load_2d(c.p, &a.tm_p[par], bar, cx, cy);
-    if (!(skip & 8)) tma_load_2d(c.h, &a.tm_h, bar, cx, cy);
-    if (!(skip & 16)) tma_load_2d(c.x, &a.tm_x, bar, cxw, cy);
-    if (!(skip & 32)) tma_load_2d(c.m, &a.tm_m, bar, cxw, cy);
-    if (!pure && !(skip & 64)) tma_load_2d(c.lab, &a.tm_lab, bar, cx, cy);
-  }
-}
-
-__device__ __forceinline__ const Chunk& wait_chunk(Stream& st, uint32_t s) {
-  mbar_wait(st.bar + (s % NBUF), (s / NBUF) & 1);
-  return st.buf[s % NBUF];
-}
-
-// One CG sweep over one item whose first chunk is chunk number st.used of
-// the stream.  `nxt` (valid if has_nxt) is the item after it: its chunks are
-// issued as this item's buffers retire.
+// One CG sweep over one item (see the header).
 template <int CONN, bool PURE>
-__device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const Item& it,
-                                           const Coefs& k, const Item& nxt, bool has_nxt,
-                                           int par) {
+__device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, int par) {
   const int lane = threadIdx.x & 31;
-  const uint32_t s0 = st.used;
-  const int x = it.x0 + lane;
-  const bool center_lane = x < a.W;
+  Coefs k;
+  if (!item_coefs(a, it, k)) return;
+  const int x = it.x0 - 1 + lane;
+  const bool center_lane = lane >= 1 && lane <= SW && x < a.W;
   float* rout = a.r[par ^ 1];
   float* qout = a.q[par ^ 1];
   float* pout = a.p[par ^ 1];
@@ -592,31 +459,24 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const 
   for (int j = 0; j < SLOTS; ++j)
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
-  const int nrows = min(SH, a.rows - it.y0);  // centre rows in this item
-  const Chunk* ch = &wait_chunk(st, s0);
-  Row U = smem_row<PURE>(*ch, 0, lane, it, k);
-  Row C = smem_row<PURE>(*ch, 1, lane, it, k);
-  int retired = 0;  // chunks of this item whose buffer was recycled
-#pragma unroll 1
-  for (int L = 1; L <= nrows; ++L) {
-    const int ld = L + 1;  // local row of D
-    if ((ld & (CH - 1)) == 0) ch = &wait_chunk(st, s0 + ld / CH);
-    const Row D = smem_row<PURE>(*ch, ld & (CH - 1), lane, it, k);
-    if ((ld & (CH - 1)) == CH - 1) {
-      // chunk ld / CH fully read (rows y-1, y live in registers): recycle
-      const int j = retired + NBUF;  // chunk index relative to this item
-      if (j < NCH) issue_chunk(a, st, it, j, par);
-      else if (has_nxt) issue_chunk(a, st, nxt, j - NCH, par);
-      ++retired;
-    }
+  const int yend = min(it.y0 + SH, a.rows);
+  const int ylim = min(yend, a.rows - 1);  // last row the stencil touches
+  Raw F[PF];
+#pragma unroll
+  for (int t = 0; t < PF; ++t) F[t] = load_raw<PURE>(a, par, it.y0 + 2 + t, ylim, x);
+  Row U = to_row<PURE>(load_raw<PURE>(a, par, it.y0 - 1, ylim, x), it, k);
+  Row C = to_row<PURE>(load_raw<PURE>(a, par, it.y0, ylim, x), it, k);
+  Row D = to_row<PURE>(load_raw<PURE>(a, par, it.y0 + 1, ylim, x), it, k);
+  for (int y = it.y0; y < yend; ++y) {
+    const Raw N = load_raw<PURE>(a, par, y + 2 + PF, ylim, x);  // PF rows in flight
     const int s = PURE ? 0 : int(C.m >> 8) - 1;  // this pixel's slot, -1: not in the item
-    uint8_t stt = ST_IDLE;
+    uint8_t st = ST_IDLE;
     if (PURE) {
-      stt = k.st[0];
+      st = k.st[0];
     } else {
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
-        if (j == s) stt = k.st[j];
+        if (j == s) st = k.st[j];
     }
     const bool on = center_lane && (C.m & 0xFF) != 0;
     const float pa = C.pn;
@@ -624,18 +484,16 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const 
     const uint32_t m = C.m;
     float q = 0.f;
 #define NI_NB(pp, hh) fmaf(ha + (hh), pa - (pp), q)
-// shuffle in every lane (a divergent shfl.sync is undefined), then let the
-// edge lanes take their halo value
-#define NI_UP(R, f, e) edge_sel(lane == 0, (R).e, __shfl_up_sync(0xffffffffu, (R).f, 1))
-#define NI_DN(R, f, e) edge_sel(lane == 31, (R).e, __shfl_down_sync(0xffffffffu, (R).f, 1))
+#define NI_UP(v) __shfl_up_sync(0xffffffffu, (v), 1)
+#define NI_DN(v) __shfl_down_sync(0xffffffffu, (v), 1)
     {
-      const float pCl = NI_UP(C, pn, pe), hCl = NI_UP(C, h, he);
-      const float pCr = NI_DN(C, pn, pe), hCr = NI_DN(C, h, he);
+      const float pCl = NI_UP(C.pn), hCl = NI_UP(C.h);
+      const float pCr = NI_DN(C.pn), hCr = NI_DN(C.h);
       if (CONN == 8) {
-        const float pDl = NI_UP(D, pn, pe), hDl = NI_UP(D, h, he);
-        const float pDr = NI_DN(D, pn, pe), hDr = NI_DN(D, h, he);
-        const float pUl = NI_UP(U, pn, pe), hUl = NI_UP(U, h, he);
-        const float pUr = NI_DN(U, pn, pe), hUr = NI_DN(U, h, he);
+        const float pDl = NI_UP(D.pn), hDl = NI_UP(D.h);
+        const float pDr = NI_DN(D.pn), hDr = NI_DN(D.h);
+        const float pUl = NI_UP(U.pn), hUl = NI_UP(U.h);
+        const float pUr = NI_DN(U.pn), hUr = NI_DN(U.h);
         if (m & 0x01) q = NI_NB(pCr, hCr);    // (+1, 0)
         if (m & 0x02) q = NI_NB(pDl, hDl);    // (-1,+1)
         if (m & 0x04) q = NI_NB(D.pn, D.h);   // ( 0,+1)
@@ -654,12 +512,12 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const 
 #undef NI_NB
 #undef NI_UP
 #undef NI_DN
-    const int64_t i = int64_t(it.y0 + L) * a.P + x + XM;
-    if (on && stt == ST_ACTIVE) {
-      rout[i] = C.rn;
-      pout[i] = pa;
-      qout[i] = q;
-      a.x[i] = C.xn;
+    if (on && st == ST_ACTIVE) {
+      const int64_t i = int64_t(y) * a.W + x;
+      __stcg(rout + i, C.rn);
+      __stcg(pout + i, pa);
+      __stcg(qout + i, q);
+      __stcg(a.x + i, C.xn);
       const double dp = pa, dq = q, dr = C.rn;
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
@@ -669,20 +527,16 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const 
           acc[j][2] = fma(dq, dq, acc[j][2]);
           acc[j][3] = fma(dr, dr, acc[j][3]);
         }
-    } else if (on && stt == ST_FLUSH) {
-      a.x[i] = C.xn;  // the pending x_{k+1}
+    } else if (on && st == ST_FLUSH) {
+      __stcg(a.x + int64_t(y) * a.W + x, C.xn);  // the pending x_{k+1}
     }
     U = C;
     C = D;
+    D = to_row<PURE>(F[0], it, k);
+#pragma unroll
+    for (int t = 0; t < PF - 1; ++t) F[t] = F[t + 1];
+    F[PF - 1] = N;
   }
-  // an item cut by the grid bottom leaves chunks unread: drain them too
-  for (int j = retired; j < NCH; ++j) {
-    if (j > 0) wait_chunk(st, s0 + j);  // chunk 0 was waited on above
-    const int jj = j + NBUF;
-    if (jj < NCH) issue_chunk(a, st, it, jj, par);
-    else if (has_nxt) issue_chunk(a, st, nxt, jj - NCH, par);
-  }
-  st.used = s0 + NCH;
   bool live[SLOTS];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j) live[j] = k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
@@ -750,86 +604,37 @@ __device__ void rebuild_items(const FillArgs& a, int dst, int gwarp, int nwarps)
   }
 }
 
-__device__ __forceinline__ int draw_ticket(const FillArgs& a, int par) {
-  int k = 0;
-  if ((threadIdx.x & 31) == 0) k = atomicAdd(a.ticket + par, 1);
-  return __shfl_sync(0xffffffffu, k, 0);
-}
-
-// The next item with an ACTIVE / FLUSH component, drawing tickets.
-__device__ __forceinline__ bool next_item(const FillArgs& a, int par, int n, int cur, Item& it,
-                                          Coefs& k) {
-  while (true) {
-    const int t = draw_ticket(a, par);
-    if (t >= n) return false;
-    it = a.items[__ldcg(a.active_items + cur * a.nitems + t)];
-    if (item_coefs(a, it, k)) return true;
-  }
-}
-
-template <int CONN>
-__global__ void __launch_bounds__(NT, 1) fill_cg_kernel(const __grid_constant__ FillArgs a) {
+template <int CONN, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * WPB + warp;
+  const int gwarp = blockIdx.x * WPB + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * WPB;
-  Chunk* chunks = reinterpret_cast<Chunk*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WPB) * NBUF * sizeof(Chunk));
-  Stream st;
-  st.buf = chunks + warp * NBUF;
-  st.bar = bars + warp * NBUF;
-  st.issued = 0;
-  st.used = 0;
-  if (lane < NBUF) mbar_init(st.bar + lane, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  fence_proxy_async();
-  __syncwarp();
   int cur = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.nactive_items[0] = 0;
     a.nactive_items[1] = 0;
-    a.ticket[0] = 0;
-    a.ticket[1] = 0;
   }
   grid.sync();
-  if (a.dbg & 4) return;
   rebuild_items(a, 0, gwarp, nwarps);
   grid.sync();
-  if (a.dbg & 8) return;
   for (int it = 0;; ++it) {
     if (__ldcg(a.active) == 0) break;
-    if ((a.dbg & 16) && it > 0) break;
     const int par = it & 1;
-    // the other parity's ticket was last used by the previous sweep (done)
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ticket[par ^ 1] = 0;
     const int n = __ldcg(a.nactive_items + cur);
-    Item item, nxt;
-    Coefs kc, kn;
-    bool has = next_item(a, par, n, cur, item, kc);
-    bool has_nxt = has && next_item(a, par, n, cur, nxt, kn);
-    if (has) {  // prime the stream: the first NBUF chunks of the first item
-      for (int j = 0; j < NBUF; ++j) issue_chunk(a, st, item, j, par);
-    }
-    while (has) {
-      if (item_pure(item)) sweep_item<CONN, true>(a, st, item, kc, nxt, has_nxt, par);
-      else sweep_item<CONN, false>(a, st, item, kc, nxt, has_nxt, par);
-      item = nxt;
-      kc = kn;
-      has = has_nxt;
-      has_nxt = has && next_item(a, par, n, cur, nxt, kn);
-      // the new item's chunks 0..NBUF-1 were issued as the previous item
-      // retired its buffers
+    for (int k = gwarp; k < n; k += nwarps) {
+      const Item item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
+      if (item_pure(item)) sweep_item<CONN, true>(a, item, par);
+      else sweep_item<CONN, false>(a, item, par);
     }
     grid.sync();
     if (__ldcg(a.changed)) {
-      const int nxt_list = cur ^ 1;
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.nactive_items[nxt_list] = 0;
+      const int nxt = cur ^ 1;
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.nactive_items[nxt] = 0;
       grid.sync();
-      rebuild_items(a, nxt_list, gwarp, nwarps);
+      rebuild_items(a, nxt, gwarp, nwarps);
       grid.sync();
       if (blockIdx.x == 0 && threadIdx.x == 0) *a.changed = 0;
-      cur = nxt_list;
+      cur = nxt;
       grid.sync();
     }
   }
@@ -837,15 +642,14 @@ __global__ void __launch_bounds__(NT, 1) fill_cg_kernel(const __grid_constant__ 
 
 // Initial ||b||^2 per component and the state of every component.  One warp
 // per item, like the sweeps.
-__global__ void __launch_bounds__(NT) init_norm_kernel(const __grid_constant__ FillArgs a,
-                                                       double rtol) {
+__global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) {
   const int gwarp = blockIdx.x * WPB + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * WPB;
   const int lane = threadIdx.x & 31;
   for (int k = gwarp; k < a.nitems; k += nwarps) {
     const Item it = a.items[k];
-    const int x = it.x0 + lane;
-    const bool on = x < a.W;
+    const int x = it.x0 - 1 + lane;
+    const bool on = lane >= 1 && lane <= SW && x < a.W;
     double acc[SLOTS][NDOT];
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j)
@@ -854,8 +658,8 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(const __grid_constant__ F
     const int yend = min(it.y0 + SH, a.rows);
     if (on) {
       for (int y = it.y0; y < yend; ++y) {
-        const int64_t i = int64_t(y + 1) * a.P + x + XM;
-        const int s = slot_of(it, a.lab[i]);
+        const int64_t i = int64_t(y) * a.W + x;
+        const int s = slot_of(it, a.labels[i]);
         if (s < 0) continue;
         const double rv = a.r[0][i];
 #pragma unroll
@@ -887,34 +691,29 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(const __grid_constant__ F
 
 // status ACTIVE only while the initial norm pass counts arrivals; its
 // finaliser sets the real state and the active count.
-__global__ void init_state_kernel(uint8_t* __restrict__ status, uint8_t* __restrict__ final_status,
-                                  int32_t* __restrict__ iters, int32_t* __restrict__ cap,
-                                  double* __restrict__ rho, const int32_t* __restrict__ comp_size,
-                                  int C, int cg_max_iters) {
+__global__ void init_state_kernel(FillArgs a, const int32_t* __restrict__ comp_size, int C,
+                                  int cg_max_iters) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    status[c] = comp_size[c] >= 2 ? ST_ACTIVE : ST_IDLE;
-    final_status[c] = ST_CONVERGED;
-    iters[c] = 0;
+    a.status[c] = comp_size[c] >= 2 ? ST_ACTIVE : ST_IDLE;
+    a.final_status[c] = ST_CONVERGED;
+    a.iters[c] = 0;
     const int n = comp_size[c];
-    cap[c] = n > cg_max_iters ? n : cg_max_iters;
-    rho[c] = 0.0;
+    a.cap[c] = n > cg_max_iters ? n : cg_max_iters;
+    a.rho[c] = 0.0;
   }
 }
 
 __global__ void output_kernel(const float* __restrict__ x, const int32_t* __restrict__ labels,
-                              const int32_t* __restrict__ comp_size, int W, int P, int64_t npix,
+                              const int32_t* __restrict__ comp_size, int64_t npix,
                               double* __restrict__ z) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t l = labels[i];
-    const int64_t o = (i / W + 1) * P + i % W + XM;
-    z[i] = (l >= 0 && comp_size[l] >= 2) ? double(x[o]) : 0.0;
+    z[i] = (l >= 0 && comp_size[l] >= 2) ? double(x[i]) : 0.0;
   }
 }
 
-__global__ void status_out_kernel(const uint8_t* __restrict__ status,
-                                  const int32_t* __restrict__ iters, int C,
-                                  const int32_t* __restrict__ comp_size,
+__global__ void status_out_kernel(const FillArgs a, int C, const int32_t* __restrict__ comp_size,
                                   int32_t* __restrict__ iters_out,
                                   int32_t* __restrict__ status_out,
                                   unsigned long long* __restrict__ px_iters,
@@ -922,9 +721,9 @@ __global__ void status_out_kernel(const uint8_t* __restrict__ status,
   unsigned long long acc = 0;
   int mx = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    const int it = iters[c];
+    const int it = a.iters[c];
     iters_out[c] = it;
-    status_out[c] = status[c] == ST_CAPPED ? 1 : 0;
+    status_out[c] = a.status[c] == ST_CAPPED ? 1 : 0;
     if (comp_size[c] >= 2) acc += (unsigned long long)comp_size[c] * (unsigned long long)it;
     mx = it > mx ? it : mx;
   }
@@ -937,12 +736,11 @@ __global__ void status_out_kernel(const uint8_t* __restrict__ status,
 struct FillWs {
   float *x, *r0, *r1, *q0, *q1, *p0, *p1, *hw;
   uint8_t* imask;
-  int32_t* lab_p;
   int32_t *slot_base, *nslots, *nitems_strip, *item_base, *strip_comps, *partial_comp,
       *partial_idx, *plist, *keys_sorted;
   Item* items;
   int32_t *comp_size, *comp_nparts, *comp_pstart, *comp_cnt, *iters, *cap, *active, *changed,
-      *total, *total_items, *active_items, *nactive_items, *ticket;
+      *total, *total_items, *active_items, *nactive_items;
   double *partial, *rho, *alpha, *beta, *tol;
   uint8_t *status, *final_status;
   unsigned long long* px_iters;
@@ -952,23 +750,19 @@ struct FillWs {
   void* scan_ws;
 };
 
-static int pitch_of(int W) { return (W + 2 * XM + 15) & ~15; }
-
-static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int nstrips, int C) {
-  const int64_t npad = int64_t(rows + 2) * pitch_of(W);
+static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   // every partial slot owns >= 1 pixel
   const int64_t P = npix;
   const int64_t NI = nstrips + P / SLOTS + 1;  // items
-  w.x = c.take<float>(npad);
-  w.r0 = c.take<float>(npad);
-  w.r1 = c.take<float>(npad);
-  w.q0 = c.take<float>(npad);
-  w.q1 = c.take<float>(npad);
-  w.p0 = c.take<float>(npad);
-  w.p1 = c.take<float>(npad);
-  w.hw = c.take<float>(npad);
-  w.imask = c.take<uint8_t>(npad);
-  w.lab_p = c.take<int32_t>(npad);
+  w.x = c.take<float>(npix);
+  w.r0 = c.take<float>(npix);
+  w.r1 = c.take<float>(npix);
+  w.q0 = c.take<float>(npix);
+  w.q1 = c.take<float>(npix);
+  w.p0 = c.take<float>(npix);
+  w.p1 = c.take<float>(npix);
+  w.hw = c.take<float>(npix);
+  w.imask = c.take<uint8_t>(npix);
   w.slot_base = c.take<int32_t>(nstrips + 1);
   w.nslots = c.take<int32_t>(nstrips + 1);
   w.nitems_strip = c.take<int32_t>(nstrips + 1);
@@ -977,7 +771,6 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.items = c.take<Item>(NI);
   w.active_items = c.take<int32_t>(2 * NI);
   w.nactive_items = c.take<int32_t>(2);
-  w.ticket = c.take<int32_t>(2);
   w.partial_comp = c.take<int32_t>(P);
   w.partial_idx = c.take<int32_t>(P);
   w.plist = c.take<int32_t>(P);
@@ -1009,41 +802,6 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.scan_ws = c.take<char>(scan_ws_bytes(scan_n));
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-static PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
-  }
-  return fn;
-}
-
-static int make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, int esize, int boxw,
-                    int rows, int P) {
-  PFN_cuTensorMapEncodeTiled enc = tensor_map_encoder();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return NI_ERR_CUDA;
-  }
-  cuuint64_t dims[2] = {cuuint64_t(P), cuuint64_t(rows + 2)};
-  cuuint64_t strides[1] = {cuuint64_t(P) * esize};
-  cuuint32_t box[2] = {cuuint32_t(boxw), CH};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
-    return NI_ERR_CUDA;
-  }
-  return NI_OK;
-}
-
 }  // namespace ni
 
 using namespace ni;
@@ -1061,7 +819,7 @@ extern "C" int ni_fill_workspace_size(int B, int H, int W, int connectivity, int
   strip_grid(B, H, W, &nsx, &nsy);
   Sizer s;
   FillWs w;
-  carve_fill(s, w, npix, B * H, W, nsx * nsy, count);
+  carve_fill(s, w, npix, nsx * nsy, count);
   *bytes = s.used;
   return NI_OK;
 }
@@ -1078,13 +836,12 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npix = int64_t(B) * H * W;
   const int rows = B * H;
-  const int P = pitch_of(W);
   int nsx, nsy;
   strip_grid(B, H, W, &nsx, &nsy);
   const int nstrips = nsx * nsy;
   Carver cv(workspace, workspace_bytes);
   FillWs w;
-  carve_fill(cv, w, npix, rows, W, nstrips, count);
+  carve_fill(cv, w, npix, nstrips, count);
   if (!cv.ok() || !workspace) {
     set_error("ni_fill: workspace too small (%zu < %zu)", workspace_bytes, cv.used);
     return NI_ERR_WORKSPACE;
@@ -1095,17 +852,10 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.comp_cnt, 0, sizeof(int32_t) * (count + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.active, 0, sizeof(int32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.changed, 0, sizeof(int32_t), s));
-  {  // zero the margins (and everything else) of the padded arrays
-    const size_t npad = size_t(rows + 2) * P;
-    for (float* f : {w.x, w.r0, w.r1, w.q0, w.q1, w.p0, w.p1, w.hw})
-      NI_CUDA_TRY(cudaMemsetAsync(f, 0, npad * sizeof(float), s));
-    NI_CUDA_TRY(cudaMemsetAsync(w.imask, 0, npad, s));
-    NI_CUDA_TRY(cudaMemsetAsync(w.lab_p, 0xff, npad * sizeof(int32_t), s));
-  }
 #define NI_PREP(CONN, MODEL)                                                                   \
   NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<blocks, 256, 0, s>>>(                          \
-                         labels, omega_a, omega_b, gamma, eflags, H, W, P, npix, w.hw, w.imask, \
-                         w.lab_p, w.x, w.r0, w.r1, w.q0, w.q1, w.p0, w.p1, w.comp_size)
+                         labels, omega_a, omega_b, gamma, eflags, H, W, npix, w.hw, w.imask,   \
+                         w.x, w.r0, w.r1, w.q0, w.q1, w.p0, w.p1, w.comp_size)
   if (connectivity == 8) NI_PREP(8, 0);
   else if (model == 0) NI_PREP(4, 0);
   else NI_PREP(4, 1);
@@ -1124,27 +874,21 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
                          w.nslots, w.slot_base, w.item_base, w.strip_comps, nstrips, nsx, w.items,
                          w.partial_comp, w.partial_idx, w.comp_nparts);
   NI_LAUNCH_CHECK();
-  int32_t NP = 0, NIt = 0;
-  NI_CUDA_TRY(cudaMemcpyAsync(&NP, w.total, sizeof(NP), cudaMemcpyDeviceToHost, s));
+  int32_t P = 0, NIt = 0;
+  NI_CUDA_TRY(cudaMemcpyAsync(&P, w.total, sizeof(P), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaMemcpyAsync(&NIt, w.total_items, sizeof(NIt), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaStreamSynchronize(s));
-  if (NP > 0) {
+  if (P > 0) {
     int end_bit = 1;
     while ((int64_t(1) << end_bit) <= count) ++end_bit;
     size_t sb = w.sort_bytes;
     NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_ws, sb, w.partial_comp, w.keys_sorted,
-                                                w.partial_idx, w.plist, NP, 0, end_bit, s));
+                                                w.partial_idx, w.plist, P, 0, end_bit, s));
   }
   NI_TRY(exclusive_scan_i32(w.comp_nparts, w.comp_pstart, count + 1, nullptr, w.scan_ws, s));
   FillArgs a;
-  memset(&a, 0, sizeof(a));
   a.rows = rows;
   a.W = W;
-  a.P = P;
-  {
-    const char* d = getenv("NI_FILL_DEBUG");
-    a.dbg = d ? atoi(d) : 0;
-  }
   a.x = w.x;
   a.r[0] = w.r0;
   a.r[1] = w.r1;
@@ -1154,7 +898,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.p[1] = w.p1;
   a.hw = w.hw;
   a.imask = w.imask;
-  a.lab = w.lab_p;
+  a.labels = labels;
   a.items = w.items;
   a.nitems = NIt;
   a.comp_pstart = w.comp_pstart;
@@ -1163,7 +907,6 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.partial = w.partial;
   a.active_items = w.active_items;
   a.nactive_items = w.nactive_items;
-  a.ticket = w.ticket;
   a.rho = w.rho;
   a.alpha = w.alpha;
   a.beta = w.beta;
@@ -1174,35 +917,32 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.final_status = w.final_status;
   a.active = w.active;
   a.changed = w.changed;
-  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  for (int par = 0; par < 2; ++par) {
-    NI_TRY(make_map(&a.tm_r[par], a.r[par], F32, 4, BOXH, rows, P));
-    NI_TRY(make_map(&a.tm_q[par], a.q[par], F32, 4, BOXH, rows, P));
-    NI_TRY(make_map(&a.tm_p[par], a.p[par], F32, 4, BOXH, rows, P));
-  }
-  NI_TRY(make_map(&a.tm_h, w.hw, F32, 4, BOXH, rows, P));
-  NI_TRY(make_map(&a.tm_x, w.x, F32, 4, BOXW, rows, P));
-  NI_TRY(make_map(&a.tm_m, w.imask, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, BOXW, rows, P));
-  NI_TRY(make_map(&a.tm_lab, w.lab_p, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, BOXH, rows, P));
   if (count > 0) {
-    NI_COUNT_LAUNCH(), init_state_kernel<<<div_up(count, 256), 256, 0, s>>>(
-                           w.status, w.final_status, w.iters, w.cap, w.rho, w.comp_size, count,
-                           cg_max_iters);
+    NI_COUNT_LAUNCH(), init_state_kernel<<<div_up(count, 256), 256, 0, s>>>(a, w.comp_size, count,
+                                                                           cg_max_iters);
     NI_LAUNCH_CHECK();
   }
   if (NIt > 0) {
     NI_COUNT_LAUNCH(), init_norm_kernel<<<div_up(NIt, WPB), NT, 0, s>>>(a, cg_tol);
     NI_LAUNCH_CHECK();
   }
-  // ---- the whole CG: one persistent cooperative launch, 1 CTA per SM
+  // ---- the whole CG: one persistent cooperative launch
   {
-    void* kfn = connectivity == 8 ? (void*)fill_cg_kernel<8> : (void*)fill_cg_kernel<4>;
-    NI_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kSmemBytes)));
+    // occupancy variant (experiments): NI_FILL_MINB = CTAs/SM the register
+    // budget is sized for (2: 128 regs, 3: 80, 4: 64)
+    const char* mb = getenv("NI_FILL_MINB");
+    const int minb = mb ? atoi(mb) : 3;
+    void* kfn;
+    if (connectivity == 8)
+      kfn = minb == 2 ? (void*)fill_cg_kernel<8, 2>
+                      : (minb == 4 ? (void*)fill_cg_kernel<8, 4> : (void*)fill_cg_kernel<8, 3>);
+    else
+      kfn = minb == 2 ? (void*)fill_cg_kernel<4, 2>
+                      : (minb == 4 ? (void*)fill_cg_kernel<4, 4> : (void*)fill_cg_kernel<4, 3>);
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, kSmemBytes));
+    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, 0));
     int G = per_sm * sms;
     const int need = div_up(NIt > 0 ? NIt : 1, WPB);
     if (G > need) G = need;
@@ -1213,21 +953,20 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     NI_CUDA_TRY(cudaEventCreate(&e1));
     NI_CUDA_TRY(cudaEventRecord(e0, s));
     NI_COUNT_LAUNCH();
-    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT), args, kSmemBytes, s));
+    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT), args, 0, s));
     NI_CUDA_TRY(cudaEventRecord(e1, s));
     g_fill_report.grid = G;
     g_fill_report.ntiles = NIt;
-    g_fill_report.npartials = NP;
+    g_fill_report.npartials = P;
     NI_CUDA_TRY(cudaMemsetAsync(w.px_iters, 0, sizeof(unsigned long long), s));
     NI_CUDA_TRY(cudaMemsetAsync(w.max_iters, 0, sizeof(int32_t), s));
     if (count > 0) {
       NI_COUNT_LAUNCH(), status_out_kernel<<<div_up(count, 256), 256, 0, s>>>(
-                             w.status, w.iters, count, w.comp_size, comp_iters, comp_status,
-                             w.px_iters, w.max_iters);
+                             a, count, w.comp_size, comp_iters, comp_status, w.px_iters,
+                             w.max_iters);
       NI_LAUNCH_CHECK();
     }
-    NI_COUNT_LAUNCH(), output_kernel<<<blocks, 256, 0, s>>>(w.x, labels, w.comp_size, W, P, npix,
-                                                           z_out);
+    NI_COUNT_LAUNCH(), output_kernel<<<blocks, 256, 0, s>>>(w.x, labels, w.comp_size, npix, z_out);
     NI_LAUNCH_CHECK();
     unsigned long long pxi = 0;
     int32_t mxi = 0;
