@@ -15,7 +15,7 @@ scaling: the 64 maps are fixed, each rank takes a contiguous block).
   the host->device copy of the normals+mask and the device->host copy of the
   log-depth inside the timed region.
 * ``roofline``: the dominant kernel (the persistent batched CG,
-  ``fill_cg_kernel``), algorithmic bytes per launch = 45 B x (component
+  ``fill_cg_kernel``), algorithmic bytes per launch = 37 B x (component
   size x CG iterations, summed) / its CUDA-event duration.
 * ``cpu_baseline``: the CPU oracle port (oracle/normint_oracle.py, a numpy
   restatement of the reference) on one map of the same batch, rank 0, N=1.
@@ -41,7 +41,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_PX_ITER = 45  # paper_2510_11508_b200/csrc/ni_fill.cu header
+BYTES_PER_PX_ITER = 37  # paper_2510_11508_b200/csrc/ni_fill.cu header (single-sweep CG)
 THETA_DEG = 3.5
 
 
@@ -64,8 +64,8 @@ def make_workload(config, rank, world, nmaps):
     """Return (normals (B,H,W,3) f32, masks (B,H,W) bool, intrinsics list,
     merge_freq, description, total maps)."""
     if config == "C5":
-        lo = rank * nmaps // world
-        hi = (rank + 1) * nmaps // world
+        from paper_2510_11508_b200.shard import map_range
+        lo, hi = map_range(rank, world, nmaps)
         idx = list(range(lo, hi))
         import concurrent.futures as cf
         workers = max(1, min(len(idx), (os.cpu_count() or 2) // max(1, world)))
@@ -242,11 +242,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_ms = timed(step_e2e, max(1, min(args.steps, 3)), lambda r: None)
 
-    valid_total = valid_local
-    if world > 1:
-        t = torch.tensor([valid_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        valid_total = int(t.item())
+    from paper_2510_11508_b200.shard import aggregate
+    valid_total, _ = aggregate(valid_local, ms, dev)
 
     # roofline of the dominant kernel
     cg_ms = float(np.mean([f["cg_ms"] for f in fills]))

@@ -30,4 +30,4 @@ if __name__ == "__main__":
         r = _lib.fill_report()
         print(f"minb={os.environ.get('NI_FILL_MINB', '4')} rep{rep} maps={nmaps} cg_ms={r['cg_ms']:.1f} "
               f"px_iters={r['px_iters']:.3e} max_iters={r['max_iters']} grid={r['grid']} items={r['ntiles']} "
-              f"GB/s={45 * r['px_iters'] / (r['cg_ms'] * 1e-3) / 1e9:.1f}", flush=True)
+              f"GB/s={37 * r['px_iters'] / (r['cg_ms'] * 1e-3) / 1e9:.1f}", flush=True)

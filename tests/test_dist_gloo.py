@@ -1,0 +1,63 @@
+"""World-size-2 test of the map sharding and result aggregation used by
+bench.py, on the CPU with the gloo backend (NCCL stands in on the GPUs)."""
+
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2510_11508_b200.shard import map_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, nmaps, q):
+    import torch.distributed as dist
+
+    from paper_2510_11508_b200.shard import aggregate, map_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = map_range(rank, world, nmaps)
+    valid_local = sum(1000 + i for i in range(lo, hi))
+    ms_local = 10.0 * (rank + 1)
+    total, ms = aggregate(valid_local, ms_local)
+    q.put((rank, lo, hi, total, ms))
+    dist.destroy_process_group()
+
+
+def test_map_range_partitions():
+    for world in (1, 2, 4, 8):
+        got = [map_range(r, world, 64) for r in range(world)]
+        assert got[0][0] == 0 and got[-1][1] == 64
+        assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+        assert all(hi - lo == 64 // world for lo, hi in got)
+    with pytest.raises(ValueError):
+        map_range(2, 2, 8)
+
+
+def test_two_rank_gloo_aggregation():
+    world, nmaps = 2, 10
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nmaps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect_total = sum(1000 + i for i in range(nmaps))
+    assert [o[1:3] for o in out] == [(0, 5), (5, 10)]
+    for _, _, _, total, ms in out:
+        assert total == expect_total
+        assert ms == 20.0  # the slowest rank

@@ -1,0 +1,106 @@
+"""CPU tests of the host side: the C-ABI library loads and exports every
+symbol include/normint_b200.h declares (no compute without a GPU), the
+threshold and settings logic mirrors the reference, and the product package
+never touches the oracle."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "normint_b200.h")
+
+
+def header_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\s*\**\s*(ni_\w+)\s*\(", txt, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2510_11508_b200 import _lib, build
+
+    build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_abi():
+    names = header_functions()
+    for required in ("ni_normalize", "ni_components", "ni_coefficients", "ni_fill",
+                     "ni_inter_edges", "ni_quotient_build", "ni_scale_step", "ni_merge",
+                     "ni_gauge", "ni_last_error", "ni_version"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2510_11508_b200 import _lib
+
+    for name in header_functions():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} missing from the ctypes signatures"
+
+
+def test_host_only_entry_points(lib):
+    from paper_2510_11508_b200 import _lib
+
+    assert b"sm_100a" in lib.ni_version()
+    assert _lib.size_query(lib.ni_components_workspace_size, 1, 64, 64) > 64 * 64 * 12
+    assert _lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10) > 2 * 64 * 64 * 20
+    assert _lib.size_query(lib.ni_inter_edges_workspace_size, 1, 32, 32, 4) > 0
+    assert _lib.size_query(lib.ni_quotient_workspace_size, 100, 10) > 0
+    assert _lib.size_query(lib.ni_scale_step_workspace_size, 100, 10) > 0
+    assert _lib.size_query(lib.ni_merge_workspace_size, 100, 10) > 0
+    assert _lib.size_query(lib.ni_gauge_workspace_size, 3, 16, 16) > 0
+    # argument validation happens before any device work
+    st = lib.ni_coefficients(None, None, None, 1, 4, 4, 8, 1, None, None, None, None, None, None)
+    assert st == _lib.NI_ERR_INVALID_ARG
+    assert "connectivity=4" in _lib.last_error()
+    with pytest.raises(ValueError):
+        _lib.check(st, "x")
+
+
+def test_dot_cutoff_matches_oracle():
+    from oracle import normint_oracle as O
+    from paper_2510_11508_b200 import dot_cutoff
+
+    for deg in (0.5, 2.0, 3.5, 5.0, 30.0, 179.0):
+        th = float(np.deg2rad(deg))
+        assert dot_cutoff(th) == O.dot_cutoff(th)
+    assert dot_cutoff(0.0) == float("inf")  # nothing is strictly below 0
+
+
+def test_settings_validation_mirrors_reference():
+    from paper_2510_11508_b200 import SolveSettings, WeightParams
+
+    for kw in ({"cg_tol": 0}, {"max_iters": 0}, {"alignment_iters": -1}, {"freq_merging": 0},
+               {"worker_count": 0}):
+        with pytest.raises(ValueError):
+            SolveSettings(**kw)
+    for kw in ({"k": 0}, {"outlier_low": 1e-3, "outlier_high": 1e-5}, {"reweighting_mode": "x"}):
+        with pytest.raises(ValueError):
+            WeightParams(**kw)
+    assert WeightParams(reweighting_mode="hard").mode_code == 2
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2510_11508_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    import paper_2510_11508_b200 as nb
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        nb.NormalMap.create(np.zeros((4, 4, 3), np.float32))
