@@ -314,7 +314,6 @@ def run_ours(args, rank, world, local_rank):
 
 
 def _oracle_one(payload):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
     normals, mask, intr, merge_freq = payload
     from oracle import normint_oracle as O
     t = time.perf_counter()
@@ -343,7 +342,13 @@ def run_reference(args, rank, world):
         payloads = [(n, m, i, mf)]
     warm = min(args.warmup, 1)
     times = []
-    with cf.ProcessPoolExecutor(max_workers=procs) as ex:
+    # one single-threaded process per core: pin every BLAS / OpenMP pool
+    # before the workers start (they are spawned, so they inherit this env)
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS",
+                "NUMEXPR_NUM_THREADS"):
+        os.environ[var] = "1"
+    import multiprocessing as mp
+    with cf.ProcessPoolExecutor(max_workers=procs, mp_context=mp.get_context("spawn")) as ex:
         for s in range(warm + args.steps):
             t = time.perf_counter()
             out = list(ex.map(_oracle_one, payloads))
