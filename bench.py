@@ -256,8 +256,9 @@ def run_ours(args, rank, world, local_rank):
         "kernel": "fill_cg_kernel (persistent batched CG, one launch per step)",
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4), "peak_source": peak_src,
-        "traffic": prof.get("dram_bytes_per_launch") if prof else None,
-        "traffic_note": (prof.get("note") if prof else "no ncu capture committed for this config"),
+        "traffic": (round(prof["dram_bytes_per_px_iter"] * px_iters) if prof else None),
+        "traffic_note": ((prof["source"] + "; " + prof["note"]) if prof else
+                         "no ncu capture committed"),
         "alg_bytes_per_launch": alg_bytes, "bytes_per_px_iter": BYTES_PER_PX_ITER,
         "px_iters_per_launch": px_iters, "kernel_ms": round(cg_ms, 3),
         "kernel_share_of_step": round(cg_ms / ms, 4),
