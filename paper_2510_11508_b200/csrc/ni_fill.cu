@@ -14,14 +14,18 @@
 // constants stay an exact null vector in float32 (a rounded CSR Laplacian
 // loses that and doubles the iteration count).
 //
-// Data layout in HBM (per pixel, npix = B*H*W, row-major):
-//   x             : float32 solution
-//   r[2], q[2], p[2] : float32 CG vectors, double-buffered by iteration parity
-//                   (a sweep reads its neighbours' previous values while
-//                   other warps write the new ones)
-//   hw            : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
-//   imask         : uint8, bit k = forward edge k intra-component and valid,
-//                   bit 4+k = backward edge k (pixel - offset_k)
+// Data layout in HBM.  rows = B*H; pixel (y, x) lives at padded index
+// (y + RM) * P + (x + XM) with zeroed margins, so no access needs a bounds
+// check (RM = 2 rows top / RB rows bottom, XM = 16 columns left, >= 32
+// right):
+//   v[2]  : float4 {r, q, p, x} per pixel, double-buffered by iteration
+//           parity (a sweep reads its neighbours' previous values while other
+//           warps write the new ones): one 16-B load and one 16-B store per
+//           pixel and iteration
+//   hw    : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
+//   imask : uint8, bit k = forward edge k intra-component and valid,
+//           bit 4+k = backward edge k (pixel - offset_k)
+//   lab   : int32 labels (read by mixed items only)
 //
 // ONE sweep and ONE grid sync per CG iteration.  scipy's iteration k
 //   p_k = r_k + beta p_{k-1};  q_k = A p_k;  alpha = rho_k / <p_k, q_k>;
@@ -32,17 +36,18 @@
 // rho_k = <r_k, r_k> is exact; rho_{k+1}, needed for beta and for scipy's
 // stop test before r_{k+1} exists, is rho_k - 2 alpha <r,q> + alpha^2 <q,q>
 // (float64, no cancellation at CG's per-step contraction).  A component that
-// stops gets one last "flush" sweep that applies its pending x update.
+// stops gets one last "flush" sweep that applies its pending x update; its
+// final x then lives in the buffer of that sweep's parity.
 //
-// Work decomposition: the grid is cut into strips of 30 columns x 32 rows.
-// A warp processes a strip by marching down its rows with a register ring
-// of rows y-1, y, y+1 (+ prefetched rows); lanes 0 and 31 carry the left /
-// right halo columns, so horizontal neighbours are warp shuffles and there
-// is no block barrier anywhere in a sweep.  A strip touching several
-// multi-pixel components becomes ceil(n/2) "items" of <= 2 components that
-// read the int32 labels; a strip with one component (the common case) is a
-// "pure" item that needs no label at all (singletons / invalid pixels carry
-// r = q = p = 0 and stay 0 under any update).
+// Work decomposition: strips of 30 columns x 30 rows.  A warp processes a
+// strip ("item") by marching down its rows: raw rows are prefetched into a
+// 6-row register ring four rows ahead, each row's p' = r + beta p is formed
+// once and shuffled to the neighbouring lanes (lanes 0 and 31 hold the halo
+// columns), and the row loop is unrolled by the ring period so no register
+// moves wait on loads.  No block barrier anywhere in a sweep.  A strip
+// touching several multi-pixel components becomes ceil(n/2) "mixed" items of
+// <= 2 components that read labels; a strip with one component is a "pure"
+// item (singleton / invalid pixels carry r = q = p = x = 0 and stay 0).
 //
 // Reductions are deterministic: each item writes float64 partials per
 // component (lane-local sums over rows, fixed xor tree over lanes); the last
@@ -50,8 +55,9 @@
 // partials in plan order and updates its scalars.
 // Algorithmic bytes per active pixel and iteration (pure items):
 //   read r, q, p, x, hw (20 B) + imask (1 B); write r, q, p, x (16 B) => 37 B/px
-// (halo rows/columns are re-read from L2 and not counted).
+// (halo rows/columns are re-read from L1/L2 and not counted).
 #include <cooperative_groups.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -62,37 +68,40 @@ namespace cg = cooperative_groups;
 
 namespace ni {
 
-constexpr int SW = 30;     // strip width (lanes 1..30)
-constexpr int SH = 32;     // strip height (rows per item)
+constexpr int SW = 30;     // strip width (lanes 1..30; lanes 0 / 31 are the halo)
+constexpr int SH = 30;     // strip height (centre rows per item)
 constexpr int SPX = 1024;  // padded pixels per strip (sort buffer)
 constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
-constexpr int PF = 3;     // rows prefetched ahead
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
+constexpr int RING = 6;   // raw row ring (row L+4 is loaded at centre row L)
+constexpr int XM = 16;    // left margin (columns)
+constexpr int RM = 2;     // top margin (rows)
+constexpr int RB = 8;     // bottom margin (rows)
 
 enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3, ST_FLUSH = 4 };
 
 // One work item: a strip and up to 2 of its components.
 struct __align__(16) Item {
-  int32_t x0, y0;  // top-left pixel of the strip (column of lane 1)
+  int32_t x0, y0;  // top-left centre pixel of the strip (column of lane 1)
   int32_t pbase;   // first partial slot of this item
   int32_t flags;   // bits 0-7: components in the item (1..2); bit 8: pure strip
   int32_t comp[SLOTS];
+  int32_t pad[2];
 };
 
 __device__ __forceinline__ int item_n(const Item& it) { return it.flags & 0xFF; }
 __device__ __forceinline__ bool item_pure(const Item& it) { return (it.flags >> 8) & 1; }
 
 struct FillArgs {
-  int rows, W;
-  float* x;
-  float* r[2];
-  float* q[2];
-  float* p[2];
+  int rows, W, P;
+  long long* trace;  // optional: per iteration (globaltimer, active items)
+  int trace_len;
+  float4* v[2];
   const float* hw;
   const uint8_t* imask;
-  const int32_t* labels;
+  const int32_t* lab;  // padded labels
   // plan
   const Item* items;
   int nitems;
@@ -102,6 +111,7 @@ struct FillArgs {
   double* partial;             // [P][NDOT]
   int32_t* active_items;       // [2][nitems]
   int32_t* nactive_items;      // [2]
+  int32_t* ticket;             // [2] dynamic item scheduling, by sweep parity
   // component state
   double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
   double* alpha;   // alpha of the last completed sweep
@@ -111,41 +121,34 @@ struct FillArgs {
   int32_t* cap;
   uint8_t* status;
   uint8_t* final_status;  // status after the flush sweep
-  int32_t* active;   // components still ACTIVE or FLUSH
-  int32_t* changed;  // a component changed state during the last sweep
+  uint8_t* xbuf;          // buffer holding the component's final x
+  int32_t* active;        // components still ACTIVE or FLUSH
+  int32_t* changed;       // a component changed state during the last sweep
 };
 
 // ----------------------------------------------------------------- setup
 
+// Padded-layout setup: v[0] = {b, 0, 0, 0}, hw, imask, labels.
 template <int CONN, int MODEL>
 __global__ void __launch_bounds__(256) prep_kernel(
     const int32_t* __restrict__ labels, const double* __restrict__ omega_a,
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
-    const uint8_t* __restrict__ eflags, int H, int W, int64_t npix, float* __restrict__ hw,
-    uint8_t* __restrict__ imask, float* __restrict__ x, float* __restrict__ r,
-    float* __restrict__ r1, float* __restrict__ q0, float* __restrict__ q1, float* __restrict__ p0,
-    float* __restrict__ p1, int32_t* __restrict__ comp_size) {
+    const uint8_t* __restrict__ eflags, int H, int W, int P, int64_t npix,
+    float* __restrict__ hw, uint8_t* __restrict__ imask, int32_t* __restrict__ lab_p,
+    float4* __restrict__ v0, int32_t* __restrict__ comp_size) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t lab = labels[i];
-    x[i] = 0.f;
-    r1[i] = 0.f;
-    q0[i] = 0.f;
-    q1[i] = 0.f;
-    p0[i] = 0.f;
-    p1[i] = 0.f;
-    if (lab < 0) {
-      hw[i] = 0.f;
-      imask[i] = 0;
-      r[i] = 0.f;
-      continue;
-    }
+    const int u = int(i % W);
+    const int64_t row = i / W;
+    const int vloc = int(row % H);
+    const int64_t o = (row + RM) * P + u + XM;  // padded index
+    lab_p[o] = lab;
+    if (lab < 0) continue;  // margins / invalid pixels stay zero
     atomicAdd(comp_size + lab, 1);
     const double wa = 0.5 * (gamma[i] * gamma[i]);
-    hw[i] = float(wa);
-    const int u = int(i % W);
-    const int vloc = int((i / W) % H);
+    hw[o] = float(wa);
     const uint8_t ef = eflags[i];
     uint8_t m = 0;
     double b = 0.0;
@@ -177,8 +180,8 @@ __global__ void __launch_bounds__(256) prep_kernel(
         }
       }
     }
-    imask[i] = m;
-    r[i] = float(b);
+    imask[o] = m;
+    v0[o] = make_float4(float(b), 0.f, 0.f, 0.f);
   }
 }
 
@@ -266,6 +269,7 @@ __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
         it.comp[j] = j < n ? strip_comps[int64_t(s) * SPX + k * SLOTS + j] : -1;
+      it.pad[0] = it.pad[1] = 0;
       items[ib + k] = it;
     }
     for (int j = 0; j < ns; ++j) {
@@ -382,47 +386,47 @@ __device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, Co
   return any;
 }
 
-// Raw values of one row for this lane (prefetch ring) ...
+// Raw values of one row for this lane (prefetch ring).
 struct Raw {
-  float r, q, p, h, x;
-  uint32_t m;   // imask
-  int32_t lab;  // label (mixed items only)
+  float4 v;      // r, q, p, x (previous iteration)
+  float h;
+  uint32_t m;    // imask
+  int32_t lab;   // label (mixed items only)
 };
 
-// ... and a row of the compute ring: r_k and p_k = r_k + beta p_{k-1}
-// formed with the pixel's own component (only intra-component neighbours
-// are ever read, and those share the centre's alpha and beta).
+// A row of the compute ring: r_k, p_k = r_k + beta p_{k-1}, x_k formed with
+// the pixel's own component (only intra-component neighbours are ever read,
+// and those share the centre's alpha and beta), plus the left / right
+// neighbours' p' and hw (warp shuffles; lanes 0 / 31 are the halo).
 struct Row {
-  float rn, pn, h, xn;
+  float pn, h, pl, pr, hl, hr, rn, xn;
   uint32_t m;  // imask | (slot + 1) << 8
 };
 
 template <bool PURE>
-__device__ __forceinline__ Raw load_raw(const FillArgs& a, int par, int y, int ylim, int x) {
+__device__ __forceinline__ Raw load_raw(const FillArgs& a, const float4* __restrict__ vin,
+                                        int64_t o, bool row_ok) {
   Raw w;
-  w.r = w.q = w.p = w.h = w.x = 0.f;
-  w.m = 0;
-  w.lab = -1;
-  if (y >= 0 && y <= ylim && x >= 0 && x < a.W) {
-    const int64_t i = int64_t(y) * a.W + x;
-    w.r = __ldcg(a.r[par] + i);
-    w.q = __ldcg(a.q[par] + i);
-    w.p = __ldcg(a.p[par] + i);
-    w.x = __ldcg(a.x + i);
-    w.h = __ldg(a.hw + i);
-    w.m = __ldg(a.imask + i);
-    if (!PURE) w.lab = __ldg(a.labels + i);
+  if (row_ok) {
+    w.v = __ldcg(vin + o);
+    w.h = __ldg(a.hw + o);
+    w.m = __ldg(a.imask + o);
+    w.lab = PURE ? 0 : __ldg(a.lab + o);
+  } else {
+    w.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    w.h = 0.f;
+    w.m = 0;
+    w.lab = -1;
   }
   return w;
 }
 
 template <bool PURE>
-__device__ __forceinline__ Row to_row(const Raw& w, const Item& it, const Coefs& k) {
-  Row o;
+__device__ __forceinline__ Row derive(const Raw& w, const Item& it, const Coefs& k) {
   float al = k.al[0], be = k.be[0];
-  uint32_t m = w.m;
+  int s = 0;
   if (!PURE) {
-    const int s = slot_of(it, w.lab);
+    s = slot_of(it, w.lab);
     al = 0.f;
     be = 0.f;
 #pragma unroll
@@ -431,111 +435,101 @@ __device__ __forceinline__ Row to_row(const Raw& w, const Item& it, const Coefs&
         al = k.al[j];
         be = k.be[j];
       }
-    m |= uint32_t(s + 1) << 8;
-  } else {
-    m |= 1u << 8;
   }
-  o.rn = fmaf(-al, w.q, w.r);
-  o.pn = fmaf(be, w.p, o.rn);
-  o.xn = fmaf(al, w.p, w.x);
+  Row o;
+  o.rn = fmaf(-al, w.v.y, w.v.x);
+  o.pn = fmaf(be, w.v.z, o.rn);
+  o.xn = fmaf(al, w.v.z, w.v.w);
   o.h = w.h;
-  o.m = m;
+  o.m = w.m | (uint32_t(s + 1) << 8);
+  o.pl = __shfl_up_sync(0xffffffffu, o.pn, 1);
+  o.pr = __shfl_down_sync(0xffffffffu, o.pn, 1);
+  o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
+  o.hr = __shfl_down_sync(0xffffffffu, o.h, 1);
   return o;
 }
 
 // One CG sweep over one item (see the header).
 template <int CONN, bool PURE>
-__device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, int par) {
+__device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, const Coefs& k,
+                                           int par) {
   const int lane = threadIdx.x & 31;
-  Coefs k;
-  if (!item_coefs(a, it, k)) return;
-  const int x = it.x0 - 1 + lane;
-  const bool center_lane = lane >= 1 && lane <= SW && x < a.W;
-  float* rout = a.r[par ^ 1];
-  float* qout = a.q[par ^ 1];
-  float* pout = a.p[par ^ 1];
+  const int xr = it.x0 - 1 + lane;  // real column of this lane
+  const bool center_lane = lane >= 1 && lane <= SW && xr < a.W;
+  const float4* __restrict__ vin = a.v[par];
+  float4* __restrict__ vout = a.v[par ^ 1];
   double acc[SLOTS][NDOT];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j)
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
-  const int yend = min(it.y0 + SH, a.rows);
-  const int ylim = min(yend, a.rows - 1);  // last row the stencil touches
-  Raw F[PF];
+  const int nrows = min(SH, a.rows - it.y0);  // centre rows (local rows 1..nrows)
+  const int lastrow = nrows + 1;              // last local row the stencil reads
+  // padded index of local row 0 (= real row y0 - 1), this lane's column
+  const int64_t o0 = int64_t(it.y0 - 1 + RM) * a.P + (xr + XM);
+  const int64_t P = a.P;
+  Raw raw[RING];
+  Row der[3];
 #pragma unroll
-  for (int t = 0; t < PF; ++t) F[t] = load_raw<PURE>(a, par, it.y0 + 2 + t, ylim, x);
-  Row U = to_row<PURE>(load_raw<PURE>(a, par, it.y0 - 1, ylim, x), it, k);
-  Row C = to_row<PURE>(load_raw<PURE>(a, par, it.y0, ylim, x), it, k);
-  Row D = to_row<PURE>(load_raw<PURE>(a, par, it.y0 + 1, ylim, x), it, k);
-  for (int y = it.y0; y < yend; ++y) {
-    const Raw N = load_raw<PURE>(a, par, y + 2 + PF, ylim, x);  // PF rows in flight
-    const int s = PURE ? 0 : int(C.m >> 8) - 1;  // this pixel's slot, -1: not in the item
-    uint8_t st = ST_IDLE;
-    if (PURE) {
-      st = k.st[0];
-    } else {
+  for (int j = 0; j < RING - 1; ++j) raw[j] = load_raw<PURE>(a, vin, o0 + j * P, j <= lastrow);
+  der[0] = derive<PURE>(raw[0], it, k);
+  der[1] = derive<PURE>(raw[1], it, k);
+  for (int g = 0; g < SH; g += RING) {
 #pragma unroll
-      for (int j = 0; j < SLOTS; ++j)
-        if (j == s) st = k.st[j];
-    }
-    const bool on = center_lane && (C.m & 0xFF) != 0;
-    const float pa = C.pn;
-    const float ha = C.h;
-    const uint32_t m = C.m;
-    float q = 0.f;
-#define NI_NB(pp, hh) fmaf(ha + (hh), pa - (pp), q)
-#define NI_UP(v) __shfl_up_sync(0xffffffffu, (v), 1)
-#define NI_DN(v) __shfl_down_sync(0xffffffffu, (v), 1)
-    {
-      const float pCl = NI_UP(C.pn), hCl = NI_UP(C.h);
-      const float pCr = NI_DN(C.pn), hCr = NI_DN(C.h);
+    for (int u = 0; u < RING; ++u) {
+      const int L = g + u + 1;      // centre local row
+      const int ln = L + RING - 2;  // row to prefetch
+      raw[(u + RING - 1) % RING] =
+          load_raw<PURE>(a, vin, o0 + int64_t(ln) * P, ln <= lastrow);
+      der[(u + 2) % 3] = derive<PURE>(raw[(u + 2) % RING], it, k);
+      const Row& U = der[u % 3];
+      const Row& C = der[(u + 1) % 3];
+      const Row& D = der[(u + 2) % 3];
+      if (L > nrows) continue;
+      const float pa = C.pn, ha = C.h;
+      const uint32_t m = C.m;
+      float q = 0.f;
+#define NI_E(bit, pp, hh) q = ((m >> (bit)) & 1u) ? fmaf(ha + (hh), pa - (pp), q) : q
       if (CONN == 8) {
-        const float pDl = NI_UP(D.pn), hDl = NI_UP(D.h);
-        const float pDr = NI_DN(D.pn), hDr = NI_DN(D.h);
-        const float pUl = NI_UP(U.pn), hUl = NI_UP(U.h);
-        const float pUr = NI_DN(U.pn), hUr = NI_DN(U.h);
-        if (m & 0x01) q = NI_NB(pCr, hCr);    // (+1, 0)
-        if (m & 0x02) q = NI_NB(pDl, hDl);    // (-1,+1)
-        if (m & 0x04) q = NI_NB(D.pn, D.h);   // ( 0,+1)
-        if (m & 0x08) q = NI_NB(pDr, hDr);    // (+1,+1)
-        if (m & 0x10) q = NI_NB(pCl, hCl);    // (-1, 0)
-        if (m & 0x20) q = NI_NB(pUr, hUr);    // (+1,-1)
-        if (m & 0x40) q = NI_NB(U.pn, U.h);   // ( 0,-1)
-        if (m & 0x80) q = NI_NB(pUl, hUl);    // (-1,-1)
+        NI_E(0, C.pr, C.hr);  // (+1, 0)
+        NI_E(1, D.pl, D.hl);  // (-1,+1)
+        NI_E(2, D.pn, D.h);   // ( 0,+1)
+        NI_E(3, D.pr, D.hr);  // (+1,+1)
+        NI_E(4, C.pl, C.hl);  // (-1, 0)
+        NI_E(5, U.pr, U.hr);  // (+1,-1)
+        NI_E(6, U.pn, U.h);   // ( 0,-1)
+        NI_E(7, U.pl, U.hl);  // (-1,-1)
       } else {
-        if (m & 0x01) q = NI_NB(pCr, hCr);    // (+1, 0)
-        if (m & 0x02) q = NI_NB(D.pn, D.h);   // ( 0,+1)
-        if (m & 0x10) q = NI_NB(pCl, hCl);    // (-1, 0)
-        if (m & 0x20) q = NI_NB(U.pn, U.h);   // ( 0,-1)
+        NI_E(0, C.pr, C.hr);  // (+1, 0)
+        NI_E(1, D.pn, D.h);   // ( 0,+1)
+        NI_E(4, C.pl, C.hl);  // (-1, 0)
+        NI_E(5, U.pn, U.h);   // ( 0,-1)
+      }
+#undef NI_E
+      const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
+      uint8_t st = ST_IDLE;
+      if (PURE) {
+        st = k.st[0];
+      } else {
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j)
+          if (j == s) st = k.st[j];
+      }
+      if (center_lane && (m & 0xFFu) != 0 && (st == ST_ACTIVE || st == ST_FLUSH)) {
+        vout[o0 + int64_t(L) * P] = make_float4(C.rn, q, pa, C.xn);
+        if (st == ST_ACTIVE) {
+          const double dp = pa, dq = q, dr = C.rn;
+#pragma unroll
+          for (int j = 0; j < SLOTS; ++j)
+            if (j == s) {
+              acc[j][0] = fma(dp, dq, acc[j][0]);
+              acc[j][1] = fma(dr, dq, acc[j][1]);
+              acc[j][2] = fma(dq, dq, acc[j][2]);
+              acc[j][3] = fma(dr, dr, acc[j][3]);
+            }
+        }
       }
     }
-#undef NI_NB
-#undef NI_UP
-#undef NI_DN
-    if (on && st == ST_ACTIVE) {
-      const int64_t i = int64_t(y) * a.W + x;
-      __stcg(rout + i, C.rn);
-      __stcg(pout + i, pa);
-      __stcg(qout + i, q);
-      __stcg(a.x + i, C.xn);
-      const double dp = pa, dq = q, dr = C.rn;
-#pragma unroll
-      for (int j = 0; j < SLOTS; ++j)
-        if (j == s) {
-          acc[j][0] = fma(dp, dq, acc[j][0]);
-          acc[j][1] = fma(dr, dq, acc[j][1]);
-          acc[j][2] = fma(dq, dq, acc[j][2]);
-          acc[j][3] = fma(dr, dr, acc[j][3]);
-        }
-    } else if (on && st == ST_FLUSH) {
-      __stcg(a.x + int64_t(y) * a.W + x, C.xn);  // the pending x_{k+1}
-    }
-    U = C;
-    C = D;
-    D = to_row<PURE>(F[0], it, k);
-#pragma unroll
-    for (int t = 0; t < PF - 1; ++t) F[t] = F[t + 1];
-    F[PF - 1] = N;
   }
   bool live[SLOTS];
 #pragma unroll
@@ -543,6 +537,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, in
   item_finish(a, it, acc, live, [&](int32_t c, const double* d) {
     if (__ldcg(a.status + c) == ST_FLUSH) {  // the pending update is applied
       a.status[c] = __ldcg(a.final_status + c);
+      a.xbuf[c] = uint8_t(par ^ 1);
       atomicSub(a.active, 1);
       atomicExch(a.changed, 1);
       return;
@@ -604,6 +599,12 @@ __device__ void rebuild_items(const FillArgs& a, int dst, int gwarp, int nwarps)
   }
 }
 
+__device__ __forceinline__ int draw_ticket(const FillArgs& a, int par) {
+  int k = 0;
+  if ((threadIdx.x & 31) == 0) k = atomicAdd(a.ticket + par, 1);
+  return __shfl_sync(0xffffffffu, k, 0);
+}
+
 template <int CONN, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -613,6 +614,8 @@ __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.nactive_items[0] = 0;
     a.nactive_items[1] = 0;
+    a.ticket[0] = 0;
+    a.ticket[1] = 0;
   }
   grid.sync();
   rebuild_items(a, 0, gwarp, nwarps);
@@ -620,11 +623,27 @@ __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   for (int it = 0;; ++it) {
     if (__ldcg(a.active) == 0) break;
     const int par = it & 1;
+    // the other parity's ticket was last used by the previous sweep (done)
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ticket[par ^ 1] = 0;
     const int n = __ldcg(a.nactive_items + cur);
-    for (int k = gwarp; k < n; k += nwarps) {
+    if (a.trace && it < a.trace_len && blockIdx.x == 0 && threadIdx.x == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[2 * it] = t;
+      a.trace[2 * it + 1] = n;
+    }
+    // dynamic item scheduling: the next ticket is drawn before the current
+    // item is processed so its latency is hidden
+    int k = draw_ticket(a, par);
+    while (k < n) {
+      const int nk = draw_ticket(a, par);
       const Item item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
-      if (item_pure(item)) sweep_item<CONN, true>(a, item, par);
-      else sweep_item<CONN, false>(a, item, par);
+      Coefs kc;
+      if (item_coefs(a, item, kc)) {
+        if (item_pure(item)) sweep_item<CONN, true>(a, item, kc, par);
+        else sweep_item<CONN, false>(a, item, kc, par);
+      }
+      k = nk;
     }
     grid.sync();
     if (__ldcg(a.changed)) {
@@ -648,8 +667,8 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
   const int lane = threadIdx.x & 31;
   for (int k = gwarp; k < a.nitems; k += nwarps) {
     const Item it = a.items[k];
-    const int x = it.x0 - 1 + lane;
-    const bool on = lane >= 1 && lane <= SW && x < a.W;
+    const int xr = it.x0 - 1 + lane;
+    const bool on = lane >= 1 && lane <= SW && xr < a.W;
     double acc[SLOTS][NDOT];
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j)
@@ -658,10 +677,10 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
     const int yend = min(it.y0 + SH, a.rows);
     if (on) {
       for (int y = it.y0; y < yend; ++y) {
-        const int64_t i = int64_t(y) * a.W + x;
-        const int s = slot_of(it, a.labels[i]);
+        const int64_t o = int64_t(y + RM) * a.P + xr + XM;
+        const int s = slot_of(it, a.lab[o]);
         if (s < 0) continue;
-        const double rv = a.r[0][i];
+        const double rv = a.v[0][o].x;
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j)
           if (j == s) acc[j][3] += rv * rv;
@@ -691,29 +710,41 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
 
 // status ACTIVE only while the initial norm pass counts arrivals; its
 // finaliser sets the real state and the active count.
-__global__ void init_state_kernel(FillArgs a, const int32_t* __restrict__ comp_size, int C,
-                                  int cg_max_iters) {
+__global__ void init_state_kernel(uint8_t* __restrict__ status, uint8_t* __restrict__ final_status,
+                                  uint8_t* __restrict__ xbuf, int32_t* __restrict__ iters,
+                                  int32_t* __restrict__ cap, double* __restrict__ rho,
+                                  const int32_t* __restrict__ comp_size, int C, int cg_max_iters) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    a.status[c] = comp_size[c] >= 2 ? ST_ACTIVE : ST_IDLE;
-    a.final_status[c] = ST_CONVERGED;
-    a.iters[c] = 0;
+    status[c] = comp_size[c] >= 2 ? ST_ACTIVE : ST_IDLE;
+    final_status[c] = ST_CONVERGED;
+    xbuf[c] = 0;
+    iters[c] = 0;
     const int n = comp_size[c];
-    a.cap[c] = n > cg_max_iters ? n : cg_max_iters;
-    a.rho[c] = 0.0;
+    cap[c] = n > cg_max_iters ? n : cg_max_iters;
+    rho[c] = 0.0;
   }
 }
 
-__global__ void output_kernel(const float* __restrict__ x, const int32_t* __restrict__ labels,
-                              const int32_t* __restrict__ comp_size, int64_t npix,
+__global__ void output_kernel(const float4* __restrict__ v0, const float4* __restrict__ v1,
+                              const int32_t* __restrict__ labels,
+                              const int32_t* __restrict__ comp_size,
+                              const uint8_t* __restrict__ xbuf, int W, int P, int64_t npix,
                               double* __restrict__ z) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t l = labels[i];
-    z[i] = (l >= 0 && comp_size[l] >= 2) ? double(x[i]) : 0.0;
+    double out = 0.0;
+    if (l >= 0 && comp_size[l] >= 2) {
+      const int64_t o = (i / W + RM) * P + i % W + XM;
+      out = double((xbuf[l] ? v1 : v0)[o].w);
+    }
+    z[i] = out;
   }
 }
 
-__global__ void status_out_kernel(const FillArgs a, int C, const int32_t* __restrict__ comp_size,
+__global__ void status_out_kernel(const uint8_t* __restrict__ status,
+                                  const int32_t* __restrict__ iters, int C,
+                                  const int32_t* __restrict__ comp_size,
                                   int32_t* __restrict__ iters_out,
                                   int32_t* __restrict__ status_out,
                                   unsigned long long* __restrict__ px_iters,
@@ -721,9 +752,9 @@ __global__ void status_out_kernel(const FillArgs a, int C, const int32_t* __rest
   unsigned long long acc = 0;
   int mx = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    const int it = a.iters[c];
+    const int it = iters[c];
     iters_out[c] = it;
-    status_out[c] = a.status[c] == ST_CAPPED ? 1 : 0;
+    status_out[c] = status[c] == ST_CAPPED ? 1 : 0;
     if (comp_size[c] >= 2) acc += (unsigned long long)comp_size[c] * (unsigned long long)it;
     mx = it > mx ? it : mx;
   }
@@ -734,15 +765,17 @@ __global__ void status_out_kernel(const FillArgs a, int C, const int32_t* __rest
 // ------------------------------------------------------------ workspace
 
 struct FillWs {
-  float *x, *r0, *r1, *q0, *q1, *p0, *p1, *hw;
+  float4 *v0, *v1;
+  float* hw;
   uint8_t* imask;
+  int32_t* lab_p;
   int32_t *slot_base, *nslots, *nitems_strip, *item_base, *strip_comps, *partial_comp,
       *partial_idx, *plist, *keys_sorted;
   Item* items;
   int32_t *comp_size, *comp_nparts, *comp_pstart, *comp_cnt, *iters, *cap, *active, *changed,
-      *total, *total_items, *active_items, *nactive_items;
+      *total, *total_items, *active_items, *nactive_items, *ticket;
   double *partial, *rho, *alpha, *beta, *tol;
-  uint8_t *status, *final_status;
+  uint8_t *status, *final_status, *xbuf;
   unsigned long long* px_iters;
   int32_t* max_iters;
   void* sort_ws;
@@ -750,19 +783,19 @@ struct FillWs {
   void* scan_ws;
 };
 
-static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
+static int pitch_of(int W) { return (W + XM + 48 + 15) & ~15; }
+static int64_t padded_len(int rows, int W) { return int64_t(rows + RM + RB) * pitch_of(W); }
+
+static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int nstrips, int C) {
+  const int64_t npad = padded_len(rows, W);
   // every partial slot owns >= 1 pixel
   const int64_t P = npix;
   const int64_t NI = nstrips + P / SLOTS + 1;  // items
-  w.x = c.take<float>(npix);
-  w.r0 = c.take<float>(npix);
-  w.r1 = c.take<float>(npix);
-  w.q0 = c.take<float>(npix);
-  w.q1 = c.take<float>(npix);
-  w.p0 = c.take<float>(npix);
-  w.p1 = c.take<float>(npix);
-  w.hw = c.take<float>(npix);
-  w.imask = c.take<uint8_t>(npix);
+  w.v0 = c.take<float4>(npad);
+  w.v1 = c.take<float4>(npad);
+  w.hw = c.take<float>(npad);
+  w.imask = c.take<uint8_t>(npad);
+  w.lab_p = c.take<int32_t>(npad);
   w.slot_base = c.take<int32_t>(nstrips + 1);
   w.nslots = c.take<int32_t>(nstrips + 1);
   w.nitems_strip = c.take<int32_t>(nstrips + 1);
@@ -771,6 +804,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   w.items = c.take<Item>(NI);
   w.active_items = c.take<int32_t>(2 * NI);
   w.nactive_items = c.take<int32_t>(2);
+  w.ticket = c.take<int32_t>(2);
   w.partial_comp = c.take<int32_t>(P);
   w.partial_idx = c.take<int32_t>(P);
   w.plist = c.take<int32_t>(P);
@@ -788,6 +822,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int nstrips, int C) {
   w.tol = c.take<double>(C + 1);
   w.status = c.take<uint8_t>(C + 1);
   w.final_status = c.take<uint8_t>(C + 1);
+  w.xbuf = c.take<uint8_t>(C + 1);
   w.active = c.take<int32_t>(1);
   w.changed = c.take<int32_t>(1);
   w.total = c.take<int32_t>(1);
@@ -819,7 +854,7 @@ extern "C" int ni_fill_workspace_size(int B, int H, int W, int connectivity, int
   strip_grid(B, H, W, &nsx, &nsy);
   Sizer s;
   FillWs w;
-  carve_fill(s, w, npix, nsx * nsy, count);
+  carve_fill(s, w, npix, B * H, W, nsx * nsy, count);
   *bytes = s.used;
   return NI_OK;
 }
@@ -836,12 +871,13 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npix = int64_t(B) * H * W;
   const int rows = B * H;
+  const int P = pitch_of(W);
   int nsx, nsy;
   strip_grid(B, H, W, &nsx, &nsy);
   const int nstrips = nsx * nsy;
   Carver cv(workspace, workspace_bytes);
   FillWs w;
-  carve_fill(cv, w, npix, nstrips, count);
+  carve_fill(cv, w, npix, rows, W, nstrips, count);
   if (!cv.ok() || !workspace) {
     set_error("ni_fill: workspace too small (%zu < %zu)", workspace_bytes, cv.used);
     return NI_ERR_WORKSPACE;
@@ -852,10 +888,18 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.comp_cnt, 0, sizeof(int32_t) * (count + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.active, 0, sizeof(int32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.changed, 0, sizeof(int32_t), s));
+  {  // zero margins and buffers of the padded layout
+    const size_t npad = size_t(padded_len(rows, W));
+    NI_CUDA_TRY(cudaMemsetAsync(w.v0, 0, npad * sizeof(float4), s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.v1, 0, npad * sizeof(float4), s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.hw, 0, npad * sizeof(float), s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.imask, 0, npad, s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.lab_p, 0xff, npad * sizeof(int32_t), s));
+  }
 #define NI_PREP(CONN, MODEL)                                                                   \
   NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<blocks, 256, 0, s>>>(                          \
-                         labels, omega_a, omega_b, gamma, eflags, H, W, npix, w.hw, w.imask,   \
-                         w.x, w.r0, w.r1, w.q0, w.q1, w.p0, w.p1, w.comp_size)
+                         labels, omega_a, omega_b, gamma, eflags, H, W, P, npix, w.hw, w.imask, \
+                         w.lab_p, w.v0, w.comp_size)
   if (connectivity == 8) NI_PREP(8, 0);
   else if (model == 0) NI_PREP(4, 0);
   else NI_PREP(4, 1);
@@ -874,31 +918,35 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
                          w.nslots, w.slot_base, w.item_base, w.strip_comps, nstrips, nsx, w.items,
                          w.partial_comp, w.partial_idx, w.comp_nparts);
   NI_LAUNCH_CHECK();
-  int32_t P = 0, NIt = 0;
-  NI_CUDA_TRY(cudaMemcpyAsync(&P, w.total, sizeof(P), cudaMemcpyDeviceToHost, s));
+  int32_t NP = 0, NIt = 0;
+  NI_CUDA_TRY(cudaMemcpyAsync(&NP, w.total, sizeof(NP), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaMemcpyAsync(&NIt, w.total_items, sizeof(NIt), cudaMemcpyDeviceToHost, s));
   NI_CUDA_TRY(cudaStreamSynchronize(s));
-  if (P > 0) {
+  if (NP > 0) {
     int end_bit = 1;
     while ((int64_t(1) << end_bit) <= count) ++end_bit;
     size_t sb = w.sort_bytes;
     NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_ws, sb, w.partial_comp, w.keys_sorted,
-                                                w.partial_idx, w.plist, P, 0, end_bit, s));
+                                                w.partial_idx, w.plist, NP, 0, end_bit, s));
   }
   NI_TRY(exclusive_scan_i32(w.comp_nparts, w.comp_pstart, count + 1, nullptr, w.scan_ws, s));
   FillArgs a;
+  memset(&a, 0, sizeof(a));
+  static long long* trace_buf = nullptr;
+  if (getenv("NI_FILL_TRACE")) {  // debug: per-iteration timeline
+    if (!trace_buf) NI_CUDA_TRY(cudaMalloc(&trace_buf, sizeof(long long) * 2 * 65536));
+    NI_CUDA_TRY(cudaMemsetAsync(trace_buf, 0, sizeof(long long) * 2 * 65536, s));
+    a.trace = trace_buf;
+    a.trace_len = 65536;
+  }
   a.rows = rows;
   a.W = W;
-  a.x = w.x;
-  a.r[0] = w.r0;
-  a.r[1] = w.r1;
-  a.q[0] = w.q0;
-  a.q[1] = w.q1;
-  a.p[0] = w.p0;
-  a.p[1] = w.p1;
+  a.P = P;
+  a.v[0] = w.v0;
+  a.v[1] = w.v1;
   a.hw = w.hw;
   a.imask = w.imask;
-  a.labels = labels;
+  a.lab = w.lab_p;
   a.items = w.items;
   a.nitems = NIt;
   a.comp_pstart = w.comp_pstart;
@@ -907,6 +955,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.partial = w.partial;
   a.active_items = w.active_items;
   a.nactive_items = w.nactive_items;
+  a.ticket = w.ticket;
   a.rho = w.rho;
   a.alpha = w.alpha;
   a.beta = w.beta;
@@ -915,11 +964,13 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.cap = w.cap;
   a.status = w.status;
   a.final_status = w.final_status;
+  a.xbuf = w.xbuf;
   a.active = w.active;
   a.changed = w.changed;
   if (count > 0) {
-    NI_COUNT_LAUNCH(), init_state_kernel<<<div_up(count, 256), 256, 0, s>>>(a, w.comp_size, count,
-                                                                           cg_max_iters);
+    NI_COUNT_LAUNCH(), init_state_kernel<<<div_up(count, 256), 256, 0, s>>>(
+                           w.status, w.final_status, w.xbuf, w.iters, w.cap, w.rho, w.comp_size,
+                           count, cg_max_iters);
     NI_LAUNCH_CHECK();
   }
   if (NIt > 0) {
@@ -928,17 +979,14 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   }
   // ---- the whole CG: one persistent cooperative launch
   {
-    // occupancy variant (experiments): NI_FILL_MINB = CTAs/SM the register
-    // budget is sized for (2: 128 regs, 3: 80, 4: 64)
+    // register budget variant (NI_FILL_MINB = CTAs/SM it is sized for)
     const char* mb = getenv("NI_FILL_MINB");
-    const int minb = mb ? atoi(mb) : 3;
+    const int minb = mb ? atoi(mb) : 2;
     void* kfn;
     if (connectivity == 8)
-      kfn = minb == 2 ? (void*)fill_cg_kernel<8, 2>
-                      : (minb == 4 ? (void*)fill_cg_kernel<8, 4> : (void*)fill_cg_kernel<8, 3>);
+      kfn = minb == 3 ? (void*)fill_cg_kernel<8, 3> : (void*)fill_cg_kernel<8, 2>;
     else
-      kfn = minb == 2 ? (void*)fill_cg_kernel<4, 2>
-                      : (minb == 4 ? (void*)fill_cg_kernel<4, 4> : (void*)fill_cg_kernel<4, 3>);
+      kfn = minb == 3 ? (void*)fill_cg_kernel<4, 3> : (void*)fill_cg_kernel<4, 2>;
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -957,16 +1005,17 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     NI_CUDA_TRY(cudaEventRecord(e1, s));
     g_fill_report.grid = G;
     g_fill_report.ntiles = NIt;
-    g_fill_report.npartials = P;
+    g_fill_report.npartials = NP;
     NI_CUDA_TRY(cudaMemsetAsync(w.px_iters, 0, sizeof(unsigned long long), s));
     NI_CUDA_TRY(cudaMemsetAsync(w.max_iters, 0, sizeof(int32_t), s));
     if (count > 0) {
       NI_COUNT_LAUNCH(), status_out_kernel<<<div_up(count, 256), 256, 0, s>>>(
-                             a, count, w.comp_size, comp_iters, comp_status, w.px_iters,
-                             w.max_iters);
+                             w.status, w.iters, count, w.comp_size, comp_iters, comp_status,
+                             w.px_iters, w.max_iters);
       NI_LAUNCH_CHECK();
     }
-    NI_COUNT_LAUNCH(), output_kernel<<<blocks, 256, 0, s>>>(w.x, labels, w.comp_size, npix, z_out);
+    NI_COUNT_LAUNCH(), output_kernel<<<blocks, 256, 0, s>>>(w.v0, w.v1, labels, w.comp_size,
+                                                           w.xbuf, W, P, npix, z_out);
     NI_LAUNCH_CHECK();
     unsigned long long pxi = 0;
     int32_t mxi = 0;
@@ -980,6 +1029,16 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     g_fill_report.max_iters = mxi;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (a.trace) {  // debug trace dump (NI_FILL_TRACE=path)
+      static long long host[2 * 65536];
+      NI_CUDA_TRY(cudaMemcpy(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost));
+      FILE* f = fopen(getenv("NI_FILL_TRACE"), "w");
+      if (f) {
+        for (int k = 0; k < 65536 && host[2 * k]; ++k)
+          fprintf(f, "%lld %lld\n", host[2 * k], host[2 * k + 1]);
+        fclose(f);
+      }
+    }
   }
   return NI_OK;
 }
