@@ -78,7 +78,7 @@ constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 constexpr int RING = 6;   // raw row ring (row L+4 is loaded at centre row L)
 constexpr int XM = 16;    // left margin (columns)
 constexpr int RM = 2;     // top margin (rows)
-constexpr int RB = 8;     // bottom margin (rows)
+constexpr int RB = 34;    // bottom margin (rows): every item streams 32 rows
 
 enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3, ST_FLUSH = 4 };
 
@@ -386,13 +386,56 @@ __device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, Co
   return any;
 }
 
-// Raw values of one row for this lane (prefetch ring).
-struct Raw {
-  float4 v;      // r, q, p, x (previous iteration)
-  float h;
-  uint32_t m;    // imask
-  int32_t lab;   // label (mixed items only)
+// ---- the per-warp row stream (cp.async into a shared-memory ring)
+//
+// Every item is a stream of 32 rows (local rows 0..31 = real rows y0-1 ..
+// y0+30) of its 32 columns (real x0-1 .. x0+30).  A warp's items follow each
+// other in one continuous stream; row s of the stream lives in ring slot
+// s % NS and is copied NS-2 rows ahead of its use, so the next item's first
+// rows are in flight while the current item finishes.  Copies are
+// cp.async (LDGSTS): no registers are held by in-flight loads.
+constexpr int NS = 8;     // ring slots per warp
+constexpr int IROWS = 32;  // stream rows per item
+
+struct RowSlot {
+  float4 v[32];      // r, q, p, x of lanes 0..31
+  float h[36];       // hw window from the 16-B aligned column at or before lane 0
+  int32_t lab[36];   // labels (mixed items), same window
+  uint8_t m[48];     // imask window from the 16-B aligned column at or before lane 0
 };
+constexpr size_t kSmemPerWarp = sizeof(RowSlot) * NS;
+constexpr size_t kSmemBytes = kSmemPerWarp * WPB;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issue the copies of local row `j` of item `it` into `slot` (one commit
+// group per row, possibly empty, in every lane).
+__device__ __forceinline__ void issue_row(const FillArgs& a, const float4* __restrict__ vin,
+                                          const Item* it, int j, RowSlot& slot) {
+  const int lane = threadIdx.x & 31;
+  if (it) {
+    const int c0 = it->x0 - 1 + XM;                      // padded column of lane 0
+    const int64_t rowo = int64_t(it->y0 - 1 + j + RM) * a.P;
+    cp_async16(&slot.v[lane], vin + rowo + c0 + lane);
+    const int ah = c0 & ~3;  // 16-B aligned float window
+    if (lane < 9) cp_async16(&slot.h[4 * lane], a.hw + rowo + ah + 4 * lane);
+    if (!item_pure(*it) && lane < 9) cp_async16(&slot.lab[4 * lane], a.lab + rowo + ah + 4 * lane);
+    const int am = c0 & ~15;  // 16-B aligned byte window
+    if (lane < 3) cp_async16(&slot.m[16 * lane], a.imask + rowo + am + 16 * lane);
+  }
+  cp_commit();
+}
 
 // A row of the compute ring: r_k, p_k = r_k + beta p_{k-1}, x_k formed with
 // the pixel's own component (only intra-component neighbours are ever read,
@@ -404,29 +447,15 @@ struct Row {
 };
 
 template <bool PURE>
-__device__ __forceinline__ Raw load_raw(const FillArgs& a, const float4* __restrict__ vin,
-                                        int64_t o, bool row_ok) {
-  Raw w;
-  if (row_ok) {
-    w.v = __ldcg(vin + o);
-    w.h = __ldg(a.hw + o);
-    w.m = __ldg(a.imask + o);
-    w.lab = PURE ? 0 : __ldg(a.lab + o);
-  } else {
-    w.v = make_float4(0.f, 0.f, 0.f, 0.f);
-    w.h = 0.f;
-    w.m = 0;
-    w.lab = -1;
-  }
-  return w;
-}
-
-template <bool PURE>
-__device__ __forceinline__ Row derive(const Raw& w, const Item& it, const Coefs& k) {
+__device__ __forceinline__ Row derive(const RowSlot& sl, const Item& it, const Coefs& k) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = it.x0 - 1 + XM;
+  const int dh = c0 & 3, dm = c0 & 15;
+  const float4 v = sl.v[lane];
   float al = k.al[0], be = k.be[0];
   int s = 0;
   if (!PURE) {
-    s = slot_of(it, w.lab);
+    s = slot_of(it, sl.lab[dh + lane]);
     al = 0.f;
     be = 0.f;
 #pragma unroll
@@ -437,11 +466,11 @@ __device__ __forceinline__ Row derive(const Raw& w, const Item& it, const Coefs&
       }
   }
   Row o;
-  o.rn = fmaf(-al, w.v.y, w.v.x);
-  o.pn = fmaf(be, w.v.z, o.rn);
-  o.xn = fmaf(al, w.v.z, w.v.w);
-  o.h = w.h;
-  o.m = w.m | (uint32_t(s + 1) << 8);
+  o.rn = fmaf(-al, v.y, v.x);
+  o.pn = fmaf(be, v.z, o.rn);
+  o.xn = fmaf(al, v.z, v.w);
+  o.h = sl.h[dh + lane];
+  o.m = uint32_t(sl.m[dm + lane]) | (uint32_t(s + 1) << 8);
   o.pl = __shfl_up_sync(0xffffffffu, o.pn, 1);
   o.pr = __shfl_down_sync(0xffffffffu, o.pn, 1);
   o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
@@ -449,10 +478,17 @@ __device__ __forceinline__ Row derive(const Raw& w, const Item& it, const Coefs&
   return o;
 }
 
-// One CG sweep over one item (see the header).
+struct Stream {
+  RowSlot* ring;  // NS slots of this warp
+  uint32_t pos;   // stream row of the current item's local row 0
+};
+
+// One CG sweep over one item (see the header).  On entry the stream holds
+// this item's rows 0..NS-3 (issued); `nxt` is the following item (or null)
+// whose first rows are issued as this item's rows run out.
 template <int CONN, bool PURE>
-__device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, const Coefs& k,
-                                           int par) {
+__device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const Item& it,
+                                           const Coefs& k, int par, const Item* nxt) {
   const int lane = threadIdx.x & 31;
   const int xr = it.x0 - 1 + lane;  // real column of this lane
   const bool center_lane = lane >= 1 && lane <= SW && xr < a.W;
@@ -464,24 +500,32 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, co
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
   const int nrows = min(SH, a.rows - it.y0);  // centre rows (local rows 1..nrows)
-  const int lastrow = nrows + 1;              // last local row the stencil reads
-  // padded index of local row 0 (= real row y0 - 1), this lane's column
   const int64_t o0 = int64_t(it.y0 - 1 + RM) * a.P + (xr + XM);
   const int64_t P = a.P;
-  Raw raw[RING];
+  // top up: rows NS-2 and NS-1... so that rows 0..NS-2 are issued here
+  // (the previous item issued this item's rows 0..NS-4)
+  auto issue_local = [&](int j) {  // local row j of this item or of the next
+    const uint32_t sp = st.pos + j;
+    if (j < IROWS) issue_row(a, vin, &it, j, st.ring[sp % NS]);
+    else issue_row(a, vin, nxt, j - IROWS, st.ring[sp % NS]);
+  };
+  issue_local(NS - 3);
+  issue_local(NS - 2);
+  // rows 0 and 1 are complete once at most NS-3 younger groups are pending
+  cp_wait<NS - 3>();
+  __syncwarp();
   Row der[3];
+  der[0] = derive<PURE>(st.ring[(st.pos + 0) % NS], it, k);
+  der[1] = derive<PURE>(st.ring[(st.pos + 1) % NS], it, k);
+  for (int g = 0; g < SH; g += 3) {
 #pragma unroll
-  for (int j = 0; j < RING - 1; ++j) raw[j] = load_raw<PURE>(a, vin, o0 + j * P, j <= lastrow);
-  der[0] = derive<PURE>(raw[0], it, k);
-  der[1] = derive<PURE>(raw[1], it, k);
-  for (int g = 0; g < SH; g += RING) {
-#pragma unroll
-    for (int u = 0; u < RING; ++u) {
-      const int L = g + u + 1;      // centre local row
-      const int ln = L + RING - 2;  // row to prefetch
-      raw[(u + RING - 1) % RING] =
-          load_raw<PURE>(a, vin, o0 + int64_t(ln) * P, ln <= lastrow);
-      der[(u + 2) % 3] = derive<PURE>(raw[(u + 2) % RING], it, k);
+    for (int u = 0; u < 3; ++u) {
+      const int L = g + u + 1;  // centre local row
+      // keep NS-2 rows ahead: row L+NS-2 (of this item or the next)
+      issue_local(L + NS - 2);
+      cp_wait<NS - 3>();  // row L+1 has landed
+      __syncwarp();
+      der[(u + 2) % 3] = derive<PURE>(st.ring[(st.pos + L + 1) % NS], it, k);
       const Row& U = der[u % 3];
       const Row& C = der[(u + 1) % 3];
       const Row& D = der[(u + 2) % 3];
@@ -507,17 +551,17 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, co
       }
 #undef NI_E
       const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
-      uint8_t st = ST_IDLE;
+      uint8_t stt = ST_IDLE;
       if (PURE) {
-        st = k.st[0];
+        stt = k.st[0];
       } else {
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j)
-          if (j == s) st = k.st[j];
+          if (j == s) stt = k.st[j];
       }
-      if (center_lane && (m & 0xFFu) != 0 && (st == ST_ACTIVE || st == ST_FLUSH)) {
+      if (center_lane && (m & 0xFFu) != 0 && (stt == ST_ACTIVE || stt == ST_FLUSH)) {
         vout[o0 + int64_t(L) * P] = make_float4(C.rn, q, pa, C.xn);
-        if (st == ST_ACTIVE) {
+        if (stt == ST_ACTIVE) {
           const double dp = pa, dq = q, dr = C.rn;
 #pragma unroll
           for (int j = 0; j < SLOTS; ++j)
@@ -531,6 +575,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const Item& it, co
       }
     }
   }
+  st.pos += IROWS;
   bool live[SLOTS];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j) live[j] = k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
@@ -632,19 +677,36 @@ __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
       a.trace[2 * it] = t;
       a.trace[2 * it + 1] = n;
     }
-    // dynamic item scheduling: the next ticket is drawn before the current
-    // item is processed so its latency is hidden
+    // dynamic item scheduling: tickets are drawn one item ahead; the row
+    // stream runs straight from one item into the next
+    extern __shared__ __align__(16) unsigned char smem[];
+    Stream st;
+    st.ring = reinterpret_cast<RowSlot*>(smem + kSmemPerWarp * (threadIdx.x >> 5));
+    st.pos = 0;
     int k = draw_ticket(a, par);
-    while (k < n) {
-      const int nk = draw_ticket(a, par);
-      const Item item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
-      Coefs kc;
-      if (item_coefs(a, item, kc)) {
-        if (item_pure(item)) sweep_item<CONN, true>(a, item, kc, par);
-        else sweep_item<CONN, false>(a, item, kc, par);
-      }
-      k = nk;
+    Item item, nitem;
+    Coefs kc, kn;
+    bool has = k < n;
+    if (has) {
+      item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
+      item_coefs(a, item, kc);
+      for (int j = 0; j < NS - 3; ++j)
+        issue_row(a, a.v[par], &item, j, st.ring[j % NS]);
     }
+    while (has) {
+      const int nk = draw_ticket(a, par);
+      const bool has_next = nk < n;
+      if (has_next) {
+        nitem = a.items[__ldcg(a.active_items + cur * a.nitems + nk)];
+        item_coefs(a, nitem, kn);
+      }
+      if (item_pure(item)) sweep_item<CONN, true>(a, st, item, kc, par, has_next ? &nitem : nullptr);
+      else sweep_item<CONN, false>(a, st, item, kc, par, has_next ? &nitem : nullptr);
+      item = nitem;
+      kc = kn;
+      has = has_next;
+    }
+    cp_wait<0>();
     grid.sync();
     if (__ldcg(a.changed)) {
       const int nxt = cur ^ 1;
@@ -990,7 +1052,9 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, 0));
+    NI_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kSmemBytes)));
+    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, kSmemBytes));
     int G = per_sm * sms;
     const int need = div_up(NIt > 0 ? NIt : 1, WPB);
     if (G > need) G = need;
@@ -1001,7 +1065,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     NI_CUDA_TRY(cudaEventCreate(&e1));
     NI_CUDA_TRY(cudaEventRecord(e0, s));
     NI_COUNT_LAUNCH();
-    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT), args, 0, s));
+    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT), args, kSmemBytes, s));
     NI_CUDA_TRY(cudaEventRecord(e1, s));
     g_fill_report.grid = G;
     g_fill_report.ntiles = NIt;
