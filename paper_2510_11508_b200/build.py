@@ -55,19 +55,23 @@ def up_to_date() -> bool:
     return os.path.getmtime(OUT) >= _newest(sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build the library; ``defines``/``out`` build an experiment variant elsewhere."""
+    if out is None and not defines and not force and up_to_date():
         return OUT
-    os.makedirs(OBJ, exist_ok=True)
+    variant = bool(defines) or out is not None
+    objdir = OBJ + ("_" + "_".join(d.replace("=", "") for d in defines) if defines else "")
+    out = out or OUT
+    os.makedirs(objdir, exist_ok=True)
     cc = nvcc()
     hdr_time = _newest(headers() + [__file__])
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-        if (not force and os.path.exists(obj)
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if (not force and not variant and os.path.exists(obj)
                 and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_time)):
             return obj
-        cmd = [cc, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [cc, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -79,21 +83,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[],
+                    help="extra preprocessor define (experiment variants; needs --out)")
+    ap.add_argument("--out", default=None, help="output path for a variant build")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, tuple(a.defines), a.out))
 
 
 if __name__ == "__main__":

@@ -161,4 +161,35 @@ size_t scan_ws_bytes(int64_t n);
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* total_dev, void* ws,
                        cudaStream_t s);
 
+// Lock-free union-find over int32 parents: parent[x] <= x, roots hooked
+// under the smaller id (so a flattened root is the smallest member).
+__device__ __forceinline__ int uf_find(volatile int32_t* parent, int32_t x) {
+  int32_t p = parent[x];
+  while (p != x) {
+    x = p;
+    p = parent[x];
+  }
+  return x;
+}
+
+// Union by hooking the larger root under the smaller one (atomicMin), retried
+// until both endpoints share a root.  parent[x] <= x always holds.
+__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
+  volatile int32_t* vp = parent;
+  while (true) {
+    a = uf_find(vp, a);
+    b = uf_find(vp, b);
+    if (a == b) return;
+    if (a < b) {
+      int32_t t = a;
+      a = b;
+      b = t;
+    }
+    // a > b: try to hook root a under b
+    int32_t old = atomicMin(parent + a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
 }  // namespace ni

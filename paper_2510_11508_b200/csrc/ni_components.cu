@@ -72,35 +72,6 @@ __global__ void __launch_bounds__(256) normalize_kernel(const T* __restrict__ in
 
 // ------------------------------------------------------------------ K1
 
-__device__ __forceinline__ int uf_find(volatile int32_t* parent, int32_t x) {
-  int32_t p = parent[x];
-  while (p != x) {
-    x = p;
-    p = parent[x];
-  }
-  return x;
-}
-
-// Union by hooking the larger root under the smaller one (atomicMin), retried
-// until both endpoints share a root.  parent[x] <= x always holds.
-__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
-  volatile int32_t* vp = parent;
-  while (true) {
-    a = uf_find(vp, a);
-    b = uf_find(vp, b);
-    if (a == b) return;
-    if (a < b) {
-      int32_t t = a;
-      a = b;
-      b = t;
-    }
-    // a > b: try to hook root a under b
-    int32_t old = atomicMin(parent + a, b);
-    if (old == a) return;
-    a = old;
-  }
-}
-
 __global__ void uf_init_kernel(const uint8_t* __restrict__ valid, int64_t npix,
                                int32_t* __restrict__ parent) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;

@@ -75,7 +75,6 @@ constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
-constexpr int RING = 6;   // raw row ring (row L+4 is loaded at centre row L)
 constexpr int XM = 16;    // left margin (columns)
 constexpr int RM = 2;     // top margin (rows)
 constexpr int RB = 34;    // bottom margin (rows): every item streams 32 rows
@@ -88,16 +87,16 @@ struct __align__(16) Item {
   int32_t pbase;   // first partial slot of this item
   int32_t flags;   // bits 0-7: components in the item (1..2); bit 8: pure strip
   int32_t comp[SLOTS];
-  int32_t pad[2];
+  int32_t y1;  // end row of the strip (strips never straddle two maps)
+  int32_t pad;
 };
 
 __device__ __forceinline__ int item_n(const Item& it) { return it.flags & 0xFF; }
 __device__ __forceinline__ bool item_pure(const Item& it) { return (it.flags >> 8) & 1; }
+__device__ __forceinline__ int item_n_flags(int32_t flags) { return flags & 0xFF; }
 
 struct FillArgs {
   int rows, W, P;
-  long long* trace;  // optional: per iteration (globaltimer, active items)
-  int trace_len;
   float4* v[2];
   const float* hw;
   const uint8_t* imask;
@@ -109,9 +108,21 @@ struct FillArgs {
   const int32_t* comp_plist;   // [P] partial indices grouped by component
   int32_t* comp_cnt;           // [C] arrival counters (zero between sweeps)
   double* partial;             // [P][NDOT]
-  int32_t* active_items;       // [2][nitems]
-  int32_t* nactive_items;      // [2]
-  int32_t* ticket;             // [2] dynamic item scheduling, by sweep parity
+  // dataflow schedule: components sharing an item form a "group" that
+  // iterates in lockstep; groups advance independently (see fill_cg_kernel)
+  int G;                       // groups
+  const int32_t* cgrp;         // [C] group of a component
+  const int32_t* gstart;       // [G+1] region of a group in active_items
+  int32_t* active_items;       // [nitems] per-group lists of live items
+  int32_t* gcnt;               // [G] live items of the group
+  unsigned long long* gtk;     // [G] open batch: parity << 63 | n << 32 | next ticket
+  int32_t* gdone;              // [G] items finished in the open batch
+  int32_t* gchg;               // [G] a component of the group reached its final state
+  unsigned long long* ring;    // [R] published batches: seq << 32 | group
+  uint32_t R;                  // ring capacity (power of two)
+  uint32_t* ring_tail;
+  uint32_t* ring_hint;         // every ring entry below it is exhausted
+  int32_t* gactive;            // groups with live items
   // component state
   double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
   double* alpha;   // alpha of the last completed sweep
@@ -122,8 +133,6 @@ struct FillArgs {
   uint8_t* status;
   uint8_t* final_status;  // status after the flush sweep
   uint8_t* xbuf;          // buffer holding the component's final x
-  int32_t* active;        // components still ACTIVE or FLUSH
-  int32_t* changed;       // a component changed state during the last sweep
 };
 
 // ----------------------------------------------------------------- setup
@@ -185,21 +194,32 @@ __global__ void __launch_bounds__(256) prep_kernel(
   }
 }
 
+// Strip s of the grid: nsx strips across, nsym per map (the last one of a
+// map may be short), map-major.
+__device__ __forceinline__ void strip_rect(int s, int nsx, int nsym, int H, int& x0, int& y0,
+                                           int& y1) {
+  const int r = s / nsx, m = r / nsym;
+  x0 = (s % nsx) * SW;
+  y0 = m * H + (r % nsym) * SH;
+  y1 = min(y0 + SH, (m + 1) * H);
+}
+
 // One CTA per strip: its distinct multi-pixel components, ascending.
 __global__ void __launch_bounds__(NT) strip_comps_kernel(const int32_t* __restrict__ labels,
                                                          const int32_t* __restrict__ comp_size,
-                                                         int rows, int W, int nsx,
+                                                         int H, int W, int nsx, int nsym,
                                                          int32_t* __restrict__ nslots,
                                                          int32_t* __restrict__ strip_comps) {
   __shared__ int32_t key[SPX];
   __shared__ int32_t wcount[WPB];
   const int strip = blockIdx.x, tid = threadIdx.x;
-  const int x0 = (strip % nsx) * SW, y0 = (strip / nsx) * SH;
+  int x0, y0, y1;
+  strip_rect(strip, nsx, nsym, H, x0, y0, y1);
   for (int e = tid; e < SPX; e += NT) {
     int32_t lab = -1;
     if (e < SW * SH) {
       const int gx = x0 + (e % SW), gy = y0 + (e / SW);
-      if (gx < W && gy < rows) {
+      if (gx < W && gy < y1) {
         lab = labels[int64_t(gy) * W + gx];
         if (lab >= 0 && comp_size[lab] < 2) lab = -1;  // singletons never iterate (solver.py:220)
       }
@@ -251,7 +271,7 @@ __global__ void __launch_bounds__(NT) strip_comps_kernel(const int32_t* __restri
 __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
                                    const int32_t* __restrict__ slot_base,
                                    const int32_t* __restrict__ item_base,
-                                   const int32_t* __restrict__ strip_comps, int nstrips, int nsx,
+                                   const int32_t* __restrict__ strip_comps, int nstrips, int nsx, int nsym, int H,
                                    Item* __restrict__ items, int32_t* __restrict__ partial_comp,
                                    int32_t* __restrict__ partial_idx,
                                    int32_t* __restrict__ comp_nparts) {
@@ -261,15 +281,14 @@ __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
     const int pb = slot_base[s], ib = item_base[s];
     for (int k = 0; k * SLOTS < ns; ++k) {
       Item it;
-      it.x0 = (s % nsx) * SW;
-      it.y0 = (s / nsx) * SH;
+      strip_rect(s, nsx, nsym, H, it.x0, it.y0, it.y1);
       it.pbase = pb + k * SLOTS;
       const int n = min(SLOTS, ns - k * SLOTS);
       it.flags = n | ((ns == 1 ? 1 : 0) << 8);
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
         it.comp[j] = j < n ? strip_comps[int64_t(s) * SPX + k * SLOTS + j] : -1;
-      it.pad[0] = it.pad[1] = 0;
+      it.pad = 0;
       items[ib + k] = it;
     }
     for (int j = 0; j < ns; ++j) {
@@ -301,7 +320,7 @@ __device__ __forceinline__ int slot_of(const Item& it, int32_t lab) {
 // Write the item's per-component partials (NDOT each), count arrivals, and
 // let the last arriving warp of a component reduce its partials in plan
 // order and call fin(c, dots).
-template <class Fin>
+template <int NSUM = SLOTS, class Fin>
 __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
                                             double (&acc)[SLOTS][NDOT], const bool* live, Fin fin) {
   const int lane = threadIdx.x & 31;
@@ -310,7 +329,7 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
 #pragma unroll
-    for (int d = 0; d < NDOT; ++d) tot[s][d] = warp_sum(acc[s][d]);
+    for (int d = 0; d < NDOT; ++d) tot[s][d] = s < NSUM ? warp_sum(acc[s][d]) : 0.0;
   unsigned last = 0;
   if (lane < n) {
     int32_t c = it.comp[0];
@@ -361,57 +380,51 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
   }
 }
 
-// Per-slot coefficients of the item for this sweep.
-struct Coefs {
-  float al[SLOTS], be[SLOTS];
-  uint8_t st[SLOTS];
-};
-
-__device__ __forceinline__ bool item_coefs(const FillArgs& a, const Item& it, Coefs& k) {
-  bool any = false;
-  const int n = item_n(it);
-#pragma unroll
-  for (int j = 0; j < SLOTS; ++j) {
-    k.al[j] = 0.f;
-    k.be[j] = 0.f;
-    k.st[j] = ST_IDLE;
-    if (j < n) {
-      const int32_t c = it.comp[j];
-      k.st[j] = __ldcg(a.status + c);
-      k.al[j] = float(__ldcg(a.alpha + c));
-      k.be[j] = float(__ldcg(a.beta + c));
-      any |= k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
-    }
-  }
-  return any;
-}
-
 // ---- the per-warp row stream (cp.async into a shared-memory ring)
 //
 // Every item is a stream of 32 rows (local rows 0..31 = real rows y0-1 ..
 // y0+30) of its 32 columns (real x0-1 .. x0+30).  A warp's items follow each
-// other in one continuous stream; row s of the stream lives in ring slot
-// s % NS and is copied NS-2 rows ahead of its use, so the next item's first
-// rows are in flight while the current item finishes.  Copies are
-// cp.async (LDGSTS): no registers are held by in-flight loads.
-constexpr int NS = 8;     // ring slots per warp
+// other in one continuous stream; local row j lives in ring slot j % NS
+// (IROWS is a multiple of NS) and is copied LA rows ahead of its use, so the
+// next item's first rows are in flight while the current item finishes.
+// Copies are cp.async (LDGSTS): in-flight rows hold no registers.  Per row
+// every lane copies 16 B of {r,q,p,x}; lanes 0-8 copy the hw window, lanes
+// 9-17 the label window (mixed items only), lanes 18-20 the imask window.
+#ifndef NI_NS
+#define NI_NS 8
+#endif
+constexpr int NS = NI_NS;  // ring slots per warp
 constexpr int IROWS = 32;  // stream rows per item
+constexpr int GR = 2;      // centre rows computed per step (between two waits)
+constexpr int LA = NS - GR;  // rows in flight beyond the ones being derived
+static_assert((NS & (NS - 1)) == 0 && IROWS % NS == 0, "ring slots must tile an item");
+static_assert(SH % GR == 0 && (IROWS - 2 - LA) % GR == 0, "row steps must align");
+static_assert(LA >= 2, "ring too small");
 
-struct RowSlot {
-  float4 v[32];      // r, q, p, x of lanes 0..31
-  float h[36];       // hw window from the 16-B aligned column at or before lane 0
-  int32_t lab[36];   // labels (mixed items), same window
-  uint8_t m[48];     // imask window from the 16-B aligned column at or before lane 0
+// ring slot layout (bytes): {r,q,p,x}[32] | hw[36] | labels[36] | imask[48]
+constexpr int SL_V = 0, SL_H = 512, SL_LAB = 656, SL_M = 800, SLOT_BYTES = 848;
+
+// A claimed item with its coefficients; the next item's lives in shared
+// memory (one per warp) so it holds no registers while the current item runs.
+struct Claim {
+  Item item;
+  float al[SLOTS], be[SLOTS];
+  int32_t g, par, n, live;  // live: bit j = slot j is ACTIVE or FLUSH
+  uint8_t st[SLOTS];
 };
-constexpr size_t kSmemPerWarp = sizeof(RowSlot) * NS;
+constexpr size_t kRingBytes = size_t(SLOT_BYTES) * NS;
+constexpr size_t kSmemPerWarp = (kRingBytes + sizeof(Claim) + 15) & ~size_t(15);
 constexpr size_t kSmemBytes = kSmemPerWarp * WPB;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
+__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool on) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+      " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(dst),
+      "l"(src), "r"(int(on))
+      : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -419,22 +432,51 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Issue the copies of local row `j` of item `it` into `slot` (one commit
-// group per row, possibly empty, in every lane).
-__device__ __forceinline__ void issue_row(const FillArgs& a, const float4* __restrict__ vin,
-                                          const Item* it, int j, RowSlot& slot) {
+// The copy side of a warp's row stream (per-lane source pointers).
+struct Issuer {
+  const char* v;    // this lane's 16 B of {r,q,p,x} in the next row
+  const char* aux;  // this lane's 16 B of hw / labels / imask in the next row
+  uint32_t apitch;  // aux row pitch in bytes
+  uint32_t adst;    // aux destination offset in a slot
+  bool on, aon;     // off: past the last item / lane copies no aux bytes
+};
+
+__device__ __forceinline__ void issuer_start(const FillArgs& a, const Item& it, int par,
+                                             Issuer& is) {
   const int lane = threadIdx.x & 31;
-  if (it) {
-    const int c0 = it->x0 - 1 + XM;                      // padded column of lane 0
-    const int64_t rowo = int64_t(it->y0 - 1 + j + RM) * a.P;
-    cp_async16(&slot.v[lane], vin + rowo + c0 + lane);
-    const int ah = c0 & ~3;  // 16-B aligned float window
-    if (lane < 9) cp_async16(&slot.h[4 * lane], a.hw + rowo + ah + 4 * lane);
-    if (!item_pure(*it) && lane < 9) cp_async16(&slot.lab[4 * lane], a.lab + rowo + ah + 4 * lane);
-    const int am = c0 & ~15;  // 16-B aligned byte window
-    if (lane < 3) cp_async16(&slot.m[16 * lane], a.imask + rowo + am + 16 * lane);
+  const int c0 = it.x0 - 1 + XM;  // padded column of lane 0
+  const int64_t row0 = int64_t(it.y0 - 1 + RM) * a.P;
+  const int ah = c0 & ~3, am = c0 & ~15;  // 16-B aligned windows
+  is.v = reinterpret_cast<const char*>(a.v[par] + row0 + c0 + lane);
+  is.on = true;
+  if (lane < 9) {
+    is.aux = reinterpret_cast<const char*>(a.hw + row0 + ah + 4 * lane);
+    is.apitch = 4u * a.P;
+    is.adst = SL_H + 16 * lane;
+    is.aon = true;
+  } else if (lane < 18) {
+    is.aux = reinterpret_cast<const char*>(a.lab + row0 + ah + 4 * (lane - 9));
+    is.apitch = 4u * a.P;
+    is.adst = SL_LAB + 16 * (lane - 9);
+    is.aon = !item_pure(it);
+  } else {
+    is.aux = reinterpret_cast<const char*>(a.imask + row0 + am + 16 * (lane - 18));
+    is.apitch = a.P;
+    is.adst = SL_M + 16 * (lane - 18);
+    is.aon = lane < 21;
   }
+}
+
+// Copy the issuer's next row into ring slot `j % NS` (one commit group per
+// row in every lane, empty once the stream is off).
+__device__ __forceinline__ void issue_row(uint32_t ring, int j, Issuer& is, uint32_t vpitch) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t slot = ring + uint32_t(j & (NS - 1)) * SLOT_BYTES;
+  cp_async16_if(slot + SL_V + 16 * lane, is.v, is.on);
+  cp_async16_if(slot + is.adst, is.aux, is.on && is.aon);
   cp_commit();
+  is.v += vpitch;
+  is.aux += is.apitch;
 }
 
 // A row of the compute ring: r_k, p_k = r_k + beta p_{k-1}, x_k formed with
@@ -446,31 +488,48 @@ struct Row {
   uint32_t m;  // imask | (slot + 1) << 8
 };
 
+struct Cur {  // the current item, in registers
+  int32_t x0, y0, y1, flags, pbase, g, par, n, live;
+  int32_t comp[SLOTS];
+  float al[SLOTS], be[SLOTS];
+};
+
+__device__ __forceinline__ void load_cur(const Claim& c, Cur& k) {
+  k.x0 = c.item.x0;
+  k.y0 = c.item.y0;
+  k.y1 = c.item.y1;
+  k.flags = c.item.flags;
+  k.pbase = c.item.pbase;
+  k.g = c.g;
+  k.par = c.par;
+  k.n = c.n;
+  k.live = c.live;
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) {
+    k.comp[j] = c.item.comp[j];
+    k.al[j] = c.al[j];
+    k.be[j] = c.be[j];
+  }
+}
+
 template <bool PURE>
-__device__ __forceinline__ Row derive(const RowSlot& sl, const Item& it, const Coefs& k) {
-  const int lane = threadIdx.x & 31;
-  const int c0 = it.x0 - 1 + XM;
-  const int dh = c0 & 3, dm = c0 & 15;
-  const float4 v = sl.v[lane];
+__device__ __forceinline__ Row derive(const unsigned char* slot, int lane, int dh, int dm,
+                                      const Cur& k) {
+  const float4 v = *reinterpret_cast<const float4*>(slot + SL_V + 16 * lane);
   float al = k.al[0], be = k.be[0];
   int s = 0;
   if (!PURE) {
-    s = slot_of(it, sl.lab[dh + lane]);
-    al = 0.f;
-    be = 0.f;
-#pragma unroll
-    for (int j = 0; j < SLOTS; ++j)
-      if (j == s) {
-        al = k.al[j];
-        be = k.be[j];
-      }
+    const int32_t lab = *reinterpret_cast<const int32_t*>(slot + SL_LAB + 4 * (dh + lane));
+    s = lab == k.comp[0] ? 0 : (item_n_flags(k.flags) > 1 && lab == k.comp[1] ? 1 : -1);
+    al = s == 0 ? k.al[0] : (s == 1 ? k.al[1] : 0.f);
+    be = s == 0 ? k.be[0] : (s == 1 ? k.be[1] : 0.f);
   }
   Row o;
   o.rn = fmaf(-al, v.y, v.x);
   o.pn = fmaf(be, v.z, o.rn);
   o.xn = fmaf(al, v.z, v.w);
-  o.h = sl.h[dh + lane];
-  o.m = uint32_t(sl.m[dm + lane]) | (uint32_t(s + 1) << 8);
+  o.h = *reinterpret_cast<const float*>(slot + SL_H + 4 * (dh + lane));
+  o.m = uint32_t(slot[SL_M + dm + lane]) | (uint32_t(s + 1) << 8);
   o.pl = __shfl_up_sync(0xffffffffu, o.pn, 1);
   o.pr = __shfl_down_sync(0xffffffffu, o.pn, 1);
   o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
@@ -478,58 +537,250 @@ __device__ __forceinline__ Row derive(const RowSlot& sl, const Item& it, const C
   return o;
 }
 
-struct Stream {
-  RowSlot* ring;  // NS slots of this warp
-  uint32_t pos;   // stream row of the current item's local row 0
-};
+// ---- the batch scheduler
+//
+// A group's open batch is one 64-bit word: parity << 63 | n << 32 | ticket.
+// Claiming is one atomicAdd on it: a ticket t < n of the returned word is
+// item t of that batch, whatever ring entry led there.  Published batches
+// are announced in a ring (seq << 32 | group); warps probe 32 entries from
+// the hint at once and take the first open one, so batches drain in
+// publication order and the hint only passes exhausted entries.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Claim an item into c (shared memory); false when no batch is open.
+__device__ __noinline__ bool try_claim(const FillArgs& a, Claim* c) {
+  const int lane = threadIdx.x & 31;
+  uint32_t h = *reinterpret_cast<const volatile uint32_t*>(a.ring_hint);
+  for (int round = 0; round < 64; ++round) {
+    const uint32_t p = h + lane;
+    const unsigned long long e = ld_relaxed_u64(a.ring + (p & (a.R - 1)));
+    const uint32_t seq = uint32_t(e >> 32);
+    const bool pub = seq == p;
+    const bool stale = int32_t(seq - p) > 0;  // lapped: long exhausted
+    const int32_t g = int32_t(e & 0xffffffffu);
+    bool open = false;
+    if (pub) {
+      const unsigned long long w = __ldcg(a.gtk + g);
+      open = (w & 0xffffffffu) < ((w >> 32) & 0x7fffffffu);
+    }
+    const unsigned openm = __ballot_sync(0xffffffffu, open);
+    const unsigned donem = __ballot_sync(0xffffffffu, (pub && !open) || stale);
+    const int lead = __ffs(~donem) - 1;  // leading exhausted entries (-1: all 32)
+    const int k = lead < 0 ? 32 : lead;
+    if (lane == 0 && k > 0) atomicCAS(a.ring_hint, h, h + k);
+    if (openm) {
+      const int l = __ffs(openm) - 1;
+      const int32_t gg = __shfl_sync(0xffffffffu, g, l);
+      unsigned long long w = 0;
+      if (lane == 0) w = atomicAdd(a.gtk + gg, 1ull);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      const int32_t t = int32_t(w & 0xffffffffu), n = int32_t((w >> 32) & 0x7fffffffu);
+      if (t < n) {
+        // the batch's coefficients were published before its word
+        const int32_t k = __ldcg(a.active_items + __ldcg(a.gstart + gg) + t);
+        const Item it = a.items[k];
+        const int ni = item_n(it);
+        int live = 0;
+        float al[SLOTS], be[SLOTS];
+        uint8_t st[SLOTS];
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j) {
+          al[j] = 0.f;
+          be[j] = 0.f;
+          st[j] = ST_IDLE;
+          if (j < ni) {
+            const int32_t cc = it.comp[j];
+            st[j] = __ldcg(a.status + cc);
+            al[j] = float(__ldcg(a.alpha + cc));
+            be[j] = float(__ldcg(a.beta + cc));
+            if (st[j] == ST_ACTIVE || st[j] == ST_FLUSH) live |= 1 << j;
+          }
+        }
+        if (lane == 0) {
+          c->item = it;
+          c->g = gg;
+          c->par = int32_t(w >> 63);
+          c->n = n;
+          c->live = live;
+#pragma unroll
+          for (int j = 0; j < SLOTS; ++j) {
+            c->al[j] = al[j];
+            c->be[j] = be[j];
+            c->st[j] = st[j];
+          }
+        }
+        __syncwarp();
+        return true;
+      }
+      continue;  // lost the race for the last tickets: probe again
+    }
+    if (donem != 0xffffffffu) return false;  // reached the unpublished tail
+    h += 32;
+  }
+  return false;
+}
+
+// Announce group g's next batch (lane 0).
+__device__ __forceinline__ void publish(const FillArgs& a, int32_t g, int par, int32_t n) {
+  a.gdone[g] = 0;
+  __threadfence();
+  atomicExch(a.gtk + g, (static_cast<unsigned long long>(par) << 63) |
+                            (static_cast<unsigned long long>(n) << 32));
+  __threadfence();
+  const uint32_t p = atomicAdd(a.ring_tail, 1u);
+  const unsigned long long e = (static_cast<unsigned long long>(p) << 32) | uint32_t(g);
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.ring + (p & (a.R - 1))), "l"(e)
+               : "memory");
+}
+
+__device__ __forceinline__ bool item_live(const FillArgs& a, int32_t k) {
+  const Item it = a.items[k];
+  const int n = item_n(it);
+  bool act = false;
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j)
+    if (j < n) {
+      const uint8_t st = __ldcg(a.status + it.comp[j]);
+      if (st == ST_ACTIVE || st == ST_FLUSH) act = true;
+    }
+  return act;
+}
+
+// The warp that finishes a group's batch: drop items whose components are
+// all final (in-place stable compaction), then publish the next batch or
+// retire the group.
+__device__ __noinline__ void advance_group(const FillArgs& a, int32_t g, int par) {
+  const int lane = threadIdx.x & 31;
+  __threadfence();
+  int32_t n = __ldcg(a.gcnt + g);
+  if (__ldcg(a.gchg + g)) {
+    int32_t* list = a.active_items + __ldcg(a.gstart + g);
+    int32_t out = 0;
+    constexpr int U = 8;  // independent loads in flight per lane
+    for (int b = 0; b < n; b += 32 * U) {
+      int32_t kk[U];
+      bool keep[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = b + 32 * u + lane;
+        kk[u] = i < n ? __ldcg(list + i) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) keep[u] = kk[u] >= 0 && item_live(a, kk[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned m = __ballot_sync(0xffffffffu, keep[u]);
+        if (keep[u]) list[out + __popc(m & ((1u << lane) - 1))] = kk[u];
+        out += __popc(m);
+      }
+    }
+    n = out;
+    if (lane == 0) {
+      a.gcnt[g] = n;
+      a.gchg[g] = 0;
+    }
+  }
+  if (lane == 0) {
+    if (n > 0) publish(a, g, par ^ 1, n);
+    else atomicSub(a.gactive, 1);
+  }
+  __syncwarp();
+}
+
+// Per-component scalar update once all of its items reported (lane 0 of
+// the last arriving warp).
+__device__ __forceinline__ void finalize_component(const FillArgs& a, int32_t c, const double* d,
+                                                   int par) {
+  if (__ldcg(a.status + c) == ST_FLUSH) {  // the pending update is applied
+    a.status[c] = __ldcg(a.final_status + c);
+    a.xbuf[c] = uint8_t(par ^ 1);
+    a.gchg[a.cgrp[c]] = 1;
+    return;
+  }
+  const double pq = d[0], rq = d[1], qq = d[2], rr = d[3];
+  const int n = __ldcg(a.iters + c) + 1;  // updates once this sweep's alpha is applied
+  a.iters[c] = n;
+  a.rho[c] = rr;
+  double alpha = 0.0, rho1 = 0.0;
+  bool stop = false;
+  uint8_t fin = ST_CONVERGED;
+  if (pq > 0.0) {
+    alpha = rr / pq;
+    rho1 = rr - 2.0 * alpha * rq + alpha * alpha * qq;
+    if (rho1 < 0.0) rho1 = 0.0;
+    if (n < __ldcg(a.cap + c) && sqrt(rho1) < __ldcg(a.tol + c)) {
+      stop = true;  // scipy's top-of-loop test before iteration n
+    } else if (n >= __ldcg(a.cap + c)) {
+      stop = true;  // loop exhausted: info = maxiter
+      fin = ST_CAPPED;
+    }
+  } else {
+    stop = true;  // breakdown: p in the null space (only once r == 0)
+  }
+  a.alpha[c] = alpha;
+  if (stop) {
+    a.final_status[c] = fin;
+    a.status[c] = ST_FLUSH;
+  } else {
+    a.beta[c] = rho1 / rr;
+    a.rho[c] = rho1;
+  }
+}
 
 // One CG sweep over one item (see the header).  On entry the stream holds
-// this item's rows 0..NS-3 (issued); `nxt` is the following item (or null)
-// whose first rows are issued as this item's rows run out.
+// this item's rows 0..LA-1 (issued); as its last rows are issued the warp
+// claims its next item (into nx) and starts that item's rows.
 template <int CONN, bool PURE>
-__device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const Item& it,
-                                           const Coefs& k, int par, const Item* nxt) {
+__device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned char* ring,
+                                           Claim* nx, Issuer& is, const Cur& k, bool& has_next) {
   const int lane = threadIdx.x & 31;
-  const int xr = it.x0 - 1 + lane;  // real column of this lane
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t vpitch = 16u * a.P;
+  const int xr = k.x0 - 1 + lane;  // real column of this lane
   const bool center_lane = lane >= 1 && lane <= SW && xr < a.W;
-  const float4* __restrict__ vin = a.v[par];
-  float4* __restrict__ vout = a.v[par ^ 1];
+  const int c0 = k.x0 - 1 + XM;
+  const int dh = c0 & 3, dm = c0 & 15;
+  float4* __restrict__ out =
+      a.v[k.par ^ 1] + int64_t(k.y0 - 1 + RM) * a.P + (xr + XM);  // local row 0
+  const int nrows = k.y1 - k.y0;  // centre rows (local rows 1..nrows)
   double acc[SLOTS][NDOT];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j)
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
-  const int nrows = min(SH, a.rows - it.y0);  // centre rows (local rows 1..nrows)
-  const int64_t o0 = int64_t(it.y0 - 1 + RM) * a.P + (xr + XM);
-  const int64_t P = a.P;
-  // top up: rows NS-2 and NS-1... so that rows 0..NS-2 are issued here
-  // (the previous item issued this item's rows 0..NS-4)
-  auto issue_local = [&](int j) {  // local row j of this item or of the next
-    const uint32_t sp = st.pos + j;
-    if (j < IROWS) issue_row(a, vin, &it, j, st.ring[sp % NS]);
-    else issue_row(a, vin, nxt, j - IROWS, st.ring[sp % NS]);
-  };
-  issue_local(NS - 3);
-  issue_local(NS - 2);
-  // rows 0 and 1 are complete once at most NS-3 younger groups are pending
-  cp_wait<NS - 3>();
+  has_next = false;
+  // rows LA and LA+1; rows 0 and 1 have landed once at most LA younger
+  // row groups are pending
+  issue_row(ring_s, LA, is, vpitch);
+  issue_row(ring_s, LA + 1, is, vpitch);
+  cp_wait<LA>();
   __syncwarp();
-  Row der[3];
-  der[0] = derive<PURE>(st.ring[(st.pos + 0) % NS], it, k);
-  der[1] = derive<PURE>(st.ring[(st.pos + 1) % NS], it, k);
-  for (int g = 0; g < SH; g += 3) {
+  Row der[GR + 2];  // derived rows g .. g+GR+1 around the centre rows g+1 .. g+GR
+  der[0] = derive<PURE>(ring, lane, dh, dm, k);
+  der[1] = derive<PURE>(ring + SLOT_BYTES, lane, dh, dm, k);
+  for (int g = 0; g < SH; g += GR) {
+    if (g + 2 + LA == IROWS) {  // the stream moves on to the next item here
+      has_next = try_claim(a, nx);
+      if (has_next) issuer_start(a, nx->item, nx->par, is);
+      else is.on = false;
+    }
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
+    for (int u = 0; u < GR; ++u) issue_row(ring_s, g + 2 + LA + u, is, vpitch);
+    cp_wait<LA>();  // rows up to g+GR+1 have landed
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < GR; ++u)
+      der[2 + u] = derive<PURE>(ring + ((g + 2 + u) & (NS - 1)) * SLOT_BYTES, lane, dh, dm, k);
+#pragma unroll
+    for (int u = 0; u < GR; ++u) {
       const int L = g + u + 1;  // centre local row
-      // keep NS-2 rows ahead: row L+NS-2 (of this item or the next)
-      issue_local(L + NS - 2);
-      cp_wait<NS - 3>();  // row L+1 has landed
-      __syncwarp();
-      der[(u + 2) % 3] = derive<PURE>(st.ring[(st.pos + L + 1) % NS], it, k);
-      const Row& U = der[u % 3];
-      const Row& C = der[(u + 1) % 3];
-      const Row& D = der[(u + 2) % 3];
-      if (L > nrows) continue;
+      const Row& U = der[u];
+      const Row& C = der[u + 1];
+      const Row& D = der[u + 2];
       const float pa = C.pn, ha = C.h;
       const uint32_t m = C.m;
       float q = 0.f;
@@ -550,175 +801,115 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, Stream& st, const 
         NI_E(5, U.pn, U.h);   // ( 0,-1)
       }
 #undef NI_E
+      // pure: every centre pixel is the component's or zero (invalid /
+      // singleton pixels carry r = q = p = x = 0 and stay 0); mixed: only
+      // pixels of a live slot are written.  Dots are summed for every
+      // slot and ignored for a flushing one.
       const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
-      uint8_t stt = ST_IDLE;
-      if (PURE) {
-        stt = k.st[0];
-      } else {
+      bool mine = center_lane && L <= nrows;
+      if (!PURE) mine = mine && s >= 0 && ((k.live >> s) & 1);
+      if (mine) {
+        out[int64_t(L) * a.P] = make_float4(C.rn, q, pa, C.xn);
+        const double dp = pa, dq = q, dr = C.rn;
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j)
-          if (j == s) stt = k.st[j];
-      }
-      if (center_lane && (m & 0xFFu) != 0 && (stt == ST_ACTIVE || stt == ST_FLUSH)) {
-        vout[o0 + int64_t(L) * P] = make_float4(C.rn, q, pa, C.xn);
-        if (stt == ST_ACTIVE) {
-          const double dp = pa, dq = q, dr = C.rn;
-#pragma unroll
-          for (int j = 0; j < SLOTS; ++j)
-            if (j == s) {
-              acc[j][0] = fma(dp, dq, acc[j][0]);
-              acc[j][1] = fma(dr, dq, acc[j][1]);
-              acc[j][2] = fma(dq, dq, acc[j][2]);
-              acc[j][3] = fma(dr, dr, acc[j][3]);
-            }
-        }
+          if (j == s) {
+            acc[j][0] = fma(dp, dq, acc[j][0]);
+            acc[j][1] = fma(dr, dq, acc[j][1]);
+            acc[j][2] = fma(dq, dq, acc[j][2]);
+            acc[j][3] = fma(dr, dr, acc[j][3]);
+          }
       }
     }
+    der[0] = der[GR];
+    der[1] = der[GR + 1];
   }
-  st.pos += IROWS;
+  Item it;
+  it.x0 = k.x0;
+  it.y0 = k.y0;
+  it.y1 = k.y1;
+  it.flags = k.flags;
+  it.pbase = k.pbase;
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) it.comp[j] = k.comp[j];
   bool live[SLOTS];
 #pragma unroll
-  for (int j = 0; j < SLOTS; ++j) live[j] = k.st[j] == ST_ACTIVE || k.st[j] == ST_FLUSH;
-  item_finish(a, it, acc, live, [&](int32_t c, const double* d) {
-    if (__ldcg(a.status + c) == ST_FLUSH) {  // the pending update is applied
-      a.status[c] = __ldcg(a.final_status + c);
-      a.xbuf[c] = uint8_t(par ^ 1);
-      atomicSub(a.active, 1);
-      atomicExch(a.changed, 1);
-      return;
-    }
-    const double pq = d[0], rq = d[1], qq = d[2], rr = d[3];
-    const int n = __ldcg(a.iters + c) + 1;  // updates once this sweep's alpha is applied
-    a.iters[c] = n;
-    a.rho[c] = rr;
-    double alpha = 0.0, rho1 = 0.0;
-    bool stop = false;
-    uint8_t fin = ST_CONVERGED;
-    if (pq > 0.0) {
-      alpha = rr / pq;
-      rho1 = rr - 2.0 * alpha * rq + alpha * alpha * qq;
-      if (rho1 < 0.0) rho1 = 0.0;
-      if (n < __ldcg(a.cap + c) && sqrt(rho1) < __ldcg(a.tol + c)) {
-        stop = true;  // scipy's top-of-loop test before iteration n
-      } else if (n >= __ldcg(a.cap + c)) {
-        stop = true;  // loop exhausted: info = maxiter
-        fin = ST_CAPPED;
-      }
-    } else {
-      stop = true;  // breakdown: p in the null space (only once r == 0)
-    }
-    a.alpha[c] = alpha;
-    if (stop) {
-      a.final_status[c] = fin;
-      a.status[c] = ST_FLUSH;
-      atomicExch(a.changed, 1);
-    } else {
-      a.beta[c] = rho1 / rr;
-      a.rho[c] = rho1;
-    }
+  for (int j = 0; j < SLOTS; ++j) live[j] = (k.live >> j) & 1;
+  item_finish<PURE ? 1 : SLOTS>(a, it, acc, live, [&](int32_t c, const double* d) {
+    finalize_component(a, c, d, k.par);
   });
 }
 
-// Rebuild the list of items with an ACTIVE or FLUSH component (order is
-// irrelevant: the partial slots are fixed per item).
-__device__ void rebuild_items(const FillArgs& a, int dst, int gwarp, int nwarps) {
+// Initial live-item lists per group.
+__device__ void initial_lists(const FillArgs& a, int gwarp, int nwarps) {
   const int lane = threadIdx.x & 31;
-  for (int k0 = gwarp * 32; k0 < a.nitems; k0 += nwarps * 32) {
-    const int k = k0 + lane;
-    bool act = false;
-    if (k < a.nitems) {
-      const Item it = a.items[k];
-      const int n = item_n(it);
-#pragma unroll
-      for (int j = 0; j < SLOTS; ++j)
-        if (j < n) {
-          const uint8_t st = __ldcg(a.status + it.comp[j]);
-          if (st == ST_ACTIVE || st == ST_FLUSH) act = true;
-        }
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, act);
-    int base = 0;
-    if (lane == 0 && m) base = atomicAdd(a.nactive_items + dst, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (act) a.active_items[dst * a.nitems + base + __popc(m & ((1u << lane) - 1))] = k;
+  for (int k = gwarp * 32 + lane; k < a.nitems; k += nwarps * 32) {
+    if (!item_live(a, k)) continue;
+    const int32_t g = a.cgrp[a.items[k].comp[0]];
+    const int32_t pos = atomicAdd(a.gcnt + g, 1);
+    a.active_items[a.gstart[g] + pos] = k;
   }
 }
 
-__device__ __forceinline__ int draw_ticket(const FillArgs& a, int par) {
-  int k = 0;
-  if ((threadIdx.x & 31) == 0) k = atomicAdd(a.ticket + par, 1);
-  return __shfl_sync(0xffffffffu, k, 0);
-}
-
+// The whole CG of every component: one persistent cooperative launch whose
+// warps claim items from the open batches of all groups.  A group's batch
+// is one CG iteration of its components; the warp that finishes the last
+// item of a batch (after the per-component finalisers of all its items ran)
+// publishes the group's next batch.  No grid-wide barrier per iteration:
+// groups drift apart and every warp stays busy while any batch is open.
 template <int CONN, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int gwarp = blockIdx.x * WPB + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * WPB;
-  int cur = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.nactive_items[0] = 0;
-    a.nactive_items[1] = 0;
-    a.ticket[0] = 0;
-    a.ticket[1] = 0;
+  const int lane = threadIdx.x & 31;
+  initial_lists(a, gwarp, nwarps);
+  grid.sync();
+  for (int g = blockIdx.x * NT + threadIdx.x; g < a.G; g += gridDim.x * NT) {
+    const int32_t n = __ldcg(a.gcnt + g);
+    if (n > 0) {
+      atomicAdd(a.gactive, 1);
+      publish(a, g, 0, n);  // every group starts at parity 0 (v[0] holds b)
+    }
   }
   grid.sync();
-  rebuild_items(a, 0, gwarp, nwarps);
-  grid.sync();
-  for (int it = 0;; ++it) {
-    if (__ldcg(a.active) == 0) break;
-    const int par = it & 1;
-    // the other parity's ticket was last used by the previous sweep (done)
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ticket[par ^ 1] = 0;
-    const int n = __ldcg(a.nactive_items + cur);
-    if (a.trace && it < a.trace_len && blockIdx.x == 0 && threadIdx.x == 0) {
-      long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.trace[2 * it] = t;
-      a.trace[2 * it + 1] = n;
-    }
-    // dynamic item scheduling: tickets are drawn one item ahead; the row
-    // stream runs straight from one item into the next
-    extern __shared__ __align__(16) unsigned char smem[];
-    Stream st;
-    st.ring = reinterpret_cast<RowSlot*>(smem + kSmemPerWarp * (threadIdx.x >> 5));
-    st.pos = 0;
-    int k = draw_ticket(a, par);
-    Item item, nitem;
-    Coefs kc, kn;
-    bool has = k < n;
-    if (has) {
-      item = a.items[__ldcg(a.active_items + cur * a.nitems + k)];
-      item_coefs(a, item, kc);
-      for (int j = 0; j < NS - 3; ++j)
-        issue_row(a, a.v[par], &item, j, st.ring[j % NS]);
-    }
-    while (has) {
-      const int nk = draw_ticket(a, par);
-      const bool has_next = nk < n;
-      if (has_next) {
-        nitem = a.items[__ldcg(a.active_items + cur * a.nitems + nk)];
-        item_coefs(a, nitem, kn);
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* ring = smem + kSmemPerWarp * (threadIdx.x >> 5);
+  Claim* nx = reinterpret_cast<Claim*>(ring + kRingBytes);
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t vpitch = 16u * a.P;
+  Issuer is;
+  Cur cur;
+  bool have = false;
+  for (;;) {
+    if (!have) {
+      if (!try_claim(a, nx)) {
+        if (*reinterpret_cast<volatile int32_t*>(a.gactive) == 0) break;
+        __nanosleep(256);
+        continue;
       }
-      if (item_pure(item)) sweep_item<CONN, true>(a, st, item, kc, par, has_next ? &nitem : nullptr);
-      else sweep_item<CONN, false>(a, st, item, kc, par, has_next ? &nitem : nullptr);
-      item = nitem;
-      kc = kn;
-      has = has_next;
+      have = true;
+      issuer_start(a, nx->item, nx->par, is);
+      for (int j = 0; j < LA; ++j) issue_row(ring_s, j, is, vpitch);
     }
-    cp_wait<0>();
-    grid.sync();
-    if (__ldcg(a.changed)) {
-      const int nxt = cur ^ 1;
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.nactive_items[nxt] = 0;
-      grid.sync();
-      rebuild_items(a, nxt, gwarp, nwarps);
-      grid.sync();
-      if (blockIdx.x == 0 && threadIdx.x == 0) *a.changed = 0;
-      cur = nxt;
-      grid.sync();
+    load_cur(*nx, cur);
+    __syncwarp();
+    bool has_next = false;
+    if (cur.flags & 0x100) sweep_item<CONN, true>(a, ring, nx, is, cur, has_next);
+    else sweep_item<CONN, false>(a, ring, nx, is, cur, has_next);
+    // batch accounting: the finalisers of this item ran above
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(a.gdone + cur.g, 1) == cur.n - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) advance_group(a, cur.g, cur.par);
+    if (!has_next) {
+      cp_wait<0>();
+      have = false;
     }
   }
+  cp_wait<0>();
 }
 
 // Initial ||b||^2 per component and the state of every component.  One warp
@@ -736,7 +927,7 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
     for (int j = 0; j < SLOTS; ++j)
 #pragma unroll
       for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
-    const int yend = min(it.y0 + SH, a.rows);
+    const int yend = it.y1;
     if (on) {
       for (int y = it.y0; y < yend; ++y) {
         const int64_t o = int64_t(y + RM) * a.P + xr + XM;
@@ -764,7 +955,6 @@ __global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) 
         a.status[c] = ST_CAPPED;
       } else {
         a.status[c] = ST_ACTIVE;
-        atomicAdd(a.active, 1);
       }
     });
   }
@@ -824,6 +1014,44 @@ __global__ void status_out_kernel(const uint8_t* __restrict__ status,
   atomicMax(max_iters, mx);
 }
 
+// ---- lockstep groups: components that share an item (union-find over the
+// item pairs); only components with items get a group
+__global__ void grp_init_kernel(int32_t* __restrict__ parent, int C) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x)
+    parent[c] = c;
+}
+
+__global__ void grp_union_kernel(const Item* __restrict__ items, int nitems,
+                                 int32_t* __restrict__ parent) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nitems; k += gridDim.x * blockDim.x) {
+    const Item it = items[k];
+    if (item_n(it) == 2) uf_union(parent, it.comp[0], it.comp[1]);
+  }
+}
+
+__global__ void grp_root_kernel(int32_t* __restrict__ parent,
+                                const int32_t* __restrict__ comp_nparts, int C,
+                                int32_t* __restrict__ isroot) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    const int32_t r = uf_find(parent, c);
+    isroot[c] = r == c && comp_nparts[c] > 0;
+  }
+}
+
+__global__ void grp_assign_kernel(const int32_t* __restrict__ parent,
+                                  const int32_t* __restrict__ gid,
+                                  const int32_t* __restrict__ comp_nparts, int C,
+                                  int32_t* __restrict__ cgrp) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x)
+    cgrp[c] = comp_nparts[c] > 0 ? gid[uf_find(const_cast<int32_t*>(parent), c)] : -1;
+}
+
+__global__ void grp_size_kernel(const Item* __restrict__ items, int nitems,
+                                const int32_t* __restrict__ cgrp, int32_t* __restrict__ gsize) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nitems; k += gridDim.x * blockDim.x)
+    atomicAdd(gsize + cgrp[items[k].comp[0]], 1);
+}
+
 // ------------------------------------------------------------ workspace
 
 struct FillWs {
@@ -834,8 +1062,12 @@ struct FillWs {
   int32_t *slot_base, *nslots, *nitems_strip, *item_base, *strip_comps, *partial_comp,
       *partial_idx, *plist, *keys_sorted;
   Item* items;
-  int32_t *comp_size, *comp_nparts, *comp_pstart, *comp_cnt, *iters, *cap, *active, *changed,
-      *total, *total_items, *active_items, *nactive_items, *ticket;
+  int32_t *comp_size, *comp_nparts, *comp_pstart, *comp_cnt, *iters, *cap, *total, *total_items,
+      *active_items;
+  int32_t *parent, *isroot, *gid, *cgrp, *gsize, *gstart, *gcnt, *gdone, *gchg, *gactive, *ngroups;
+  unsigned long long *gtk, *ring;
+  uint32_t *ring_tail, *ring_hint;
+  uint32_t R;
   double *partial, *rho, *alpha, *beta, *tol;
   uint8_t *status, *final_status, *xbuf;
   unsigned long long* px_iters;
@@ -844,6 +1076,14 @@ struct FillWs {
   size_t sort_bytes;
   void* scan_ws;
 };
+
+// Batch ring capacity: at most one open batch per group sits ahead of the
+// hint, plus exhausted entries the hint has not passed yet.
+static uint32_t ring_cap(int C) {
+  uint32_t r = 8192;
+  while (r < 4u * uint32_t(C + 1) + 8192u) r <<= 1;
+  return r;
+}
 
 static int pitch_of(int W) { return (W + XM + 48 + 15) & ~15; }
 static int64_t padded_len(int rows, int W) { return int64_t(rows + RM + RB) * pitch_of(W); }
@@ -864,9 +1104,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.item_base = c.take<int32_t>(nstrips + 1);
   w.strip_comps = c.take<int32_t>(int64_t(nstrips) * SPX);
   w.items = c.take<Item>(NI);
-  w.active_items = c.take<int32_t>(2 * NI);
-  w.nactive_items = c.take<int32_t>(2);
-  w.ticket = c.take<int32_t>(2);
+  w.active_items = c.take<int32_t>(NI);
   w.partial_comp = c.take<int32_t>(P);
   w.partial_idx = c.take<int32_t>(P);
   w.plist = c.take<int32_t>(P);
@@ -885,8 +1123,22 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.status = c.take<uint8_t>(C + 1);
   w.final_status = c.take<uint8_t>(C + 1);
   w.xbuf = c.take<uint8_t>(C + 1);
-  w.active = c.take<int32_t>(1);
-  w.changed = c.take<int32_t>(1);
+  w.parent = c.take<int32_t>(C + 1);
+  w.isroot = c.take<int32_t>(C + 1);
+  w.gid = c.take<int32_t>(C + 1);
+  w.cgrp = c.take<int32_t>(C + 1);
+  w.gsize = c.take<int32_t>(C + 1);
+  w.gstart = c.take<int32_t>(C + 1);
+  w.gcnt = c.take<int32_t>(C + 1);
+  w.gdone = c.take<int32_t>(C + 1);
+  w.gchg = c.take<int32_t>(C + 1);
+  w.gtk = c.take<unsigned long long>(C + 1);
+  w.R = ring_cap(C);
+  w.ring = c.take<unsigned long long>(w.R);
+  w.ring_tail = c.take<uint32_t>(1);
+  w.ring_hint = c.take<uint32_t>(1);
+  w.gactive = c.take<int32_t>(1);
+  w.ngroups = c.take<int32_t>(1);
   w.total = c.take<int32_t>(1);
   w.total_items = c.take<int32_t>(1);
   w.px_iters = c.take<unsigned long long>(1);
@@ -905,7 +1157,7 @@ using namespace ni;
 
 static void strip_grid(int B, int H, int W, int* nsx, int* nsy) {
   *nsx = div_up(W, SW);
-  *nsy = div_up(int64_t(B) * H, SH);
+  *nsy = B * div_up(H, SH);
 }
 
 extern "C" int ni_fill_workspace_size(int B, int H, int W, int connectivity, int count,
@@ -948,8 +1200,6 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.comp_size, 0, sizeof(int32_t) * (count + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.comp_nparts, 0, sizeof(int32_t) * (count + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.comp_cnt, 0, sizeof(int32_t) * (count + 1), s));
-  NI_CUDA_TRY(cudaMemsetAsync(w.active, 0, sizeof(int32_t), s));
-  NI_CUDA_TRY(cudaMemsetAsync(w.changed, 0, sizeof(int32_t), s));
   {  // zero margins and buffers of the padded layout
     const size_t npad = size_t(padded_len(rows, W));
     NI_CUDA_TRY(cudaMemsetAsync(w.v0, 0, npad * sizeof(float4), s));
@@ -968,8 +1218,8 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
 #undef NI_PREP
   NI_LAUNCH_CHECK();
   // ---- static reduction plan: strips -> items -> partial slots
-  NI_COUNT_LAUNCH(), strip_comps_kernel<<<nstrips, NT, 0, s>>>(labels, w.comp_size, rows, W, nsx,
-                                                              w.nslots, w.strip_comps);
+  NI_COUNT_LAUNCH(), strip_comps_kernel<<<nstrips, NT, 0, s>>>(
+                         labels, w.comp_size, H, W, nsx, nsy / B, w.nslots, w.strip_comps);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(w.nslots, w.slot_base, nstrips, w.total, w.scan_ws, s));
   NI_COUNT_LAUNCH(), item_counts_kernel<<<div_up(nstrips, 256), 256, 0, s>>>(w.nslots, nstrips,
@@ -977,8 +1227,8 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(w.nitems_strip, w.item_base, nstrips, w.total_items, w.scan_ws, s));
   NI_COUNT_LAUNCH(), strip_items_kernel<<<div_up(nstrips, 128), 128, 0, s>>>(
-                         w.nslots, w.slot_base, w.item_base, w.strip_comps, nstrips, nsx, w.items,
-                         w.partial_comp, w.partial_idx, w.comp_nparts);
+                         w.nslots, w.slot_base, w.item_base, w.strip_comps, nstrips, nsx, nsy / B,
+                         H, w.items, w.partial_comp, w.partial_idx, w.comp_nparts);
   NI_LAUNCH_CHECK();
   int32_t NP = 0, NIt = 0;
   NI_CUDA_TRY(cudaMemcpyAsync(&NP, w.total, sizeof(NP), cudaMemcpyDeviceToHost, s));
@@ -992,15 +1242,42 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
                                                 w.partial_idx, w.plist, NP, 0, end_bit, s));
   }
   NI_TRY(exclusive_scan_i32(w.comp_nparts, w.comp_pstart, count + 1, nullptr, w.scan_ws, s));
+  // ---- lockstep groups and their item regions
+  int32_t G = 0;
+  if (count > 0) {
+    const int cb = div_up(count, 256);
+    NI_COUNT_LAUNCH(), grp_init_kernel<<<cb, 256, 0, s>>>(w.parent, count);
+    NI_LAUNCH_CHECK();
+    if (NIt > 0) {
+      NI_COUNT_LAUNCH(), grp_union_kernel<<<div_up(NIt, 256), 256, 0, s>>>(w.items, NIt, w.parent);
+      NI_LAUNCH_CHECK();
+    }
+    NI_COUNT_LAUNCH(), grp_root_kernel<<<cb, 256, 0, s>>>(w.parent, w.comp_nparts, count, w.isroot);
+    NI_LAUNCH_CHECK();
+    NI_TRY(exclusive_scan_i32(w.isroot, w.gid, count, w.ngroups, w.scan_ws, s));
+    NI_COUNT_LAUNCH(), grp_assign_kernel<<<cb, 256, 0, s>>>(w.parent, w.gid, w.comp_nparts, count,
+                                                           w.cgrp);
+    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemcpyAsync(&G, w.ngroups, sizeof(G), cudaMemcpyDeviceToHost, s));
+    NI_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  NI_CUDA_TRY(cudaMemsetAsync(w.gsize, 0, sizeof(int32_t) * (G + 1), s));
+  if (NIt > 0) {
+    NI_COUNT_LAUNCH(), grp_size_kernel<<<div_up(NIt, 256), 256, 0, s>>>(w.items, NIt, w.cgrp,
+                                                                       w.gsize);
+    NI_LAUNCH_CHECK();
+  }
+  NI_TRY(exclusive_scan_i32(w.gsize, w.gstart, G + 1, nullptr, w.scan_ws, s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gcnt, 0, sizeof(int32_t) * (G + 1), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gdone, 0, sizeof(int32_t) * (G + 1), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gchg, 0, sizeof(int32_t) * (G + 1), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gtk, 0, sizeof(unsigned long long) * (G + 1), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.ring, 0xff, sizeof(unsigned long long) * w.R, s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.ring_tail, 0, sizeof(uint32_t), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.ring_hint, 0, sizeof(uint32_t), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gactive, 0, sizeof(int32_t), s));
   FillArgs a;
   memset(&a, 0, sizeof(a));
-  static long long* trace_buf = nullptr;
-  if (getenv("NI_FILL_TRACE")) {  // debug: per-iteration timeline
-    if (!trace_buf) NI_CUDA_TRY(cudaMalloc(&trace_buf, sizeof(long long) * 2 * 65536));
-    NI_CUDA_TRY(cudaMemsetAsync(trace_buf, 0, sizeof(long long) * 2 * 65536, s));
-    a.trace = trace_buf;
-    a.trace_len = 65536;
-  }
   a.rows = rows;
   a.W = W;
   a.P = P;
@@ -1015,9 +1292,19 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.comp_plist = w.plist;
   a.comp_cnt = w.comp_cnt;
   a.partial = w.partial;
+  a.G = G;
+  a.cgrp = w.cgrp;
+  a.gstart = w.gstart;
   a.active_items = w.active_items;
-  a.nactive_items = w.nactive_items;
-  a.ticket = w.ticket;
+  a.gcnt = w.gcnt;
+  a.gtk = w.gtk;
+  a.gdone = w.gdone;
+  a.gchg = w.gchg;
+  a.ring = w.ring;
+  a.R = w.R;
+  a.ring_tail = w.ring_tail;
+  a.ring_hint = w.ring_hint;
+  a.gactive = w.gactive;
   a.rho = w.rho;
   a.alpha = w.alpha;
   a.beta = w.beta;
@@ -1027,8 +1314,6 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.status = w.status;
   a.final_status = w.final_status;
   a.xbuf = w.xbuf;
-  a.active = w.active;
-  a.changed = w.changed;
   if (count > 0) {
     NI_COUNT_LAUNCH(), init_state_kernel<<<div_up(count, 256), 256, 0, s>>>(
                            w.status, w.final_status, w.xbuf, w.iters, w.cap, w.rho, w.comp_size,
@@ -1093,16 +1378,6 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     g_fill_report.max_iters = mxi;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (a.trace) {  // debug trace dump (NI_FILL_TRACE=path)
-      static long long host[2 * 65536];
-      NI_CUDA_TRY(cudaMemcpy(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost));
-      FILE* f = fopen(getenv("NI_FILL_TRACE"), "w");
-      if (f) {
-        for (int k = 0; k < 65536 && host[2 * k]; ++k)
-          fprintf(f, "%lld %lld\n", host[2 * k], host[2 * k + 1]);
-        fclose(f);
-      }
-    }
   }
   return NI_OK;
 }

@@ -367,41 +367,15 @@ __global__ void part_init_kernel(StepWs w, int C) {
     w.parent[c] = c;
 }
 
-__device__ __forceinline__ int find_root(volatile int32_t* parent, int x) {
-  int p = parent[x];
-  while (p != x) {
-    x = p;
-    p = parent[x];
-  }
-  return x;
-}
-
-__device__ __forceinline__ void union_min(int32_t* parent, int a, int b) {
-  volatile int32_t* vp = parent;
-  while (true) {
-    a = find_root(vp, a);
-    b = find_root(vp, b);
-    if (a == b) return;
-    if (a < b) {
-      int t = a;
-      a = b;
-      b = t;
-    }
-    int old = atomicMin(parent + a, b);
-    if (old == a) return;
-    a = old;
-  }
-}
-
 __global__ void part_union_kernel(Quot q, StepWs w, const int32_t* __restrict__ nU_dev) {
   const int U = nU_dev[0];
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x)
-    if (w.S[u] > 0.0) union_min(w.parent, q.pp[u], q.pq[u]);
+    if (w.S[u] > 0.0) uf_union(w.parent, q.pp[u], q.pq[u]);
 }
 
 __global__ void part_flatten_kernel(StepWs w, int C) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    const int r = find_root(w.parent, c);
+    const int r = uf_find(w.parent, c);
     w.pkey[c] = r;
     w.pval[c] = c;
   }
@@ -613,13 +587,13 @@ __global__ void merge_select_kernel(Quot q, const double* __restrict__ residual,
 __global__ void merge_union_kernel(Quot q, MergeWs m) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < q.C; c += gridDim.x * blockDim.x) {
     const int e = m.sel[c];
-    if (e >= 0) union_min(m.parent, q.pa[e], q.pb[e]);
+    if (e >= 0) uf_union(m.parent, q.pa[e], q.pb[e]);
   }
 }
 
 __global__ void merge_flatten_kernel(MergeWs m, int C) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    const int r = find_root(m.parent, c);
+    const int r = uf_find(m.parent, c);
     m.parent[c] = r;
     m.flag[c] = r == c;
   }
