@@ -321,7 +321,7 @@ __device__ __forceinline__ int slot_of(const Item& it, int32_t lab) {
 // let the last arriving warp of a component reduce its partials in plan
 // order and call fin(c, dots).
 template <int NSUM = SLOTS, class Fin>
-__device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
+__device__ __forceinline__ bool item_finish(const FillArgs& a, const Item& it,
                                             double (&acc)[SLOTS][NDOT], const bool* live, Fin fin) {
   const int lane = threadIdx.x & 31;
   const int n = item_n(it);
@@ -355,6 +355,7 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
     }
   }
   unsigned lastmask = __ballot_sync(0xffffffffu, last);
+  const bool ran = lastmask != 0;
   while (lastmask) {
     const int s = __ffs(lastmask) - 1;
     lastmask &= lastmask - 1;
@@ -378,6 +379,7 @@ __device__ __forceinline__ void item_finish(const FillArgs& a, const Item& it,
     }
     __syncwarp();
   }
+  return ran;
 }
 
 // ---- the per-warp row stream (cp.async into a shared-memory ring)
@@ -735,7 +737,7 @@ __device__ __forceinline__ void finalize_component(const FillArgs& a, int32_t c,
 // this item's rows 0..LA-1 (issued); as its last rows are issued the warp
 // claims its next item (into nx) and starts that item's rows.
 template <int CONN, bool PURE>
-__device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned char* ring,
+__device__ __forceinline__ bool sweep_item(const FillArgs& a, const unsigned char* ring,
                                            Claim* nx, Issuer& is, const Cur& k, bool& has_next) {
   const int lane = threadIdx.x & 31;
   const uint32_t ring_s = smem_u32(ring);
@@ -835,7 +837,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   bool live[SLOTS];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j) live[j] = (k.live >> j) & 1;
-  item_finish<PURE ? 1 : SLOTS>(a, it, acc, live, [&](int32_t c, const double* d) {
+  return item_finish<PURE ? 1 : SLOTS>(a, it, acc, live, [&](int32_t c, const double* d) {
     finalize_component(a, c, d, k.par);
   });
 }
@@ -895,12 +897,13 @@ __global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
     load_cur(*nx, cur);
     __syncwarp();
     bool has_next = false;
-    if (cur.flags & 0x100) sweep_item<CONN, true>(a, ring, nx, is, cur, has_next);
-    else sweep_item<CONN, false>(a, ring, nx, is, cur, has_next);
-    // batch accounting: the finalisers of this item ran above
+    const bool fin = (cur.flags & 0x100) ? sweep_item<CONN, true>(a, ring, nx, is, cur, has_next)
+                                         : sweep_item<CONN, false>(a, ring, nx, is, cur, has_next);
+    // batch accounting: this item's partials were fenced before their
+    // arrival counts; scalar updates of a finaliser run here are fenced now
     int last = 0;
     if (lane == 0) {
-      __threadfence();
+      if (fin) __threadfence();
       last = atomicAdd(a.gdone + cur.g, 1) == cur.n - 1;
     }
     if (__shfl_sync(0xffffffffu, last, 0)) advance_group(a, cur.g, cur.par);
