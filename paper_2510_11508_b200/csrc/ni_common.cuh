@@ -172,13 +172,27 @@ __device__ __forceinline__ int uf_find(volatile int32_t* parent, int32_t x) {
   return x;
 }
 
+// Find with path halving: every visited node is re-pointed to its
+// grandparent (an ancestor with a smaller id, so parent[x] <= x still holds
+// and a concurrent hook is never lost: its union is retried from the old root).
+__device__ __forceinline__ int uf_find_halve(volatile int32_t* parent, int32_t x) {
+  int32_t p = parent[x];
+  while (p != x) {
+    const int32_t gp = parent[p];
+    if (gp != p) parent[x] = gp;
+    x = gp;
+    p = parent[x];
+  }
+  return x;
+}
+
 // Union by hooking the larger root under the smaller one (atomicMin), retried
 // until both endpoints share a root.  parent[x] <= x always holds.
 __device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
   volatile int32_t* vp = parent;
   while (true) {
-    a = uf_find(vp, a);
-    b = uf_find(vp, b);
+    a = uf_find_halve(vp, a);
+    b = uf_find_halve(vp, b);
     if (a == b) return;
     if (a < b) {
       int32_t t = a;

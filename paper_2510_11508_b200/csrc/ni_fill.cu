@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(256) prep_kernel(
     const int64_t o = (row + RM) * P + u + XM;  // padded index
     lab_p[o] = lab;
     if (lab < 0) continue;  // margins / invalid pixels stay zero
-    atomicAdd(comp_size + lab, 1);
+    {  // one atomic per distinct label of the warp (neighbours share labels)
+      const unsigned peers = __match_any_sync(__activemask(), lab);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(comp_size + lab, __popc(peers));
+    }
     const double wa = 0.5 * (gamma[i] * gamma[i]);
     hw[o] = float(wa);
     const uint8_t ef = eflags[i];

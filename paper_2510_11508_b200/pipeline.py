@@ -13,9 +13,11 @@ components of all maps), then the small per-map outer loops.
 
 from __future__ import annotations
 
+import concurrent.futures as cf
 import ctypes as C
 import hashlib
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -28,6 +30,7 @@ from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _stream
 from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
 
 ENERGY_FLOOR = 1e-300  # pipeline.py:55
+MAP_THREADS = 32  # host threads driving the per-map outer loops of a batch
 
 
 def _ptr(t: torch.Tensor | None) -> C.c_void_p:
@@ -222,14 +225,18 @@ class _MapLoop:
     """The outer relative-scale loop of one map (pipeline.py:169-227)."""
 
     def __init__(self, g: _Grid, m: int, labels: torch.Tensor, base: int, count: int, co,
-                 settings: SolveSettings, weights: WeightParams):
+                 settings: SolveSettings, weights: WeightParams, stream: int):
         self.g, self.m, self.labels, self.base, self.count = g, m, labels, base, count
+        self.stream = stream
         self.co = co
         self.settings, self.weights = settings, weights
         self.version = 0
         self.keys = None
         self.K = 0
         self.quot = None
+
+    def s(self):
+        return C.c_void_p(self.stream)
 
     def rebuild(self, keys: torch.Tensor | None = None):
         g, lib = self.g, self.g.lib
@@ -241,7 +248,7 @@ class _MapLoop:
             n = torch.zeros(1, dtype=torch.int32, device=g.dev)
             ws = _ws(_lib.size_query(lib.ni_inter_edges_workspace_size, 1, g.H, g.W, g.conn), g.dev)
             _lib.check(lib.ni_inter_edges(_ptr(lab), _ptr(ef), 1, g.H, g.W, g.conn, _ptr(out), _ptr(n),
-                                          _ptr(ws), ws.numel(), g.s()), "build_quotient")
+                                          _ptr(ws), ws.numel(), self.s()), "build_quotient")
             K = int(n.item())
             keys = out[:K] + self.m * hw * g.kf
         self.keys = keys.contiguous()
@@ -251,7 +258,7 @@ class _MapLoop:
         npairs = C.c_int32(0)
         _lib.check(lib.ni_quotient_build(_ptr(self.keys), self.K, _ptr(self.labels), self.base,
                                          self.count, g.W, g.conn, _ptr(self.quot), self.quot.numel(),
-                                         C.byref(npairs), g.s()), "build_quotient")
+                                         C.byref(npairs), self.s()), "build_quotient")
 
     def step(self, z: torch.Tensor, t: int):
         g, lib = self.g, self.g.lib
@@ -270,7 +277,7 @@ class _MapLoop:
             self.m, t, st.alignment_iters, wp.mode_code, C.c_double(wp.k),
             C.c_double(wp.outlier_low), C.c_double(wp.outlier_high), C.c_double(st.cg_tol),
             int(st.cg_max_iters), _ptr(z), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(out),
-            _ptr(ok), _ptr(ws), ws.numel(), g.s()), "relative_scale_step")
+            _ptr(ok), _ptr(ws), ws.numel(), self.s()), "relative_scale_step")
         return scales, residual, wts, out, ok
 
     def merge(self, residual, wts):
@@ -281,7 +288,7 @@ class _MapLoop:
         _lib.check(lib.ni_merge(_ptr(self.quot), self.quot.numel(), self.K, self.count,
                                 _ptr(self.labels), self.base, g.H, g.W, self.m, _ptr(residual),
                                 _ptr(wts), _ptr(new_count), _ptr(energy), _ptr(ws), ws.numel(),
-                                g.s()), "merge_components")
+                                self.s()), "merge_components")
         return new_count, energy
 
 
@@ -370,45 +377,68 @@ def run_pipeline_batch(
     filled = z.clone()
     fit = fill_iters.cpu().numpy()
 
-    results = []
     valid = g.nmap.valid_t
-    for m in range(B):
-        loop = _MapLoop(g, m, labels, int(first[m]), counts[m], co, settings, weights)
-        energies = []
-        e_prev = ENERGY_FLOOR
-        t = 0
-        converged = False
-        version = 0
-        loop.rebuild()
-        zm = z[m * g.hw:(m + 1) * g.hw]
-        while not converged:
-            it_start = time.perf_counter()
-            scales, residual, wts, out, ok = loop.step(z, t)
-            if not bool(ok.item()):
-                warnings[m].append(f"iteration {t}: cg hit iteration cap")
-            t += 1
-            merge_performed = False
-            extra = {}
-            if (settings.freq_merging is not None and t % settings.freq_merging == 0
-                    and loop.count > 1 and loop.K > 0):
-                digest = _digest(zm)
-                new_count, energy = loop.merge(residual, wts)
-                nc = int(new_count.item())
-                e_t = float(energy.item())
-                extra = {"components_before": loop.count, "components_after": nc,
-                         "z_digest_before": digest, "z_digest_after": _digest(zm)}
-                loop.count = nc
-                version += 1
-                loop.rebuild()
-                merge_performed = True
-            else:
-                e_t = float(out[0].item())
-            converged = _has_converged(e_t, e_prev, t, settings)
-            e_prev = e_t
-            energies.append(e_t)
-            records[m].append({"t": t, "E_t": e_t, "component_count": loop.count,
-                               "merge_performed": merge_performed, "wall_ms": _ms(it_start), **extra})
-        results.append((loop, energies, t, version))
+    # The outer loops of the B maps are independent (each touches only its
+    # own labels / z slice): run them concurrently, one CUDA stream each, from
+    # a small pool of host threads (the C calls and CUDA syncs release the GIL).
+    ready = torch.cuda.Event()
+    ready.record(torch.cuda.current_stream(g.dev))
+
+    def map_loop(m):
+        ms = torch.cuda.Stream(device=g.dev)
+        with torch.cuda.stream(ms):
+            ms.wait_event(ready)
+            loop = _MapLoop(g, m, labels, int(first[m]), counts[m], co, settings, weights,
+                            ms.cuda_stream)
+            energies = []
+            e_prev = ENERGY_FLOOR
+            t = 0
+            converged = False
+            version = 0
+            loop.rebuild()
+            zm = z[m * g.hw:(m + 1) * g.hw]
+            while not converged:
+                it_start = time.perf_counter()
+                scales, residual, wts, out, ok = loop.step(z, t)
+                if not bool(ok.item()):
+                    warnings[m].append(f"iteration {t}: cg hit iteration cap")
+                t += 1
+                merge_performed = False
+                extra = {}
+                if (settings.freq_merging is not None and t % settings.freq_merging == 0
+                        and loop.count > 1 and loop.K > 0):
+                    digest = _digest(zm)
+                    new_count, energy = loop.merge(residual, wts)
+                    nc = int(new_count.item())
+                    e_t = float(energy.item())
+                    extra = {"components_before": loop.count, "components_after": nc,
+                             "z_digest_before": digest, "z_digest_after": _digest(zm)}
+                    loop.count = nc
+                    version += 1
+                    loop.rebuild()
+                    merge_performed = True
+                else:
+                    e_t = float(out[0].item())
+                converged = _has_converged(e_t, e_prev, t, settings)
+                e_prev = e_t
+                energies.append(e_t)
+                records[m].append({"t": t, "E_t": e_t, "component_count": loop.count,
+                                   "merge_performed": merge_performed,
+                                   "wall_ms": _ms(it_start), **extra})
+            done = torch.cuda.Event()
+            done.record(ms)
+        return (loop, energies, t, version), done
+
+    if B == 1:
+        outs = [map_loop(0)]
+    else:
+        nthreads = int(os.environ.get("NI_MAP_THREADS", MAP_THREADS))
+        with cf.ThreadPoolExecutor(max_workers=min(B, nthreads)) as ex:
+            outs = list(ex.map(map_loop, range(B)))
+    cur = torch.cuda.current_stream(g.dev)
+    for _, done in outs:
+        cur.wait_event(done)
+    results = [r for r, _ in outs]
 
     target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
     lib = g.lib
