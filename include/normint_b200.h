@@ -118,43 +118,60 @@ int ni_inter_edges(const int32_t* labels, const uint8_t* eflags, int B, int H, i
                    int connectivity, int32_t* keys_out, int32_t* n_out, void* workspace,
                    size_t workspace_bytes, ni_stream_t stream);
 
-/* Static structure of the inter-component system of one map's partition
+/* Keep the inter keys (ascending, from ni_inter_edges) of maps with
+ * map_keep[m] != 0 whose endpoints now carry different labels, in order
+ * (after a merge, or when maps leave the outer loop; graph.py:186-196).
+ * keys_out must not alias keys; n_out is a device int32. */
+int ni_keys_filter_workspace_size(int K, size_t* bytes);
+int ni_keys_filter(const int32_t* keys, int K, const int32_t* labels, const uint8_t* map_keep,
+                   int H, int W, int connectivity, int32_t* keys_out, int32_t* n_out,
+                   void* workspace, size_t workspace_bytes, ni_stream_t stream);
+
+/* Static structure of the inter-component system of a batch's partition
  * (solver.py:153-180): per-edge endpoints and component pairs, runs of edges
  * per unordered component pair (sorted by edge index inside a run),
- * per-component incidence lists and the sparsity of the component
- * Laplacian A^T W A.  keys: the map's K inter edge keys (from ni_inter_edges,
- * ascending); labels of the map lie in [label_base, label_base + count).
- * SYNCHRONOUS (reads back the number of distinct pairs into n_pairs_host). */
-int ni_quotient_workspace_size(int K, int count, size_t* bytes);
-int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int label_base, int count,
+ * per-component incidence lists, the sparsity of the component Laplacian
+ * A^T W A and the per-map edge ranges.  Component ids are the batch's global
+ * labels in [0, count); keys: K inter edge keys (ascending, map-major).
+ * SYNCHRONOUS (reads back the number of distinct pairs into n_pairs_host and,
+ * when map_edges_host != NULL, the B per-map edge counts). */
+int ni_quotient_workspace_size(int K, int count, int B, size_t* bytes);
+int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int count, int B, int H,
                       int W, int connectivity, void* quot_ws, size_t quot_bytes,
-                      int32_t* n_pairs_host, ni_stream_t stream);
+                      int32_t* n_pairs_host, int32_t* map_edges_host, ni_stream_t stream);
 
-/* K4-K7 -- relative_scale_step (solver.py:253-303) for map `map_index` at
- * 0-based iteration t, followed by z[valid] += s[label] (pipeline.py:181-182)
- * on that map's pixels.  mode: 0 off, 1 soft, 2 hard
- * (continuity.py:140-158).  Outputs scales[count], residual[2K] (rows a, b
- * interleaved like solver.py:_pair_system), weights[2K], energy_out[0],
- * cg_ok_out[0].  The right-hand side's roundoff null-space component is
- * removed before the CG ("Reference numerics").
- * SYNCHRONOUS: one 4-byte read-back (does A^T W b vanish, solver.py:112). */
-int ni_scale_step_workspace_size(int K, int count, size_t* bytes);
-int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, const int32_t* labels,
-                  int label_base, const double* omega_a, const double* omega_b,
-                  const double* gamma, const uint8_t* eflags, int B, int H, int W,
-                  int connectivity, int model, int map_index, int t, int alignment_iters,
-                  int mode, double k, double outlier_low, double outlier_high, double cg_tol,
-                  int cg_max_iters, double* z, double* scales, double* residual, double* weights,
-                  double* energy_out, int32_t* cg_ok_out, void* workspace,
-                  size_t workspace_bytes, ni_stream_t stream);
+/* K4-K7 -- relative_scale_step (solver.py:253-303) at 0-based iteration t for
+ * the maps active[0..nact) of the batch, each solved as its own CG (one CTA
+ * per map, a cooperative launch for maps above 8192 components), followed by
+ * z[valid] += s[label] (pipeline.py:181-182) on those maps' pixels.
+ * map_first[B+1], map_count[B] and active[nact] are HOST arrays (map m owns
+ * component ids [map_first[m], map_first[m] + map_count[m])).  mode: 0 off,
+ * 1 soft, 2 hard (continuity.py:140-158).  Outputs (device): scales[count],
+ * residual[2K] (rows a, b interleaved like solver.py:_pair_system),
+ * weights[2K], energy_out[B] and cg_ok_out[B] (entries of active maps).  The
+ * right-hand side's roundoff null-space component is removed before the CG
+ * ("Reference numerics").  Asynchronous. */
+int ni_scale_step_workspace_size(int K, int count, int B, size_t* bytes);
+int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+                  const int32_t* map_first, const int32_t* map_count, const int32_t* active,
+                  int nact, const int32_t* labels, const double* omega_a, const double* omega_b,
+                  const double* gamma, const uint8_t* eflags, int H, int W, int connectivity,
+                  int model, int t, int alignment_iters, int mode, double k, double outlier_low,
+                  double outlier_high, double cg_tol, int cg_max_iters, double* z,
+                  double* scales, double* residual, double* weights, double* energy_out,
+                  int32_t* cg_ok_out, void* workspace, size_t workspace_bytes,
+                  ni_stream_t stream);
 
-/* K8 -- merge_components (graph.py:207-250) with |residual[2e]| as the merge
- * key, plus the energy restricted to edges that stay inter-component
- * (pipeline.py:187-203).  Relabels the map's pixels in place (labels stay
- * in [label_base, label_base + new_count)). */
-int ni_merge_workspace_size(int K, int count, size_t* bytes);
-int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int32_t* labels,
-             int label_base, int H, int W, int map_index, const double* residual,
+/* K8 -- merge_components (graph.py:207-250) for the maps merging[0..nmerge)
+ * with |residual[2e]| as the merge key, plus their energies restricted to
+ * edges that stay inter-component (pipeline.py:187-203) in energy_out[m].
+ * Relabels those maps' pixels in place (labels of map m stay in
+ * [map_first[m], map_first[m] + new_count)); new_count_out[B] (device) gets
+ * every map's count.  Map tables are HOST arrays as for ni_scale_step. */
+int ni_merge_workspace_size(int K, int count, int B, size_t* bytes);
+int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+             const int32_t* map_first, const int32_t* map_count, const int32_t* merging,
+             int nmerge, int32_t* labels, int H, int W, const double* residual,
              const double* weights, int32_t* new_count_out, double* energy_out, void* workspace,
              size_t workspace_bytes, ni_stream_t stream);
 

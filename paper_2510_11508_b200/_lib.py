@@ -46,13 +46,16 @@ SIGNATURES = {
     "ni_fill": ([_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ, _P], _I),
     "ni_inter_edges_workspace_size": ([_I, _I, _I, _I, _PSZ], _I),
     "ni_inter_edges": ([_P, _P, _I, _I, _I, _I, _P, _P, _P, _SZ, _P], _I),
-    "ni_quotient_workspace_size": ([_I, _I, _PSZ], _I),
-    "ni_quotient_build": ([_P, _I, _P, _I, _I, _I, _I, _P, _SZ, _PI32, _P], _I),
-    "ni_scale_step_workspace_size": ([_I, _I, _PSZ], _I),
-    "ni_scale_step": ([_P, _SZ, _I, _I, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I,
-                       _I, _D, _D, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], _I),
-    "ni_merge_workspace_size": ([_I, _I, _PSZ], _I),
-    "ni_merge": ([_P, _SZ, _I, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_keys_filter_workspace_size": ([_I, _PSZ], _I),
+    "ni_keys_filter": ([_P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _SZ, _P], _I),
+    "ni_quotient_workspace_size": ([_I, _I, _I, _PSZ], _I),
+    "ni_quotient_build": ([_P, _I, _P, _I, _I, _I, _I, _I, _P, _SZ, _PI32, _P, _P], _I),
+    "ni_scale_step_workspace_size": ([_I, _I, _I, _PSZ], _I),
+    "ni_scale_step": ([_P, _SZ, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _I, _I, _I,
+                       _I, _I, _I, _D, _D, _D, _D, _I, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_merge_workspace_size": ([_I, _I, _I, _PSZ], _I),
+    "ni_merge": ([_P, _SZ, _I, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P, _P, _P, _P, _P, _SZ, _P],
+                 _I),
     "ni_gauge_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_gauge": ([_P, _P, _I, _I, _I, _D, _P, _P, _SZ, _P], _I),
 }

@@ -1,20 +1,30 @@
-// K4-K8: the relative-scale loop over the quotient graph.
+// K4-K8: the relative-scale loop over the quotient graph, for a whole batch
+// of maps at once.
 //
 //  * ni_inter_edges      graph.py:186-196   ordered compaction of inter edges
+//  * ni_keys_filter      graph.py:186-196   the same, incrementally (after a
+//                                           merge / when maps leave the loop)
 //  * ni_quotient_build   solver.py:153-180  static structure of the pair system
 //                                           (pair runs, component incidence,
-//                                           Laplacian sparsity) per partition
+//                                           Laplacian sparsity, per-map edge
+//                                           ranges) of the batch's partition
 //  * ni_scale_step       solver.py:253-303  weights (K4), segmented pair sums
-//                                           (K5), small CG (K6), residuals +
-//                                           energy, z += s[label] (K7,
-//                                           pipeline.py:181-182)
+//                                           (K5), one CG per map (K6),
+//                                           residuals + per-map energy, z +=
+//                                           s[label] (K7, pipeline.py:181-182)
 //  * ni_merge            graph.py:207-250 + pipeline.py:187-203  (K8)
 //
-// Every floating-point sum runs in a fixed order (runs sorted by edge index,
-// block partials summed in block order), so reruns are bit-identical.
+// Component ids are the batch's global labels: map m owns [first[m],
+// first[m] + count[m]) (first[] fixed, count[] shrinking with merges); no
+// edge, pair or part ever spans two maps, so the batch system is block
+// diagonal and every per-map quantity (CG scalars, energy, merge ranks) is a
+// segmented reduction.  Every floating-point sum runs in a fixed order (runs
+// sorted by edge index, one block per map for per-map sums), so reruns are
+// bit-identical and independent of which other maps share the batch.
 #include <cooperative_groups.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <vector>
 
 #include "ni_common.cuh"
 
@@ -55,11 +65,11 @@ __global__ void compact_kernel(const int32_t* __restrict__ flag, const int32_t* 
 // ------------------------------------------------------- quotient layout
 
 struct Quot {
-  int K, C;
+  int K, C, B;
   int32_t* ea;        // [K] pixel a
   int32_t* eb;        // [K] pixel b
   int32_t* ek;        // [K] direction
-  int32_t* pa;        // [K] component of a (local, 0..C-1)
+  int32_t* pa;        // [K] component of a (global id, 0..C-1)
   int32_t* pb;        // [K] component of b
   int32_t* order;     // [K] edges sorted by (min, max) component pair
   int32_t* pstart;    // [K+1] pair runs in `order`; first U+1 used
@@ -71,6 +81,7 @@ struct Quot {
   int32_t* lcol;      // [2K] column
   int32_t* lpair;     // [2K] pair index
   int32_t* nU;        // [1]
+  int32_t* estart;    // [B+1] edges of map m: [estart[m], estart[m+1]) (keys are map-major)
   // scratch used while building
   long long* k64a;
   long long* k64b;
@@ -83,10 +94,11 @@ struct Quot {
   void* scan_ws;
 };
 
-static void carve_quot(Carver& c, Quot& q, int K, int C) {
+static void carve_quot(Carver& c, Quot& q, int K, int C, int B) {
   const int64_t K2 = 2 * int64_t(K) + 1;
   q.K = K;
   q.C = C;
+  q.B = B;
   q.ea = c.take<int32_t>(K + 1);
   q.eb = c.take<int32_t>(K + 1);
   q.ek = c.take<int32_t>(K + 1);
@@ -102,6 +114,7 @@ static void carve_quot(Carver& c, Quot& q, int K, int C) {
   q.lcol = c.take<int32_t>(K2);
   q.lpair = c.take<int32_t>(K2);
   q.nU = c.take<int32_t>(1);
+  q.estart = c.take<int32_t>(B + 1);
   q.k64a = c.take<long long>(K2);
   q.k64b = c.take<long long>(K2);
   q.v32a = c.take<int32_t>(K2);
@@ -120,14 +133,13 @@ static void carve_quot(Carver& c, Quot& q, int K, int C) {
 
 template <int CONN>
 __global__ void quot_edges_kernel(const int32_t* __restrict__ keys, int K,
-                                  const int32_t* __restrict__ labels, int label_base, int W, int C,
-                                  Quot q) {
+                                  const int32_t* __restrict__ labels, int W, int C, Quot q) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K; e += gridDim.x * blockDim.x) {
     const int32_t key = keys[e];
     const int32_t a = key / KF, k = key % KF;
     const int32_t b = a + fwd_dv(CONN, k) * W + fwd_du(CONN, k);
-    const int32_t la = labels[a] - label_base, lb = labels[b] - label_base;
+    const int32_t la = labels[a], lb = labels[b];
     q.ea[e] = a;
     q.eb[e] = b;
     q.ek[e] = k;
@@ -142,6 +154,21 @@ __global__ void quot_edges_kernel(const int32_t* __restrict__ keys, int K,
     q.flag[2 * e] = la;
     q.flag[2 * e + 1] = lb;
   }
+}
+
+// Per-map edge ranges: keys are ascending pixel-edge ids, map-major.
+__global__ void edge_ranges_kernel(const int32_t* __restrict__ keys, int K, int B,
+                                   int64_t keys_per_map, int32_t* __restrict__ estart) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m > B) return;
+  const int64_t target = int64_t(m) * keys_per_map;
+  int lo = 0, hi = K;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (int64_t(keys[mid]) < target) lo = mid + 1;
+    else hi = mid;
+  }
+  estart[m] = lo;
 }
 
 __global__ void pair_runs_kernel(const long long* __restrict__ sk, int K, int C,
@@ -201,21 +228,67 @@ static int end_bits_for(int64_t maxval) {
   return b;
 }
 
+// Keep inter keys of kept maps whose endpoints carry different labels.
+template <int CONN>
+__global__ void keys_flag_kernel(const int32_t* __restrict__ keys, int K,
+                                 const int32_t* __restrict__ labels,
+                                 const uint8_t* __restrict__ map_keep, int64_t per_map, int W,
+                                 int32_t* __restrict__ flag) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K; e += gridDim.x * blockDim.x) {
+    const int32_t key = keys[e];
+    const int32_t a = key / KF, k = key % KF;
+    const int32_t b = a + fwd_dv(CONN, k) * W + fwd_du(CONN, k);
+    flag[e] = map_keep[a / per_map] && labels[a] != labels[b];
+  }
+}
+
+__global__ void keys_compact_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ flag,
+                                    const int32_t* __restrict__ pos, int K,
+                                    int32_t* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K; e += gridDim.x * blockDim.x)
+    if (flag[e]) out[pos[e]] = keys[e];
+}
+
 // ------------------------------------------------------------ scale step
 
+// Per-map tables, copied from the host into the workspace each call.
+struct Maps {
+  int B, nact;
+  int32_t* first;   // [B+1]
+  int32_t* count;   // [B]
+  int32_t* active;  // [nact] maps taking part in this call
+};
+
+static void carve_maps(Carver& c, Maps& mp, int B) {
+  mp.B = B;
+  mp.first = c.take<int32_t>(B + 1);
+  mp.count = c.take<int32_t>(B + 1);
+  mp.active = c.take<int32_t>(B + 1);
+}
+
+static int upload_maps(Maps& mp, const int32_t* first, const int32_t* count, const int32_t* active,
+                       int nact, cudaStream_t s) {
+  mp.nact = nact;
+  NI_CUDA_TRY(cudaMemcpyAsync(mp.first, first, sizeof(int32_t) * (mp.B + 1), cudaMemcpyHostToDevice, s));
+  NI_CUDA_TRY(cudaMemcpyAsync(mp.count, count, sizeof(int32_t) * mp.B, cudaMemcpyHostToDevice, s));
+  if (nact > 0)
+    NI_CUDA_TRY(cudaMemcpyAsync(mp.active, active, sizeof(int32_t) * nact, cudaMemcpyHostToDevice, s));
+  return NI_OK;
+}
+
 struct StepWs {
-  double *wa, *wb, *ba, *bb, *S, *diag, *rhs, *s, *r, *p0, *p1, *q, *part;
-  double* epart;
-  int32_t *anyflag, *parent, *pflag, *prank, *ptotal, *pkey, *pkey_s, *pval, *pval_s, *okflag;
+  double *wa, *wb, *ba, *bb, *S, *diag, *rhs, *r, *p0, *p1, *q, *part;
+  int32_t *parent, *pkey, *pkey_s, *pval, *pval_s;
+  Maps mp;
   void* sort_ws;
   size_t sort_bytes;
-  void* scan_ws;
 };
 
 constexpr int kCgThreads = 512;
-constexpr int kResBlocks = 296;
+constexpr int kBlockCgMax = 8192;  // maps up to this many components: one CTA each
 
-static void carve_step(Carver& c, StepWs& w, int K, int C) {
+static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
   w.wa = c.take<double>(K + 1);
   w.wb = c.take<double>(K + 1);
   w.ba = c.take<double>(K + 1);
@@ -223,28 +296,21 @@ static void carve_step(Carver& c, StepWs& w, int K, int C) {
   w.S = c.take<double>(K + 1);
   w.diag = c.take<double>(C + 1);
   w.rhs = c.take<double>(C + 1);
-  w.s = c.take<double>(C + 1);
   w.r = c.take<double>(C + 1);
   w.p0 = c.take<double>(C + 1);
   w.p1 = c.take<double>(C + 1);
   w.q = c.take<double>(C + 1);
   w.part = c.take<double>(4 * kSMs + 8);
-  w.epart = c.take<double>(kResBlocks + 1);
-  w.anyflag = c.take<int32_t>(1);
-  w.okflag = c.take<int32_t>(1);
   w.parent = c.take<int32_t>(C + 1);
-  w.pflag = c.take<int32_t>(C + 1);
-  w.prank = c.take<int32_t>(C + 1);
-  w.ptotal = c.take<int32_t>(1);
   w.pkey = c.take<int32_t>(C + 1);
   w.pkey_s = c.take<int32_t>(C + 1);
   w.pval = c.take<int32_t>(C + 1);
   w.pval_s = c.take<int32_t>(C + 1);
+  carve_maps(c, w.mp, B);
   w.sort_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, w.sort_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
                                   (const int32_t*)nullptr, (int32_t*)nullptr, C + 1);
   w.sort_ws = c.take<char>(w.sort_bytes);
-  w.scan_ws = c.take<char>(scan_ws_bytes(C + 2));
 }
 
 __device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
@@ -337,7 +403,9 @@ __global__ void pair_sum_kernel(Quot q, StepWs w, const int32_t* __restrict__ nU
 }
 
 // K5b: diagonal and A^T W b per component, summed over its incident edges in
-// edge order (solver.py:108-111).  One warp per component.
+// edge order (solver.py:108-111).  One warp per component.  A map whose
+// A^T W b vanishes (solver.py:112-113) needs no special case: its CG starts
+// from b = 0 and stops at once with s = 0.
 __global__ void comp_sum_kernel(Quot q, StepWs w) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -356,7 +424,6 @@ __global__ void comp_sum_kernel(Quot q, StepWs w) {
     if (lane == 0) {
       w.diag[c] = d;
       w.rhs[c] = r;
-      if (r != 0.0) atomicOr(w.anyflag, 1);
     }
   }
 }
@@ -410,9 +477,98 @@ __global__ void part_sub_kernel(StepWs w, int C) {
     w.rhs[c] = w.rhs[c] - w.r[c];
 }
 
-// K6: scipy-equivalent CG on the component Laplacian (solver.py:97-122).
-// Cooperative kernel; every block redundantly sums the per-block partials in
-// block order, so all blocks agree bit for bit on every scalar.
+// K6: scipy-equivalent CG on one map's component Laplacian (solver.py:97-122):
+// x0 = 0, stop when ||r|| < rtol ||b|| at the top of an iteration, at most
+// maxiter = max(cg_max_iters, C_m) iterations.  Rows [c0, c1) are the map's
+// components; its Laplacian never references another map's columns.
+struct CgArgs {
+  int c0, c1, maxiter;
+  double rtol;
+  double* s;     // the map's scales (global id space)
+  int32_t* ok;   // the map's "converged" flag
+};
+
+// apply the Laplacian to p = r + beta pold for rows [c0, c1) with stride
+template <class Sum>
+__device__ __forceinline__ double cg_sweep(const Quot& q, const StepWs& w, const CgArgs& g,
+                                           int tid, int stride, double beta, const double* pold,
+                                           double* pnew) {
+  double pq = 0.0;
+  for (int c = g.c0 + tid; c < g.c1; c += stride) {
+    const double pc = w.r[c] + beta * pold[c];
+    double acc = w.diag[c] * pc;
+    for (int j = q.lstart[c]; j < q.lstart[c + 1]; ++j) {
+      const int nb = q.lcol[j];
+      acc -= w.S[q.lpair[j]] * (w.r[nb] + beta * pold[nb]);
+    }
+    pnew[c] = pc;
+    w.q[c] = acc;
+    pq += pc * acc;
+  }
+  return pq;
+}
+
+// One CTA per map (maps with <= kBlockCgMax components): every reduction is
+// a block reduction, so the whole solve runs without a grid barrier.
+__global__ void __launch_bounds__(kCgThreads) scale_cg_block_kernel(Quot q, StepWs w, double rtol,
+                                                                    int cg_max_iters, double* s,
+                                                                    int32_t* ok_out) {
+  __shared__ double red[32];
+  const int m = w.mp.active[blockIdx.x];
+  const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
+  if (n > kBlockCgMax) return;  // solved by the cooperative kernel
+  const int tid = threadIdx.x, stride = blockDim.x;
+  const int maxiter = cg_max_iters > n ? cg_max_iters : n;
+  double rr = 0.0;
+  for (int c = c0 + tid; c < c1; c += stride) {
+    const double b = w.rhs[c];
+    s[c] = 0.0;
+    w.r[c] = b;
+    w.p0[c] = 0.0;
+    rr += b * b;
+  }
+  rr = block_sum(rr, red);
+  const double bnrm = sqrt(rr);
+  if (bnrm == 0.0) {
+    if (tid == 0) ok_out[m] = 1;
+    return;
+  }
+  const double atol = rtol * bnrm;
+  double rho_prev = 0.0;
+  double* pold = w.p0;
+  double* pnew = w.p1;
+  int ok = 0;
+  CgArgs g{c0, c1, maxiter, rtol, s, ok_out};
+  for (int it = 0; it < maxiter; ++it) {
+    if (sqrt(rr) < atol) {
+      ok = 1;
+      break;
+    }
+    const double rho = rr;
+    const double beta = it == 0 ? 0.0 : rho / rho_prev;
+    __syncthreads();  // every thread's reads of the previous r / pold are done
+    double pq = cg_sweep<int>(q, w, g, tid, stride, beta, pold, pnew);
+    pq = block_sum(pq, red);
+    const double alpha = rho / pq;
+    double rn = 0.0;
+    for (int c = c0 + tid; c < c1; c += stride) {
+      s[c] += alpha * pnew[c];
+      const double r2 = w.r[c] - alpha * w.q[c];
+      w.r[c] = r2;
+      rn += r2 * r2;
+    }
+    rr = block_sum(rn, red);
+    rho_prev = rho;
+    double* t = pold;
+    pold = pnew;
+    pnew = t;
+  }
+  if (tid == 0) ok_out[m] = ok;
+}
+
+// Maps with more components: one cooperative launch per map; every block
+// redundantly sums the per-block partials in block order, so all blocks
+// agree bit for bit on every scalar.
 __device__ __forceinline__ double grid_sum(cg::grid_group& grid, double v, double* part, int slot,
                                            double* red) {
   v = block_sum(v, red);
@@ -423,17 +579,15 @@ __device__ __forceinline__ double grid_sum(cg::grid_group& grid, double v, doubl
   return t;
 }
 
-__global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, double rtol,
-                                                              int maxiter) {
+__global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, CgArgs g) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
-  const int C = q.C;
-  const int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid0 = g.c0 + blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
   double rr = 0.0;
-  for (int c = tid0; c < C; c += stride) {
+  for (int c = tid0; c < g.c1; c += stride) {
     const double b = w.rhs[c];
-    w.s[c] = 0.0;
+    g.s[c] = 0.0;
     w.r[c] = b;
     w.p0[c] = 0.0;
     rr += b * b;
@@ -441,38 +595,27 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, 
   rr = grid_sum(grid, rr, w.part, 0, red);
   const double bnrm = sqrt(rr);
   if (bnrm == 0.0) {
-    if (tid0 == 0) w.okflag[0] = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) g.ok[0] = 1;
     return;
   }
-  const double atol = rtol * bnrm;
+  const double atol = g.rtol * bnrm;
   double rho_prev = 0.0;
   double* pold = w.p0;
   double* pnew = w.p1;
   int ok = 0;
-  for (int it = 0; it < maxiter; ++it) {
+  for (int it = 0; it < g.maxiter; ++it) {
     if (sqrt(rr) < atol) {
       ok = 1;
       break;
     }
     const double rho = rr;
     const double beta = it == 0 ? 0.0 : rho / rho_prev;
-    double pq = 0.0;
-    for (int c = tid0; c < C; c += stride) {
-      const double pc = w.r[c] + beta * pold[c];
-      double acc = w.diag[c] * pc;
-      for (int j = q.lstart[c]; j < q.lstart[c + 1]; ++j) {
-        const int nb = q.lcol[j];
-        acc -= w.S[q.lpair[j]] * (w.r[nb] + beta * pold[nb]);
-      }
-      pnew[c] = pc;
-      w.q[c] = acc;
-      pq += pc * acc;
-    }
+    double pq = cg_sweep<int>(q, w, g, tid0 - g.c0, stride, beta, pold, pnew);
     pq = grid_sum(grid, pq, w.part, 1, red);
     const double alpha = rho / pq;
     double rn = 0.0;
-    for (int c = tid0; c < C; c += stride) {
-      w.s[c] += alpha * pnew[c];
+    for (int c = tid0; c < g.c1; c += stride) {
+      g.s[c] += alpha * pnew[c];
       const double r2 = w.r[c] - alpha * w.q[c];
       w.r[c] = r2;
       rn += r2 * r2;
@@ -483,17 +626,20 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, 
     pold = pnew;
     pnew = t;
   }
-  if (tid0 == 0) w.okflag[0] = ok;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g.ok[0] = ok;
 }
 
-// K7a: residual rows and the energy (solver.py:301-302)
-__global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, double* __restrict__ scales,
+// K7a: residual rows and the per-map energy (solver.py:301-302); one CTA
+// per map over the map's edge range, in edge order.
+__global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const double* __restrict__ s,
                                                        double* __restrict__ residual,
-                                                       double* __restrict__ weights) {
+                                                       double* __restrict__ weights,
+                                                       double* __restrict__ energy_out) {
   __shared__ double red[32];
+  const int m = w.mp.active[blockIdx.x];
   double en = 0.0;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < q.K; e += gridDim.x * blockDim.x) {
-    const double sa = w.s[q.pa[e]], sb = w.s[q.pb[e]];
+  for (int e = q.estart[m] + threadIdx.x; e < q.estart[m + 1]; e += blockDim.x) {
+    const double sa = s[q.pa[e]], sb = s[q.pb[e]];
     const double ra = sa - sb - w.ba[e];
     const double rb = sb - sa - w.bb[e];
     residual[2 * e] = ra;
@@ -503,78 +649,102 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, double*
     en += ra * (w.wa[e] * ra) + rb * (w.wb[e] * rb);
   }
   en = block_sum(en, red);
-  if (threadIdx.x == 0) w.epart[blockIdx.x] = en;
+  if (threadIdx.x == 0) energy_out[m] = en;
 }
 
-__global__ void energy_final_kernel(StepWs w, int nblocks, double* __restrict__ scales_out, int C,
-                                    double* __restrict__ energy_out, int32_t* __restrict__ ok_out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double e = 0.0;
-    for (int b = 0; b < nblocks; ++b) e += w.epart[b];
-    energy_out[0] = e;
-    ok_out[0] = w.okflag[0];
-  }
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x)
-    scales_out[c] = w.s[c];
-}
-
-// K7b: z[valid] += s[label] on the map's pixel range (pipeline.py:181-182)
+// K7b: z[valid] += s[label] on the active maps' pixels (pipeline.py:181-182)
 __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__ labels,
-                             const double* __restrict__ s, int label_base, int64_t p0, int64_t p1) {
-  for (int64_t i = p0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p1;
-       i += int64_t(gridDim.x) * blockDim.x) {
+                             const double* __restrict__ s, const int32_t* __restrict__ active,
+                             int64_t per_map, int64_t n) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = int64_t(active[j / per_map]) * per_map + j % per_map;
     const int32_t l = labels[i];
-    if (l >= 0) z[i] += s[l - label_base];
+    if (l >= 0) z[i] += s[l];
   }
 }
 
-__global__ void set_int_kernel(int32_t* __restrict__ a, int v) { a[0] = v; }
+__global__ void set_ok_kernel(int32_t* __restrict__ ok, const int32_t* __restrict__ active, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) ok[active[j]] = 1;
+}
 
-__global__ void zero_kernel(double* __restrict__ a, int n) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) a[j] = 0.0;
+__global__ void zero_map_kernel(double* __restrict__ energy, const int32_t* __restrict__ active,
+                                int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) energy[active[j]] = 0.0;
 }
 
 // ----------------------------------------------------------------- merge
 
 struct MergeWs {
-  int32_t *sel, *parent, *flag, *rank, *total;
-  double* epart;
+  int32_t *sel, *parent, *flag, *rank, *cmap;
+  uint8_t* merging;  // [B]
+  Maps mp;
   void* scan_ws;
 };
 
-static void carve_merge(Carver& c, MergeWs& m, int K, int C) {
+static void carve_merge(Carver& c, MergeWs& m, int K, int C, int B) {
   m.sel = c.take<int32_t>(C + 1);
   m.parent = c.take<int32_t>(C + 1);
-  m.flag = c.take<int32_t>(C + 1);
-  m.rank = c.take<int32_t>(C + 1);
-  m.total = c.take<int32_t>(1);
-  m.epart = c.take<double>(kResBlocks + 1);
+  m.flag = c.take<int32_t>(C + 2);
+  m.rank = c.take<int32_t>(C + 2);
+  m.cmap = c.take<int32_t>(C + 1);
+  m.merging = c.take<uint8_t>(B + 1);
+  carve_maps(c, m.mp, B);
   m.scan_ws = c.take<char>(scan_ws_bytes(C + 2));
 }
 
+// map of every live component id (-1: id above its map's current count)
+__global__ void comp_map_kernel(MergeWs m, int C) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    int lo = 0, hi = m.mp.B;  // last map with first <= c
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (m.mp.first[mid] <= c) lo = mid;
+      else hi = mid;
+    }
+    m.cmap[c] = c < m.mp.first[lo] + m.mp.count[lo] ? lo : -1;
+  }
+}
+
+__global__ void merging_flags_kernel(MergeWs m) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= m.mp.B; j += gridDim.x * blockDim.x)
+    m.merging[j] = 0;
+}
+
+__global__ void merging_set_kernel(MergeWs m) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m.mp.nact) m.merging[m.mp.active[j]] = 1;
+}
+
 // argmin over incident inter edges of (|residual_a|, edge index)
-// (graph.py:230-239); one warp per component, lexicographic warp argmin.
+// (graph.py:230-239); one warp per component of a merging map,
+// lexicographic warp argmin.
 __global__ void merge_select_kernel(Quot q, const double* __restrict__ residual, MergeWs m) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < q.C; c += warps) {
+    const int mc = m.cmap[c];
     int best_e = -1;
     double best = 0.0;
-    for (int j = q.cstart[c] + lane; j < q.cstart[c + 1]; j += 32) {
-      const int e = q.cent[j] >> 1;
-      const double r = fabs(residual[2 * e]);
-      if (best_e < 0 || r < best || (r == best && e < best_e)) {
-        best = r;
-        best_e = e;
+    if (mc >= 0 && m.merging[mc]) {
+      for (int j = q.cstart[c] + lane; j < q.cstart[c + 1]; j += 32) {
+        const int e = q.cent[j] >> 1;
+        const double r = fabs(residual[2 * e]);
+        if (best_e < 0 || r < best || (r == best && e < best_e)) {
+          best = r;
+          best_e = e;
+        }
       }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
-      if (oe >= 0 && (best_e < 0 || ob < best || (ob == best && oe < best_e))) {
-        best = ob;
-        best_e = oe;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+        if (oe >= 0 && (best_e < 0 || ob < best || (ob == best && oe < best_e))) {
+          best = ob;
+          best_e = oe;
+        }
       }
     }
     if (lane == 0) {
@@ -592,44 +762,56 @@ __global__ void merge_union_kernel(Quot q, MergeWs m) {
 }
 
 __global__ void merge_flatten_kernel(MergeWs m, int C) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x) {
+    if (c == C) {
+      m.flag[C] = 0;
+      continue;
+    }
     const int r = uf_find(m.parent, c);
     m.parent[c] = r;
-    m.flag[c] = r == c;
+    m.flag[c] = r == c && m.cmap[c] >= 0;
   }
 }
 
-__global__ void merge_relabel_kernel(int32_t* __restrict__ labels, const MergeWs m, int label_base,
-                                     int64_t p0, int64_t p1) {
-  for (int64_t i = p0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p1;
-       i += int64_t(gridDim.x) * blockDim.x) {
+// new count of every map (unchanged for maps that do not merge)
+__global__ void merge_counts_kernel(MergeWs m, int32_t* __restrict__ new_count) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m.mp.B; j += gridDim.x * blockDim.x) {
+    const int f = m.mp.first[j];
+    new_count[j] = m.rank[f + m.mp.count[j]] - m.rank[f];
+  }
+}
+
+__global__ void merge_relabel_kernel(int32_t* __restrict__ labels, const MergeWs m, int64_t per_map,
+                                     int64_t n) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int mm = m.mp.active[j / per_map];
+    const int64_t i = int64_t(mm) * per_map + j % per_map;
     const int32_t l = labels[i];
-    if (l >= 0) labels[i] = label_base + m.rank[m.parent[l - label_base]];
+    if (l >= 0) {
+      const int f = m.mp.first[mm];
+      labels[i] = f + m.rank[m.parent[l]] - m.rank[f];
+    }
   }
 }
 
-// energy restricted to edges that stay inter-component (pipeline.py:196-203)
+// energy restricted to edges that stay inter-component (pipeline.py:196-203);
+// one CTA per merging map, in edge order
 __global__ void __launch_bounds__(256) merge_energy_kernel(Quot q, const MergeWs m,
                                                            const double* __restrict__ residual,
-                                                           const double* __restrict__ weights) {
+                                                           const double* __restrict__ weights,
+                                                           double* __restrict__ energy_out) {
   __shared__ double red[32];
+  const int mm = m.mp.active[blockIdx.x];
   double en = 0.0;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < q.K; e += gridDim.x * blockDim.x) {
+  for (int e = q.estart[mm] + threadIdx.x; e < q.estart[mm + 1]; e += blockDim.x) {
     if (m.parent[q.pa[e]] != m.parent[q.pb[e]]) {
       const double ra = residual[2 * e], rb = residual[2 * e + 1];
       en += ra * (weights[2 * e] * ra) + rb * (weights[2 * e + 1] * rb);
     }
   }
   en = block_sum(en, red);
-  if (threadIdx.x == 0) m.epart[blockIdx.x] = en;
-}
-
-__global__ void merge_final_kernel(const MergeWs m, int nblocks, double* __restrict__ energy_out,
-                                   int32_t* __restrict__ count_out) {
-  double e = 0.0;
-  for (int b = 0; b < nblocks; ++b) e += m.epart[b];
-  energy_out[0] = e;
-  count_out[0] = m.total[0];
+  if (threadIdx.x == 0) energy_out[mm] = en;
 }
 
 }  // namespace ni
@@ -677,64 +859,111 @@ extern "C" int ni_inter_edges(const int32_t* labels, const uint8_t* eflags, int 
   return NI_OK;
 }
 
-extern "C" int ni_quotient_workspace_size(int K, int count, size_t* bytes) {
-  NI_CHECK_ARG(bytes && K >= 0 && count >= 0, "bad argument");
+extern "C" int ni_keys_filter_workspace_size(int K, size_t* bytes) {
+  NI_CHECK_ARG(bytes && K >= 0, "bad argument");
   Sizer z;
-  Quot q;
-  carve_quot(z, q, K, count);
+  z.take<int32_t>(K + 1);
+  z.take<int32_t>(K + 1);
+  z.take<char>(scan_ws_bytes(K + 1));
   *bytes = z.used;
   return NI_OK;
 }
 
-// Static structure of the inter system for one partition (one map).
-// SYNCHRONOUS (reads back the number of distinct component pairs).
-extern "C" int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int label_base,
-                                 int count, int W, int connectivity, void* quot_ws,
-                                 size_t quot_bytes, int32_t* n_pairs_host, ni_stream_t stream) {
+extern "C" int ni_keys_filter(const int32_t* keys, int K, const int32_t* labels,
+                              const uint8_t* map_keep, int H, int W, int connectivity,
+                              int32_t* keys_out, int32_t* n_out, void* workspace,
+                              size_t workspace_bytes, ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
-  NI_CHECK_ARG(K >= 0 && count >= 1, "bad sizes");
+  NI_CHECK_ARG(K >= 0 && keys_out != keys, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver c(workspace, workspace_bytes);
+  int32_t* flag = c.take<int32_t>(K + 1);
+  int32_t* pos = c.take<int32_t>(K + 1);
+  void* sws = c.take<char>(scan_ws_bytes(K + 1));
+  if (!c.ok() || !workspace) {
+    set_error("ni_keys_filter: workspace too small");
+    return NI_ERR_WORKSPACE;
+  }
+  if (K == 0) {
+    NI_CUDA_TRY(cudaMemsetAsync(n_out, 0, sizeof(int32_t), s));
+    return NI_OK;
+  }
+  const int64_t per_map = int64_t(H) * W;
+  if (connectivity == 8)
+    NI_COUNT_LAUNCH(), keys_flag_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, map_keep,
+                                                                       per_map, W, flag);
+  else
+    NI_COUNT_LAUNCH(), keys_flag_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, map_keep,
+                                                                       per_map, W, flag);
+  NI_LAUNCH_CHECK();
+  NI_TRY(exclusive_scan_i32(flag, pos, K, n_out, sws, s));
+  NI_COUNT_LAUNCH(), keys_compact_kernel<<<blocks_for(K), 256, 0, s>>>(keys, flag, pos, K, keys_out);
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}
+
+extern "C" int ni_quotient_workspace_size(int K, int count, int B, size_t* bytes) {
+  NI_CHECK_ARG(bytes && K >= 0 && count >= 0 && B >= 1, "bad argument");
+  Sizer z;
+  Quot q;
+  carve_quot(z, q, K, count, B);
+  *bytes = z.used;
+  return NI_OK;
+}
+
+// Static structure of the inter system of the batch's partition.
+// SYNCHRONOUS (reads back the number of distinct component pairs and, if
+// map_edges_host is given, the B per-map edge counts).
+extern "C" int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int count,
+                                 int B, int H, int W, int connectivity, void* quot_ws,
+                                 size_t quot_bytes, int32_t* n_pairs_host, int32_t* map_edges_host,
+                                 ni_stream_t stream) {
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  NI_CHECK_ARG(K >= 0 && count >= 1 && B >= 1, "bad sizes");
   NI_CHECK_ARG((int64_t)count * count < (int64_t(1) << 62), "too many components");
   cudaStream_t s = (cudaStream_t)stream;
   Carver c(quot_ws, quot_bytes);
   Quot q;
-  carve_quot(c, q, K, count);
+  carve_quot(c, q, K, count, B);
   if (!c.ok() || !quot_ws) {
     set_error("ni_quotient_build: workspace too small");
     return NI_ERR_WORKSPACE;
   }
   const int C = count;
+  const int kf = connectivity == 8 ? 4 : 2;
+  NI_COUNT_LAUNCH(), edge_ranges_kernel<<<div_up(B + 1, 128), 128, 0, s>>>(
+                         keys, K, B, int64_t(H) * W * kf, q.estart);
+  NI_LAUNCH_CHECK();
+  int32_t U = 0;
   if (K == 0) {
     NI_CUDA_TRY(cudaMemsetAsync(q.nU, 0, sizeof(int32_t), s));
     NI_CUDA_TRY(cudaMemsetAsync(q.cstart, 0, sizeof(int32_t) * (C + 1), s));
     NI_CUDA_TRY(cudaMemsetAsync(q.lstart, 0, sizeof(int32_t) * (C + 1), s));
-    if (n_pairs_host) *n_pairs_host = 0;
-    return NI_OK;
-  }
-  if (connectivity == 8)
-    NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
-  else
-    NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
-  NI_LAUNCH_CHECK();
-  const int pbits = end_bits_for((int64_t)C * C);
-  size_t sb = q.sort_bytes;
-  // (1) edges sorted by component pair (stable => edge order within a run)
-  NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.order, K, 0,
-                                              pbits, s));
-  NI_COUNT_LAUNCH(), run_flags_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, q.flag);
-  NI_LAUNCH_CHECK();
-  // q.v32b holds incidence values; use q.lcol as scratch for run positions
-  NI_TRY(exclusive_scan_i32(q.flag, q.lcol, K, q.nU, q.scan_ws, s));
-  NI_COUNT_LAUNCH(), pair_runs_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, C, q.lcol, q);
-  NI_LAUNCH_CHECK();
-  NI_COUNT_LAUNCH(), set_tail_kernel<<<1, 1, 0, s>>>(q.pstart, q.nU, K);
-  NI_LAUNCH_CHECK();
-  // (2) incidence lists: (component, 2e+side) sorted by component, stable
-  // keys are in q.flag? rebuild them (flag was overwritten by run flags)
-  {
+  } else {
     if (connectivity == 8)
-      NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+      NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, W, C, q);
     else
-      NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, label_base, W, C, q);
+      NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, W, C, q);
+    NI_LAUNCH_CHECK();
+    const int pbits = end_bits_for((int64_t)C * C);
+    size_t sb = q.sort_bytes;
+    // (1) edges sorted by component pair (stable => edge order within a run)
+    NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.order, K,
+                                                0, pbits, s));
+    NI_COUNT_LAUNCH(), run_flags_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, q.flag);
+    NI_LAUNCH_CHECK();
+    // q.lcol as scratch for run positions
+    NI_TRY(exclusive_scan_i32(q.flag, q.lcol, K, q.nU, q.scan_ws, s));
+    NI_COUNT_LAUNCH(), pair_runs_kernel<<<blocks_for(K), 256, 0, s>>>(q.k64b, K, C, q.lcol, q);
+    NI_LAUNCH_CHECK();
+    NI_COUNT_LAUNCH(), set_tail_kernel<<<1, 1, 0, s>>>(q.pstart, q.nU, K);
+    NI_LAUNCH_CHECK();
+    // (2) incidence lists: (component, 2e+side) sorted by component, stable
+    // (the incidence keys in q.flag were overwritten by the run flags)
+    if (connectivity == 8)
+      NI_COUNT_LAUNCH(), quot_edges_kernel<8><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, W, C, q);
+    else
+      NI_COUNT_LAUNCH(), quot_edges_kernel<4><<<blocks_for(K), 256, 0, s>>>(keys, K, labels, W, C, q);
     NI_LAUNCH_CHECK();
     const int cbits = end_bits_for(C);
     sb = q.sort_bytes;
@@ -744,171 +973,184 @@ extern "C" int ni_quotient_build(const int32_t* keys, int K, const int32_t* labe
     NI_COUNT_LAUNCH(), hist_kernel<<<blocks_for(2 * int64_t(K)), 256, 0, s>>>(q.flag, 2 * K, q.hist);
     NI_LAUNCH_CHECK();
     NI_TRY(exclusive_scan_i32(q.hist, q.cstart, C + 1, nullptr, q.scan_ws, s));
+    NI_CUDA_TRY(cudaMemcpyAsync(&U, q.nU, sizeof(U), cudaMemcpyDeviceToHost, s));
+    NI_CUDA_TRY(cudaStreamSynchronize(s));
+    // (3) Laplacian sparsity: entries (row, col) for both directions of a pair
+    NI_COUNT_LAUNCH(), lap_entries_kernel<<<blocks_for(U), 256, 0, s>>>(q, q.nU);
+    NI_LAUNCH_CHECK();
+    sb = q.sort_bytes;
+    NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.lpair,
+                                                2 * U, 0, pbits, s));
+    NI_COUNT_LAUNCH(), lap_cols_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q, q.k64b, 2 * U);
+    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemsetAsync(q.hist, 0, sizeof(int32_t) * (C + 1), s));
+    NI_COUNT_LAUNCH(), hist_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q.flag, 2 * U, q.hist);
+    NI_LAUNCH_CHECK();
+    NI_TRY(exclusive_scan_i32(q.hist, q.lstart, C + 1, nullptr, q.scan_ws, s));
   }
-  int32_t U = 0;
-  NI_CUDA_TRY(cudaMemcpyAsync(&U, q.nU, sizeof(U), cudaMemcpyDeviceToHost, s));
-  NI_CUDA_TRY(cudaStreamSynchronize(s));
-  // (3) Laplacian sparsity: entries (row, col) for both directions of a pair
-  NI_COUNT_LAUNCH(), lap_entries_kernel<<<blocks_for(U), 256, 0, s>>>(q, q.nU);
-  NI_LAUNCH_CHECK();
-  sb = q.sort_bytes;
-  NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(q.sort_ws, sb, q.k64a, q.k64b, q.v32a, q.lpair, 2 * U,
-                                              0, pbits, s));
-  NI_COUNT_LAUNCH(), lap_cols_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q, q.k64b, 2 * U);
-  NI_LAUNCH_CHECK();
-  NI_CUDA_TRY(cudaMemsetAsync(q.hist, 0, sizeof(int32_t) * (C + 1), s));
-  NI_COUNT_LAUNCH(), hist_kernel<<<blocks_for(2 * int64_t(U)), 256, 0, s>>>(q.flag, 2 * U, q.hist);
-  NI_LAUNCH_CHECK();
-  NI_TRY(exclusive_scan_i32(q.hist, q.lstart, C + 1, nullptr, q.scan_ws, s));
+  if (map_edges_host) {
+    std::vector<int32_t> es(B + 1);
+    NI_CUDA_TRY(cudaMemcpyAsync(es.data(), q.estart, sizeof(int32_t) * (B + 1),
+                                cudaMemcpyDeviceToHost, s));
+    NI_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int m = 0; m < B; ++m) map_edges_host[m] = es[m + 1] - es[m];
+  }
   if (n_pairs_host) *n_pairs_host = U;
   return NI_OK;
 }
 
-extern "C" int ni_scale_step_workspace_size(int K, int count, size_t* bytes) {
-  NI_CHECK_ARG(bytes, "null pointer");
+extern "C" int ni_scale_step_workspace_size(int K, int count, int B, size_t* bytes) {
+  NI_CHECK_ARG(bytes && K >= 0 && count >= 0 && B >= 1, "bad argument");
   Sizer z;
   StepWs w;
-  carve_step(z, w, K, count);
+  carve_step(z, w, K, count, B);
   *bytes = z.used;
   return NI_OK;
 }
 
-extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count,
-                             const int32_t* labels, int label_base, const double* omega_a,
-                             const double* omega_b, const double* gamma, const uint8_t* eflags,
-                             int B, int H, int W, int connectivity, int model, int map_index, int t,
+extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+                             const int32_t* map_first, const int32_t* map_count,
+                             const int32_t* active, int nact, const int32_t* labels,
+                             const double* omega_a, const double* omega_b, const double* gamma,
+                             const uint8_t* eflags, int H, int W, int connectivity, int model, int t,
                              int alignment_iters, int mode, double k, double outlier_low,
                              double outlier_high, double cg_tol, int cg_max_iters, double* z,
-                             double* scales, double* residual, double* weights, double* energy_out,
-                             int32_t* cg_ok_out, void* workspace, size_t workspace_bytes,
-                             ni_stream_t stream) {
+                             double* scales, double* residual, double* weights,
+                             double* energy_out, int32_t* cg_ok_out, void* workspace,
+                             size_t workspace_bytes, ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
-  NI_CHECK_ARG(count >= 1 && K >= 0, "bad sizes");
+  NI_CHECK_ARG(count >= 1 && K >= 0 && B >= 1 && nact >= 0 && nact <= B, "bad sizes");
+  NI_CHECK_ARG(map_first && map_count && (active || nact == 0), "null map table");
   cudaStream_t s = (cudaStream_t)stream;
   Carver cq(const_cast<void*>(quot_ws), quot_bytes);
   Quot q;
-  carve_quot(cq, q, K, count);
+  carve_quot(cq, q, K, count, B);
   Carver c(workspace, workspace_bytes);
   StepWs w;
-  carve_step(c, w, K, count);
+  carve_step(c, w, K, count, B);
   if (!c.ok() || !workspace || !cq.ok()) {
     set_error("ni_scale_step: workspace too small");
     return NI_ERR_WORKSPACE;
   }
+  if (nact == 0) return NI_OK;
+  NI_TRY(upload_maps(w.mp, map_first, map_count, active, nact, s));
   const int C = count;
   const int64_t npix = int64_t(B) * H * W;
-  if (K == 0) {  // solver.py:293-295
-    NI_COUNT_LAUNCH(), zero_kernel<<<blocks_for(C), 256, 0, s>>>(scales, C);
+  if (K == 0) {  // solver.py:293-295: no inter edge anywhere in the batch
+    NI_COUNT_LAUNCH(), zero_map_kernel<<<div_up(nact, 128), 128, 0, s>>>(energy_out, w.mp.active, nact);
+    NI_COUNT_LAUNCH(), set_ok_kernel<<<div_up(nact, 128), 128, 0, s>>>(cg_ok_out, w.mp.active, nact);
     NI_LAUNCH_CHECK();
-    NI_CUDA_TRY(cudaMemsetAsync(energy_out, 0, sizeof(double), s));
-    NI_COUNT_LAUNCH(), set_int_kernel<<<1, 1, 0, s>>>(cg_ok_out, 1);
-    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemsetAsync(scales, 0, sizeof(double) * C, s));
     return NI_OK;
   }
   const int uniform = t < alignment_iters;
   const double lt = log10(outlier_low), ut = log10(outlier_high);
   if (connectivity == 8)
-    NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
-                                                       npix, uniform, mode, k, lt, ut, outlier_high, w);
+    NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
+                           ut, outlier_high, w);
   else if (model == 0)
-    NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
-                                                       npix, uniform, mode, k, lt, ut, outlier_high, w);
+    NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
+                           ut, outlier_high, w);
   else
-    NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(q, z, omega_a, omega_b, gamma, eflags, H, W,
-                                                       npix, uniform, mode, k, lt, ut, outlier_high, w);
+    NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
+                           ut, outlier_high, w);
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
-  NI_CUDA_TRY(cudaMemsetAsync(w.anyflag, 0, sizeof(int32_t), s));
   NI_COUNT_LAUNCH(), comp_sum_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, w);
   NI_LAUNCH_CHECK();
-  int32_t any = 0;
-  NI_CUDA_TRY(cudaMemcpyAsync(&any, w.anyflag, sizeof(any), cudaMemcpyDeviceToHost, s));
-  NI_CUDA_TRY(cudaStreamSynchronize(s));
-  if (!any) {  // solver.py:112-113
-    NI_COUNT_LAUNCH(), zero_kernel<<<blocks_for(C), 256, 0, s>>>(w.s, C);
-    NI_LAUNCH_CHECK();
-    NI_COUNT_LAUNCH(), set_int_kernel<<<1, 1, 0, s>>>(w.okflag, 1);
-  } else {
-    // remove the roundoff null-space component of A^T W b
-    NI_COUNT_LAUNCH(), part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
-    NI_COUNT_LAUNCH(), part_union_kernel<<<blocks_for(K), 256, 0, s>>>(q, w, q.nU);
-    NI_COUNT_LAUNCH(), part_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
-    NI_LAUNCH_CHECK();
-    size_t sb = w.sort_bytes;
-    NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_ws, sb, w.pkey, w.pkey_s, w.pval, w.pval_s, C,
-                                                0, end_bits_for(C), s));
-    NI_COUNT_LAUNCH(), part_mean_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(w, C);
-    NI_COUNT_LAUNCH(), part_sub_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
-    NI_LAUNCH_CHECK();
-    // K6
-    int dev = 0;
-    NI_CUDA_TRY(cudaGetDevice(&dev));
-    int per_sm = 0;
-    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scale_cg_kernel, kCgThreads, 0));
-    int sms = 0;
-    NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int G = div_up(C, 4 * kCgThreads);
-    const int gmax = per_sm * sms;
-    if (G > gmax) G = gmax;
-    if (G > kSMs) G = kSMs;
-    if (G < 1) G = 1;
-    const int maxiter = cg_max_iters > C ? cg_max_iters : C;
-    double rtol = cg_tol;
-    void* args[] = {&q, &w, &rtol, (void*)&maxiter};
-    NI_COUNT_LAUNCH();
-    NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(G), dim3(kCgThreads), args, 0,
-                                            s));
-  }
-  NI_COUNT_LAUNCH(), residual_kernel<<<kResBlocks, 256, 0, s>>>(q, w, scales, residual, weights);
+  // remove the roundoff null-space component of A^T W b
+  NI_COUNT_LAUNCH(), part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
+  NI_COUNT_LAUNCH(), part_union_kernel<<<blocks_for(K), 256, 0, s>>>(q, w, q.nU);
+  NI_COUNT_LAUNCH(), part_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
   NI_LAUNCH_CHECK();
-  NI_COUNT_LAUNCH(), energy_final_kernel<<<blocks_for(C), 256, 0, s>>>(w, kResBlocks, scales, C, energy_out, cg_ok_out);
+  size_t sb = w.sort_bytes;
+  NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_ws, sb, w.pkey, w.pkey_s, w.pval, w.pval_s, C,
+                                              0, end_bits_for(C), s));
+  NI_COUNT_LAUNCH(), part_mean_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(w, C);
+  NI_COUNT_LAUNCH(), part_sub_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
+  NI_LAUNCH_CHECK();
+  // K6: one CTA per map, and one cooperative launch per large map
+  NI_COUNT_LAUNCH(), scale_cg_block_kernel<<<nact, kCgThreads, 0, s>>>(q, w, cg_tol, cg_max_iters,
+                                                                      scales, cg_ok_out);
+  NI_LAUNCH_CHECK();
+  int G = 0;
+  for (int j = 0; j < nact; ++j) {
+    const int m = active[j];
+    const int n = map_count[m];
+    if (n <= kBlockCgMax) continue;
+    if (G == 0) {
+      int dev = 0, per_sm = 0, sms = 0;
+      NI_CUDA_TRY(cudaGetDevice(&dev));
+      NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scale_cg_kernel, kCgThreads, 0));
+      NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      G = per_sm * sms < kSMs ? per_sm * sms : kSMs;
+    }
+    int g = div_up(n, 4 * kCgThreads);
+    if (g > G) g = G;
+    if (g < 1) g = 1;
+    CgArgs ca{map_first[m], map_first[m] + n, cg_max_iters > n ? cg_max_iters : n, cg_tol, scales,
+              cg_ok_out + m};
+    void* args[] = {&q, &w, &ca};
+    NI_COUNT_LAUNCH();
+    NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(g), dim3(kCgThreads), args,
+                                            0, s));
+  }
+  NI_COUNT_LAUNCH(), residual_kernel<<<nact, 256, 0, s>>>(q, w, scales, residual, weights, energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  NI_COUNT_LAUNCH(), apply_kernel<<<blocks_for(per_map), 256, 0, s>>>(z, labels, w.s, label_base, map_index * per_map,
-                                                   (map_index + 1) * per_map);
+  NI_COUNT_LAUNCH(), apply_kernel<<<blocks_for(nact * per_map), 256, 0, s>>>(
+                         z, labels, scales, w.mp.active, per_map, nact * per_map);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }
 
-extern "C" int ni_merge_workspace_size(int K, int count, size_t* bytes) {
-  NI_CHECK_ARG(bytes, "null pointer");
+extern "C" int ni_merge_workspace_size(int K, int count, int B, size_t* bytes) {
+  NI_CHECK_ARG(bytes && K >= 0 && count >= 0 && B >= 1, "bad argument");
   Sizer z;
   MergeWs m;
-  carve_merge(z, m, K, count);
+  carve_merge(z, m, K, count, B);
   *bytes = z.used;
   return NI_OK;
 }
 
-extern "C" int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int32_t* labels,
-                        int label_base, int H, int W, int map_index, const double* residual,
+extern "C" int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+                        const int32_t* map_first, const int32_t* map_count, const int32_t* merging,
+                        int nmerge, int32_t* labels, int H, int W, const double* residual,
                         const double* weights, int32_t* new_count_out, double* energy_out,
                         void* workspace, size_t workspace_bytes, ni_stream_t stream) {
-  NI_CHECK_ARG(K >= 1 && count >= 1, "merge needs inter edges and components");
+  NI_CHECK_ARG(K >= 1 && count >= 1 && B >= 1 && nmerge >= 1 && nmerge <= B,
+               "merge needs inter edges, components and merging maps");
+  NI_CHECK_ARG(map_first && map_count && merging, "null map table");
   cudaStream_t s = (cudaStream_t)stream;
   Carver cq(const_cast<void*>(quot_ws), quot_bytes);
   Quot q;
-  carve_quot(cq, q, K, count);
+  carve_quot(cq, q, K, count, B);
   Carver c(workspace, workspace_bytes);
   MergeWs m;
-  carve_merge(c, m, K, count);
+  carve_merge(c, m, K, count, B);
   if (!c.ok() || !workspace || !cq.ok()) {
     set_error("ni_merge: workspace too small");
     return NI_ERR_WORKSPACE;
   }
+  NI_TRY(upload_maps(m.mp, map_first, map_count, merging, nmerge, s));
   const int C = count;
+  NI_COUNT_LAUNCH(), comp_map_kernel<<<blocks_for(C), 256, 0, s>>>(m, C);
+  NI_COUNT_LAUNCH(), merging_flags_kernel<<<div_up(B + 1, 256), 256, 0, s>>>(m);
+  NI_COUNT_LAUNCH(), merging_set_kernel<<<div_up(nmerge, 256), 256, 0, s>>>(m);
   NI_COUNT_LAUNCH(), merge_select_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, residual, m);
   NI_COUNT_LAUNCH(), merge_union_kernel<<<blocks_for(C), 256, 0, s>>>(q, m);
-  NI_COUNT_LAUNCH(), merge_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(m, C);
+  NI_COUNT_LAUNCH(), merge_flatten_kernel<<<blocks_for(C + 1), 256, 0, s>>>(m, C);
   NI_LAUNCH_CHECK();
-  NI_TRY(exclusive_scan_i32(m.flag, m.rank, C, m.total, m.scan_ws, s));
-  NI_COUNT_LAUNCH(), merge_energy_kernel<<<kResBlocks, 256, 0, s>>>(q, m, residual, weights);
-  NI_LAUNCH_CHECK();
-  NI_COUNT_LAUNCH(), merge_final_kernel<<<1, 1, 0, s>>>(m, kResBlocks, energy_out, new_count_out);
+  NI_TRY(exclusive_scan_i32(m.flag, m.rank, C + 1, nullptr, m.scan_ws, s));
+  NI_COUNT_LAUNCH(), merge_counts_kernel<<<div_up(B, 256), 256, 0, s>>>(m, new_count_out);
+  NI_COUNT_LAUNCH(), merge_energy_kernel<<<nmerge, 256, 0, s>>>(q, m, residual, weights, energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  NI_COUNT_LAUNCH(), merge_relabel_kernel<<<blocks_for(per_map), 256, 0, s>>>(labels, m, label_base,
-                                                           map_index * per_map,
-                                                           (map_index + 1) * per_map);
+  NI_COUNT_LAUNCH(), merge_relabel_kernel<<<blocks_for(nmerge * per_map), 256, 0, s>>>(
+                         labels, m, per_map, nmerge * per_map);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }

@@ -13,11 +13,9 @@ components of all maps), then the small per-map outer loops.
 
 from __future__ import annotations
 
-import concurrent.futures as cf
 import ctypes as C
 import hashlib
 import math
-import os
 import time
 from dataclasses import dataclass, field
 
@@ -30,7 +28,6 @@ from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _stream
 from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
 
 ENERGY_FLOOR = 1e-300  # pipeline.py:55
-MAP_THREADS = 32  # host threads driving the per-map outer loops of a batch
 
 
 def _ptr(t: torch.Tensor | None) -> C.c_void_p:
@@ -221,75 +218,96 @@ def _fill(g: _Grid, labels, count, co, settings: SolveSettings):
     return z, iters[:count], status[:count]
 
 
-class _MapLoop:
-    """The outer relative-scale loop of one map (pipeline.py:169-227)."""
+class _BatchLoop:
+    """The outer relative-scale loops of all maps of a batch in lockstep
+    (pipeline.py:169-227): the maps step together through one batched call
+    per stage, each keeping its own CG, energy, merges and convergence test;
+    a map leaves the loop once it has converged.  Component ids are the
+    batch's global labels (map m owns [first[m], first[m] + count[m]))."""
 
-    def __init__(self, g: _Grid, m: int, labels: torch.Tensor, base: int, count: int, co,
-                 settings: SolveSettings, weights: WeightParams, stream: int):
-        self.g, self.m, self.labels, self.base, self.count = g, m, labels, base, count
-        self.stream = stream
+    def __init__(self, g: _Grid, labels: torch.Tensor, first: np.ndarray, counts, co,
+                 settings: SolveSettings, weights: WeightParams):
+        self.g, self.labels = g, labels
+        self.first = np.ascontiguousarray(first, dtype=np.int32)  # [B+1], fixed
+        self.count = np.ascontiguousarray(counts, dtype=np.int32)  # [B], shrinks with merges
+        self.C = max(int(self.first[-1]), 1)  # component id space
         self.co = co
         self.settings, self.weights = settings, weights
-        self.version = 0
         self.keys = None
         self.K = 0
         self.quot = None
+        self.map_edges = np.zeros(g.B, dtype=np.int32)
+        dev = g.dev
+        self.energy = torch.zeros(g.B, dtype=torch.float64, device=dev)
+        self.ok = torch.zeros(g.B, dtype=torch.int32, device=dev)
+        self.merge_energy = torch.zeros(g.B, dtype=torch.float64, device=dev)
+        self.new_count = torch.zeros(g.B, dtype=torch.int32, device=dev)
 
-    def s(self):
-        return C.c_void_p(self.stream)
+    @staticmethod
+    def _hp(a: np.ndarray) -> C.c_void_p:
+        return C.c_void_p(a.ctypes.data)
 
-    def rebuild(self, keys: torch.Tensor | None = None):
+    def initial_keys(self):
         g, lib = self.g, self.g.lib
-        if keys is None:
-            hw = g.hw
-            lab = self.labels[self.m * hw:(self.m + 1) * hw]
-            ef = self.co[3][self.m * hw:(self.m + 1) * hw]
-            out = torch.empty(hw * g.kf, dtype=torch.int32, device=g.dev)
-            n = torch.zeros(1, dtype=torch.int32, device=g.dev)
-            ws = _ws(_lib.size_query(lib.ni_inter_edges_workspace_size, 1, g.H, g.W, g.conn), g.dev)
-            _lib.check(lib.ni_inter_edges(_ptr(lab), _ptr(ef), 1, g.H, g.W, g.conn, _ptr(out), _ptr(n),
-                                          _ptr(ws), ws.numel(), self.s()), "build_quotient")
-            K = int(n.item())
-            keys = out[:K] + self.m * hw * g.kf
-        self.keys = keys.contiguous()
-        self.K = int(self.keys.numel())
-        qbytes = _lib.size_query(lib.ni_quotient_workspace_size, self.K, self.count)
+        out = torch.empty(g.npix * g.kf, dtype=torch.int32, device=g.dev)
+        n = torch.zeros(1, dtype=torch.int32, device=g.dev)
+        ws = _ws(_lib.size_query(lib.ni_inter_edges_workspace_size, g.B, g.H, g.W, g.conn), g.dev)
+        _lib.check(lib.ni_inter_edges(_ptr(self.labels), _ptr(self.co[3]), g.B, g.H, g.W, g.conn,
+                                      _ptr(out), _ptr(n), _ptr(ws), ws.numel(), g.s()),
+                   "build_quotient")
+        self.K = int(n.item())
+        self.keys = out[:self.K].clone()
+
+    def filter_keys(self, keep: np.ndarray):
+        """Drop edges of maps that left the loop and edges a merge made intra."""
+        g, lib = self.g, self.g.lib
+        mk = torch.from_numpy(keep.astype(np.uint8)).to(g.dev)
+        out = torch.empty(max(self.K, 1), dtype=torch.int32, device=g.dev)
+        n = torch.zeros(1, dtype=torch.int32, device=g.dev)
+        ws = _ws(_lib.size_query(lib.ni_keys_filter_workspace_size, self.K), g.dev)
+        _lib.check(lib.ni_keys_filter(_ptr(self.keys), self.K, _ptr(self.labels), _ptr(mk), g.H,
+                                      g.W, g.conn, _ptr(out), _ptr(n), _ptr(ws), ws.numel(), g.s()),
+                   "build_quotient")
+        self.K = int(n.item())
+        self.keys = out[:self.K]
+
+    def build(self):
+        g, lib = self.g, self.g.lib
+        qbytes = _lib.size_query(lib.ni_quotient_workspace_size, self.K, self.C, g.B)
         self.quot = _ws(qbytes, g.dev)
         npairs = C.c_int32(0)
-        _lib.check(lib.ni_quotient_build(_ptr(self.keys), self.K, _ptr(self.labels), self.base,
-                                         self.count, g.W, g.conn, _ptr(self.quot), self.quot.numel(),
-                                         C.byref(npairs), self.s()), "build_quotient")
+        self.map_edges = np.zeros(g.B, dtype=np.int32)
+        _lib.check(lib.ni_quotient_build(_ptr(self.keys), self.K, _ptr(self.labels), self.C, g.B,
+                                         g.H, g.W, g.conn, _ptr(self.quot), self.quot.numel(),
+                                         C.byref(npairs), self._hp(self.map_edges), g.s()),
+                   "build_quotient")
 
-    def step(self, z: torch.Tensor, t: int):
+    def step(self, z: torch.Tensor, t: int, active: np.ndarray):
         g, lib = self.g, self.g.lib
         st, wp = self.settings, self.weights
         omega_a, omega_b, gamma, eflags = self.co
-        C_ = self.count
-        scales = torch.empty(max(C_, 1), dtype=torch.float64, device=g.dev)
+        scales = torch.empty(self.C, dtype=torch.float64, device=g.dev)
         residual = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
         wts = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
-        out = torch.zeros(2, dtype=torch.float64, device=g.dev)
-        ok = torch.zeros(1, dtype=torch.int32, device=g.dev)
-        ws = _ws(_lib.size_query(lib.ni_scale_step_workspace_size, self.K, C_), g.dev)
+        ws = _ws(_lib.size_query(lib.ni_scale_step_workspace_size, self.K, self.C, g.B), g.dev)
         _lib.check(lib.ni_scale_step(
-            _ptr(self.quot), self.quot.numel(), self.K, C_, _ptr(self.labels), self.base,
-            _ptr(omega_a), _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
-            self.m, t, st.alignment_iters, wp.mode_code, C.c_double(wp.k),
-            C.c_double(wp.outlier_low), C.c_double(wp.outlier_high), C.c_double(st.cg_tol),
-            int(st.cg_max_iters), _ptr(z), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(out),
-            _ptr(ok), _ptr(ws), ws.numel(), self.s()), "relative_scale_step")
-        return scales, residual, wts, out, ok
+            _ptr(self.quot), self.quot.numel(), self.K, self.C, g.B, self._hp(self.first),
+            self._hp(self.count), self._hp(active), len(active), _ptr(self.labels),
+            _ptr(omega_a), _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.H, g.W, g.conn, g.model, t,
+            st.alignment_iters, wp.mode_code, C.c_double(wp.k), C.c_double(wp.outlier_low),
+            C.c_double(wp.outlier_high), C.c_double(st.cg_tol), int(st.cg_max_iters), _ptr(z),
+            _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
+            ws.numel(), g.s()), "relative_scale_step")
+        return residual, wts
 
-    def merge(self, residual, wts):
+    def merge(self, residual, wts, merging: np.ndarray):
         g, lib = self.g, self.g.lib
-        new_count = torch.zeros(1, dtype=torch.int32, device=g.dev)
-        energy = torch.zeros(1, dtype=torch.float64, device=g.dev)
-        ws = _ws(_lib.size_query(lib.ni_merge_workspace_size, self.K, self.count), g.dev)
-        _lib.check(lib.ni_merge(_ptr(self.quot), self.quot.numel(), self.K, self.count,
-                                _ptr(self.labels), self.base, g.H, g.W, self.m, _ptr(residual),
-                                _ptr(wts), _ptr(new_count), _ptr(energy), _ptr(ws), ws.numel(),
-                                self.s()), "merge_components")
-        return new_count, energy
+        ws = _ws(_lib.size_query(lib.ni_merge_workspace_size, self.K, self.C, g.B), g.dev)
+        _lib.check(lib.ni_merge(_ptr(self.quot), self.quot.numel(), self.K, self.C, g.B,
+                                self._hp(self.first), self._hp(self.count), self._hp(merging),
+                                len(merging), _ptr(self.labels), g.H, g.W, _ptr(residual),
+                                _ptr(wts), _ptr(self.new_count), _ptr(self.merge_energy),
+                                _ptr(ws), ws.numel(), g.s()), "merge_components")
 
 
 def _validate(model, connectivity):
@@ -378,67 +396,64 @@ def run_pipeline_batch(
     fit = fill_iters.cpu().numpy()
 
     valid = g.nmap.valid_t
-    # The outer loops of the B maps are independent (each touches only its
-    # own labels / z slice): run them concurrently, one CUDA stream each, from
-    # a small pool of host threads (the C calls and CUDA syncs release the GIL).
-    ready = torch.cuda.Event()
-    ready.record(torch.cuda.current_stream(g.dev))
-
-    def map_loop(m):
-        ms = torch.cuda.Stream(device=g.dev)
-        with torch.cuda.stream(ms):
-            ms.wait_event(ready)
-            loop = _MapLoop(g, m, labels, int(first[m]), counts[m], co, settings, weights,
-                            ms.cuda_stream)
-            energies = []
-            e_prev = ENERGY_FLOOR
-            t = 0
-            converged = False
-            version = 0
-            loop.rebuild()
-            zm = z[m * g.hw:(m + 1) * g.hw]
-            while not converged:
-                it_start = time.perf_counter()
-                scales, residual, wts, out, ok = loop.step(z, t)
-                if not bool(ok.item()):
-                    warnings[m].append(f"iteration {t}: cg hit iteration cap")
-                t += 1
-                merge_performed = False
-                extra = {}
-                if (settings.freq_merging is not None and t % settings.freq_merging == 0
-                        and loop.count > 1 and loop.K > 0):
-                    digest = _digest(zm)
-                    new_count, energy = loop.merge(residual, wts)
-                    nc = int(new_count.item())
-                    e_t = float(energy.item())
-                    extra = {"components_before": loop.count, "components_after": nc,
-                             "z_digest_before": digest, "z_digest_after": _digest(zm)}
-                    loop.count = nc
-                    version += 1
-                    loop.rebuild()
-                    merge_performed = True
-                else:
-                    e_t = float(out[0].item())
-                converged = _has_converged(e_t, e_prev, t, settings)
-                e_prev = e_t
-                energies.append(e_t)
-                records[m].append({"t": t, "E_t": e_t, "component_count": loop.count,
-                                   "merge_performed": merge_performed,
-                                   "wall_ms": _ms(it_start), **extra})
-            done = torch.cuda.Event()
-            done.record(ms)
-        return (loop, energies, t, version), done
-
-    if B == 1:
-        outs = [map_loop(0)]
-    else:
-        nthreads = int(os.environ.get("NI_MAP_THREADS", MAP_THREADS))
-        with cf.ThreadPoolExecutor(max_workers=min(B, nthreads)) as ex:
-            outs = list(ex.map(map_loop, range(B)))
-    cur = torch.cuda.current_stream(g.dev)
-    for _, done in outs:
-        cur.wait_event(done)
-    results = [r for r, _ in outs]
+    loop = _BatchLoop(g, labels, first, counts, co, settings, weights)
+    loop.initial_keys()
+    loop.build()
+    active = np.arange(B, dtype=np.int32)
+    e_prev = np.full(B, ENERGY_FLOOR)
+    energies = [[] for _ in range(B)]
+    iters = np.zeros(B, dtype=np.int64)
+    version = np.zeros(B, dtype=np.int64)
+    t = 0
+    while len(active):
+        it_start = time.perf_counter()
+        residual, wts = loop.step(z, t, active)
+        t_step = t
+        t += 1
+        merging = np.array([m for m in active
+                            if settings.freq_merging is not None and t % settings.freq_merging == 0
+                            and loop.count[m] > 1 and loop.map_edges[m] > 0], dtype=np.int32)
+        digests = {}
+        if len(merging):
+            digests = {int(m): _digest(z[m * g.hw:(m + 1) * g.hw]) for m in merging}
+            loop.merge(residual, wts, merging)
+        # one read-back per iteration for every map
+        host = torch.cat([loop.energy, loop.ok.to(torch.float64), loop.merge_energy,
+                          loop.new_count.to(torch.float64)]).cpu().numpy()
+        e_step, ok, e_merge, new_count = host[:B], host[B:2 * B], host[2 * B:3 * B], host[3 * B:]
+        wall = _ms(it_start)
+        merged = set(int(m) for m in merging)
+        still = []
+        for m in active:
+            m = int(m)
+            if not ok[m]:
+                warnings[m].append(f"iteration {t_step}: cg hit iteration cap")
+            extra = {}
+            if m in merged:
+                nc = int(new_count[m])
+                e_t = float(e_merge[m])
+                extra = {"components_before": int(loop.count[m]), "components_after": nc,
+                         "z_digest_before": digests[m],
+                         "z_digest_after": _digest(z[m * g.hw:(m + 1) * g.hw])}
+                loop.count[m] = nc
+                version[m] += 1
+            else:
+                e_t = float(e_step[m])
+            converged = _has_converged(e_t, e_prev[m], t, settings)
+            e_prev[m] = e_t
+            energies[m].append(e_t)
+            records[m].append({"t": t, "E_t": e_t, "component_count": int(loop.count[m]),
+                               "merge_performed": m in merged, "wall_ms": wall, **extra})
+            if converged:
+                iters[m] = t
+            else:
+                still.append(m)
+        if len(still) and (merged or len(still) != len(active)):
+            keep = np.zeros(B, dtype=bool)
+            keep[still] = True
+            loop.filter_keys(keep)
+            loop.build()
+        active = np.array(still, dtype=np.int32)
 
     target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
     lib = g.lib
@@ -446,21 +461,21 @@ def run_pipeline_batch(
     _lib.check(lib.ni_gauge(_ptr(z), _ptr(valid), g.B, g.H, g.W, C.c_double(target), C.c_void_p(0),
                             _ptr(ws), ws.numel(), g.s()), "gauge")
     out = []
-    for m, (loop, energies, t, version) in enumerate(results):
+    for m in range(B):
         sl = slice(m * g.hw, (m + 1) * g.hw)
-        records[m].append({"stage": "done", "iterations": t, "warnings": len(warnings[m]),
-                           "wall_ms": _ms(run_start)})
+        records[m].append({"stage": "done", "iterations": int(iters[m]),
+                           "warnings": len(warnings[m]), "wall_ms": _ms(run_start)})
         vm = valid[sl]
         out.append(PipelineResult(
             log_depth=LogDepthMap(z[sl], vm, g.H, g.W),
             filled=LogDepthMap(torch.where(vm.bool(), filled[sl], torch.zeros_like(filled[sl])), vm,
                                g.H, g.W),
             partition0=Partition(labels0[sl], counts[m], 0, int(first[m])),
-            partition=Partition(labels[sl], loop.count, version, int(first[m])),
+            partition=Partition(labels[sl], int(loop.count[m]), int(version[m]), int(first[m])),
             records=records[m],
             warnings=warnings[m],
-            iterations=t,
-            energies=energies,
+            iterations=int(iters[m]),
+            energies=energies[m],
             fill_iterations=fit[first[m]:first[m + 1]],
             fill_report=report,
         ))

@@ -51,9 +51,10 @@ def test_host_only_entry_points(lib):
     assert _lib.size_query(lib.ni_components_workspace_size, 1, 64, 64) > 64 * 64 * 12
     assert _lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10) > 2 * 64 * 64 * 20
     assert _lib.size_query(lib.ni_inter_edges_workspace_size, 1, 32, 32, 4) > 0
-    assert _lib.size_query(lib.ni_quotient_workspace_size, 100, 10) > 0
-    assert _lib.size_query(lib.ni_scale_step_workspace_size, 100, 10) > 0
-    assert _lib.size_query(lib.ni_merge_workspace_size, 100, 10) > 0
+    assert _lib.size_query(lib.ni_keys_filter_workspace_size, 100) > 0
+    assert _lib.size_query(lib.ni_quotient_workspace_size, 100, 10, 2) > 0
+    assert _lib.size_query(lib.ni_scale_step_workspace_size, 100, 10, 2) > 0
+    assert _lib.size_query(lib.ni_merge_workspace_size, 100, 10, 2) > 0
     assert _lib.size_query(lib.ni_gauge_workspace_size, 3, 16, 16) > 0
     # argument validation happens before any device work
     st = lib.ni_coefficients(None, None, None, 1, 4, 4, 8, 1, None, None, None, None, None, None)
