@@ -418,8 +418,12 @@ struct Claim {
   uint8_t st[SLOTS];
 };
 constexpr size_t kRingBytes = size_t(SLOT_BYTES) * NS;
-constexpr size_t kSmemPerWarp = (kRingBytes + sizeof(Claim) + 15) & ~size_t(15);
-constexpr size_t kSmemBytes = kSmemPerWarp * WPB;
+constexpr size_t kSmemPerWarp = kRingBytes;
+#ifndef NI_WORKERS
+#define NI_WORKERS 15
+#endif
+constexpr int WORKERS = NI_WORKERS;          // sweeping warps per CTA (one CTA per SM)
+constexpr int NT_FILL = (WORKERS + 1) * 32;  // + one scheduler warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -542,22 +546,80 @@ __device__ __forceinline__ Row derive(const unsigned char* slot, int lane, int d
   return o;
 }
 
+#ifndef NI_FILL_STATS
+#define NI_FILL_STATS 0
+#endif
+#if NI_FILL_STATS
+// debug counters (variant build): 0 worker cycles, 1 worker idle (empty
+// mailbox), 2 worker waits for a finish slot, 3 items, 4 scheduler cycles,
+// 5 scheduler retire cycles, 6 scheduler claim cycles, 7 claims
+__device__ unsigned long long g_fill_stats[8];
+#define NI_STAT(i, v) atomicAdd(&g_fill_stats[i], (unsigned long long)(v))
+#else
+#define NI_STAT(i, v) ((void)0)
+#endif
+
+// ---- warp roles
+//
+// A CTA is WORKERS sweeping warps plus one scheduler warp.  The scheduler
+// claims items for the workers (into a per-worker mailbox in shared memory)
+// and retires finished items (partials, per-component finalisers, batch
+// accounting), so a worker only ever streams rows: the dependent global
+// round trips of claiming and retiring overlap the sweeps instead of
+// stalling them.
+constexpr int MB = 2;  // claimed items per worker mailbox
+constexpr int FQ = 2;  // finished-item records per worker
+
+struct Mailbox {  // scheduler -> worker (single producer, single consumer)
+  Claim slot[MB];
+  int head;  // items the worker has started (worker-owned)
+  int tail;  // items the scheduler has posted (scheduler-owned)
+  int pad[2];
+};
+
+struct FinishRec {
+  double sum[SLOTS][NDOT];  // warp-summed <p,q>, <r,q>, <q,q>, <r,r> per slot
+  int32_t comp[SLOTS];
+  int32_t pbase, nslot, g, n, par, live;
+};
+
+struct FinishBox {  // worker -> scheduler (single producer, single consumer)
+  FinishRec rec[FQ];
+  int head;  // records retired (scheduler-owned)
+  int tail;  // records posted (worker-owned)
+  int pad[2];
+};
+
+struct CtaShared {
+  Mailbox mb[WORKERS];
+  FinishBox fb[WORKERS];
+  int done;  // set by the scheduler once every group retired
+  int pad[3];
+};
+
+constexpr size_t kSmemBytes = kSmemPerWarp * WORKERS + sizeof(CtaShared);
+
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
 // ---- the batch scheduler
 //
 // A group's open batch is one 64-bit word: parity << 63 | n << 32 | ticket.
-// Claiming is one atomicAdd on it: a ticket t < n of the returned word is
-// item t of that batch, whatever ring entry led there.  Published batches
-// are announced in a ring (seq << 32 | group); warps probe 32 entries from
-// the hint at once and take the first open one, so batches drain in
-// publication order and the hint only passes exhausted entries.
+// Claiming is one atomicAdd on it: tickets t < n of the returned word are
+// items of that batch, whatever ring entry led there.  Published batches
+// are announced in a ring (seq << 32 | group); the scheduler probes 32
+// entries from the hint at once and takes the first open one, so batches
+// drain in publication order and the hint only passes exhausted entries.
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
-// Claim an item into c (shared memory); false when no batch is open.
-__device__ __noinline__ bool try_claim(const FillArgs& a, Claim* c) {
+// Claim up to `want` (<= 32) items of one open batch with a single ticket
+// atomic; lane j < got writes item t + j into *dst[j] (shared memory).
+// Returns how many (0: no batch is open).
+__device__ __noinline__ int claim_items(const FillArgs& a, int want, Claim* const* dst) {
   const int lane = threadIdx.x & 31;
   uint32_t h = *reinterpret_cast<const volatile uint32_t*>(a.ring_hint);
   for (int round = 0; round < 64; ++round) {
@@ -581,52 +643,51 @@ __device__ __noinline__ bool try_claim(const FillArgs& a, Claim* c) {
       const int l = __ffs(openm) - 1;
       const int32_t gg = __shfl_sync(0xffffffffu, g, l);
       unsigned long long w = 0;
-      if (lane == 0) w = atomicAdd(a.gtk + gg, 1ull);
+      int32_t gs = 0;
+      if (lane == 0) w = atomicAdd(a.gtk + gg, static_cast<unsigned long long>(want));
+      if (lane == 1) gs = __ldcg(a.gstart + gg);
       w = __shfl_sync(0xffffffffu, w, 0);
+      gs = __shfl_sync(0xffffffffu, gs, 1);
       const int32_t t = int32_t(w & 0xffffffffu), n = int32_t((w >> 32) & 0x7fffffffu);
-      if (t < n) {
+      const int got = max(0, min(want, n - t));
+      if (got > 0) {
         // the batch's coefficients were published before its word
-        const int32_t k = __ldcg(a.active_items + __ldcg(a.gstart + gg) + t);
-        const Item it = a.items[k];
-        const int ni = item_n(it);
-        int live = 0;
-        float al[SLOTS], be[SLOTS];
-        uint8_t st[SLOTS];
-#pragma unroll
-        for (int j = 0; j < SLOTS; ++j) {
-          al[j] = 0.f;
-          be[j] = 0.f;
-          st[j] = ST_IDLE;
-          if (j < ni) {
-            const int32_t cc = it.comp[j];
-            st[j] = __ldcg(a.status + cc);
-            al[j] = float(__ldcg(a.alpha + cc));
-            be[j] = float(__ldcg(a.beta + cc));
-            if (st[j] == ST_ACTIVE || st[j] == ST_FLUSH) live |= 1 << j;
-          }
-        }
-        if (lane == 0) {
-          c->item = it;
-          c->g = gg;
-          c->par = int32_t(w >> 63);
-          c->n = n;
-          c->live = live;
+        if (lane < got) {
+          const int32_t k = __ldcg(a.active_items + gs + t + lane);
+          const Item it = a.items[k];
+          const int ni = item_n(it);
+          int live = 0;
+          Claim& cj = *dst[lane];
 #pragma unroll
           for (int j = 0; j < SLOTS; ++j) {
-            c->al[j] = al[j];
-            c->be[j] = be[j];
-            c->st[j] = st[j];
+            float al = 0.f, be = 0.f;
+            uint8_t st = ST_IDLE;
+            if (j < ni) {
+              const int32_t cc = it.comp[j];
+              st = __ldcg(a.status + cc);
+              al = float(__ldcg(a.alpha + cc));
+              be = float(__ldcg(a.beta + cc));
+              if (st == ST_ACTIVE || st == ST_FLUSH) live |= 1 << j;
+            }
+            cj.al[j] = al;
+            cj.be[j] = be;
+            cj.st[j] = st;
           }
+          cj.item = it;
+          cj.g = gg;
+          cj.par = int32_t(w >> 63);
+          cj.n = n;
+          cj.live = live;
         }
         __syncwarp();
-        return true;
+        return got;
       }
       continue;  // lost the race for the last tickets: probe again
     }
-    if (donem != 0xffffffffu) return false;  // reached the unpublished tail
+    if (donem != 0xffffffffu) return 0;  // reached the unpublished tail
     h += 32;
   }
-  return false;
+  return 0;
 }
 
 // Announce group g's next batch (lane 0).
@@ -655,7 +716,7 @@ __device__ __forceinline__ bool item_live(const FillArgs& a, int32_t k) {
   return act;
 }
 
-// The warp that finishes a group's batch: drop items whose components are
+// The warp that retires a group's batch: drop items whose components are
 // all final (in-place stable compaction), then publish the next batch or
 // retire the group.
 __device__ __noinline__ void advance_group(const FillArgs& a, int32_t g, int par) {
@@ -696,8 +757,7 @@ __device__ __noinline__ void advance_group(const FillArgs& a, int32_t g, int par
   __syncwarp();
 }
 
-// Per-component scalar update once all of its items reported (lane 0 of
-// the last arriving warp).
+// Per-component scalar update once all of its items reported (one lane).
 __device__ __forceinline__ void finalize_component(const FillArgs& a, int32_t c, const double* d,
                                                    int par) {
   if (__ldcg(a.status + c) == ST_FLUSH) {  // the pending update is applied
@@ -736,22 +796,292 @@ __device__ __forceinline__ void finalize_component(const FillArgs& a, int32_t c,
   }
 }
 
-// One CG sweep over one item (see the header).  On entry the stream holds
-// this item's rows 0..LA-1 (issued); as its last rows are issued the warp
-// claims its next item (into nx) and starts that item's rows.
+// Retire up to 32 finished items at once, one per lane (lane < cnt holds
+// `r`): partials, arrival counts, the finalisers of components whose last
+// item this was (in plan order, warp-cooperative), then batch accounting.
+__device__ void retire_items(const FillArgs& a, const FinishRec& r, int cnt) {
+  const int lane = threadIdx.x & 31;
+  const bool mine = lane < cnt;
+  // (1) partials of live slots
+  if (mine) {
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s)
+      if (s < r.nslot && ((r.live >> s) & 1)) {
+        double* dst = a.partial + size_t(r.pbase + s) * NDOT;
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) dst[d] = r.sum[s][d];
+      }
+  }
+  __threadfence();
+  // (2) arrivals; a lane whose item completes a component reports it
+  unsigned lastbits = 0;
+  if (mine) {
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s)
+      if (s < r.nslot && ((r.live >> s) & 1)) {
+        const int32_t c = r.comp[s];
+        const int32_t np = __ldcg(a.comp_pstart + c + 1) - __ldcg(a.comp_pstart + c);
+        if (atomicAdd(a.comp_cnt + c, 1) == np - 1) lastbits |= 1u << s;
+      }
+  }
+  // (3) finalisers, one component at a time over the whole warp
+  unsigned todo = __ballot_sync(0xffffffffu, lastbits != 0);
+  const bool any_fin = todo != 0;
+  if (any_fin) __threadfence();
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const unsigned bits = __shfl_sync(0xffffffffu, lastbits, src);
+    const int par = __shfl_sync(0xffffffffu, r.par, src);
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      if (!((bits >> s) & 1)) continue;
+      const int32_t c = __shfl_sync(0xffffffffu, r.comp[s], src);
+      const int32_t q0 = __ldcg(a.comp_pstart + c), q1 = __ldcg(a.comp_pstart + c + 1);
+      double sum[NDOT] = {0.0, 0.0, 0.0, 0.0};
+      for (int j = q0 + lane; j < q1; j += 32) {
+        const double* p = a.partial + size_t(__ldcg(a.comp_plist + j)) * NDOT;
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) sum[d] += __ldcg(p + d);
+      }
+#pragma unroll
+      for (int d = 0; d < NDOT; ++d) sum[d] = warp_sum(sum[d]);
+      if (lane == 0) {
+        finalize_component(a, c, sum, par);
+        a.comp_cnt[c] = 0;
+      }
+      __syncwarp();
+    }
+  }
+  if (any_fin) __threadfence();
+  // (4) batch accounting; the item that completes a batch advances its group
+  bool glast = false;
+  if (mine) glast = atomicAdd(a.gdone + r.g, 1) == r.n - 1;
+  unsigned adv = __ballot_sync(0xffffffffu, glast);
+  while (adv) {
+    const int src = __ffs(adv) - 1;
+    adv &= adv - 1;
+    advance_group(a, __shfl_sync(0xffffffffu, r.g, src), __shfl_sync(0xffffffffu, r.par, src));
+  }
+}
+
+// The scheduler warp of a CTA.
+__device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
+  const int lane = threadIdx.x & 31;
+  __shared__ Claim* targets[32];
+#if NI_FILL_STATS
+  const long long t_start = clock64();
+  long long t_ret = 0, t_claim = 0, n_claims = 0;
+#endif
+  for (;;) {
+    bool busy = false;
+#if NI_FILL_STATS
+    const long long t0 = clock64();
+#endif
+    // -- retire finished items (lane l < WORKERS looks at worker l's box)
+    int pend = 0, fh = 0;
+    if (lane < WORKERS) {
+      fh = vload(&sh.fb[lane].head);
+      pend = vload(&sh.fb[lane].tail) - fh;
+    }
+    // one record per lane: exclusive prefix over the workers' pending counts
+    int incl = pend;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total > 0) {
+      busy = true;
+      __threadfence_block();
+      // lane j takes record j: find its worker by the prefix sums
+      int w = 0, base = 0;
+#pragma unroll
+      for (int l = 0; l < WORKERS; ++l) {
+        const int in = __shfl_sync(0xffffffffu, incl, l);
+        const int ex = in - __shfl_sync(0xffffffffu, pend, l);
+        if (lane >= ex && lane < in) {
+          w = l;
+          base = ex;
+        }
+      }
+      FinishRec r;
+      if (lane < total) {
+        const int h0 = vload(&sh.fb[w].head);
+        r = sh.fb[w].rec[(h0 + lane - base) % FQ];
+      }
+      retire_items(a, r, min(total, 32));
+      __syncwarp();
+      if (lane < WORKERS && pend > 0) vstore(&sh.fb[lane].head, fh + pend);
+    }
+#if NI_FILL_STATS
+    const long long t1 = clock64();
+    t_ret += t1 - t0;
+#endif
+    // -- keep every mailbox full
+    int need = 0, mt = 0;
+    if (lane < WORKERS) {
+      mt = vload(&sh.mb[lane].tail);
+      need = MB - (mt - vload(&sh.mb[lane].head));
+    }
+    int nin = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, nin, o);
+      if (lane >= o) nin += t;
+    }
+    const int want = __shfl_sync(0xffffffffu, nin, 31);
+    if (want > 0) {
+      // claim targets: slot j of the claim goes to the j-th free mailbox slot
+      if (lane < WORKERS) {
+        const int ex = nin - need;
+        for (int j = 0; j < need; ++j)
+          targets[ex + j] = &sh.mb[lane].slot[(mt + j) % MB];
+      }
+      __syncwarp();
+      const int got = claim_items(a, want, targets);
+#if NI_FILL_STATS
+      t_claim += clock64() - t1;
+      n_claims += got > 0;
+#endif
+      if (got > 0) {
+        busy = true;
+        __threadfence_block();
+        if (lane < WORKERS) {
+          const int ex = nin - need;
+          const int mine = max(0, min(need, got - ex));
+          if (mine > 0) vstore(&sh.mb[lane].tail, mt + mine);
+        }
+      }
+    }
+    if (!busy) {
+      if (vload(reinterpret_cast<const int*>(a.gactive)) == 0) {
+        // every group retired: nothing will be claimed or posted any more
+        if (lane == 0) vstore(&sh.done, 1);
+#if NI_FILL_STATS
+        if (lane == 0) {
+          NI_STAT(4, clock64() - t_start);
+          NI_STAT(5, t_ret);
+          NI_STAT(6, t_claim);
+          NI_STAT(7, n_claims);
+        }
+#endif
+        return;
+      }
+      __nanosleep(128);
+    }
+    __syncwarp();
+  }
+}
+
+// Per-item state of a worker's sweep.
+struct Sweep {
+  uint32_t vdst;   // this lane's {r,q,p,x} destination in ring slot 0
+  uint32_t adst;   // this lane's aux destination in ring slot 0
+  float4* orow;    // this lane's output pixel in the next centre row
+  int nrows, dh, dm;
+  bool center;
+};
+
+// Copy the issuer's next row into ring slot j.
+__device__ __forceinline__ void issue_row_c(const Sweep& w, int j, Issuer& is, uint32_t vpitch) {
+  const uint32_t off = uint32_t(j & (NS - 1)) * SLOT_BYTES;
+  cp_async16_if(w.vdst + off, is.v, is.on);
+  cp_async16_if(w.adst + off, is.aux, is.on && is.aon);
+  cp_commit();
+  is.v += vpitch;
+  is.aux += is.apitch;
+}
+
+// One step of a sweep: centre rows g+1, g+2 (GR = 2), with GB = g % 4 known
+// at compile time so that the compute-ring indices are constants (row r
+// lives in der[r % 4]).
+template <int CONN, bool PURE, int GB>
+__device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned char* ring,
+                                           Sweep& w, Issuer& is, uint32_t vpitch, Row (&der)[4],
+                                           double (&acc)[SLOTS][NDOT], int g, int lane,
+                                           const Cur& k) {
+  static_assert(GR == 2, "the step body is written for two rows");
+  issue_row_c(w, g + 2 + LA, is, vpitch);
+  issue_row_c(w, g + 3 + LA, is, vpitch);
+  cp_wait<LA>();  // rows up to g+3 have landed
+  __syncwarp();
+  der[(GB + 2) & 3] = derive<PURE>(ring + ((g + 2) & (NS - 1)) * SLOT_BYTES, lane, w.dh, w.dm, k);
+  der[(GB + 3) & 3] = derive<PURE>(ring + ((g + 3) & (NS - 1)) * SLOT_BYTES, lane, w.dh, w.dm, k);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int L = g + u + 1;  // centre local row
+    const Row& U = der[(GB + u) & 3];
+    const Row& C = der[(GB + u + 1) & 3];
+    const Row& D = der[(GB + u + 2) & 3];
+    const float pa = C.pn, ha = C.h;
+    const uint32_t m = C.m;
+    float q = 0.f;
+#define NI_E(bit, pp, hh) q = ((m >> (bit)) & 1u) ? fmaf(ha + (hh), pa - (pp), q) : q
+    if (CONN == 8) {
+      NI_E(0, C.pr, C.hr);  // (+1, 0)
+      NI_E(1, D.pl, D.hl);  // (-1,+1)
+      NI_E(2, D.pn, D.h);   // ( 0,+1)
+      NI_E(3, D.pr, D.hr);  // (+1,+1)
+      NI_E(4, C.pl, C.hl);  // (-1, 0)
+      NI_E(5, U.pr, U.hr);  // (+1,-1)
+      NI_E(6, U.pn, U.h);   // ( 0,-1)
+      NI_E(7, U.pl, U.hl);  // (-1,-1)
+    } else {
+      NI_E(0, C.pr, C.hr);  // (+1, 0)
+      NI_E(1, D.pn, D.h);   // ( 0,+1)
+      NI_E(4, C.pl, C.hl);  // (-1, 0)
+      NI_E(5, U.pn, U.h);   // ( 0,-1)
+    }
+#undef NI_E
+    // pure: every centre pixel is the component's or zero (invalid /
+    // singleton pixels carry r = q = p = x = 0 and stay 0); mixed: only
+    // pixels of a live slot are written.  Dots are summed for every slot and
+    // ignored for a flushing one.
+    const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
+    bool mine = w.center && L <= w.nrows;
+    if (!PURE) mine = mine && s >= 0 && ((k.live >> s) & 1);
+    if (mine) {
+      *w.orow = make_float4(C.rn, q, pa, C.xn);
+      const double dp = pa, dq = q, dr = C.rn;
+#pragma unroll
+      for (int j = 0; j < SLOTS; ++j)
+        if (j == s) {
+          acc[j][0] = fma(dp, dq, acc[j][0]);
+          acc[j][1] = fma(dr, dq, acc[j][1]);
+          acc[j][2] = fma(dq, dq, acc[j][2]);
+          acc[j][3] = fma(dr, dr, acc[j][3]);
+        }
+    }
+    w.orow += a.P;
+  }
+}
+
+// One CG sweep over one item (see the header), by a worker warp.  On entry
+// the stream holds this item's rows 0..LA-1 (issued); as its last rows are
+// issued the worker peeks its mailbox for the next item (nx) and starts that
+// item's rows.  The warp-summed dots go to the scheduler as a FinishRec.
 template <int CONN, bool PURE>
-__device__ __forceinline__ bool sweep_item(const FillArgs& a, const unsigned char* ring,
-                                           Claim* nx, Issuer& is, const Cur& k, bool& has_next) {
+__device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned char* ring,
+                                           Mailbox& mb, int mbh, const Claim*& nx, Issuer& is,
+                                           const Cur& k, bool& has_next, FinishBox& fb,
+                                           int& fbt) {
+  static_assert(NS == 8 && LA == 6 && IROWS - 2 - LA == 24 && SH == 30,
+                "the unrolled step schedule below assumes these shapes");
   const int lane = threadIdx.x & 31;
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t vpitch = 16u * a.P;
+  Sweep w;
   const int xr = k.x0 - 1 + lane;  // real column of this lane
-  const bool center_lane = lane >= 1 && lane <= SW && xr < a.W;
+  w.center = lane >= 1 && lane <= SW && xr < a.W;
   const int c0 = k.x0 - 1 + XM;
-  const int dh = c0 & 3, dm = c0 & 15;
-  float4* __restrict__ out =
-      a.v[k.par ^ 1] + int64_t(k.y0 - 1 + RM) * a.P + (xr + XM);  // local row 0
-  const int nrows = k.y1 - k.y0;  // centre rows (local rows 1..nrows)
+  w.dh = c0 & 3;
+  w.dm = c0 & 15;
+  w.orow = a.v[k.par ^ 1] + int64_t(k.y0 + RM) * a.P + (xr + XM);  // centre row 1
+  w.nrows = k.y1 - k.y0;  // centre rows (local rows 1..nrows)
+  w.vdst = ring_s + SL_V + 16 * lane;
+  w.adst = ring_s + is.adst;
   double acc[SLOTS][NDOT];
 #pragma unroll
   for (int j = 0; j < SLOTS; ++j)
@@ -760,89 +1090,63 @@ __device__ __forceinline__ bool sweep_item(const FillArgs& a, const unsigned cha
   has_next = false;
   // rows LA and LA+1; rows 0 and 1 have landed once at most LA younger
   // row groups are pending
-  issue_row(ring_s, LA, is, vpitch);
-  issue_row(ring_s, LA + 1, is, vpitch);
+  issue_row_c(w, LA, is, vpitch);
+  issue_row_c(w, LA + 1, is, vpitch);
   cp_wait<LA>();
   __syncwarp();
-  Row der[GR + 2];  // derived rows g .. g+GR+1 around the centre rows g+1 .. g+GR
-  der[0] = derive<PURE>(ring, lane, dh, dm, k);
-  der[1] = derive<PURE>(ring + SLOT_BYTES, lane, dh, dm, k);
-  for (int g = 0; g < SH; g += GR) {
-    if (g + 2 + LA == IROWS) {  // the stream moves on to the next item here
-      has_next = try_claim(a, nx);
-      if (has_next) issuer_start(a, nx->item, nx->par, is);
-      else is.on = false;
-    }
-#pragma unroll
-    for (int u = 0; u < GR; ++u) issue_row(ring_s, g + 2 + LA + u, is, vpitch);
-    cp_wait<LA>();  // rows up to g+GR+1 have landed
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < GR; ++u)
-      der[2 + u] = derive<PURE>(ring + ((g + 2 + u) & (NS - 1)) * SLOT_BYTES, lane, dh, dm, k);
-#pragma unroll
-    for (int u = 0; u < GR; ++u) {
-      const int L = g + u + 1;  // centre local row
-      const Row& U = der[u];
-      const Row& C = der[u + 1];
-      const Row& D = der[u + 2];
-      const float pa = C.pn, ha = C.h;
-      const uint32_t m = C.m;
-      float q = 0.f;
-#define NI_E(bit, pp, hh) q = ((m >> (bit)) & 1u) ? fmaf(ha + (hh), pa - (pp), q) : q
-      if (CONN == 8) {
-        NI_E(0, C.pr, C.hr);  // (+1, 0)
-        NI_E(1, D.pl, D.hl);  // (-1,+1)
-        NI_E(2, D.pn, D.h);   // ( 0,+1)
-        NI_E(3, D.pr, D.hr);  // (+1,+1)
-        NI_E(4, C.pl, C.hl);  // (-1, 0)
-        NI_E(5, U.pr, U.hr);  // (+1,-1)
-        NI_E(6, U.pn, U.h);   // ( 0,-1)
-        NI_E(7, U.pl, U.hl);  // (-1,-1)
+  Row der[4];  // row r of the item lives in der[r % 4]
+  der[0] = derive<PURE>(ring, lane, w.dh, w.dm, k);
+  der[1] = derive<PURE>(ring + SLOT_BYTES, lane, w.dh, w.dm, k);
+#pragma unroll 1
+  for (int g = 0; g < 28; g += 4) {
+    if (g == 24) {  // the stream moves on to the next item with the rows issued from here on
+      has_next = mbh < vload(&mb.tail);
+      if (has_next) {
+        __threadfence_block();
+        nx = &mb.slot[mbh % MB];
+        issuer_start(a, nx->item, nx->par, is);
       } else {
-        NI_E(0, C.pr, C.hr);  // (+1, 0)
-        NI_E(1, D.pn, D.h);   // ( 0,+1)
-        NI_E(4, C.pl, C.hl);  // (-1, 0)
-        NI_E(5, U.pn, U.h);   // ( 0,-1)
-      }
-#undef NI_E
-      // pure: every centre pixel is the component's or zero (invalid /
-      // singleton pixels carry r = q = p = x = 0 and stay 0); mixed: only
-      // pixels of a live slot are written.  Dots are summed for every
-      // slot and ignored for a flushing one.
-      const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
-      bool mine = center_lane && L <= nrows;
-      if (!PURE) mine = mine && s >= 0 && ((k.live >> s) & 1);
-      if (mine) {
-        out[int64_t(L) * a.P] = make_float4(C.rn, q, pa, C.xn);
-        const double dp = pa, dq = q, dr = C.rn;
-#pragma unroll
-        for (int j = 0; j < SLOTS; ++j)
-          if (j == s) {
-            acc[j][0] = fma(dp, dq, acc[j][0]);
-            acc[j][1] = fma(dr, dq, acc[j][1]);
-            acc[j][2] = fma(dq, dq, acc[j][2]);
-            acc[j][3] = fma(dr, dr, acc[j][3]);
-          }
+        is.on = false;
       }
     }
-    der[0] = der[GR];
-    der[1] = der[GR + 1];
+    sweep_step<CONN, PURE, 0>(a, ring, w, is, vpitch, der, acc, g, lane, k);
+    sweep_step<CONN, PURE, 2>(a, ring, w, is, vpitch, der, acc, g + 2, lane, k);
   }
-  Item it;
-  it.x0 = k.x0;
-  it.y0 = k.y0;
-  it.y1 = k.y1;
-  it.flags = k.flags;
-  it.pbase = k.pbase;
+  sweep_step<CONN, PURE, 0>(a, ring, w, is, vpitch, der, acc, 28, lane, k);
+  // post the item's dots (fixed xor tree over lanes) for the scheduler
+  constexpr int NS_ = PURE ? 1 : SLOTS;
+  double tot[SLOTS][NDOT];
 #pragma unroll
-  for (int j = 0; j < SLOTS; ++j) it.comp[j] = k.comp[j];
-  bool live[SLOTS];
+  for (int j = 0; j < SLOTS; ++j)
 #pragma unroll
-  for (int j = 0; j < SLOTS; ++j) live[j] = (k.live >> j) & 1;
-  return item_finish<PURE ? 1 : SLOTS>(a, it, acc, live, [&](int32_t c, const double* d) {
-    finalize_component(a, c, d, k.par);
-  });
+    for (int d = 0; d < NDOT; ++d) tot[j][d] = j < NS_ ? warp_sum(acc[j][d]) : 0.0;
+#if NI_FILL_STATS
+  const long long tw0 = clock64();
+#endif
+  while (fbt - vload(&fb.head) >= FQ) __nanosleep(32);
+#if NI_FILL_STATS
+  if (lane == 0) NI_STAT(2, clock64() - tw0);
+#endif
+  FinishRec& r = fb.rec[fbt % FQ];
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j)
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d)
+      if (lane == j * NDOT + d) r.sum[j][d] = tot[j][d];
+  if (lane == 8) r.comp[0] = k.comp[0];
+  if (lane == 9) r.comp[1] = k.comp[1];
+  if (lane == 10) r.pbase = k.pbase;
+  if (lane == 11) r.nslot = item_n_flags(k.flags);
+  if (lane == 12) r.g = k.g;
+  if (lane == 13) r.n = k.n;
+  if (lane == 14) r.par = k.par;
+  if (lane == 15) r.live = k.live;
+  __syncwarp();
+  ++fbt;
+  if (lane == 0) {
+    __threadfence_block();
+    vstore(&fb.tail, fbt);
+  }
 }
 
 // Initial live-item lists per group.
@@ -856,66 +1160,98 @@ __device__ void initial_lists(const FillArgs& a, int gwarp, int nwarps) {
   }
 }
 
-// The whole CG of every component: one persistent cooperative launch whose
-// warps claim items from the open batches of all groups.  A group's batch
-// is one CG iteration of its components; the warp that finishes the last
-// item of a batch (after the per-component finalisers of all its items ran)
-// publishes the group's next batch.  No grid-wide barrier per iteration:
-// groups drift apart and every warp stays busy while any batch is open.
-template <int CONN, int MINB>
-__global__ void __launch_bounds__(NT, MINB) fill_cg_kernel(FillArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  const int gwarp = blockIdx.x * WPB + (threadIdx.x >> 5);
-  const int nwarps = gridDim.x * WPB;
+// A worker warp: take items from its mailbox and sweep them, streaming rows
+// from one item into the next.
+template <int CONN>
+__device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb, FinishBox& fb,
+                            const CtaShared& sh) {
   const int lane = threadIdx.x & 31;
-  initial_lists(a, gwarp, nwarps);
-  grid.sync();
-  for (int g = blockIdx.x * NT + threadIdx.x; g < a.G; g += gridDim.x * NT) {
-    const int32_t n = __ldcg(a.gcnt + g);
-    if (n > 0) {
-      atomicAdd(a.gactive, 1);
-      publish(a, g, 0, n);  // every group starts at parity 0 (v[0] holds b)
-    }
-  }
-  grid.sync();
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned char* ring = smem + kSmemPerWarp * (threadIdx.x >> 5);
-  Claim* nx = reinterpret_cast<Claim*>(ring + kRingBytes);
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t vpitch = 16u * a.P;
   Issuer is;
   Cur cur;
+  const Claim* nx = nullptr;
+  int mbh = 0, fbt = 0;  // worker-owned counters (mailbox head, finish tail)
   bool have = false;
+#if NI_FILL_STATS
+  const long long t_start = clock64();
+  long long t_idle = 0, n_items = 0;
+#endif
   for (;;) {
     if (!have) {
-      if (!try_claim(a, nx)) {
-        if (*reinterpret_cast<volatile int32_t*>(a.gactive) == 0) break;
-        __nanosleep(256);
+      if (mbh == vload(&mb.tail)) {
+        if (vload(&sh.done)) break;
+#if NI_FILL_STATS
+        const long long ti = clock64();
+        __nanosleep(64);
+        t_idle += clock64() - ti + 40;
+#else
+        __nanosleep(64);
+#endif
         continue;
       }
+      __threadfence_block();
+      nx = &mb.slot[mbh % MB];
       have = true;
       issuer_start(a, nx->item, nx->par, is);
       for (int j = 0; j < LA; ++j) issue_row(ring_s, j, is, vpitch);
     }
     load_cur(*nx, cur);
     __syncwarp();
+    ++mbh;
+    if (lane == 0) vstore(&mb.head, mbh);
     bool has_next = false;
-    const bool fin = (cur.flags & 0x100) ? sweep_item<CONN, true>(a, ring, nx, is, cur, has_next)
-                                         : sweep_item<CONN, false>(a, ring, nx, is, cur, has_next);
-    // batch accounting: this item's partials were fenced before their
-    // arrival counts; scalar updates of a finaliser run here are fenced now
-    int last = 0;
-    if (lane == 0) {
-      if (fin) __threadfence();
-      last = atomicAdd(a.gdone + cur.g, 1) == cur.n - 1;
-    }
-    if (__shfl_sync(0xffffffffu, last, 0)) advance_group(a, cur.g, cur.par);
+    if (cur.flags & 0x100)
+      sweep_item<CONN, true>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
+    else
+      sweep_item<CONN, false>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
     if (!has_next) {
       cp_wait<0>();
       have = false;
     }
+#if NI_FILL_STATS
+    ++n_items;
+#endif
   }
   cp_wait<0>();
+#if NI_FILL_STATS
+  if (lane == 0) {
+    NI_STAT(0, clock64() - t_start);
+    NI_STAT(1, t_idle);
+    NI_STAT(3, n_items);
+  }
+#endif
+}
+
+// The whole CG of every component: one persistent cooperative launch.  A
+// group's batch is one CG iteration of its components; the scheduler warp
+// that retires the last item of a batch (after the per-component finalisers
+// of all its items ran) publishes the group's next batch.  No grid-wide
+// barrier per iteration: groups drift apart and every worker stays busy
+// while any batch is open.
+template <int CONN, int MINB>
+__global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int WPC = NT_FILL / 32;
+  const int gwarp = blockIdx.x * WPC + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * WPC;
+  initial_lists(a, gwarp, nwarps);
+  grid.sync();
+  for (int g = blockIdx.x * NT_FILL + threadIdx.x; g < a.G; g += gridDim.x * NT_FILL) {
+    const int32_t n = __ldcg(a.gcnt + g);
+    if (n > 0) {
+      atomicAdd(a.gactive, 1);
+      publish(a, g, 0, n);  // every group starts at parity 0 (v[0] holds b)
+    }
+  }
+  extern __shared__ __align__(16) unsigned char smem[];
+  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem + kSmemPerWarp * WORKERS);
+  for (int i = threadIdx.x; i < int(sizeof(CtaShared) / sizeof(int)); i += NT_FILL)
+    reinterpret_cast<int*>(&sh)[i] = 0;
+  grid.sync();
+  const int w = threadIdx.x >> 5;
+  if (w == WORKERS) scheduler_loop(a, sh);
+  else worker_loop<CONN>(a, smem + kSmemPerWarp * w, sh.mb[w], sh.fb[w], sh);
 }
 
 // Initial ||b||^2 per component and the state of every component.  One warp
@@ -1332,31 +1668,28 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   }
   // ---- the whole CG: one persistent cooperative launch
   {
-    // register budget variant (NI_FILL_MINB = CTAs/SM it is sized for)
-    const char* mb = getenv("NI_FILL_MINB");
-    const int minb = mb ? atoi(mb) : 2;
-    void* kfn;
-    if (connectivity == 8)
-      kfn = minb == 3 ? (void*)fill_cg_kernel<8, 3> : (void*)fill_cg_kernel<8, 2>;
-    else
-      kfn = minb == 3 ? (void*)fill_cg_kernel<4, 3> : (void*)fill_cg_kernel<4, 2>;
+    void* kfn = connectivity == 8 ? (void*)fill_cg_kernel<8, 1> : (void*)fill_cg_kernel<4, 1>;
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     NI_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kSmemBytes)));
-    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, kSmemBytes));
+    NI_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT_FILL, kSmemBytes));
     int G = per_sm * sms;
-    const int need = div_up(NIt > 0 ? NIt : 1, WPB);
+    const int need = div_up(NIt > 0 ? NIt : 1, WORKERS);
     if (G > need) G = need;
     if (G < 1) G = 1;
     void* args[] = {&a};
     cudaEvent_t e0, e1;
     NI_CUDA_TRY(cudaEventCreate(&e0));
     NI_CUDA_TRY(cudaEventCreate(&e1));
+#if NI_FILL_STATS
+    unsigned long long zst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    NI_CUDA_TRY(cudaMemcpyToSymbolAsync(g_fill_stats, zst, sizeof(zst), 0, cudaMemcpyHostToDevice, s));
+#endif
     NI_CUDA_TRY(cudaEventRecord(e0, s));
     NI_COUNT_LAUNCH();
-    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT), args, kSmemBytes, s));
+    NI_CUDA_TRY(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(NT_FILL), args, kSmemBytes, s));
     NI_CUDA_TRY(cudaEventRecord(e1, s));
     g_fill_report.grid = G;
     g_fill_report.ntiles = NIt;
@@ -1384,6 +1717,15 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     g_fill_report.max_iters = mxi;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+#if NI_FILL_STATS
+    unsigned long long h[8];
+    NI_CUDA_TRY(cudaMemcpyFromSymbol(h, g_fill_stats, sizeof(h)));
+    fprintf(stderr,
+            "fill stats: groups=%d worker idle=%.1f%% finish-wait=%.1f%% cycles/item=%.0f | "
+            "scheduler retire=%.1f%% claim=%.1f%% items/claim=%.2f\n",
+            a.G, 100.0 * h[1] / h[0], 100.0 * h[2] / h[0], double(h[0]) / double(h[3]),
+            100.0 * h[5] / h[4], 100.0 * h[6] / h[4], double(h[3]) / double(h[7]));
+#endif
   }
   return NI_OK;
 }
