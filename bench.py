@@ -42,6 +42,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_PX_ITER = 37  # paper_2510_11508_b200/csrc/ni_fill.cu header (single-sweep CG)
+# canonical bytes per px-iteration of a two-sweep PCG at 8-conn
+# (56 + 4 K_f); the single-sweep kernel needs only BYTES_PER_PX_ITER of them.
+SURVEY_BYTES_PER_PX_ITER = 72
+SURVEY_PEAK_GBS = 8000.0  # SURVEY.md 8(d) north-star denominator
 THETA_DEG = 3.5
 
 
@@ -260,6 +264,13 @@ def run_ours(args, rank, world, local_rank):
         "traffic_note": ((prof["source"] + "; " + prof["note"]) if prof else
                          "no ncu capture committed"),
         "alg_bytes_per_launch": alg_bytes, "bytes_per_px_iter": BYTES_PER_PX_ITER,
+        "survey_units": {
+            "bytes_per_px_iter": SURVEY_BYTES_PER_PX_ITER,
+            "achieved": round(SURVEY_BYTES_PER_PX_ITER * px_iters / (cg_ms * 1e-3) / 1e9, 1),
+            "peak": SURVEY_PEAK_GBS,
+            "note": "px-iterations/s x the SURVEY 8(d) two-sweep figure (72 B at 8-conn); the "
+                    "single-sweep CG moves 37 B per px-iteration, so this exceeds what a "
+                    "two-sweep PCG could reach at the same HBM traffic"},
         "px_iters_per_launch": px_iters, "kernel_ms": round(cg_ms, 3),
         "kernel_share_of_step": round(cg_ms / ms, 4),
         "fill_grid_ctas": fills[0]["grid"], "max_cg_iters": fills[0]["max_iters"],
