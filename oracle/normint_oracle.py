@@ -650,3 +650,75 @@ def run_pipeline(normals, mask, intr, theta_c, st: Settings | None = None,
                     "wall_ms": (time.perf_counter() - t_run) * 1e3})
     return OracleResult(np.where(m.ravel(), z, 0.0).reshape(h, w), filled, labels0, count0,
                         labels, count, records, warnings, t, energies, fit, scales)
+
+
+@dataclass
+class BaselineOracleResult:
+    log_depth: np.ndarray  # (H, W) float64, 0 outside the mask
+    records: list = field(default_factory=list)
+    warnings: list = field(default_factory=list)
+    iterations: int = 0
+    energies: list = field(default_factory=list)
+    cg_iters: list = field(default_factory=list)
+
+
+def run_pixel_baseline(normals, mask, intr, st: Settings | None = None, connectivity=8,
+                       model="milano", gauge_depth=None) -> BaselineOracleResult:
+    """Iteratively reweighted per-pixel integration (pipeline.py:297-369).
+
+    Every outer iteration re-solves the full pixel system (one CG over all
+    valid pixels, x0 = 0, pipeline.py:261-285 + solver.py:97-122) with the
+    weight schedule of the inter system (solver.py:253-278), and the solution
+    replaces z.
+    """
+    st = st or Settings()
+    if model == "bini" and connectivity == 8:
+        raise ValueError("bini needs connectivity=4")
+    n64, m = normalize_normals(normals, mask)
+    h, w = m.shape
+    records, warnings, energies, cg_iters = [], [], [], []
+    t_run = time.perf_counter()
+    edges, _ = pixel_edges(m, connectivity)
+    co = edge_coefficients(n64, m, edges, intr, model)
+    flat = m.ravel()
+    vid = np.flatnonzero(flat)
+    compact = np.full(flat.size, -1, np.int64)
+    compact[vid] = np.arange(len(vid))
+    ca, cb = compact[edges[:, 0]], compact[edges[:, 1]]
+    eids = np.arange(len(edges))
+    n = len(vid)
+    z = np.zeros(flat.size)
+    e_prev = ENERGY_FLOOR
+    t = 0
+    done = False
+    while not done:
+        ti = time.perf_counter()
+        wa, wb = inter_weights(co, edges, eids, z, t, st)
+        mat, rhs = pair_normal_system(ca, cb, co.omega_a, co.omega_b, wa, wb, n)
+        if n == 0 or len(edges) == 0 or not np.any(rhs):
+            x, ok, it = np.zeros(n), True, 0
+        else:
+            x, ok, it = conjugate_gradient(mat.dot, rhs, st.cg_tol, max(st.cg_max_iters, n))
+        if not ok:
+            warnings.append(f"iteration {t}: cg hit iteration cap")
+        res = np.empty(2 * len(edges))
+        res[0::2] = x[ca] - x[cb] - co.omega_a
+        res[1::2] = x[cb] - x[ca] - co.omega_b
+        wts = np.empty(2 * len(edges))
+        wts[0::2], wts[1::2] = wa, wb
+        e_t = float(res @ (wts * res))
+        z[vid] = x
+        cg_iters.append(it)
+        t += 1
+        done = converged(e_t, e_prev, t, st)
+        e_prev = e_t
+        energies.append(e_t)
+        records.append({"t": t, "E_t": e_t, "component_count": n, "merge_performed": False,
+                        "wall_ms": (time.perf_counter() - ti) * 1e3})
+    target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
+    z += (target - float(np.median(z[flat]))) * flat
+    records.append({"stage": "done", "iterations": t, "warnings": len(warnings),
+                    "wall_ms": (time.perf_counter() - t_run) * 1e3})
+    return BaselineOracleResult(np.where(flat, z, 0.0).reshape(h, w), records, warnings, t,
+                                energies, cg_iters)
+

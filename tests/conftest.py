@@ -10,6 +10,17 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
+def golden_cases(prefix=None):
+    """Names of the golden fixtures: run_pipeline cases (prefix None), or the
+    ``pb_`` (run_pixel_baseline) / ``seam_`` ones."""
+    import glob
+
+    names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    if prefix is None:
+        return [n for n in names if not n.startswith(("seam_", "pb_"))]
+    return [n for n in names if n.startswith(prefix)]
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")

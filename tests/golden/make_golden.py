@@ -70,6 +70,20 @@ CASES = {
     "gauge_depth": (lambda: _scene_case(scenes.config1(4, size=40, radius=12.0, step=3.0, sigma_deg=0.3)),
                     {"gauge_depth": 2.5}),
     "theta2_noisy": (lambda: _scene_case(scenes.config2(9, h=60, w=64, f=420.0, frac=0.6)), {"theta_c_deg": 2.0}),
+    # second fill pass with bilateral weights at the filled state (solver.py:237-238)
+    "refill_voronoi48": (lambda: _scene_case(scenes.config5_map(3, size=48, cells=5)), {"refill": True}),
+    "refill_bump_merge": (lambda: _ref_scene("sphere_on_plane", 48, 0.2, 5), {"refill": True, "merge_freq": 5}),
+}
+
+# run_pixel_baseline (pipeline.py:297-369) cases
+BASELINE_CASES = {
+    "pb_hemi40": (lambda: _scene_case(scenes.config1(0, size=40, radius=12.0, step=3.0)), {}),
+    "pb_voronoi40": (lambda: _scene_case(scenes.config3(2, size=40, cells=4)), {}),
+    "pb_blob_conn4_bini": (lambda: _scene_case(scenes.config2(5, h=40, w=48, f=300.0, frac=0.5)),
+                           {"connectivity": 4, "model": "bini"}),
+    "pb_hard_gauge": (lambda: _scene_case(scenes.config3(7, size=36, cells=4, sigma_deg=0.5)),
+                      {"reweighting": "hard", "gauge_depth": 3.0}),
+    "pb_patch_ref": (lambda: _ref_scene("sphere_patch", 32), {}),
 }
 
 
@@ -78,7 +92,8 @@ def run_case(name, factory, opts):
     theta = opts.get("theta_c_deg", 3.5)
     conn = opts.get("connectivity", 8)
     model = opts.get("model", "milano")
-    settings = nsolver.SolveSettings(freq_merging=opts.get("merge_freq"), worker_count=1)
+    settings = nsolver.SolveSettings(freq_merging=opts.get("merge_freq"), worker_count=1,
+                                     refill_reweighted=bool(opts.get("refill", False)))
     weights = ncont.WeightParams(reweighting_mode=opts.get("reweighting", "soft"))
     nm = NormalMap.create(n32.astype(np.float64), mask)
     cam = CameraIntrinsics(*intr)
@@ -95,6 +110,23 @@ def run_case(name, factory, opts):
         options=json.dumps(opts), records=json.dumps(rec),
     )
     return out
+
+
+def run_baseline_case(name, factory, opts):
+    n32, mask, intr = factory()
+    conn = opts.get("connectivity", 8)
+    model = opts.get("model", "milano")
+    settings = nsolver.SolveSettings(worker_count=1)
+    weights = ncont.WeightParams(reweighting_mode=opts.get("reweighting", "soft"))
+    nm = NormalMap.create(n32.astype(np.float64), mask)
+    cam = CameraIntrinsics(*intr)
+    res = normint.run_pixel_baseline(nm, cam, settings, weights, conn, model, opts.get("gauge_depth"))
+    rec = [{k: v for k, v in r.items() if k != "wall_ms"} for r in res.records]
+    return dict(
+        normals=n32, mask=mask, intr=np.array(intr, np.float64), log_depth=res.log_depth.values,
+        energies=np.array(res.energies), iterations=res.iterations, warnings=len(res.warnings),
+        warning_text=json.dumps(res.warnings), options=json.dumps(opts), records=json.dumps(rec),
+    )
 
 
 def seam_case():
@@ -132,11 +164,22 @@ def seam_case():
 
 def main():
     out_dir = HERE
+    only = set(sys.argv[1:])
+    for name, (factory, opts) in BASELINE_CASES.items():
+        if only and name not in only:
+            continue
+        d = run_baseline_case(name, factory, opts)
+        np.savez_compressed(os.path.join(out_dir, f"{name}.npz"), **d)
+        print(f"{name}: {d['mask'].shape} valid={int(d['mask'].sum())} iters={d['iterations']}")
     for name, (factory, opts) in CASES.items():
+        if only and name not in only:
+            continue
         d = run_case(name, factory, opts)
         np.savez_compressed(os.path.join(out_dir, f"{name}.npz"), **d)
         print(f"{name}: {d['mask'].shape} valid={int(d['mask'].sum())} comps={d['count0']}->{d['count']} "
               f"iters={d['iterations']}")
+    if only and "seam_voronoi32" not in only:
+        return
     d = seam_case()
     np.savez_compressed(os.path.join(out_dir, "seam_voronoi32.npz"), **d)
     print("seam_voronoi32: comps", d["count0"], "edges", len(d["edges"]))

@@ -15,7 +15,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.conftest import GOLDEN
+from tests.conftest import GOLDEN, golden_cases
 from tests.parity import assert_depth_close, depth_error
 
 pytestmark = pytest.mark.gpu
@@ -28,9 +28,8 @@ import paper_2510_11508_b200 as nb  # noqa: E402
 from paper_2510_11508_b200 import scenes  # noqa: E402
 from oracle import normint_oracle as O  # noqa: E402
 
-PIPE_CASES = sorted(
-    os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if "seam_" not in p
-)
+PIPE_CASES = golden_cases()
+BASELINE_CASES = golden_cases("pb_")
 
 
 def load(name):
