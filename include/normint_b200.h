@@ -100,16 +100,44 @@ int ni_coefficients(const double* n, const uint8_t* valid, const double* intrins
                     double* gamma, uint8_t* eflags, ni_stats* stats, ni_stream_t stream);
 
 /* K3 -- fill_components (solver.py:195-239): per-component CG on the
- * weighted normal equations at z = 0, all components in one batched solve.
+ * weighted normal equations, all components in one batched solve.
+ * Weights: w_a = w_b = NULL is the fill at z = 0 (W = gamma^2 / 2 on both
+ * rows, continuity.py:302-308); otherwise w_a / w_b are the directed weights
+ * of every forward pixel edge (planes w[k*npix + a], see ni_edge_weights):
+ * the refill pass (solver.py:237-238) and the pixel-level baseline
+ * (pipeline.py:261-285, one "component" per map).  The CG always starts at
+ * x0 = 0 and the solution is returned (the right-hand side is the full
+ * A^T W omega, not an increment).
  * SYNCHRONOUS (polls convergence).  Writes z_out (float64, npix; 0 on invalid
  * pixels, singletons and zero-RHS components), comp_iters[count] and
  * comp_status[count] (0 converged / zero RHS / singleton, 1 hit the cap
- * max(cg_max_iters, size)).  precision: 0 = fp32 vectors + fp64 dots. */
-int ni_fill_workspace_size(int B, int H, int W, int connectivity, int count, size_t* bytes);
+ * max(cg_max_iters, size)).  fp32 vectors + fp64 dots. */
+int ni_fill_workspace_size(int B, int H, int W, int connectivity, int count, int weighted,
+                           size_t* bytes);
 int ni_fill(const int32_t* labels, int count, const double* omega_a, const double* omega_b,
-            const double* gamma, const uint8_t* eflags, int B, int H, int W, int connectivity,
-            int model, double cg_tol, int cg_max_iters, double* z_out, int32_t* comp_iters,
-            int32_t* comp_status, void* workspace, size_t workspace_bytes, ni_stream_t stream);
+            const double* gamma, const uint8_t* eflags, const double* w_a, const double* w_b,
+            int B, int H, int W, int connectivity, int model, double cg_tol, int cg_max_iters,
+            double* z_out, int32_t* comp_iters, int32_t* comp_status, void* workspace,
+            size_t workspace_bytes, ni_stream_t stream);
+
+/* Directed weights of every forward pixel edge at log-depth state z
+ * (continuity.py:292-331, solver.py:253-278): wmode 0 = valid (uniform,
+ * t < alignment_iters), 1 = valid * gamma^2 * bilateral(z) (edge_weights,
+ * the refill pass), 2 = mode 1 * outlier weight (mode 0 off, 1 soft, 2
+ * hard).  w_a / w_b: KF planes of npix doubles, 0 where no edge. */
+int ni_edge_weights(const double* z, const double* omega_a, const double* omega_b,
+                    const double* gamma, const uint8_t* eflags, int B, int H, int W,
+                    int connectivity, int model, int wmode, int mode, double k, double outlier_low,
+                    double outlier_high, double* w_a, double* w_b, ni_stream_t stream);
+
+/* Energy of the pixel pair system at x, per map (pipeline.py:336-337):
+ * energy_out[m] = sum over map m's edges of W_a res_a^2 + W_b res_b^2 with
+ * res_a = x_a - x_b - omega_a, res_b = x_b - x_a - omega_b (fixed order). */
+int ni_pair_energy_workspace_size(int B, size_t* bytes);
+int ni_pair_energy(const double* x, const double* omega_a, const double* omega_b,
+                   const double* w_a, const double* w_b, const uint8_t* eflags, int B, int H,
+                   int W, int connectivity, int model, double* energy_out, void* workspace,
+                   size_t workspace_bytes, ni_stream_t stream);
 
 /* Inter-component edge list of a partition (graph.py:186-196): edge keys
  * (a*KF + k) with differing endpoint labels, ascending.  n_out[0] = K. */

@@ -42,8 +42,13 @@ SIGNATURES = {
     "ni_components_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_components": ([_P, _P, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
     "ni_coefficients": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P], _I),
-    "ni_fill_workspace_size": ([_I, _I, _I, _I, _I, _PSZ], _I),
-    "ni_fill": ([_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ, _P], _I),
+    "ni_fill_workspace_size": ([_I, _I, _I, _I, _I, _I, _PSZ], _I),
+    "ni_fill": ([_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ,
+                 _P], _I),
+    "ni_edge_weights": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D, _P, _P, _P],
+                        _I),
+    "ni_pair_energy_workspace_size": ([_I, _PSZ], _I),
+    "ni_pair_energy": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _SZ, _P], _I),
     "ni_inter_edges_workspace_size": ([_I, _I, _I, _I, _PSZ], _I),
     "ni_inter_edges": ([_P, _P, _I, _I, _I, _I, _P, _P, _P, _SZ, _P], _I),
     "ni_keys_filter_workspace_size": ([_I, _PSZ], _I),

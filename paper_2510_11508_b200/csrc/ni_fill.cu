@@ -98,7 +98,8 @@ __device__ __forceinline__ int item_n_flags(int32_t flags) { return flags & 0xFF
 struct FillArgs {
   int rows, W, P;
   float4* v[2];
-  const float* hw;
+  const float* hw;        // fill: W_a = gamma_a^2 / 2 (c_ab = hw_a + hw_b)
+  const float4* cf;       // EW passes: forward-edge conductances W_a + W_b, edges 0..3
   const uint8_t* imask;
   const int32_t* lab;  // padded labels
   // plan
@@ -137,13 +138,15 @@ struct FillArgs {
 
 // ----------------------------------------------------------------- setup
 
-// Padded-layout setup: v[0] = {b, 0, 0, 0}, hw, imask, labels.
-template <int CONN, int MODEL>
+// Padded-layout setup: v[0] = {b, 0, 0, 0}, hw (fill) or the forward-edge
+// conductances cf (EW: per-edge weights w_a / w_b given), imask, labels.
+template <int CONN, int MODEL, bool EW>
 __global__ void __launch_bounds__(256) prep_kernel(
     const int32_t* __restrict__ labels, const double* __restrict__ omega_a,
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
-    const uint8_t* __restrict__ eflags, int H, int W, int P, int64_t npix,
-    float* __restrict__ hw, uint8_t* __restrict__ imask, int32_t* __restrict__ lab_p,
+    const uint8_t* __restrict__ eflags, const double* __restrict__ w_a,
+    const double* __restrict__ w_b, int H, int W, int P, int64_t npix, float* __restrict__ hw,
+    float4* __restrict__ cf, uint8_t* __restrict__ imask, int32_t* __restrict__ lab_p,
     float4* __restrict__ v0, int32_t* __restrict__ comp_size) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
@@ -159,8 +162,10 @@ __global__ void __launch_bounds__(256) prep_kernel(
       const unsigned peers = __match_any_sync(__activemask(), lab);
       if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(comp_size + lab, __popc(peers));
     }
-    const double wa = 0.5 * (gamma[i] * gamma[i]);
-    hw[o] = float(wa);
+    // fill weights at z = 0: every bilateral factor is 1/2 (continuity.py:302-308)
+    const double wself = 0.5 * (gamma[i] * gamma[i]);
+    if (!EW) hw[o] = float(wself);
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
     const uint8_t ef = eflags[i];
     uint8_t m = 0;
     double b = 0.0;
@@ -172,10 +177,12 @@ __global__ void __launch_bounds__(256) prep_kernel(
         const int64_t j = i + int64_t(dv) * W + du;
         if (labels[j] == lab) {
           m |= uint8_t(1u << k);
-          const double wb = 0.5 * (gamma[j] * gamma[j]);
+          const double wa = EW ? w_a[k * npix + i] : wself;
+          const double wb = EW ? w_b[k * npix + i] : 0.5 * (gamma[j] * gamma[j]);
           const double oa = omega_a[k * npix + i];
           const double ob = MODEL == 0 ? -oa : omega_b[k * npix + i];
           b += wa * oa - wb * ob;  // A^T W b of rows 2e, 2e+1 (solver.py:83-93)
+          c[k] = float(wa + wb);
         }
       }
       // backward edge (j -> i), j = i - offset_k: i is the "b" endpoint
@@ -185,14 +192,16 @@ __global__ void __launch_bounds__(256) prep_kernel(
         const uint8_t efj = eflags[j];
         if (((efj >> k) & (efj >> (4 + k)) & 1) && labels[j] == lab) {
           m |= uint8_t(1u << (4 + k));
-          const double wj = 0.5 * (gamma[j] * gamma[j]);
+          const double wj = EW ? w_a[k * npix + j] : 0.5 * (gamma[j] * gamma[j]);
+          const double wi = EW ? w_b[k * npix + j] : wself;
           const double oa = omega_a[k * npix + j];
           const double ob = MODEL == 0 ? -oa : omega_b[k * npix + j];
-          b += wa * ob - wj * oa;
+          b += wi * ob - wj * oa;
         }
       }
     }
     imask[o] = m;
+    if (EW) cf[o] = make_float4(c[0], c[1], c[2], c[3]);
     v0[o] = make_float4(float(b), 0.f, 0.f, 0.f);
   }
 }
@@ -406,8 +415,16 @@ static_assert((NS & (NS - 1)) == 0 && IROWS % NS == 0, "ring slots must tile an 
 static_assert(SH % GR == 0 && (IROWS - 2 - LA) % GR == 0, "row steps must align");
 static_assert(LA >= 2, "ring too small");
 
-// ring slot layout (bytes): {r,q,p,x}[32] | hw[36] | labels[36] | imask[48]
-constexpr int SL_V = 0, SL_H = 512, SL_LAB = 656, SL_M = 800, SLOT_BYTES = 848;
+// Ring slot layouts (bytes).  Fill: {r,q,p,x}[32] | hw[36] | labels[36] |
+// imask[48].  Edge-weighted passes (EW: refill, pixel baseline): {r,q,p,x}[32]
+// | forward conductances float4[32] | labels[36] | imask[48].
+template <bool EW>
+struct Slot {
+  static constexpr int V = 0, H = 512, C = 512;
+  static constexpr int LAB = EW ? 1024 : 656;
+  static constexpr int M = LAB + 144;
+  static constexpr int BYTES = M + 48;
+};
 
 // A claimed item with its coefficients; the next item's lives in shared
 // memory (one per warp) so it holds no registers while the current item runs.
@@ -417,8 +434,10 @@ struct Claim {
   int32_t g, par, n, live;  // live: bit j = slot j is ACTIVE or FLUSH
   uint8_t st[SLOTS];
 };
-constexpr size_t kRingBytes = size_t(SLOT_BYTES) * NS;
-constexpr size_t kSmemPerWarp = kRingBytes;
+template <bool EW>
+constexpr size_t ring_bytes() {
+  return size_t(Slot<EW>::BYTES) * NS;
+}
 #ifndef NI_WORKERS
 #define NI_WORKERS 15
 #endif
@@ -444,44 +463,68 @@ __device__ __forceinline__ void cp_wait() {
 // The copy side of a warp's row stream (per-lane source pointers).
 struct Issuer {
   const char* v;    // this lane's 16 B of {r,q,p,x} in the next row
+  const char* c;    // this lane's 16 B of forward conductances (EW passes)
   const char* aux;  // this lane's 16 B of hw / labels / imask in the next row
   uint32_t apitch;  // aux row pitch in bytes
   uint32_t adst;    // aux destination offset in a slot
   bool on, aon;     // off: past the last item / lane copies no aux bytes
 };
 
+template <bool EW>
 __device__ __forceinline__ void issuer_start(const FillArgs& a, const Item& it, int par,
                                              Issuer& is) {
+  using L = Slot<EW>;
   const int lane = threadIdx.x & 31;
   const int c0 = it.x0 - 1 + XM;  // padded column of lane 0
   const int64_t row0 = int64_t(it.y0 - 1 + RM) * a.P;
   const int ah = c0 & ~3, am = c0 & ~15;  // 16-B aligned windows
   is.v = reinterpret_cast<const char*>(a.v[par] + row0 + c0 + lane);
   is.on = true;
+  if (EW) {
+    is.c = reinterpret_cast<const char*>(a.cf + row0 + c0 + lane);
+    if (lane < 9) {
+      is.aux = reinterpret_cast<const char*>(a.lab + row0 + ah + 4 * lane);
+      is.apitch = 4u * a.P;
+      is.adst = L::LAB + 16 * lane;
+      is.aon = !item_pure(it);
+    } else {
+      is.aux = reinterpret_cast<const char*>(a.imask + row0 + am + 16 * (lane - 9));
+      is.apitch = a.P;
+      is.adst = L::M + 16 * (lane - 9);
+      is.aon = lane < 12;
+    }
+    return;
+  }
   if (lane < 9) {
     is.aux = reinterpret_cast<const char*>(a.hw + row0 + ah + 4 * lane);
     is.apitch = 4u * a.P;
-    is.adst = SL_H + 16 * lane;
+    is.adst = L::H + 16 * lane;
     is.aon = true;
   } else if (lane < 18) {
     is.aux = reinterpret_cast<const char*>(a.lab + row0 + ah + 4 * (lane - 9));
     is.apitch = 4u * a.P;
-    is.adst = SL_LAB + 16 * (lane - 9);
+    is.adst = L::LAB + 16 * (lane - 9);
     is.aon = !item_pure(it);
   } else {
     is.aux = reinterpret_cast<const char*>(a.imask + row0 + am + 16 * (lane - 18));
     is.apitch = a.P;
-    is.adst = SL_M + 16 * (lane - 18);
+    is.adst = L::M + 16 * (lane - 18);
     is.aon = lane < 21;
   }
 }
 
 // Copy the issuer's next row into ring slot `j % NS` (one commit group per
 // row in every lane, empty once the stream is off).
+template <bool EW>
 __device__ __forceinline__ void issue_row(uint32_t ring, int j, Issuer& is, uint32_t vpitch) {
+  using L = Slot<EW>;
   const int lane = threadIdx.x & 31;
-  const uint32_t slot = ring + uint32_t(j & (NS - 1)) * SLOT_BYTES;
-  cp_async16_if(slot + SL_V + 16 * lane, is.v, is.on);
+  const uint32_t slot = ring + uint32_t(j & (NS - 1)) * L::BYTES;
+  cp_async16_if(slot + L::V + 16 * lane, is.v, is.on);
+  if (EW) {
+    cp_async16_if(slot + L::C + 16 * lane, is.c, is.on);
+    is.c += vpitch;
+  }
   cp_async16_if(slot + is.adst, is.aux, is.on && is.aon);
   cp_commit();
   is.v += vpitch;
@@ -492,8 +535,18 @@ __device__ __forceinline__ void issue_row(uint32_t ring, int j, Issuer& is, uint
 // the pixel's own component (only intra-component neighbours are ever read,
 // and those share the centre's alpha and beta), plus the left / right
 // neighbours' p' and hw (warp shuffles; lanes 0 / 31 are the halo).
-struct Row {
+// EW rows carry the pixel's forward conductances c0..c3 and the backward
+// ones it needs from its neighbours: c0l (left pixel's c0), c1r (right
+// pixel's c1), c3l (left pixel's c3).
+template <bool EW>
+struct RowT {
   float pn, h, pl, pr, hl, hr, rn, xn;
+  uint32_t m;  // imask | (slot + 1) << 8
+};
+template <>
+struct RowT<true> {
+  float pn, pl, pr, rn, xn;
+  float c0, c1, c2, c3, c0l, c1r, c3l;
   uint32_t m;  // imask | (slot + 1) << 8
 };
 
@@ -521,28 +574,40 @@ __device__ __forceinline__ void load_cur(const Claim& c, Cur& k) {
   }
 }
 
-template <bool PURE>
-__device__ __forceinline__ Row derive(const unsigned char* slot, int lane, int dh, int dm,
-                                      const Cur& k) {
-  const float4 v = *reinterpret_cast<const float4*>(slot + SL_V + 16 * lane);
+template <bool PURE, bool EW>
+__device__ __forceinline__ RowT<EW> derive(const unsigned char* slot, int lane, int dh, int dm,
+                                           const Cur& k) {
+  using L = Slot<EW>;
+  const float4 v = *reinterpret_cast<const float4*>(slot + L::V + 16 * lane);
   float al = k.al[0], be = k.be[0];
   int s = 0;
   if (!PURE) {
-    const int32_t lab = *reinterpret_cast<const int32_t*>(slot + SL_LAB + 4 * (dh + lane));
+    const int32_t lab = *reinterpret_cast<const int32_t*>(slot + L::LAB + 4 * (dh + lane));
     s = lab == k.comp[0] ? 0 : (item_n_flags(k.flags) > 1 && lab == k.comp[1] ? 1 : -1);
     al = s == 0 ? k.al[0] : (s == 1 ? k.al[1] : 0.f);
     be = s == 0 ? k.be[0] : (s == 1 ? k.be[1] : 0.f);
   }
-  Row o;
+  RowT<EW> o;
   o.rn = fmaf(-al, v.y, v.x);
   o.pn = fmaf(be, v.z, o.rn);
   o.xn = fmaf(al, v.z, v.w);
-  o.h = *reinterpret_cast<const float*>(slot + SL_H + 4 * (dh + lane));
-  o.m = uint32_t(slot[SL_M + dm + lane]) | (uint32_t(s + 1) << 8);
+  o.m = uint32_t(slot[L::M + dm + lane]) | (uint32_t(s + 1) << 8);
   o.pl = __shfl_up_sync(0xffffffffu, o.pn, 1);
   o.pr = __shfl_down_sync(0xffffffffu, o.pn, 1);
-  o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
-  o.hr = __shfl_down_sync(0xffffffffu, o.h, 1);
+  if constexpr (EW) {
+    const float4 c = *reinterpret_cast<const float4*>(slot + L::C + 16 * lane);
+    o.c0 = c.x;
+    o.c1 = c.y;
+    o.c2 = c.z;
+    o.c3 = c.w;
+    o.c0l = __shfl_up_sync(0xffffffffu, c.x, 1);
+    o.c1r = __shfl_down_sync(0xffffffffu, c.y, 1);
+    o.c3l = __shfl_up_sync(0xffffffffu, c.w, 1);
+  } else {
+    o.h = *reinterpret_cast<const float*>(slot + L::H + 4 * (dh + lane));
+    o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
+    o.hr = __shfl_down_sync(0xffffffffu, o.h, 1);
+  }
   return o;
 }
 
@@ -597,7 +662,10 @@ struct CtaShared {
   int pad[3];
 };
 
-constexpr size_t kSmemBytes = kSmemPerWarp * WORKERS + sizeof(CtaShared);
+template <bool EW>
+constexpr size_t smem_bytes() {
+  return ring_bytes<EW>() * WORKERS + sizeof(CtaShared);
+}
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
@@ -978,6 +1046,7 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
 // Per-item state of a worker's sweep.
 struct Sweep {
   uint32_t vdst;   // this lane's {r,q,p,x} destination in ring slot 0
+  uint32_t cdst;   // this lane's conductance destination in ring slot 0 (EW)
   uint32_t adst;   // this lane's aux destination in ring slot 0
   float4* orow;    // this lane's output pixel in the next centre row
   int nrows, dh, dm;
@@ -985,9 +1054,14 @@ struct Sweep {
 };
 
 // Copy the issuer's next row into ring slot j.
+template <bool EW>
 __device__ __forceinline__ void issue_row_c(const Sweep& w, int j, Issuer& is, uint32_t vpitch) {
-  const uint32_t off = uint32_t(j & (NS - 1)) * SLOT_BYTES;
+  const uint32_t off = uint32_t(j & (NS - 1)) * Slot<EW>::BYTES;
   cp_async16_if(w.vdst + off, is.v, is.on);
+  if (EW) {
+    cp_async16_if(w.cdst + off, is.c, is.on);
+    is.c += vpitch;
+  }
   cp_async16_if(w.adst + off, is.aux, is.on && is.aon);
   cp_commit();
   is.v += vpitch;
@@ -997,27 +1071,53 @@ __device__ __forceinline__ void issue_row_c(const Sweep& w, int j, Issuer& is, u
 // One step of a sweep: centre rows g+1, g+2 (GR = 2), with GB = g % 4 known
 // at compile time so that the compute-ring indices are constants (row r
 // lives in der[r % 4]).
-template <int CONN, bool PURE, int GB>
+template <int CONN, bool PURE, bool EW, int GB>
 __device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned char* ring,
-                                           Sweep& w, Issuer& is, uint32_t vpitch, Row (&der)[4],
+                                           Sweep& w, Issuer& is, uint32_t vpitch,
+                                           RowT<EW> (&der)[4],
                                            double (&acc)[SLOTS][NDOT], int g, int lane,
                                            const Cur& k) {
   static_assert(GR == 2, "the step body is written for two rows");
-  issue_row_c(w, g + 2 + LA, is, vpitch);
-  issue_row_c(w, g + 3 + LA, is, vpitch);
+  using L = Slot<EW>;
+  issue_row_c<EW>(w, g + 2 + LA, is, vpitch);
+  issue_row_c<EW>(w, g + 3 + LA, is, vpitch);
   cp_wait<LA>();  // rows up to g+3 have landed
   __syncwarp();
-  der[(GB + 2) & 3] = derive<PURE>(ring + ((g + 2) & (NS - 1)) * SLOT_BYTES, lane, w.dh, w.dm, k);
-  der[(GB + 3) & 3] = derive<PURE>(ring + ((g + 3) & (NS - 1)) * SLOT_BYTES, lane, w.dh, w.dm, k);
+  der[(GB + 2) & 3] =
+      derive<PURE, EW>(ring + ((g + 2) & (NS - 1)) * L::BYTES, lane, w.dh, w.dm, k);
+  der[(GB + 3) & 3] =
+      derive<PURE, EW>(ring + ((g + 3) & (NS - 1)) * L::BYTES, lane, w.dh, w.dm, k);
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int L = g + u + 1;  // centre local row
-    const Row& U = der[(GB + u) & 3];
-    const Row& C = der[(GB + u + 1) & 3];
-    const Row& D = der[(GB + u + 2) & 3];
-    const float pa = C.pn, ha = C.h;
+    const RowT<EW>& U = der[(GB + u) & 3];
+    const RowT<EW>& C = der[(GB + u + 1) & 3];
+    const RowT<EW>& D = der[(GB + u + 2) & 3];
+    const float pa = C.pn;
     const uint32_t m = C.m;
     float q = 0.f;
+    if constexpr (EW) {
+      // per-edge conductances: forward ones are the pixel's own, backward
+      // ones the forward conductance of the neighbour the edge starts at
+#define NI_C(bit, pp, cc) q = ((m >> (bit)) & 1u) ? fmaf(cc, pa - (pp), q) : q
+      if (CONN == 8) {
+        NI_C(0, C.pr, C.c0);   // (+1, 0)
+        NI_C(1, D.pl, C.c1);   // (-1,+1)
+        NI_C(2, D.pn, C.c2);   // ( 0,+1)
+        NI_C(3, D.pr, C.c3);   // (+1,+1)
+        NI_C(4, C.pl, C.c0l);  // (-1, 0): left pixel's (+1, 0)
+        NI_C(5, U.pr, U.c1r);  // (+1,-1): up-right pixel's (-1,+1)
+        NI_C(6, U.pn, U.c2);   // ( 0,-1): up pixel's (0,+1)
+        NI_C(7, U.pl, U.c3l);  // (-1,-1): up-left pixel's (+1,+1)
+      } else {
+        NI_C(0, C.pr, C.c0);   // (+1, 0)
+        NI_C(1, D.pn, C.c1);   // ( 0,+1)
+        NI_C(4, C.pl, C.c0l);  // (-1, 0)
+        NI_C(5, U.pn, U.c1);   // ( 0,-1)
+      }
+#undef NI_C
+    } else {
+    const float ha = C.h;
 #define NI_E(bit, pp, hh) q = ((m >> (bit)) & 1u) ? fmaf(ha + (hh), pa - (pp), q) : q
     if (CONN == 8) {
       NI_E(0, C.pr, C.hr);  // (+1, 0)
@@ -1035,6 +1135,7 @@ __device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned cha
       NI_E(5, U.pn, U.h);   // ( 0,-1)
     }
 #undef NI_E
+    }
     // pure: every centre pixel is the component's or zero (invalid /
     // singleton pixels carry r = q = p = x = 0 and stay 0); mixed: only
     // pixels of a live slot are written.  Dots are summed for every slot and
@@ -1062,7 +1163,7 @@ __device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned cha
 // the stream holds this item's rows 0..LA-1 (issued); as its last rows are
 // issued the worker peeks its mailbox for the next item (nx) and starts that
 // item's rows.  The warp-summed dots go to the scheduler as a FinishRec.
-template <int CONN, bool PURE>
+template <int CONN, bool PURE, bool EW>
 __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned char* ring,
                                            Mailbox& mb, int mbh, const Claim*& nx, Issuer& is,
                                            const Cur& k, bool& has_next, FinishBox& fb,
@@ -1080,7 +1181,8 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   w.dm = c0 & 15;
   w.orow = a.v[k.par ^ 1] + int64_t(k.y0 + RM) * a.P + (xr + XM);  // centre row 1
   w.nrows = k.y1 - k.y0;  // centre rows (local rows 1..nrows)
-  w.vdst = ring_s + SL_V + 16 * lane;
+  w.vdst = ring_s + Slot<EW>::V + 16 * lane;
+  w.cdst = ring_s + Slot<EW>::C + 16 * lane;
   w.adst = ring_s + is.adst;
   double acc[SLOTS][NDOT];
 #pragma unroll
@@ -1090,13 +1192,13 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   has_next = false;
   // rows LA and LA+1; rows 0 and 1 have landed once at most LA younger
   // row groups are pending
-  issue_row_c(w, LA, is, vpitch);
-  issue_row_c(w, LA + 1, is, vpitch);
+  issue_row_c<EW>(w, LA, is, vpitch);
+  issue_row_c<EW>(w, LA + 1, is, vpitch);
   cp_wait<LA>();
   __syncwarp();
-  Row der[4];  // row r of the item lives in der[r % 4]
-  der[0] = derive<PURE>(ring, lane, w.dh, w.dm, k);
-  der[1] = derive<PURE>(ring + SLOT_BYTES, lane, w.dh, w.dm, k);
+  RowT<EW> der[4];  // row r of the item lives in der[r % 4]
+  der[0] = derive<PURE, EW>(ring, lane, w.dh, w.dm, k);
+  der[1] = derive<PURE, EW>(ring + Slot<EW>::BYTES, lane, w.dh, w.dm, k);
 #pragma unroll 1
   for (int g = 0; g < 28; g += 4) {
     if (g == 24) {  // the stream moves on to the next item with the rows issued from here on
@@ -1104,15 +1206,15 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
       if (has_next) {
         __threadfence_block();
         nx = &mb.slot[mbh % MB];
-        issuer_start(a, nx->item, nx->par, is);
+        issuer_start<EW>(a, nx->item, nx->par, is);
       } else {
         is.on = false;
       }
     }
-    sweep_step<CONN, PURE, 0>(a, ring, w, is, vpitch, der, acc, g, lane, k);
-    sweep_step<CONN, PURE, 2>(a, ring, w, is, vpitch, der, acc, g + 2, lane, k);
+    sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, g, lane, k);
+    sweep_step<CONN, PURE, EW, 2>(a, ring, w, is, vpitch, der, acc, g + 2, lane, k);
   }
-  sweep_step<CONN, PURE, 0>(a, ring, w, is, vpitch, der, acc, 28, lane, k);
+  sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, 28, lane, k);
   // post the item's dots (fixed xor tree over lanes) for the scheduler
   constexpr int NS_ = PURE ? 1 : SLOTS;
   double tot[SLOTS][NDOT];
@@ -1162,7 +1264,7 @@ __device__ void initial_lists(const FillArgs& a, int gwarp, int nwarps) {
 
 // A worker warp: take items from its mailbox and sweep them, streaming rows
 // from one item into the next.
-template <int CONN>
+template <int CONN, bool EW>
 __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb, FinishBox& fb,
                             const CtaShared& sh) {
   const int lane = threadIdx.x & 31;
@@ -1193,8 +1295,8 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
       __threadfence_block();
       nx = &mb.slot[mbh % MB];
       have = true;
-      issuer_start(a, nx->item, nx->par, is);
-      for (int j = 0; j < LA; ++j) issue_row(ring_s, j, is, vpitch);
+      issuer_start<EW>(a, nx->item, nx->par, is);
+      for (int j = 0; j < LA; ++j) issue_row<EW>(ring_s, j, is, vpitch);
     }
     load_cur(*nx, cur);
     __syncwarp();
@@ -1202,9 +1304,9 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
     if (lane == 0) vstore(&mb.head, mbh);
     bool has_next = false;
     if (cur.flags & 0x100)
-      sweep_item<CONN, true>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
+      sweep_item<CONN, true, EW>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
     else
-      sweep_item<CONN, false>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
+      sweep_item<CONN, false, EW>(a, ring, mb, mbh, nx, is, cur, has_next, fb, fbt);
     if (!has_next) {
       cp_wait<0>();
       have = false;
@@ -1229,8 +1331,9 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
 // of all its items ran) publishes the group's next batch.  No grid-wide
 // barrier per iteration: groups drift apart and every worker stays busy
 // while any batch is open.
-template <int CONN, int MINB>
+template <int CONN, int MINB, bool EW>
 __global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
+  constexpr size_t kRing = ring_bytes<EW>();
   cg::grid_group grid = cg::this_grid();
   constexpr int WPC = NT_FILL / 32;
   const int gwarp = blockIdx.x * WPC + (threadIdx.x >> 5);
@@ -1245,13 +1348,13 @@ __global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
     }
   }
   extern __shared__ __align__(16) unsigned char smem[];
-  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem + kSmemPerWarp * WORKERS);
+  CtaShared& sh = *reinterpret_cast<CtaShared*>(smem + kRing * WORKERS);
   for (int i = threadIdx.x; i < int(sizeof(CtaShared) / sizeof(int)); i += NT_FILL)
     reinterpret_cast<int*>(&sh)[i] = 0;
   grid.sync();
   const int w = threadIdx.x >> 5;
   if (w == WORKERS) scheduler_loop(a, sh);
-  else worker_loop<CONN>(a, smem + kSmemPerWarp * w, sh.mb[w], sh.fb[w], sh);
+  else worker_loop<CONN, EW>(a, smem + kRing * w, sh.mb[w], sh.fb[w], sh);
 }
 
 // Initial ||b||^2 per component and the state of every component.  One warp
@@ -1397,7 +1500,7 @@ __global__ void grp_size_kernel(const Item* __restrict__ items, int nitems,
 // ------------------------------------------------------------ workspace
 
 struct FillWs {
-  float4 *v0, *v1;
+  float4 *v0, *v1, *cf;
   float* hw;
   uint8_t* imask;
   int32_t* lab_p;
@@ -1430,14 +1533,16 @@ static uint32_t ring_cap(int C) {
 static int pitch_of(int W) { return (W + XM + 48 + 15) & ~15; }
 static int64_t padded_len(int rows, int W) { return int64_t(rows + RM + RB) * pitch_of(W); }
 
-static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int nstrips, int C) {
+static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int nstrips, int C,
+                       bool weighted) {
   const int64_t npad = padded_len(rows, W);
   // every partial slot owns >= 1 pixel
   const int64_t P = npix;
   const int64_t NI = nstrips + P / SLOTS + 1;  // items
   w.v0 = c.take<float4>(npad);
   w.v1 = c.take<float4>(npad);
-  w.hw = c.take<float>(npad);
+  w.hw = c.take<float>(weighted ? 1 : npad);
+  w.cf = c.take<float4>(weighted ? npad : 1);
   w.imask = c.take<uint8_t>(npad);
   w.lab_p = c.take<int32_t>(npad);
   w.slot_base = c.take<int32_t>(nstrips + 1);
@@ -1503,27 +1608,30 @@ static void strip_grid(int B, int H, int W, int* nsx, int* nsy) {
 }
 
 extern "C" int ni_fill_workspace_size(int B, int H, int W, int connectivity, int count,
-                                      size_t* bytes) {
+                                      int weighted, size_t* bytes) {
   NI_CHECK_ARG(bytes, "null pointer");
   const int64_t npix = int64_t(B) * H * W;
   int nsx, nsy;
   strip_grid(B, H, W, &nsx, &nsy);
   Sizer s;
   FillWs w;
-  carve_fill(s, w, npix, B * H, W, nsx * nsy, count);
+  carve_fill(s, w, npix, B * H, W, nsx * nsy, count, weighted != 0);
   *bytes = s.used;
   return NI_OK;
 }
 
 extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
-                       const double* omega_b, const double* gamma, const uint8_t* eflags, int B,
-                       int H, int W, int connectivity, int model, double cg_tol, int cg_max_iters,
+                       const double* omega_b, const double* gamma, const uint8_t* eflags,
+                       const double* w_a, const double* w_b, int B, int H, int W,
+                       int connectivity, int model, double cg_tol, int cg_max_iters,
                        double* z_out, int32_t* comp_iters, int32_t* comp_status, void* workspace,
                        size_t workspace_bytes, ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
   NI_CHECK_ARG(model == 0 || (model == 1 && connectivity == 4), "bad model/connectivity");
   NI_CHECK_ARG(cg_tol > 0, "cg_tol must be positive");
   NI_CHECK_ARG(count >= 0, "count must be non-negative");
+  NI_CHECK_ARG((w_a == nullptr) == (w_b == nullptr), "w_a and w_b go together");
+  const bool weighted = w_a != nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npix = int64_t(B) * H * W;
   const int rows = B * H;
@@ -1533,7 +1641,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   const int nstrips = nsx * nsy;
   Carver cv(workspace, workspace_bytes);
   FillWs w;
-  carve_fill(cv, w, npix, rows, W, nstrips, count);
+  carve_fill(cv, w, npix, rows, W, nstrips, count, weighted);
   if (!cv.ok() || !workspace) {
     set_error("ni_fill: workspace too small (%zu < %zu)", workspace_bytes, cv.used);
     return NI_ERR_WORKSPACE;
@@ -1546,17 +1654,24 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
     const size_t npad = size_t(padded_len(rows, W));
     NI_CUDA_TRY(cudaMemsetAsync(w.v0, 0, npad * sizeof(float4), s));
     NI_CUDA_TRY(cudaMemsetAsync(w.v1, 0, npad * sizeof(float4), s));
-    NI_CUDA_TRY(cudaMemsetAsync(w.hw, 0, npad * sizeof(float), s));
+    if (weighted) NI_CUDA_TRY(cudaMemsetAsync(w.cf, 0, npad * sizeof(float4), s));
+    else NI_CUDA_TRY(cudaMemsetAsync(w.hw, 0, npad * sizeof(float), s));
     NI_CUDA_TRY(cudaMemsetAsync(w.imask, 0, npad, s));
     NI_CUDA_TRY(cudaMemsetAsync(w.lab_p, 0xff, npad * sizeof(int32_t), s));
   }
-#define NI_PREP(CONN, MODEL)                                                                   \
-  NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<blocks, 256, 0, s>>>(                          \
-                         labels, omega_a, omega_b, gamma, eflags, H, W, P, npix, w.hw, w.imask, \
-                         w.lab_p, w.v0, w.comp_size)
-  if (connectivity == 8) NI_PREP(8, 0);
-  else if (model == 0) NI_PREP(4, 0);
-  else NI_PREP(4, 1);
+#define NI_PREP(CONN, MODEL, EW)                                                               \
+  NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL, EW><<<blocks, 256, 0, s>>>(                      \
+                         labels, omega_a, omega_b, gamma, eflags, w_a, w_b, H, W, P, npix, w.hw, \
+                         w.cf, w.imask, w.lab_p, w.v0, w.comp_size)
+  if (weighted) {
+    if (connectivity == 8) NI_PREP(8, 0, true);
+    else if (model == 0) NI_PREP(4, 0, true);
+    else NI_PREP(4, 1, true);
+  } else {
+    if (connectivity == 8) NI_PREP(8, 0, false);
+    else if (model == 0) NI_PREP(4, 0, false);
+    else NI_PREP(4, 1, false);
+  }
 #undef NI_PREP
   NI_LAUNCH_CHECK();
   // ---- static reduction plan: strips -> items -> partial slots
@@ -1626,6 +1741,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.v[0] = w.v0;
   a.v[1] = w.v1;
   a.hw = w.hw;
+  a.cf = w.cf;
   a.imask = w.imask;
   a.lab = w.lab_p;
   a.items = w.items;
@@ -1668,7 +1784,13 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   }
   // ---- the whole CG: one persistent cooperative launch
   {
-    void* kfn = connectivity == 8 ? (void*)fill_cg_kernel<8, 1> : (void*)fill_cg_kernel<4, 1>;
+    void* kfn;
+    if (weighted)
+      kfn = connectivity == 8 ? (void*)fill_cg_kernel<8, 1, true> : (void*)fill_cg_kernel<4, 1, true>;
+    else
+      kfn = connectivity == 8 ? (void*)fill_cg_kernel<8, 1, false>
+                              : (void*)fill_cg_kernel<4, 1, false>;
+    const size_t kSmemBytes = weighted ? smem_bytes<true>() : smem_bytes<false>();
     int dev = 0, sms = 0, per_sm = 0;
     NI_CUDA_TRY(cudaGetDevice(&dev));
     NI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "ni_common.cuh"
+#include "ni_edges.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -313,8 +314,6 @@ static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
   w.sort_ws = c.take<char>(w.sort_bytes);
 }
 
-__device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
-
 // K4: weights and row right-hand sides (solver.py:253-278, 170-180)
 template <int CONN, int MODEL>
 __global__ void weights_kernel(Quot q, const double* __restrict__ z,
@@ -322,62 +321,14 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
                                const double* __restrict__ omega_b,
                                const double* __restrict__ gamma,
                                const uint8_t* __restrict__ eflags, int H, int W, int64_t npix,
-                               int uniform, int mode, double kk, double lt, double ut,
-                               double hi, StepWs w) {
+                               WeightArgs wp, StepWs w) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < q.K; e += gridDim.x * blockDim.x) {
     const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
-    const uint8_t efa = eflags[a];
-    const bool valid = (efa >> (4 + k)) & 1;
+    double wa, wb;
+    edge_weights_at<CONN, MODEL>(z, omega_a, omega_b, gamma, eflags, H, W, npix, a, k, wp, wa, wb);
     const double za = z[a], zb = z[b];
     const double oa = omega_a[k * npix + a];
     const double ob = MODEL == 0 ? -oa : omega_b[k * npix + a];
-    double wa = 0.0, wb = 0.0;
-    if (valid) {
-      if (uniform) {
-        wa = wb = 1.0;
-      } else {
-        const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
-        // opposite of b through a: a - off (continuity.py:196-207, 276)
-        const int ua = a % W, va = (a / W) % H;
-        const int uo = ua - du, vo = va - dv;
-        bool has_a = false;
-        double zoa = 0.0;
-        if (uo >= 0 && uo < W && vo >= 0) {
-          const int32_t o = a - dv * W - du;
-          if ((eflags[o] >> k) & 1) {  // edge o -> a exists: o valid, same map
-            has_a = true;
-            zoa = z[o];
-          }
-        }
-        const bool has_b = (eflags[b] >> k) & 1;  // b + off exists
-        const double zob = has_b ? z[b + dv * W + du] : 0.0;
-        const double ga = gamma[a], gb = gamma[b];
-        const double g2a = ga * ga, g2b = gb * gb;
-        double bil_a = 0.5, bil_b = 0.5;
-        if (has_a) {
-          const double dp = zoa - za, dq = zb - za;
-          bil_a = sigmoid(kk * (g2a * (dp * dp - dq * dq)));
-        }
-        if (has_b) {
-          const double dp = zob - zb, dq = za - zb;
-          bil_b = sigmoid(kk * (g2b * (dp * dp - dq * dq)));
-        }
-        wa = g2a * bil_a;
-        wb = g2b * bil_b;
-        // outlier weights on chi (continuity.py:140-158)
-        const double chia = za - zb - oa, chib = zb - za - ob;
-        if (mode == 1) {
-          const double ca = fabs(chia) > 1e-300 ? fabs(chia) : 1e-300;
-          const double cb = fabs(chib) > 1e-300 ? fabs(chib) : 1e-300;
-          const double sc = 4.0 / (lt - ut);
-          wa *= sigmoid(sc * (2.0 * log10(ca) - (lt + ut)));
-          wb *= sigmoid(sc * (2.0 * log10(cb) - (lt + ut)));
-        } else if (mode == 2) {
-          if (fabs(chia) >= hi) wa = 0.0;
-          if (fabs(chib) >= hi) wb = 0.0;
-        }
-      }
-    }
     w.wa[e] = wa;
     w.wb[e] = wb;
     w.ba[e] = oa - (za - zb);
@@ -1043,20 +994,22 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     NI_CUDA_TRY(cudaMemsetAsync(scales, 0, sizeof(double) * C, s));
     return NI_OK;
   }
-  const int uniform = t < alignment_iters;
-  const double lt = log10(outlier_low), ut = log10(outlier_high);
+  WeightArgs wp;
+  wp.wmode = t < alignment_iters ? EW_UNIFORM : EW_FULL;
+  wp.mode = mode;
+  wp.k = k;
+  wp.lt = log10(outlier_low);
+  wp.ut = log10(outlier_high);
+  wp.hi = outlier_high;
   if (connectivity == 8)
     NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
-                           ut, outlier_high, w);
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else if (model == 0)
     NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
-                           ut, outlier_high, w);
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else
     NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, uniform, mode, k, lt,
-                           ut, outlier_high, w);
+                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
   NI_COUNT_LAUNCH(), comp_sum_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, w);

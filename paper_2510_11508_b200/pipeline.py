@@ -204,17 +204,52 @@ def _coefficients(g: _Grid, intrinsics: list[CameraIntrinsics]):
     return omega_a, omega_b, gamma, eflags
 
 
-def _fill(g: _Grid, labels, count, co, settings: SolveSettings):
+# weight modes of ni_edge_weights (ni_edges.cuh)
+EW_UNIFORM, EW_BILATERAL, EW_FULL = 0, 1, 2
+
+
+def _edge_weights(g: _Grid, co, z: torch.Tensor, wmode: int, weights: WeightParams):
+    """Directed weights of every forward pixel edge at state z (continuity.py:292-331,
+    solver.py:253-278)."""
+    omega_a, omega_b, gamma, eflags = co
+    w_a = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
+    w_b = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
+    _lib.check(g.lib.ni_edge_weights(_ptr(z), _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
+                                     _ptr(eflags), g.B, g.H, g.W, g.conn, g.model, wmode,
+                                     weights.mode_code, C.c_double(weights.k),
+                                     C.c_double(weights.outlier_low),
+                                     C.c_double(weights.outlier_high), _ptr(w_a), _ptr(w_b),
+                                     g.s()), "edge_weights")
+    return w_a, w_b
+
+
+def _pair_energy(g: _Grid, co, x: torch.Tensor, wts) -> torch.Tensor:
+    """Per-map energy of the pixel pair system at x (pipeline.py:336-337)."""
+    omega_a, omega_b, _, eflags = co
+    out = torch.empty(g.B, dtype=torch.float64, device=g.dev)
+    ws = _ws(_lib.size_query(g.lib.ni_pair_energy_workspace_size, g.B), g.dev)
+    _lib.check(g.lib.ni_pair_energy(_ptr(x), _ptr(omega_a), _ptr(omega_b), _ptr(wts[0]),
+                                    _ptr(wts[1]), _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
+                                    _ptr(out), _ptr(ws), ws.numel(), g.s()), "pair_energy")
+    return out
+
+
+def _fill(g: _Grid, labels, count, co, settings: SolveSettings, wts=None):
+    """Batched per-component CG (solver.py:195-239); ``wts`` = per-edge weights
+    (w_a, w_b) for the refill pass / the pixel baseline, None for the fill."""
     lib = g.lib
     omega_a, omega_b, gamma, eflags = co
     z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
     iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
     status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
-    ws = _ws(_lib.size_query(lib.ni_fill_workspace_size, g.B, g.H, g.W, g.conn, count), g.dev)
+    ws = _ws(_lib.size_query(lib.ni_fill_workspace_size, g.B, g.H, g.W, g.conn, count,
+                             int(wts is not None)), g.dev)
+    w_a, w_b = (None, None) if wts is None else wts
     _lib.check(lib.ni_fill(_ptr(labels), count, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
-                           _ptr(eflags), g.B, g.H, g.W, g.conn, g.model, C.c_double(settings.cg_tol),
-                           int(settings.cg_max_iters), _ptr(z), _ptr(iters), _ptr(status), _ptr(ws),
-                           ws.numel(), g.s()), "fill_components")
+                           _ptr(eflags), _ptr(w_a), _ptr(w_b), g.B, g.H, g.W, g.conn, g.model,
+                           C.c_double(settings.cg_tol), int(settings.cg_max_iters), _ptr(z),
+                           _ptr(iters), _ptr(status), _ptr(ws), ws.numel(), g.s()),
+               "fill_components")
     return z, iters[:count], status[:count]
 
 
@@ -341,9 +376,6 @@ def run_pipeline_batch(
     settings = settings or SolveSettings()
     weights = weights or WeightParams()
     _validate(model, connectivity)
-    if settings.refill_reweighted:
-        # solver.py:237-238 -- SURVEY.md §8(f) row 2, not built yet
-        raise NotImplementedError("refill_reweighted is not implemented on the GPU path yet")
     B = nmap.batch
     intr = list(intrinsics) if isinstance(intrinsics, (list, tuple)) else [intrinsics] * B
     if len(intr) != B:
@@ -383,12 +415,18 @@ def run_pipeline_batch(
 
     t0 = time.perf_counter()
     total = int(first[B])
-    z, fill_iters, fill_status = _fill(g, labels, total, co, settings)
+    passes = 2 if settings.refill_reweighted else 1
+    z = None
+    for pas in range(passes):
+        # pass 2 (solver.py:237-238): same components, weights re-evaluated
+        # with the bilateral factors at the filled state (edge_weights at z)
+        wts = None if pas == 0 else _edge_weights(g, co, z, EW_BILATERAL, weights)
+        z, fill_iters, fill_status = _fill(g, labels, total, co, settings, wts)
+        capped = np.flatnonzero(fill_status.cpu().numpy())
+        for c in capped:
+            m = int(np.searchsorted(first, c, side="right") - 1)
+            warnings[m].append(f"component {int(c - first[m])}: cg hit iteration cap")
     report = _lib.fill_report()
-    capped = np.flatnonzero(fill_status.cpu().numpy())
-    for c in capped:
-        m = int(np.searchsorted(first, c, side="right") - 1)
-        warnings[m].append(f"component {int(c - first[m])}: cg hit iteration cap")
     fill_ms = _ms(t0)
     for m in range(B):
         records[m].append({"stage": "fill", "wall_ms": fill_ms})
@@ -520,3 +558,115 @@ def run_pipeline(
         raise ValueError("run_pipeline takes a single map; use run_pipeline_batch")
     return run_pipeline_batch(nmap, [intr], theta_c, settings, weights, connectivity, model,
                               gauge_depth)[0]
+
+
+@dataclass
+class BaselineResult:
+    """pipeline.py:288-294."""
+
+    log_depth: LogDepthMap
+    records: list
+    warnings: list = field(default_factory=list)
+    iterations: int = 0
+    energies: list = field(default_factory=list)
+
+
+def run_pixel_baseline_batch(
+    nmap: NormalMap,
+    intrinsics,
+    settings: SolveSettings | None = None,
+    weights: WeightParams | None = None,
+    connectivity: int = 8,
+    model: str = "milano",
+    gauge_depth: float | None = None,
+) -> list[BaselineResult]:
+    """``run_pixel_baseline`` (pipeline.py:297-369) over the B maps of a batch.
+
+    Each outer iteration re-solves the full pixel system of every map that has
+    not converged -- one CG per map over all its valid pixels, from x0 = 0,
+    with the inter-system weight schedule (pipeline.py:261-285) -- in one
+    batched weighted-fill launch, and the solutions replace z.
+    """
+    settings = settings or SolveSettings()
+    weights = weights or WeightParams()
+    _validate(model, connectivity)
+    B = nmap.batch
+    intr = list(intrinsics) if isinstance(intrinsics, (list, tuple)) else [intrinsics] * B
+    if len(intr) != B:
+        raise ValueError("need one CameraIntrinsics per map")
+    run_start = time.perf_counter()
+    g = _Grid(nmap, connectivity, model)
+    if nmap.valid_count == 0:
+        raise EmptyMask("normal map has no valid pixel")
+    co = _coefficients(g, intr)
+    valid = g.nmap.valid_t
+    vbool = valid.bool()
+    nvalid = valid.view(B, -1).sum(dim=1, dtype=torch.int64).cpu().numpy()
+    mapid = (torch.arange(g.npix, device=g.dev, dtype=torch.int64) // g.hw).to(torch.int32)
+    z = torch.zeros(g.npix, dtype=torch.float64, device=g.dev)
+    records = [[] for _ in range(B)]
+    warnings = [[] for _ in range(B)]
+    energies = [[] for _ in range(B)]
+    iters = np.zeros(B, dtype=np.int64)
+    e_prev = np.full(B, ENERGY_FLOOR)
+    active = np.ones(B, dtype=bool)
+    t = 0
+    while active.any():
+        it_start = time.perf_counter()
+        act_t = torch.from_numpy(active).to(g.dev)
+        live = vbool & act_t[mapid.long()]
+        labels = torch.where(live, mapid, torch.full_like(mapid, -1))
+        wts = _edge_weights(g, co, z, EW_UNIFORM if t < settings.alignment_iters else EW_FULL,
+                            weights)
+        x, _, status = _fill(g, labels, B, co, settings, wts)
+        energy = _pair_energy(g, co, x, wts)
+        z = torch.where(live, x, z)
+        host = torch.cat([energy, status.to(torch.float64)]).cpu().numpy()
+        e_now, capped = host[:B], host[B:]
+        wall = _ms(it_start)
+        t_step = t
+        t += 1
+        for m in np.flatnonzero(active):
+            m = int(m)
+            if capped[m]:
+                warnings[m].append(f"iteration {t_step}: cg hit iteration cap")
+            e_t = float(e_now[m])
+            conv = _has_converged(e_t, e_prev[m], t, settings)
+            e_prev[m] = e_t
+            energies[m].append(e_t)
+            records[m].append({"t": t, "E_t": e_t, "component_count": int(nvalid[m]),
+                               "merge_performed": False, "wall_ms": wall})
+            if conv:
+                active[m] = False
+                iters[m] = t
+    target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
+    ws = _ws(_lib.size_query(g.lib.ni_gauge_workspace_size, g.B, g.H, g.W), g.dev)
+    _lib.check(g.lib.ni_gauge(_ptr(z), _ptr(valid), g.B, g.H, g.W, C.c_double(target),
+                              C.c_void_p(0), _ptr(ws), ws.numel(), g.s()), "gauge")
+    out = []
+    for m in range(B):
+        sl = slice(m * g.hw, (m + 1) * g.hw)
+        records[m].append({"stage": "done", "iterations": int(iters[m]),
+                           "warnings": len(warnings[m]), "wall_ms": _ms(run_start)})
+        out.append(BaselineResult(LogDepthMap(z[sl], valid[sl], g.H, g.W), records[m],
+                                  warnings[m], int(iters[m]), energies[m]))
+    return out
+
+
+def run_pixel_baseline(
+    nmap: NormalMap,
+    intr: CameraIntrinsics,
+    settings: SolveSettings | None = None,
+    weights: WeightParams | None = None,
+    connectivity: int = 8,
+    model: str = "milano",
+    gauge_depth: float | None = None,
+) -> BaselineResult:
+    """Iteratively reweighted per-pixel log-depth integration
+    (pipeline.py:297-369): same weight schedule and convergence test as
+    ``run_pipeline``, but the full pixel system is re-solved every iteration."""
+    if nmap.batch != 1:
+        raise ValueError("run_pixel_baseline takes a single map; use run_pixel_baseline_batch")
+    return run_pixel_baseline_batch(nmap, [intr], settings, weights, connectivity, model,
+                                    gauge_depth)[0]
+

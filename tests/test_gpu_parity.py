@@ -43,7 +43,8 @@ def opts_of(d):
 def run_gpu(normals, mask, intr, opts):
     theta = opts.get("theta_c_deg", 3.5)
     nm = nb.NormalMap.create(normals, mask)
-    st = nb.SolveSettings(freq_merging=opts.get("merge_freq"))
+    st = nb.SolveSettings(freq_merging=opts.get("merge_freq"),
+                          refill_reweighted=bool(opts.get("refill", False)))
     wp = nb.WeightParams(reweighting_mode=opts.get("reweighting", "soft"))
     return nb.run_pipeline(nm, nb.CameraIntrinsics(*intr),
                            None if theta is None else float(np.deg2rad(theta)), st, wp,
@@ -105,7 +106,8 @@ def test_pipeline_vs_oracle(name):
     ref = O.run_pipeline(d["normals"].astype(np.float64), mask, tuple(d["intr"]),
                          None if theta is None else float(np.deg2rad(theta)),
                          O.Settings(freq_merging=o.get("merge_freq"),
-                                    reweighting_mode=o.get("reweighting", "soft")),
+                                    reweighting_mode=o.get("reweighting", "soft"),
+                                    refill_reweighted=bool(o.get("refill", False))),
                          o.get("connectivity", 8), o.get("model", "milano"), o.get("gauge_depth"))
     assert np.array_equal(r.partition0.labels, ref.labels0)
     if ref.iterations < 150:
@@ -167,3 +169,63 @@ def test_errors_like_reference():
     nm = nb.NormalMap.create(n)
     with pytest.raises(ValueError):
         nb.run_pipeline(nm, nb.CameraIntrinsics(1, 1, 0, 0), 0.1, connectivity=8, model="bini")
+
+
+# ------------------------------------------------------- pixel-level baseline
+
+
+def run_gpu_baseline(d):
+    o = opts_of(d)
+    nm = nb.NormalMap.create(d["normals"], d["mask"])
+    return nb.run_pixel_baseline(nm, nb.CameraIntrinsics(*tuple(d["intr"])), nb.SolveSettings(),
+                                 nb.WeightParams(reweighting_mode=o.get("reweighting", "soft")),
+                                 o.get("connectivity", 8), o.get("model", "milano"),
+                                 o.get("gauge_depth"))
+
+
+@pytest.mark.parametrize("name", BASELINE_CASES)
+def test_pixel_baseline_vs_reference(name):
+    """run_pixel_baseline (pipeline.py:297-369) on the GPU: same outer
+    iterations, records and warnings as the reference, depth within the
+    north-star tolerance, energies to the fp32-CG precision."""
+    d = load(name)
+    mask = d["mask"]
+    r = run_gpu_baseline(d)
+    assert r.iterations == int(d["iterations"])
+    assert len(r.warnings) == int(d["warnings"])
+    assert_depth_close(r.log_depth.values, d["log_depth"], mask, float(d["intr"][0]))
+    np.testing.assert_allclose(r.energies, d["energies"], rtol=2e-3, atol=1e-9)
+    rec = json.loads(str(d["records"]))
+    assert [x.get("stage") for x in r.records] == [x.get("stage") for x in rec]
+    for a, b in zip(r.records, rec):
+        assert set(a) == set(b) | {"wall_ms"}
+        for k in ("t", "component_count", "merge_performed", "iterations", "warnings"):
+            if k in b:
+                assert a[k] == b[k], (k, a[k], b[k])
+
+
+def test_pixel_baseline_batch_equals_single_maps():
+    cases = [load(n) for n in ("pb_voronoi40", "pb_hemi40")]
+    # same size maps only: pad the hemisphere case's mask/normals are 40x40 too
+    normals = np.stack([c["normals"] for c in cases])
+    masks = np.stack([c["mask"] for c in cases])
+    nm = nb.NormalMap.create(normals, masks)
+    res = nb.run_pixel_baseline_batch(nm, [nb.CameraIntrinsics(*tuple(c["intr"])) for c in cases])
+    for c, rb in zip(cases, res):
+        rs = run_gpu_baseline(c)
+        assert rb.iterations == rs.iterations
+        assert np.array_equal(rb.log_depth.values, rs.log_depth.values)
+        assert rb.energies == rs.energies
+
+
+def test_refill_changes_the_fill():
+    """solver.py:237-238: the second pass uses bilateral weights at the filled
+    state (reference test_solver.py:218-231)."""
+    d = load("refill_voronoi48")
+    o = opts_of(d)
+    a = run_gpu(d["normals"], d["mask"], tuple(d["intr"]), {k: v for k, v in o.items() if k != "refill"})
+    b = run_gpu(d["normals"], d["mask"], tuple(d["intr"]), o)
+    assert not np.array_equal(a.filled.values, b.filled.values)
+    err = np.abs(b.filled.values - d["filled"])[d["mask"]]
+    assert err.max() < 2e-5, err.max()
+

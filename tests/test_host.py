@@ -49,7 +49,10 @@ def test_host_only_entry_points(lib):
 
     assert b"sm_100a" in lib.ni_version()
     assert _lib.size_query(lib.ni_components_workspace_size, 1, 64, 64) > 64 * 64 * 12
-    assert _lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10) > 2 * 64 * 64 * 20
+    assert _lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10, 0) > 2 * 64 * 64 * 20
+    assert (_lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10, 1)
+            > _lib.size_query(lib.ni_fill_workspace_size, 2, 64, 64, 8, 10, 0))
+    assert _lib.size_query(lib.ni_pair_energy_workspace_size, 3) > 0
     assert _lib.size_query(lib.ni_inter_edges_workspace_size, 1, 32, 32, 4) > 0
     assert _lib.size_query(lib.ni_keys_filter_workspace_size, 100) > 0
     assert _lib.size_query(lib.ni_quotient_workspace_size, 100, 10, 2) > 0
