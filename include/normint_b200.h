@@ -203,6 +203,23 @@ int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
              const double* weights, int32_t* new_count_out, double* energy_out, void* workspace,
              size_t workspace_bytes, ni_stream_t stream);
 
+/* Evaluation (metrics.py:44-113), per map of a batch.  ni_evaluate: median
+ * of gt/pred over jointly valid pixels (finite, > 0, in mask; mask may be
+ * NULL) as the aligned scale, then out[4m..4m+3] = MADE, relative error,
+ * scale, valid count (count 0: no overlap).  ni_min_theoretical_made: labels
+ * = the partition's global labels, map_first[B+1] a HOST array of the maps'
+ * label ranges; each component gets its exactly L1-optimal scale (weighted
+ * median ratio); out[2m] = pixel-count weighted mean error, out[2m+1] = the
+ * pixel count. */
+int ni_evaluate_workspace_size(int B, int H, int W, size_t* bytes);
+int ni_evaluate(const double* pred, const double* gt, const uint8_t* mask, int B, int H, int W,
+                double* out, void* workspace, size_t workspace_bytes, ni_stream_t stream);
+int ni_min_theoretical_made_workspace_size(int B, int H, int W, size_t* bytes);
+int ni_min_theoretical_made(const double* pred, const double* gt, const uint8_t* mask,
+                            const int32_t* labels, const int32_t* map_first, int B, int H, int W,
+                            double* out, void* workspace, size_t workspace_bytes,
+                            ni_stream_t stream);
+
 /* K9 -- gauge fix (pipeline.py:86-88, 229): z += target - median(z[valid])
  * for each map separately (B medians); target = log(gauge_depth) or 0.
  * Optionally writes depth_out = exp(z) on valid pixels (geometry.py:180-184). */

@@ -722,3 +722,58 @@ def run_pixel_baseline(normals, mask, intr, st: Settings | None = None, connecti
     return BaselineOracleResult(np.where(flat, z, 0.0).reshape(h, w), records, warnings, t,
                                 energies, cg_iters)
 
+
+# ------------------------------------------------------------------ metrics
+
+
+def _joint_valid(pred, gt, mask):
+    """metrics.py:37-41."""
+    ok = np.isfinite(pred) & np.isfinite(gt) & (pred > 0) & (gt > 0)
+    if mask is not None:
+        ok &= np.asarray(mask, dtype=bool)
+    return ok
+
+
+def evaluate(pred, gt, mask=None):
+    """Median-ratio aligned MADE / relative error (metrics.py:44-65).
+    Returns (made, relative_error, aligned_scale, valid_pixel_count)."""
+    pred = np.asarray(pred, np.float64)
+    gt = np.asarray(gt, np.float64)
+    ok = _joint_valid(pred, gt, mask)
+    if not ok.any():
+        raise OracleError("no jointly valid pixel")
+    p, g = pred[ok], gt[ok]
+    scale = float(np.median(g / p))
+    err = np.abs(scale * p - g)
+    return float(np.mean(err)), float(np.mean(err / g)), scale, int(ok.sum())
+
+
+def l1_optimal_scale(pred, gt):
+    """Weighted median of gt/pred with weights pred (metrics.py:68-84)."""
+    pred = np.asarray(pred, np.float64).ravel()
+    gt = np.asarray(gt, np.float64).ravel()
+    ratios = gt / pred
+    order = np.argsort(ratios, kind="stable")
+    cum = np.cumsum(pred[order])
+    return float(ratios[order][int(np.searchsorted(cum, 0.5 * cum[-1], side="left"))])
+
+
+def min_theoretical_made(pred, gt, labels, count, mask=None):
+    """Per-component L1-optimal scales, pixel-weighted mean error
+    (metrics.py:87-113)."""
+    pred = np.asarray(pred, np.float64).ravel()
+    gt = np.asarray(gt, np.float64).ravel()
+    ok = _joint_valid(pred, gt, None if mask is None else np.asarray(mask).ravel())
+    total_err, total_px = 0.0, 0
+    for c in range(count):
+        pix = np.flatnonzero(labels == c)
+        pix = pix[ok[pix]]
+        if len(pix) == 0:
+            continue
+        s = l1_optimal_scale(pred[pix], gt[pix])
+        total_err += float(np.sum(np.abs(s * pred[pix] - gt[pix])))
+        total_px += len(pix)
+    if total_px == 0:
+        raise OracleError("no jointly valid pixel in any component")
+    return total_err / total_px
+

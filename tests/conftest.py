@@ -12,12 +12,12 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def golden_cases(prefix=None):
     """Names of the golden fixtures: run_pipeline cases (prefix None), or the
-    ``pb_`` (run_pixel_baseline) / ``seam_`` ones."""
+    ``pb_`` (run_pixel_baseline) / ``seam_`` / ``metrics_`` ones."""
     import glob
 
     names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
     if prefix is None:
-        return [n for n in names if not n.startswith(("seam_", "pb_"))]
+        return [n for n in names if not n.startswith(("seam_", "pb_", "metrics_"))]
     return [n for n in names if n.startswith(prefix)]
 
 

@@ -229,3 +229,42 @@ def test_refill_changes_the_fill():
     err = np.abs(b.filled.values - d["filled"])[d["mask"]]
     assert err.max() < 2e-5, err.max()
 
+
+
+# ------------------------------------------------------------------- metrics
+
+
+@pytest.mark.parametrize("name", golden_cases("metrics_"))
+def test_gpu_metrics_match_reference(name):
+    """ni_evaluate / ni_min_theoretical_made vs the reference's metrics.py:
+    the aligned scale (an exact median) and the count bit-exact, the sums to
+    summation-order precision."""
+    from paper_2510_11508_b200 import metrics
+
+    d = load(name)
+    rep = metrics.evaluate(d["pred"], d["gt"], d["mask"])
+    assert rep.valid_pixel_count == int(d["valid_pixel_count"])
+    assert rep.aligned_scale == float(d["aligned_scale"])
+    assert np.isclose(rep.made, float(d["made"]), rtol=1e-12)
+    assert np.isclose(rep.relative_error, float(d["relative_error"]), rtol=1e-12)
+
+    class P:  # a reference-style partition of this map
+        labels = d["labels"]
+        component_count = int(d["ncomp"])
+
+    mtm = metrics.min_theoretical_made(d["pred"], d["gt"], P, d["mask"])
+    assert np.isclose(mtm, float(d["min_theoretical_made"]), rtol=1e-12)
+    ok = np.isfinite(d["pred"]) & (d["pred"] > 0) & d["mask"]
+    assert metrics.l1_optimal_scale(d["pred"][ok][:500], d["gt"][ok][:500]) == float(d["l1_scale"])
+
+
+def test_gpu_metrics_batch_equals_single():
+    from paper_2510_11508_b200 import metrics
+
+    a, b = load("metrics_c"), load("metrics_c")
+    b = {k: v for k, v in b.items()}
+    b["pred"] = b["pred"] * 1.7
+    reps = metrics.evaluate_batch(np.stack([a["pred"], b["pred"]]), np.stack([a["gt"], b["gt"]]),
+                                  np.stack([a["mask"], b["mask"]]))
+    assert reps[0] == metrics.evaluate(a["pred"], a["gt"], a["mask"])
+    assert reps[1] == metrics.evaluate(b["pred"], b["gt"], b["mask"])

@@ -204,3 +204,18 @@ def test_oracle_matches_reference_pixel_baseline(name):
     assert [x.keys() for x in rec] == [x.keys() for x in ref]
     assert [x.get("t") for x in rec] == [x.get("t") for x in ref]
 
+
+
+@pytest.mark.parametrize("name", golden_cases("metrics_"))
+def test_oracle_metrics_match_reference(name):
+    """evaluate / l1_optimal_scale / min_theoretical_made (metrics.py:44-113)."""
+    d = load(name)
+    made, rel, scale, n = O.evaluate(d["pred"], d["gt"], d["mask"])
+    assert n == int(d["valid_pixel_count"])
+    assert scale == float(d["aligned_scale"])
+    assert np.isclose(made, float(d["made"]), rtol=1e-12)
+    assert np.isclose(rel, float(d["relative_error"]), rtol=1e-12)
+    mtm = O.min_theoretical_made(d["pred"], d["gt"], d["labels"], int(d["ncomp"]), d["mask"])
+    assert np.isclose(mtm, float(d["min_theoretical_made"]), rtol=1e-12)
+    ok = np.isfinite(d["pred"]) & (d["pred"] > 0) & d["mask"]
+    assert O.l1_optimal_scale(d["pred"][ok][:500], d["gt"][ok][:500]) == float(d["l1_scale"])
