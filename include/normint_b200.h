@@ -203,6 +203,13 @@ int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
              const double* weights, int32_t* new_count_out, double* energy_out, void* workspace,
              size_t workspace_bytes, ni_stream_t stream);
 
+/* 16-bit PNG normals (fileio.py:134-161): bgr = the inflated (H, W, 3)
+ * uint16 samples as stored (BGR); writes n_out (H, W, 3) float64 = v / 65535
+ * * 2 - 1 per channel (z negated if flip_z) divided by its norm, and
+ * mask_out (all-zero pixels and zero norms are invalid); float64-exact. */
+int ni_decode_png16(const uint16_t* bgr, int H, int W, int flip_z, double* n_out,
+                    uint8_t* mask_out, ni_stream_t stream);
+
 /* Evaluation (metrics.py:44-113), per map of a batch.  ni_evaluate: median
  * of gt/pred over jointly valid pixels (finite, > 0, in mask; mask may be
  * NULL) as the aligned scale, then out[4m..4m+3] = MADE, relative error,

@@ -61,6 +61,7 @@ SIGNATURES = {
     "ni_merge_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_merge": ([_P, _SZ, _I, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P, _P, _P, _P, _P, _SZ, _P],
                  _I),
+    "ni_decode_png16": ([_P, _I, _I, _I, _P, _P, _P], _I),
     "ni_evaluate_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_evaluate": ([_P, _P, _P, _I, _I, _I, _P, _P, _SZ, _P], _I),
     "ni_min_theoretical_made_workspace_size": ([_I, _I, _I, _PSZ], _I),
