@@ -632,8 +632,16 @@ __device__ unsigned long long g_fill_stats[8];
 // accounting), so a worker only ever streams rows: the dependent global
 // round trips of claiming and retiring overlap the sweeps instead of
 // stalling them.
-constexpr int MB = 2;  // claimed items per worker mailbox
-constexpr int FQ = 2;  // finished-item records per worker
+#ifndef NI_MB
+#define NI_MB 2
+#endif
+#ifndef NI_FQ
+#define NI_FQ 4
+#endif
+constexpr int MB = NI_MB;  // claimed items per worker mailbox
+constexpr int FQ = NI_FQ;  // finished-item records per worker
+static_assert(32 / NI_WORKERS >= 1, "one record per lane and wave");
+static_assert(NI_MB * NI_WORKERS <= 32, "one claim target per lane");
 
 struct Mailbox {  // scheduler -> worker (single producer, single consumer)
   Claim slot[MB];
@@ -950,7 +958,8 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
     int pend = 0, fh = 0;
     if (lane < WORKERS) {
       fh = vload(&sh.fb[lane].head);
-      pend = vload(&sh.fb[lane].tail) - fh;
+      // at most 32 records per wave (one per lane)
+      pend = min(vload(&sh.fb[lane].tail) - fh, 32 / WORKERS);
     }
     // one record per lane: exclusive prefix over the workers' pending counts
     int incl = pend;
@@ -979,7 +988,7 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
         const int h0 = vload(&sh.fb[w].head);
         r = sh.fb[w].rec[(h0 + lane - base) % FQ];
       }
-      retire_items(a, r, min(total, 32));
+      retire_items(a, r, total);
       __syncwarp();
       if (lane < WORKERS && pend > 0) vstore(&sh.fb[lane].head, fh + pend);
     }
@@ -1168,7 +1177,8 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
                                            Mailbox& mb, int mbh, const Claim*& nx, Issuer& is,
                                            const Cur& k, bool& has_next, FinishBox& fb,
                                            int& fbt) {
-  static_assert(NS == 8 && LA == 6 && IROWS - 2 - LA == 24 && SH == 30,
+  constexpr int GSW = IROWS - 2 - LA;  // first step that issues the next item's rows
+  static_assert(SH == 30 && GSW % 4 == 0 && GSW < 28 && GSW >= 0,
                 "the unrolled step schedule below assumes these shapes");
   const int lane = threadIdx.x & 31;
   const uint32_t ring_s = smem_u32(ring);
@@ -1201,7 +1211,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   der[1] = derive<PURE, EW>(ring + Slot<EW>::BYTES, lane, w.dh, w.dm, k);
 #pragma unroll 1
   for (int g = 0; g < 28; g += 4) {
-    if (g == 24) {  // the stream moves on to the next item with the rows issued from here on
+    if (g == GSW) {  // the stream moves on to the next item with the rows issued from here on
       has_next = mbh < vload(&mb.tail);
       if (has_next) {
         __threadfence_block();

@@ -17,7 +17,7 @@ def golden_cases(prefix=None):
 
     names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
     if prefix is None:
-        return [n for n in names if not n.startswith(("seam_", "pb_", "metrics_"))]
+        return [n for n in names if not n.startswith(("seam_", "pb_", "metrics_", "files_"))]
     return [n for n in names if n.startswith(prefix)]
 
 
