@@ -72,49 +72,131 @@ __global__ void __launch_bounds__(256) normalize_kernel(const T* __restrict__ in
 
 // ------------------------------------------------------------------ K1
 
-__global__ void uf_init_kernel(const uint8_t* __restrict__ valid, int64_t npix,
-                               int32_t* __restrict__ parent) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x)
-    parent[i] = valid[i] ? int32_t(i) : -1;
+// Tiled K1: union-find inside 32 x 32 tiles in shared memory (local ids are
+// row-major within the tile, so the smaller local id is the smaller pixel
+// id), then one global union per kept edge that leaves its tile.
+constexpr int UT = 32;  // tile edge
+
+__device__ __forceinline__ bool kept_edge(const double* __restrict__ n, int64_t npix, int64_t i,
+                                          int64_t j, double cutoff, int theta_none) {
+  if (theta_none) return false;
+  const double d = add_rn(add_rn(mul_rn(n[i], n[j]), mul_rn(n[npix + i], n[npix + j])),
+                          mul_rn(n[2 * npix + i], n[2 * npix + j]));
+  return d >= cutoff;
+}
+
+__device__ __forceinline__ int sm_find(volatile int* p, int x) {
+  int q = p[x];
+  while (q != x) {
+    const int gq = p[q];
+    if (gq != q) p[x] = gq;
+    x = gq;
+    q = p[x];
+  }
+  return x;
+}
+
+__device__ __forceinline__ void sm_union(int* p, int a, int b) {
+  volatile int* vp = p;
+  while (true) {
+    a = sm_find(vp, a);
+    b = sm_find(vp, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(p + a, b);
+    if (old == a) return;
+    a = old;
+  }
 }
 
 template <int CONN>
-__global__ void __launch_bounds__(256) uf_union_kernel(const double* __restrict__ n,
-                                                       const uint8_t* __restrict__ valid, int H,
-                                                       int W, int64_t npix, double cutoff,
-                                                       int theta_none, int32_t* parent,
-                                                       ni_stats* st) {
+__global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__ n,
+                                                      const uint8_t* __restrict__ valid, int H,
+                                                      int W, int64_t rows, int tiles_x,
+                                                      double cutoff, int theta_none,
+                                                      int32_t* __restrict__ parent,
+                                                      ni_stats* __restrict__ st) {
   constexpr int KF = CONN == 8 ? 4 : 2;
+  __shared__ int p[UT * UT];
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int x0 = tx * UT;
+  const int64_t y0 = int64_t(ty) * UT;
+  const int64_t npix = rows * W;
+  for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
+    const int x = x0 + (l % UT);
+    const int64_t y = y0 + l / UT;
+    p[l] = (x < W && y < rows && valid[y * W + x]) ? l : -1;
+  }
+  __syncthreads();
   long long nedges = 0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    if (!valid[i]) continue;
-    const int u = int(i % W);
-    const int vloc = int((i / W) % H);
-    double a0 = 0, a1 = 0, a2 = 0;
-    if (!theta_none) {
-      a0 = n[i];
-      a1 = n[npix + i];
-      a2 = n[2 * npix + i];
-    }
+  for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
+    if (p[l] < 0) continue;
+    const int lx = l % UT, ly = l / UT;
+    const int x = x0 + lx;
+    const int64_t y = y0 + ly;
+    const int64_t i = y * W + x;
+    const int vloc = int(y % H);
 #pragma unroll
     for (int k = 0; k < KF; ++k) {
       const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
-      if (!fwd_inside(u, vloc, du, dv, W, H)) continue;
+      if (!fwd_inside(x, vloc, du, dv, W, H)) continue;
       const int64_t j = i + int64_t(dv) * W + du;
       if (!valid[j]) continue;
       ++nedges;
-      if (theta_none) continue;
-      const double d = add_rn(add_rn(mul_rn(a0, n[j]), mul_rn(a1, n[npix + j])),
-                              mul_rn(a2, n[2 * npix + j]));
-      if (d >= cutoff) uf_union(parent, int32_t(i), int32_t(j));
+      const int jx = lx + du, jy = ly + dv;
+      if (jx < 0 || jx >= UT || jy >= UT) continue;  // crosses the tile: second pass
+      if (kept_edge(n, npix, i, j, cutoff, theta_none)) sm_union(p, l, jy * UT + jx);
     }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
+    const int x = x0 + (l % UT);
+    const int64_t y = y0 + l / UT;
+    if (x >= W || y >= rows) continue;
+    const int64_t gi = y * W + x;
+    if (p[l] < 0) {
+      parent[gi] = -1;  // invalid pixel
+      continue;
+    }
+    const int r = sm_find(p, l);
+    parent[gi] = int32_t((y0 + r / UT) * W + x0 + (r % UT));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nedges += __shfl_xor_sync(0xffffffffu, nedges, o);
   if ((threadIdx.x & 31) == 0 && nedges)
     atomicAdd((unsigned long long*)&st->edges, (unsigned long long)nedges);
+}
+
+// kept edges that leave their tile, unioned in global memory
+template <int CONN>
+__global__ void __launch_bounds__(256) uf_border_kernel(const double* __restrict__ n,
+                                                        const uint8_t* __restrict__ valid, int H,
+                                                        int W, int64_t npix, double cutoff,
+                                                        int theta_none, int32_t* parent) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int x = int(i % W);
+    const int64_t y = i / W;
+    const int lx = x % UT, ly = int(y % UT);
+    if (lx != 0 && lx != UT - 1 && ly != UT - 1) continue;  // no edge of i leaves the tile
+    if (!valid[i]) continue;
+    const int vloc = int(y % H);
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+      const int jx = lx + du, jy = ly + dv;
+      if (jx >= 0 && jx < UT && jy < UT) continue;  // inside: done by the tile pass
+      if (!fwd_inside(x, vloc, du, dv, W, H)) continue;
+      const int64_t j = i + int64_t(dv) * W + du;
+      if (!valid[j]) continue;
+      if (kept_edge(n, npix, i, j, cutoff, theta_none)) uf_union(parent, int32_t(i), int32_t(j));
+    }
+  }
 }
 
 __global__ void uf_flatten_kernel(int32_t* parent, int64_t npix, int32_t* __restrict__ root_flag) {
@@ -233,14 +315,21 @@ extern "C" int ni_components(const double* n, const uint8_t* valid, int B, int H
   }
   NI_CUDA_TRY(cudaMemsetAsync(&stats->edges, 0, sizeof(long long), s));
   const int blocks = grid_blocks(npix);
-  NI_COUNT_LAUNCH(), uf_init_kernel<<<blocks, 256, 0, s>>>(valid, npix, parent);
-  NI_LAUNCH_CHECK();
-  if (connectivity == 8)
-    NI_COUNT_LAUNCH(), uf_union_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
-                                              stats);
-  else
-    NI_COUNT_LAUNCH(), uf_union_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff, theta_none, parent,
-                                              stats);
+  const int64_t rows = int64_t(B) * H;
+  const int tiles_x = div_up(W, UT);
+  const int64_t tiles = int64_t(tiles_x) * div_up(rows, UT);
+  NI_CHECK_ARG(tiles < (int64_t(1) << 31), "grid too large");
+  if (connectivity == 8) {
+    NI_COUNT_LAUNCH(), uf_tile_kernel<8><<<int(tiles), 256, 0, s>>>(
+                           n, valid, H, W, rows, tiles_x, dot_cutoff, theta_none, parent, stats);
+    NI_COUNT_LAUNCH(), uf_border_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff,
+                                                                  theta_none, parent);
+  } else {
+    NI_COUNT_LAUNCH(), uf_tile_kernel<4><<<int(tiles), 256, 0, s>>>(
+                           n, valid, H, W, rows, tiles_x, dot_cutoff, theta_none, parent, stats);
+    NI_COUNT_LAUNCH(), uf_border_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff,
+                                                                  theta_none, parent);
+  }
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), uf_flatten_kernel<<<blocks, 256, 0, s>>>(parent, npix, flags);
   NI_LAUNCH_CHECK();

@@ -486,7 +486,9 @@ def run_pipeline_batch(
                 iters[m] = t
             else:
                 still.append(m)
-        if len(still) and (merged or len(still) != len(active)):
+        # a merge changes the quotient; maps that merely left the loop keep
+        # their edges in it (every stage restricts itself to the active maps)
+        if len(still) and merged:
             keep = np.zeros(B, dtype=bool)
             keep[still] = True
             loop.filter_keys(keep)
