@@ -69,15 +69,18 @@ namespace cg = cooperative_groups;
 namespace ni {
 
 constexpr int SW = 30;     // strip width (lanes 1..30; lanes 0 / 31 are the halo)
-constexpr int SH = 30;     // strip height (centre rows per item)
-constexpr int SPX = 1024;  // padded pixels per strip (sort buffer)
+#ifndef NI_SH
+#define NI_SH 30
+#endif
+constexpr int SH = NI_SH;  // strip height (centre rows per item)
+constexpr int SPX = SW * SH <= 1024 ? 1024 : 2048;  // padded pixels per strip (sort buffer)
 constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 constexpr int XM = 16;    // left margin (columns)
 constexpr int RM = 2;     // top margin (rows)
-constexpr int RB = 34;    // bottom margin (rows): every item streams 32 rows
+constexpr int RB = SH + 4;  // bottom margin (rows): every item streams SH + 2 rows
 
 enum : uint8_t { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_CAPPED = 2, ST_IDLE = 3, ST_FLUSH = 4 };
 
@@ -408,7 +411,7 @@ __device__ __forceinline__ bool item_finish(const FillArgs& a, const Item& it,
 #define NI_NS 8
 #endif
 constexpr int NS = NI_NS;  // ring slots per warp
-constexpr int IROWS = 32;  // stream rows per item
+constexpr int IROWS = SH + 2;  // stream rows per item
 constexpr int GR = 2;      // centre rows computed per step (between two waits)
 constexpr int LA = NS - GR;  // rows in flight beyond the ones being derived
 static_assert((NS & (NS - 1)) == 0 && IROWS % NS == 0, "ring slots must tile an item");
@@ -1178,7 +1181,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
                                            const Cur& k, bool& has_next, FinishBox& fb,
                                            int& fbt) {
   constexpr int GSW = IROWS - 2 - LA;  // first step that issues the next item's rows
-  static_assert(SH == 30 && GSW % 4 == 0 && GSW < 28 && GSW >= 0,
+  static_assert(SH % 4 == 2 && GSW % 4 == 0 && GSW < SH - 2 && GSW >= 0,
                 "the unrolled step schedule below assumes these shapes");
   const int lane = threadIdx.x & 31;
   const uint32_t ring_s = smem_u32(ring);
@@ -1210,7 +1213,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   der[0] = derive<PURE, EW>(ring, lane, w.dh, w.dm, k);
   der[1] = derive<PURE, EW>(ring + Slot<EW>::BYTES, lane, w.dh, w.dm, k);
 #pragma unroll 1
-  for (int g = 0; g < 28; g += 4) {
+  for (int g = 0; g < SH - 2; g += 4) {
     if (g == GSW) {  // the stream moves on to the next item with the rows issued from here on
       has_next = mbh < vload(&mb.tail);
       if (has_next) {
@@ -1224,7 +1227,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
     sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, g, lane, k);
     sweep_step<CONN, PURE, EW, 2>(a, ring, w, is, vpitch, der, acc, g + 2, lane, k);
   }
-  sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, 28, lane, k);
+  sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, SH - 2, lane, k);
   // post the item's dots (fixed xor tree over lanes) for the scheduler
   constexpr int NS_ = PURE ? 1 : SLOTS;
   double tot[SLOTS][NDOT];
