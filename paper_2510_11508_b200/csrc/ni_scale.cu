@@ -279,7 +279,7 @@ static int upload_maps(Maps& mp, const int32_t* first, const int32_t* count, con
 }
 
 struct StepWs {
-  double *wa, *wb, *ba, *bb, *S, *diag, *rhs, *r, *p0, *p1, *q, *part;
+  double *wa, *wb, *ba, *bb, *S, *diag, *rhs, *r, *p0, *p1, *q, *part, *epart;
   int32_t *parent, *pkey, *pkey_s, *pval, *pval_s;
   Maps mp;
   void* sort_ws;
@@ -287,6 +287,7 @@ struct StepWs {
 };
 
 constexpr int kCgThreads = 512;
+constexpr int kEChunks = 32;  // chunks of a map's edge range in per-map energies
 constexpr int kBlockCgMax = 8192;  // maps up to this many components: one CTA each
 
 static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
@@ -302,6 +303,7 @@ static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
   w.p1 = c.take<double>(C + 1);
   w.q = c.take<double>(C + 1);
   w.part = c.take<double>(4 * kSMs + 8);
+  w.epart = c.take<double>(int64_t(B) * kEChunks);
   w.parent = c.take<int32_t>(C + 1);
   w.pkey = c.take<int32_t>(C + 1);
   w.pkey_s = c.take<int32_t>(C + 1);
@@ -582,14 +584,35 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, 
 
 // K7a: residual rows and the per-map energy (solver.py:301-302); one CTA
 // per map over the map's edge range, in edge order.
+// Per-map sums over edge ranges, split in kEChunks contiguous chunks (one
+// block each, blockIdx.y = the map's slot in the active list) whose partials
+// are added in chunk order: a fixed order independent of the batch.
+
+__device__ __forceinline__ void chunk_range(int e0, int e1, int& c0, int& c1) {
+  const int len = (e1 - e0 + kEChunks - 1) / kEChunks;
+  c0 = min(e1, e0 + int(blockIdx.x) * len);
+  c1 = min(e1, c0 + len);
+}
+
+__global__ void chunk_sum_kernel(const double* __restrict__ part, const int32_t* __restrict__ maps,
+                                 int n, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double e = 0.0;
+  for (int c = 0; c < kEChunks; ++c) e += part[j * kEChunks + c];
+  out[maps[j]] = e;
+}
+
 __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const double* __restrict__ s,
                                                        double* __restrict__ residual,
                                                        double* __restrict__ weights,
-                                                       double* __restrict__ energy_out) {
+                                                       double* __restrict__ part) {
   __shared__ double red[32];
-  const int m = w.mp.active[blockIdx.x];
+  const int m = w.mp.active[blockIdx.y];
+  int c0, c1;
+  chunk_range(q.estart[m], q.estart[m + 1], c0, c1);
   double en = 0.0;
-  for (int e = q.estart[m] + threadIdx.x; e < q.estart[m + 1]; e += blockDim.x) {
+  for (int e = c0 + threadIdx.x; e < c1; e += blockDim.x) {
     const double sa = s[q.pa[e]], sb = s[q.pb[e]];
     const double ra = sa - sb - w.ba[e];
     const double rb = sb - sa - w.bb[e];
@@ -600,7 +623,7 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const d
     en += ra * (w.wa[e] * ra) + rb * (w.wb[e] * rb);
   }
   en = block_sum(en, red);
-  if (threadIdx.x == 0) energy_out[m] = en;
+  if (threadIdx.x == 0) part[blockIdx.y * kEChunks + blockIdx.x] = en;
 }
 
 // K7b: z[valid] += s[label] on the active maps' pixels (pipeline.py:181-182)
@@ -629,6 +652,7 @@ __global__ void zero_map_kernel(double* __restrict__ energy, const int32_t* __re
 // ----------------------------------------------------------------- merge
 
 struct MergeWs {
+  double* epart;
   int32_t *sel, *parent, *flag, *rank, *cmap;
   uint8_t* merging;  // [B]
   Maps mp;
@@ -636,6 +660,7 @@ struct MergeWs {
 };
 
 static void carve_merge(Carver& c, MergeWs& m, int K, int C, int B) {
+  m.epart = c.take<double>(int64_t(B) * kEChunks);
   m.sel = c.take<int32_t>(C + 1);
   m.parent = c.take<int32_t>(C + 1);
   m.flag = c.take<int32_t>(C + 2);
@@ -751,18 +776,20 @@ __global__ void merge_relabel_kernel(int32_t* __restrict__ labels, const MergeWs
 __global__ void __launch_bounds__(256) merge_energy_kernel(Quot q, const MergeWs m,
                                                            const double* __restrict__ residual,
                                                            const double* __restrict__ weights,
-                                                           double* __restrict__ energy_out) {
+                                                           double* __restrict__ part) {
   __shared__ double red[32];
-  const int mm = m.mp.active[blockIdx.x];
+  const int mm = m.mp.active[blockIdx.y];
+  int c0, c1;
+  chunk_range(q.estart[mm], q.estart[mm + 1], c0, c1);
   double en = 0.0;
-  for (int e = q.estart[mm] + threadIdx.x; e < q.estart[mm + 1]; e += blockDim.x) {
+  for (int e = c0 + threadIdx.x; e < c1; e += blockDim.x) {
     if (m.parent[q.pa[e]] != m.parent[q.pb[e]]) {
       const double ra = residual[2 * e], rb = residual[2 * e + 1];
       en += ra * (weights[2 * e] * ra) + rb * (weights[2 * e + 1] * rb);
     }
   }
   en = block_sum(en, red);
-  if (threadIdx.x == 0) energy_out[mm] = en;
+  if (threadIdx.x == 0) part[blockIdx.y * kEChunks + blockIdx.x] = en;
 }
 
 }  // namespace ni
@@ -1051,7 +1078,10 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(g), dim3(kCgThreads), args,
                                             0, s));
   }
-  NI_COUNT_LAUNCH(), residual_kernel<<<nact, 256, 0, s>>>(q, w, scales, residual, weights, energy_out);
+  NI_COUNT_LAUNCH(), residual_kernel<<<dim3(kEChunks, nact), 256, 0, s>>>(q, w, scales, residual,
+                                                                          weights, w.epart);
+  NI_COUNT_LAUNCH(), chunk_sum_kernel<<<div_up(nact, 64), 64, 0, s>>>(w.epart, w.mp.active, nact,
+                                                                     energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
   NI_COUNT_LAUNCH(), apply_kernel<<<blocks_for(nact * per_map), 256, 0, s>>>(
@@ -1099,7 +1129,10 @@ extern "C" int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(m.flag, m.rank, C + 1, nullptr, m.scan_ws, s));
   NI_COUNT_LAUNCH(), merge_counts_kernel<<<div_up(B, 256), 256, 0, s>>>(m, new_count_out);
-  NI_COUNT_LAUNCH(), merge_energy_kernel<<<nmerge, 256, 0, s>>>(q, m, residual, weights, energy_out);
+  NI_COUNT_LAUNCH(), merge_energy_kernel<<<dim3(kEChunks, nmerge), 256, 0, s>>>(q, m, residual,
+                                                                                 weights, m.epart);
+  NI_COUNT_LAUNCH(), chunk_sum_kernel<<<div_up(nmerge, 64), 64, 0, s>>>(m.epart, m.mp.active,
+                                                                       nmerge, energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
   NI_COUNT_LAUNCH(), merge_relabel_kernel<<<blocks_for(nmerge * per_map), 256, 0, s>>>(

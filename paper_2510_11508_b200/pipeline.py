@@ -13,6 +13,7 @@ components of all maps), then the small per-map outer loops.
 
 from __future__ import annotations
 
+import concurrent.futures as cf
 import ctypes as C
 import hashlib
 import math
@@ -442,6 +443,7 @@ def run_pipeline_batch(
     energies = [[] for _ in range(B)]
     iters = np.zeros(B, dtype=np.int64)
     version = np.zeros(B, dtype=np.int64)
+    hasher = None
     t = 0
     while len(active):
         it_start = time.perf_counter()
@@ -453,7 +455,12 @@ def run_pipeline_batch(
                             and loop.count[m] > 1 and loop.map_edges[m] > 0], dtype=np.int32)
         digests = {}
         if len(merging):
-            digests = {int(m): _digest(z[m * g.hw:(m + 1) * g.hw]) for m in merging}
+            # merges relabel only, so z (and its digest) is the same before
+            # and after; hash a device snapshot off the critical path
+            if hasher is None:
+                hasher = cf.ThreadPoolExecutor(max_workers=4)
+            digests = {int(m): hasher.submit(_digest, z[m * g.hw:(m + 1) * g.hw].clone())
+                       for m in merging}
             loop.merge(residual, wts, merging)
         # one read-back per iteration for every map
         host = torch.cat([loop.energy, loop.ok.to(torch.float64), loop.merge_energy,
@@ -471,8 +478,7 @@ def run_pipeline_batch(
                 nc = int(new_count[m])
                 e_t = float(e_merge[m])
                 extra = {"components_before": int(loop.count[m]), "components_after": nc,
-                         "z_digest_before": digests[m],
-                         "z_digest_after": _digest(z[m * g.hw:(m + 1) * g.hw])}
+                         "z_digest_before": digests[m], "z_digest_after": digests[m]}
                 loop.count[m] = nc
                 version[m] += 1
             else:
@@ -495,6 +501,13 @@ def run_pipeline_batch(
             loop.build()
         active = np.array(still, dtype=np.int32)
 
+    if hasher is not None:  # resolve the merge digests (pipeline.py:194-209)
+        for recs in records:
+            for r in recs:
+                for key in ("z_digest_before", "z_digest_after"):
+                    if key in r and isinstance(r[key], cf.Future):
+                        r[key] = r[key].result()
+        hasher.shutdown()
     target = 0.0 if gauge_depth is None else float(np.log(gauge_depth))
     lib = g.lib
     ws = _ws(_lib.size_query(lib.ni_gauge_workspace_size, g.B, g.H, g.W), g.dev)
