@@ -155,6 +155,19 @@ def _digest(z_map: torch.Tensor) -> str:
     return hashlib.sha256(z_map.cpu().numpy().tobytes()).hexdigest()[:16]
 
 
+def _digest_async(snap: torch.Tensor, ready: torch.cuda.Event) -> str:
+    """_digest of a device snapshot, from a worker thread: the copy runs on a
+    side stream into pinned memory (the pipeline's stream keeps going) and
+    the hash reads the pinned buffer in place with the GIL released."""
+    side = torch.cuda.Stream(device=snap.device)
+    host = torch.empty(snap.numel(), dtype=torch.float64, pin_memory=True)
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        host.copy_(snap, non_blocking=True)
+    side.synchronize()
+    return hashlib.sha256(memoryview(host.numpy())).hexdigest()[:16]
+
+
 # ------------------------------------------------------------------- engine
 
 
@@ -459,8 +472,10 @@ def run_pipeline_batch(
             # and after; hash a device snapshot off the critical path
             if hasher is None:
                 hasher = cf.ThreadPoolExecutor(max_workers=4)
-            digests = {int(m): hasher.submit(_digest, z[m * g.hw:(m + 1) * g.hw].clone())
-                       for m in merging}
+            snaps = {int(m): z[m * g.hw:(m + 1) * g.hw].clone() for m in merging}
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(g.dev))
+            digests = {m: hasher.submit(_digest_async, snp, ready) for m, snp in snaps.items()}
             loop.merge(residual, wts, merging)
         # one read-back per iteration for every map
         host = torch.cat([loop.energy, loop.ok.to(torch.float64), loop.merge_energy,

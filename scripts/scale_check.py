@@ -27,7 +27,20 @@ def run(name, sc, theta, merge=None):
           f"warnings={len(r.warnings)}", flush=True)
 
 
-if __name__ == "__main__":
+def records_c4():
+    sc = scenes.CONFIGS["C4"]()
+    nm = nb.NormalMap.create(sc.normals, sc.mask)
+    st = nb.SolveSettings(freq_merging=5)
+    for rep in range(2):
+        r = nb.run_pipeline(nm, nb.CameraIntrinsics(*sc.intrinsics()), float(np.deg2rad(3.5)), st)
+    for x in r.records:
+        print({k: (round(v, 2) if isinstance(v, float) else v) for k, v in x.items()
+               if k not in ("z_digest_before", "z_digest_after")})
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["records"]:
+    records_c4()
+elif __name__ == "__main__":
     which = sys.argv[1:] or ["none256", "C3", "C4"]
     if "none256" in which:
         run("C1 theta=None", scenes.CONFIGS["C1"](), None)

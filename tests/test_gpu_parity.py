@@ -268,3 +268,17 @@ def test_gpu_metrics_batch_equals_single():
                                   np.stack([a["mask"], b["mask"]]))
     assert reps[0] == metrics.evaluate(a["pred"], a["gt"], a["mask"])
     assert reps[1] == metrics.evaluate(b["pred"], b["gt"], b["mask"])
+
+
+def test_merge_events_preserve_depth():
+    """Reference test_pipeline.py:44-57 on the GPU path: merges relabel only,
+    so the z digests before and after a merge agree."""
+    d = load("bump_ref_merge")
+    r = run_gpu(d["normals"], d["mask"], tuple(d["intr"]), opts_of(d))
+    merges = [x for x in r.records if x.get("merge_performed")]
+    assert merges
+    for rec in merges:
+        assert isinstance(rec["z_digest_before"], str) and len(rec["z_digest_before"]) == 16
+        assert rec["z_digest_before"] == rec["z_digest_after"]
+        assert rec["components_after"] < rec["components_before"]
+    assert r.partition.component_count < r.partition0.component_count
