@@ -77,6 +77,7 @@ constexpr int SPX = SW * SH <= 1024 ? 1024 : 2048;  // padded pixels per strip (
 constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
+constexpr int kPairMaps = 8;  // batches of at least this many maps pair components in items
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 constexpr int XM = 16;    // left margin (columns)
 constexpr int RM = 2;     // top margin (rows)
@@ -287,22 +288,22 @@ __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
                                    const int32_t* __restrict__ slot_base,
                                    const int32_t* __restrict__ item_base,
                                    const int32_t* __restrict__ strip_comps, int nstrips, int nsx, int nsym, int H,
-                                   Item* __restrict__ items, int32_t* __restrict__ partial_comp,
+                                   int per, Item* __restrict__ items, int32_t* __restrict__ partial_comp,
                                    int32_t* __restrict__ partial_idx,
                                    int32_t* __restrict__ comp_nparts) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nstrips; s += gridDim.x * blockDim.x) {
     const int ns = nslots[s];
     if (ns == 0) continue;
     const int pb = slot_base[s], ib = item_base[s];
-    for (int k = 0; k * SLOTS < ns; ++k) {
+    for (int k = 0; k * per < ns; ++k) {
       Item it;
       strip_rect(s, nsx, nsym, H, it.x0, it.y0, it.y1);
-      it.pbase = pb + k * SLOTS;
-      const int n = min(SLOTS, ns - k * SLOTS);
+      it.pbase = pb + k * per;
+      const int n = min(per, ns - k * per);
       it.flags = n | ((ns == 1 ? 1 : 0) << 8);
 #pragma unroll
       for (int j = 0; j < SLOTS; ++j)
-        it.comp[j] = j < n ? strip_comps[int64_t(s) * SPX + k * SLOTS + j] : -1;
+        it.comp[j] = j < n ? strip_comps[int64_t(s) * SPX + k * per + j] : -1;
       it.pad = 0;
       items[ib + k] = it;
     }
@@ -315,10 +316,10 @@ __global__ void strip_items_kernel(const int32_t* __restrict__ nslots,
   }
 }
 
-__global__ void item_counts_kernel(const int32_t* __restrict__ nslots, int nstrips,
+__global__ void item_counts_kernel(const int32_t* __restrict__ nslots, int nstrips, int per,
                                    int32_t* __restrict__ nitems) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nstrips; s += gridDim.x * blockDim.x)
-    nitems[s] = (nslots[s] + SLOTS - 1) / SLOTS;
+    nitems[s] = (nslots[s] + per - 1) / per;
 }
 
 // ------------------------------------------------------- warp machinery
@@ -1551,7 +1552,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   const int64_t npad = padded_len(rows, W);
   // every partial slot owns >= 1 pixel
   const int64_t P = npix;
-  const int64_t NI = nstrips + P / SLOTS + 1;  // items
+  const int64_t NI = nstrips + P + 1;  // items (one per strip component at most)
   w.v0 = c.take<float4>(npad);
   w.v1 = c.take<float4>(npad);
   w.hw = c.take<float>(weighted ? 1 : npad);
@@ -1692,13 +1693,19 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
                          labels, w.comp_size, H, W, nsx, nsy / B, w.nslots, w.strip_comps);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(w.nslots, w.slot_base, nstrips, w.total, w.scan_ws, s));
-  NI_COUNT_LAUNCH(), item_counts_kernel<<<div_up(nstrips, 256), 256, 0, s>>>(w.nslots, nstrips,
+  // Items pair up to SLOTS components of a strip; pairing couples those
+  // components into one lockstep group.  With many maps the groups (about
+  // one per map) overlap each other well and pairing saves re-reading mixed
+  // strips; with few maps one group per component overlaps far better.
+  const char* pe = getenv("NI_FILL_PAIR");
+  const int per = pe ? (atoi(pe) > 1 ? SLOTS : 1) : (B >= kPairMaps ? SLOTS : 1);
+  NI_COUNT_LAUNCH(), item_counts_kernel<<<div_up(nstrips, 256), 256, 0, s>>>(w.nslots, nstrips, per,
                                                                             w.nitems_strip);
   NI_LAUNCH_CHECK();
   NI_TRY(exclusive_scan_i32(w.nitems_strip, w.item_base, nstrips, w.total_items, w.scan_ws, s));
   NI_COUNT_LAUNCH(), strip_items_kernel<<<div_up(nstrips, 128), 128, 0, s>>>(
                          w.nslots, w.slot_base, w.item_base, w.strip_comps, nstrips, nsx, nsy / B,
-                         H, w.items, w.partial_comp, w.partial_idx, w.comp_nparts);
+                         H, per, w.items, w.partial_comp, w.partial_idx, w.comp_nparts);
   NI_LAUNCH_CHECK();
   int32_t NP = 0, NIt = 0;
   NI_CUDA_TRY(cudaMemcpyAsync(&NP, w.total, sizeof(NP), cudaMemcpyDeviceToHost, s));
