@@ -77,7 +77,7 @@ constexpr int SPX = SW * SH <= 1024 ? 1024 : 2048;  // padded pixels per strip (
 constexpr int NT = 256;    // threads per CTA (8 warps)
 constexpr int WPB = NT / 32;
 constexpr int SLOTS = 2;  // components per item
-constexpr int kPairMaps = 8;  // batches of at least this many maps pair components in items
+constexpr int kPairMaps = 10;  // batches of at least this many maps pair components in items
 constexpr int NDOT = 4;   // <p,q>, <r,q>, <q,q>, <r,r>
 constexpr int XM = 16;    // left margin (columns)
 constexpr int RM = 2;     // top margin (rows)
@@ -710,9 +710,12 @@ __device__ __noinline__ int claim_items(const FillArgs& a, int want, Claim* cons
     const bool stale = int32_t(seq - p) > 0;  // lapped: long exhausted
     const int32_t g = int32_t(e & 0xffffffffu);
     bool open = false;
+    int key = -1;  // priority: the batch's item count (larger groups first)
     if (pub) {
       const unsigned long long w = __ldcg(a.gtk + g);
-      open = (w & 0xffffffffu) < ((w >> 32) & 0x7fffffffu);
+      const int n = int((w >> 32) & 0x7fffffffu);
+      open = int(w & 0xffffffffu) < n;
+      if (open) key = n;
     }
     const unsigned openm = __ballot_sync(0xffffffffu, open);
     const unsigned donem = __ballot_sync(0xffffffffu, (pub && !open) || stale);
@@ -720,7 +723,19 @@ __device__ __noinline__ int claim_items(const FillArgs& a, int want, Claim* cons
     const int k = lead < 0 ? 32 : lead;
     if (lane == 0 && k > 0) atomicCAS(a.ring_hint, h, h + k);
     if (openm) {
-      const int l = __ffs(openm) - 1;
+      // the open batch of the largest group in the window: the largest
+      // components take the most iterations, so serving them first keeps
+      // the critical path short when few groups remain
+      int best = key, l = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, l, o);
+        if (ob > best || (ob == best && ol < l)) {
+          best = ob;
+          l = ol;
+        }
+      }
       const int32_t gg = __shfl_sync(0xffffffffu, g, l);
       unsigned long long w = 0;
       int32_t gs = 0;
@@ -771,7 +786,21 @@ __device__ __noinline__ int claim_items(const FillArgs& a, int want, Claim* cons
 }
 
 // Announce group g's next batch (lane 0).
+#if NI_FILL_STATS
+constexpr int kTraceG = 256, kTraceI = 4096;
+__device__ unsigned long long g_pub_trace[kTraceG * kTraceI];
+__device__ int g_pub_n[kTraceG];
+#endif
+
 __device__ __forceinline__ void publish(const FillArgs& a, int32_t g, int par, int32_t n) {
+#if NI_FILL_STATS
+  if (g < kTraceG) {
+    const int idx = atomicAdd(&g_pub_n[g], 1);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (idx < kTraceI) g_pub_trace[g * kTraceI + idx] = t | (static_cast<unsigned long long>(n) << 48);
+  }
+#endif
   a.gdone[g] = 0;
   __threadfence();
   atomicExch(a.gtk + g, (static_cast<unsigned long long>(par) << 63) |
@@ -1828,6 +1857,10 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
 #if NI_FILL_STATS
     unsigned long long zst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     NI_CUDA_TRY(cudaMemcpyToSymbolAsync(g_fill_stats, zst, sizeof(zst), 0, cudaMemcpyHostToDevice, s));
+    {
+      static int zn[kTraceG];
+      NI_CUDA_TRY(cudaMemcpyToSymbolAsync(g_pub_n, zn, sizeof(zn), 0, cudaMemcpyHostToDevice, s));
+    }
 #endif
     NI_CUDA_TRY(cudaEventRecord(e0, s));
     NI_COUNT_LAUNCH();
@@ -1867,6 +1900,20 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
             "scheduler retire=%.1f%% claim=%.1f%% items/claim=%.2f\n",
             a.G, 100.0 * h[1] / h[0], 100.0 * h[2] / h[0], double(h[0]) / double(h[3]),
             100.0 * h[5] / h[4], 100.0 * h[6] / h[4], double(h[3]) / double(h[7]));
+    if (const char* tp = getenv("NI_FILL_TRACE")) {  // batch publish timeline per group
+      static int hn[kTraceG];
+      static unsigned long long ht[kTraceG * kTraceI];
+      NI_CUDA_TRY(cudaMemcpyFromSymbol(hn, g_pub_n, sizeof(hn)));
+      NI_CUDA_TRY(cudaMemcpyFromSymbol(ht, g_pub_trace, sizeof(ht)));
+      FILE* f = fopen(tp, "w");
+      if (f) {
+        for (int g = 0; g < kTraceG && g < a.G; ++g)
+          for (int i = 0; i < hn[g] && i < kTraceI; ++i)
+            fprintf(f, "%d %d %llu %llu\n", g, i, ht[g * kTraceI + i] & ((1ull << 48) - 1),
+                    ht[g * kTraceI + i] >> 48);
+        fclose(f);
+      }
+    }
 #endif
   }
   return NI_OK;
