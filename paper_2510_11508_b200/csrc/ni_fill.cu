@@ -128,6 +128,11 @@ struct FillArgs {
   uint32_t* ring_tail;
   uint32_t* ring_hint;         // every ring entry below it is exhausted
   int32_t* gactive;            // groups with live items
+  // admission window: at most `window` groups hold published batches at a
+  // time (0: all), so their state can stay in L2; a retiring group admits
+  // the next one (gnext) in group order
+  int window;
+  int32_t* gnext;
   // component state
   double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
   double* alpha;   // alpha of the last completed sweep
@@ -578,15 +583,48 @@ __device__ __forceinline__ void load_cur(const Claim& c, Cur& k) {
   }
 }
 
+// Shared-memory loads by 32-bit shared address (register + immediate
+// addressing; a generic pointer into the ring re-derives the shared window
+// every row).  volatile keeps them after the cp.async wait that precedes them.
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// This lane's shared addresses in ring slot 0 (a slot is + slot * BYTES).
+struct LaneOfs {
+  uint32_t v;  // {r,q,p,x}
+  uint32_t c;  // forward conductances (EW)
+  uint32_t h;  // hw
+  uint32_t l;  // label
+  uint32_t m;  // imask byte
+};
+
 template <bool PURE, bool EW>
-__device__ __forceinline__ RowT<EW> derive(const unsigned char* slot, int lane, int dh, int dm,
-                                           const Cur& k) {
-  using L = Slot<EW>;
-  const float4 v = *reinterpret_cast<const float4*>(slot + L::V + 16 * lane);
+__device__ __forceinline__ RowT<EW> derive(uint32_t slot, const LaneOfs& o_, const Cur& k) {
+  const float4 v = lds_f4(slot + o_.v);
   float al = k.al[0], be = k.be[0];
   int s = 0;
   if (!PURE) {
-    const int32_t lab = *reinterpret_cast<const int32_t*>(slot + L::LAB + 4 * (dh + lane));
+    const int32_t lab = lds_s32(slot + o_.l);
     s = lab == k.comp[0] ? 0 : (item_n_flags(k.flags) > 1 && lab == k.comp[1] ? 1 : -1);
     al = s == 0 ? k.al[0] : (s == 1 ? k.al[1] : 0.f);
     be = s == 0 ? k.be[0] : (s == 1 ? k.be[1] : 0.f);
@@ -595,11 +633,11 @@ __device__ __forceinline__ RowT<EW> derive(const unsigned char* slot, int lane, 
   o.rn = fmaf(-al, v.y, v.x);
   o.pn = fmaf(be, v.z, o.rn);
   o.xn = fmaf(al, v.z, v.w);
-  o.m = uint32_t(slot[L::M + dm + lane]) | (uint32_t(s + 1) << 8);
+  o.m = lds_u8(slot + o_.m) | (uint32_t(s + 1) << 8);
   o.pl = __shfl_up_sync(0xffffffffu, o.pn, 1);
   o.pr = __shfl_down_sync(0xffffffffu, o.pn, 1);
   if constexpr (EW) {
-    const float4 c = *reinterpret_cast<const float4*>(slot + L::C + 16 * lane);
+    const float4 c = lds_f4(slot + o_.c);
     o.c0 = c.x;
     o.c1 = c.y;
     o.c2 = c.z;
@@ -608,7 +646,7 @@ __device__ __forceinline__ RowT<EW> derive(const unsigned char* slot, int lane, 
     o.c1r = __shfl_down_sync(0xffffffffu, c.y, 1);
     o.c3l = __shfl_up_sync(0xffffffffu, c.w, 1);
   } else {
-    o.h = *reinterpret_cast<const float*>(slot + L::H + 4 * (dh + lane));
+    o.h = lds_f32(slot + o_.h);
     o.hl = __shfl_up_sync(0xffffffffu, o.h, 1);
     o.hr = __shfl_down_sync(0xffffffffu, o.h, 1);
   }
@@ -626,6 +664,10 @@ __device__ unsigned long long g_fill_stats[8];
 #define NI_STAT(i, v) atomicAdd(&g_fill_stats[i], (unsigned long long)(v))
 #else
 #define NI_STAT(i, v) ((void)0)
+#endif
+
+#ifndef NI_IDLE_NS
+#define NI_IDLE_NS 64  // a worker's poll interval on an empty mailbox
 #endif
 
 // ---- warp roles
@@ -825,6 +867,20 @@ __device__ __forceinline__ bool item_live(const FillArgs& a, int32_t k) {
   return act;
 }
 
+// A group retired under an admission window: publish the first batch of the
+// next group that has live items (lane 0).
+__device__ void admit_next(const FillArgs& a) {
+  for (;;) {
+    const int32_t g = atomicAdd(a.gnext, 1);
+    if (g >= a.G) return;
+    const int32_t n = __ldcg(a.gcnt + g);
+    if (n > 0) {
+      publish(a, g, 0, n);
+      return;
+    }
+  }
+}
+
 // The warp that retires a group's batch: drop items whose components are
 // all final (in-place stable compaction), then publish the next batch or
 // retire the group.
@@ -860,8 +916,12 @@ __device__ __noinline__ void advance_group(const FillArgs& a, int32_t g, int par
     }
   }
   if (lane == 0) {
-    if (n > 0) publish(a, g, par ^ 1, n);
-    else atomicSub(a.gactive, 1);
+    if (n > 0) {
+      publish(a, g, par ^ 1, n);
+    } else {
+      atomicSub(a.gactive, 1);
+      if (a.window > 0) admit_next(a);
+    }
   }
   __syncwarp();
 }
@@ -1035,20 +1095,17 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
       mt = vload(&sh.mb[lane].tail);
       need = MB - (mt - vload(&sh.mb[lane].head));
     }
-    int nin = need;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, nin, o);
-      if (lane >= o) nin += t;
-    }
-    const int want = __shfl_sync(0xffffffffu, nin, 31);
+    // claim targets, slot-major: the first free slot of every worker, then
+    // the second ones, so a short claim feeds the emptiest mailboxes first
+    static_assert(MB == 2, "target order below is written for two mailbox slots");
+    const unsigned m0 = __ballot_sync(0xffffffffu, need > 0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, need > 1);
+    const unsigned below = (1u << lane) - 1;
+    const int pos0 = __popc(m0 & below), pos1 = __popc(m0) + __popc(m1 & below);
+    const int want = __popc(m0) + __popc(m1);
     if (want > 0) {
-      // claim targets: slot j of the claim goes to the j-th free mailbox slot
-      if (lane < WORKERS) {
-        const int ex = nin - need;
-        for (int j = 0; j < need; ++j)
-          targets[ex + j] = &sh.mb[lane].slot[(mt + j) % MB];
-      }
+      if (need > 0) targets[pos0] = &sh.mb[lane].slot[mt % MB];
+      if (need > 1) targets[pos1] = &sh.mb[lane].slot[(mt + 1) % MB];
       __syncwarp();
       const int got = claim_items(a, want, targets);
 #if NI_FILL_STATS
@@ -1059,8 +1116,7 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
         busy = true;
         __threadfence_block();
         if (lane < WORKERS) {
-          const int ex = nin - need;
-          const int mine = max(0, min(need, got - ex));
+          const int mine = (need > 0 && pos0 < got) + (need > 1 && pos1 < got);
           if (mine > 0) vstore(&sh.mb[lane].tail, mt + mine);
         }
       }
@@ -1091,14 +1147,15 @@ struct Sweep {
   uint32_t cdst;   // this lane's conductance destination in ring slot 0 (EW)
   uint32_t adst;   // this lane's aux destination in ring slot 0
   float4* orow;    // this lane's output pixel in the next centre row
-  int nrows, dh, dm;
+  LaneOfs lo;      // this lane's shared read addresses in ring slot 0
+  int nrows;
   bool center;
 };
 
-// Copy the issuer's next row into ring slot j.
+// Copy the issuer's next row into the ring slot at byte offset `off`.
 template <bool EW>
-__device__ __forceinline__ void issue_row_c(const Sweep& w, int j, Issuer& is, uint32_t vpitch) {
-  const uint32_t off = uint32_t(j & (NS - 1)) * Slot<EW>::BYTES;
+__device__ __forceinline__ void issue_row_c(const Sweep& w, uint32_t off, Issuer& is,
+                                            uint32_t vpitch) {
   cp_async16_if(w.vdst + off, is.v, is.on);
   if (EW) {
     cp_async16_if(w.cdst + off, is.c, is.on);
@@ -1112,23 +1169,22 @@ __device__ __forceinline__ void issue_row_c(const Sweep& w, int j, Issuer& is, u
 
 // One step of a sweep: centre rows g+1, g+2 (GR = 2), with GB = g % 4 known
 // at compile time so that the compute-ring indices are constants (row r
-// lives in der[r % 4]).
+// lives in der[r % 4]).  The ring-slot byte offsets of the two rows issued
+// (g+2+LA, g+3+LA) and the two rows derived (g+2, g+3) come from the caller
+// as register + immediate values (see sweep_item).
 template <int CONN, bool PURE, bool EW, int GB>
-__device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned char* ring,
-                                           Sweep& w, Issuer& is, uint32_t vpitch,
-                                           RowT<EW> (&der)[4],
-                                           double (&acc)[SLOTS][NDOT], int g, int lane,
+__device__ __forceinline__ void sweep_step(const FillArgs& a, Sweep& w, Issuer& is,
+                                           uint32_t vpitch, RowT<EW> (&der)[4],
+                                           double (&acc)[SLOTS][NDOT], int g, uint32_t oi0,
+                                           uint32_t oi1, uint32_t od0, uint32_t od1,
                                            const Cur& k) {
   static_assert(GR == 2, "the step body is written for two rows");
-  using L = Slot<EW>;
-  issue_row_c<EW>(w, g + 2 + LA, is, vpitch);
-  issue_row_c<EW>(w, g + 3 + LA, is, vpitch);
+  issue_row_c<EW>(w, oi0, is, vpitch);
+  issue_row_c<EW>(w, oi1, is, vpitch);
   cp_wait<LA>();  // rows up to g+3 have landed
   __syncwarp();
-  der[(GB + 2) & 3] =
-      derive<PURE, EW>(ring + ((g + 2) & (NS - 1)) * L::BYTES, lane, w.dh, w.dm, k);
-  der[(GB + 3) & 3] =
-      derive<PURE, EW>(ring + ((g + 3) & (NS - 1)) * L::BYTES, lane, w.dh, w.dm, k);
+  der[(GB + 2) & 3] = derive<PURE, EW>(od0, w.lo, k);
+  der[(GB + 3) & 3] = derive<PURE, EW>(od1, w.lo, k);
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int L = g + u + 1;  // centre local row
@@ -1185,17 +1241,16 @@ __device__ __forceinline__ void sweep_step(const FillArgs& a, const unsigned cha
     const int s = PURE ? 0 : int(m >> 8) - 1;  // -1: pixel not in this item
     bool mine = w.center && L <= w.nrows;
     if (!PURE) mine = mine && s >= 0 && ((k.live >> s) & 1);
-    if (mine) {
-      *w.orow = make_float4(C.rn, q, pa, C.xn);
-      const double dp = pa, dq = q, dr = C.rn;
+    if (mine) __stcg(w.orow, make_float4(C.rn, q, pa, C.xn));
+    // branch-free dots: a pixel outside the item contributes fma(0, 0, acc)
 #pragma unroll
-      for (int j = 0; j < SLOTS; ++j)
-        if (j == s) {
-          acc[j][0] = fma(dp, dq, acc[j][0]);
-          acc[j][1] = fma(dr, dq, acc[j][1]);
-          acc[j][2] = fma(dq, dq, acc[j][2]);
-          acc[j][3] = fma(dr, dr, acc[j][3]);
-        }
+    for (int j = 0; j < (PURE ? 1 : SLOTS); ++j) {
+      const bool on = mine && (PURE || j == s);
+      const double dp = on ? pa : 0.f, dq = on ? q : 0.f, dr = on ? C.rn : 0.f;
+      acc[j][0] = fma(dp, dq, acc[j][0]);
+      acc[j][1] = fma(dr, dq, acc[j][1]);
+      acc[j][2] = fma(dq, dq, acc[j][2]);
+      acc[j][3] = fma(dr, dr, acc[j][3]);
     }
     w.orow += a.P;
   }
@@ -1220,8 +1275,15 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
   const int xr = k.x0 - 1 + lane;  // real column of this lane
   w.center = lane >= 1 && lane <= SW && xr < a.W;
   const int c0 = k.x0 - 1 + XM;
-  w.dh = c0 & 3;
-  w.dm = c0 & 15;
+  {
+    using L = Slot<EW>;
+    const int dh = c0 & 3, dm = c0 & 15;  // offsets of the hw / label and imask windows
+    w.lo.v = L::V + 16 * lane;
+    w.lo.c = L::C + 16 * lane;
+    w.lo.h = L::H + 4 * (dh + lane);
+    w.lo.l = L::LAB + 4 * (dh + lane);
+    w.lo.m = L::M + dm + lane;
+  }
   w.orow = a.v[k.par ^ 1] + int64_t(k.y0 + RM) * a.P + (xr + XM);  // centre row 1
   w.nrows = k.y1 - k.y0;  // centre rows (local rows 1..nrows)
   w.vdst = ring_s + Slot<EW>::V + 16 * lane;
@@ -1233,15 +1295,23 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) acc[j][d] = 0.0;
   has_next = false;
+  // Ring slot of local row j: j % NS.  With LA = NS - 2 a step at row g
+  // (g % 4 == 0) issues rows g+NS, g+NS+1 into the slots of rows g, g+1 and
+  // derives rows g+2, g+3; the next step (g+2) issues into the slots of g+2,
+  // g+3 and derives g+4, g+5, which sit in the next 4-slot block of the ring.
+  // hb = the byte offset of the block holding row g and hb2 that of the next
+  // one, so every slot is hb or hb2 plus a compile-time multiple of BYTES.
+  static_assert(LA == NS - 2 && NS % 4 == 0, "slot schedule below assumes LA = NS - 2");
+  constexpr uint32_t B = Slot<EW>::BYTES;
   // rows LA and LA+1; rows 0 and 1 have landed once at most LA younger
   // row groups are pending
-  issue_row_c<EW>(w, LA, is, vpitch);
-  issue_row_c<EW>(w, LA + 1, is, vpitch);
+  issue_row_c<EW>(w, LA * B, is, vpitch);
+  issue_row_c<EW>(w, (LA + 1) * B, is, vpitch);
   cp_wait<LA>();
   __syncwarp();
   RowT<EW> der[4];  // row r of the item lives in der[r % 4]
-  der[0] = derive<PURE, EW>(ring, lane, w.dh, w.dm, k);
-  der[1] = derive<PURE, EW>(ring + Slot<EW>::BYTES, lane, w.dh, w.dm, k);
+  der[0] = derive<PURE, EW>(ring_s, w.lo, k);
+  der[1] = derive<PURE, EW>(ring_s + B, w.lo, k);
 #pragma unroll 1
   for (int g = 0; g < SH - 2; g += 4) {
     if (g == GSW) {  // the stream moves on to the next item with the rows issued from here on
@@ -1254,10 +1324,18 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
         is.on = false;
       }
     }
-    sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, g, lane, k);
-    sweep_step<CONN, PURE, EW, 2>(a, ring, w, is, vpitch, der, acc, g + 2, lane, k);
+    const uint32_t hb = uint32_t(g & (NS - 4)) * B;
+    const uint32_t hb2 = hb + 4 * B == NS * B ? 0u : hb + 4 * B;
+    sweep_step<CONN, PURE, EW, 0>(a, w, is, vpitch, der, acc, g, hb, hb + B,
+                                  ring_s + hb + 2 * B, ring_s + hb + 3 * B, k);
+    sweep_step<CONN, PURE, EW, 2>(a, w, is, vpitch, der, acc, g + 2, hb + 2 * B, hb + 3 * B,
+                                  ring_s + hb2, ring_s + hb2 + B, k);
   }
-  sweep_step<CONN, PURE, EW, 0>(a, ring, w, is, vpitch, der, acc, SH - 2, lane, k);
+  {
+    constexpr uint32_t hb = uint32_t((SH - 2) & (NS - 4)) * B;
+    sweep_step<CONN, PURE, EW, 0>(a, w, is, vpitch, der, acc, SH - 2, hb, hb + B,
+                                  ring_s + hb + 2 * B, ring_s + hb + 3 * B, k);
+  }
   // post the item's dots (fixed xor tree over lanes) for the scheduler
   constexpr int NS_ = PURE ? 1 : SLOTS;
   double tot[SLOTS][NDOT];
@@ -1328,10 +1406,10 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
         if (vload(&sh.done)) break;
 #if NI_FILL_STATS
         const long long ti = clock64();
-        __nanosleep(64);
+        __nanosleep(NI_IDLE_NS);
         t_idle += clock64() - ti + 40;
 #else
-        __nanosleep(64);
+        __nanosleep(NI_IDLE_NS);
 #endif
         continue;
       }
@@ -1375,7 +1453,7 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
 // barrier per iteration: groups drift apart and every worker stays busy
 // while any batch is open.
 template <int CONN, int MINB, bool EW>
-__global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
+__global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(const __grid_constant__ FillArgs a) {
   constexpr size_t kRing = ring_bytes<EW>();
   cg::grid_group grid = cg::this_grid();
   constexpr int WPC = NT_FILL / 32;
@@ -1387,7 +1465,8 @@ __global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
     const int32_t n = __ldcg(a.gcnt + g);
     if (n > 0) {
       atomicAdd(a.gactive, 1);
-      publish(a, g, 0, n);  // every group starts at parity 0 (v[0] holds b)
+      // every group starts at parity 0 (v[0] holds b)
+      if (a.window <= 0 || g < a.window) publish(a, g, 0, n);
     }
   }
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1402,7 +1481,7 @@ __global__ void __launch_bounds__(NT_FILL, MINB) fill_cg_kernel(FillArgs a) {
 
 // Initial ||b||^2 per component and the state of every component.  One warp
 // per item, like the sweeps.
-__global__ void __launch_bounds__(NT) init_norm_kernel(FillArgs a, double rtol) {
+__global__ void __launch_bounds__(NT) init_norm_kernel(const __grid_constant__ FillArgs a, double rtol) {
   const int gwarp = blockIdx.x * WPB + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * WPB;
   const int lane = threadIdx.x & 31;
@@ -1555,6 +1634,7 @@ struct FillWs {
   int32_t *parent, *isroot, *gid, *cgrp, *gsize, *gstart, *gcnt, *gdone, *gchg, *gactive, *ngroups;
   unsigned long long *gtk, *ring;
   uint32_t *ring_tail, *ring_hint;
+  int32_t* gnext;
   uint32_t R;
   double *partial, *rho, *alpha, *beta, *tol;
   uint8_t *status, *final_status, *xbuf;
@@ -1628,6 +1708,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.ring_tail = c.take<uint32_t>(1);
   w.ring_hint = c.take<uint32_t>(1);
   w.gactive = c.take<int32_t>(1);
+  w.gnext = c.take<int32_t>(1);
   w.ngroups = c.take<int32_t>(1);
   w.total = c.take<int32_t>(1);
   w.total_items = c.take<int32_t>(1);
@@ -1782,6 +1863,9 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_tail, 0, sizeof(uint32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_hint, 0, sizeof(uint32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.gactive, 0, sizeof(int32_t), s));
+  const char* we = getenv("NI_FILL_WINDOW");
+  const int window = we ? atoi(we) : 0;
+  NI_CUDA_TRY(cudaMemcpyAsync(w.gnext, &window, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   FillArgs a;
   memset(&a, 0, sizeof(a));
   a.rows = rows;
@@ -1812,6 +1896,8 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.ring_tail = w.ring_tail;
   a.ring_hint = w.ring_hint;
   a.gactive = w.gactive;
+  a.window = window;
+  a.gnext = w.gnext;
   a.rho = w.rho;
   a.alpha = w.alpha;
   a.beta = w.beta;
