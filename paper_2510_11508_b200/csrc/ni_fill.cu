@@ -127,12 +127,14 @@ struct FillArgs {
   uint32_t R;                  // ring capacity (power of two)
   uint32_t* ring_tail;
   uint32_t* ring_hint;         // every ring entry below it is exhausted
+  uint32_t* gseq;              // [G] ring position of the group's newest entry
   int32_t* gactive;            // groups with live items
   // admission window: at most `window` groups hold published batches at a
   // time (0: all), so their state can stay in L2; a retiring group admits
   // the next one (gnext) in group order
   int window;
   int32_t* gnext;
+  int mb;  // mailbox slots the scheduler fills per worker (1..MB)
   // component state
   double* rho;     // exact <r_k, r_k> / then the rho_{k+1} estimate
   double* alpha;   // alpha of the last completed sweep
@@ -722,6 +724,12 @@ constexpr size_t smem_bytes() {
 }
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+// A poll whose outcome steers the whole warp: lane 0's read, broadcast, so
+// the lanes can never disagree (a mailbox tail posted between two lanes'
+// reads would otherwise split the warp in front of full-mask shuffles).
+__device__ __forceinline__ int vload_warp(const int* p) {
+  return __shfl_sync(0xffffffffu, vload(p), 0);
+}
 __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
 
 // ---- the batch scheduler
@@ -732,6 +740,11 @@ __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volati
 // are announced in a ring (seq << 32 | group); the scheduler probes 32
 // entries from the hint at once and takes the first open one, so batches
 // drain in publication order and the hint only passes exhausted entries.
+// Ring entries are read relaxed: the group word (gtk) and newest-entry
+// position (gseq) are then read through L2 (ld.cg) at addresses computed from
+// the entry, so they are fetched after it and see what publish() wrote before
+// its release store.  (An acquire load here costs an L1 invalidation per
+// probe: 3-6 % of the fill.)
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -753,11 +766,20 @@ __device__ __noinline__ int claim_items(const FillArgs& a, int want, Claim* cons
     const int32_t g = int32_t(e & 0xffffffffu);
     bool open = false;
     int key = -1;  // priority: the batch's item count (larger groups first)
-    if (pub) {
-      const unsigned long long w = __ldcg(a.gtk + g);
-      const int n = int((w >> 32) & 0x7fffffffu);
-      open = int(w & 0xffffffffu) < n;
-      if (open) key = n;
+    // An entry that is not its group's newest one is exhausted: its batch
+    // completed before the group published again.  (Reading the group's
+    // current batch through it instead made old entries stand in for newer
+    // batches; with the largest-first priority such stand-ins could keep a
+    // slightly smaller group's batch unclaimed until the ring lapped it.)
+    {
+      const int32_t gi = pub ? g : 0;  // both loads in flight at once
+      const uint32_t last = __ldcg(a.gseq + gi);
+      const unsigned long long w = __ldcg(a.gtk + gi);
+      if (pub && last == p) {
+        const int n = int((w >> 32) & 0x7fffffffu);
+        open = int(w & 0xffffffffu) < n;
+        if (open) key = n;
+      }
     }
     const unsigned openm = __ballot_sync(0xffffffffu, open);
     const unsigned donem = __ballot_sync(0xffffffffu, (pub && !open) || stale);
@@ -849,6 +871,7 @@ __device__ __forceinline__ void publish(const FillArgs& a, int32_t g, int par, i
                             (static_cast<unsigned long long>(n) << 32));
   __threadfence();
   const uint32_t p = atomicAdd(a.ring_tail, 1u);
+  a.gseq[g] = p;  // ordered before the entry by its release store
   const unsigned long long e = (static_cast<unsigned long long>(p) << 32) | uint32_t(g);
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.ring + (p & (a.R - 1))), "l"(e)
                : "memory");
@@ -1093,11 +1116,11 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
     int need = 0, mt = 0;
     if (lane < WORKERS) {
       mt = vload(&sh.mb[lane].tail);
-      need = MB - (mt - vload(&sh.mb[lane].head));
+      need = max(0, a.mb - (mt - vload(&sh.mb[lane].head)));
     }
     // claim targets, slot-major: the first free slot of every worker, then
     // the second ones, so a short claim feeds the emptiest mailboxes first
-    static_assert(MB == 2, "target order below is written for two mailbox slots");
+    static_assert(MB <= 2, "target order below is written for at most two mailbox slots");
     const unsigned m0 = __ballot_sync(0xffffffffu, need > 0);
     const unsigned m1 = __ballot_sync(0xffffffffu, need > 1);
     const unsigned below = (1u << lane) - 1;
@@ -1122,7 +1145,7 @@ __device__ void scheduler_loop(const FillArgs& a, CtaShared& sh) {
       }
     }
     if (!busy) {
-      if (vload(reinterpret_cast<const int*>(a.gactive)) == 0) {
+      if (vload_warp(reinterpret_cast<const int*>(a.gactive)) == 0) {
         // every group retired: nothing will be claimed or posted any more
         if (lane == 0) vstore(&sh.done, 1);
 #if NI_FILL_STATS
@@ -1315,7 +1338,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
 #pragma unroll 1
   for (int g = 0; g < SH - 2; g += 4) {
     if (g == GSW) {  // the stream moves on to the next item with the rows issued from here on
-      has_next = mbh < vload(&mb.tail);
+      has_next = mbh < vload_warp(&mb.tail);
       if (has_next) {
         __threadfence_block();
         nx = &mb.slot[mbh % MB];
@@ -1346,7 +1369,7 @@ __device__ __forceinline__ void sweep_item(const FillArgs& a, const unsigned cha
 #if NI_FILL_STATS
   const long long tw0 = clock64();
 #endif
-  while (fbt - vload(&fb.head) >= FQ) __nanosleep(32);
+  while (fbt - vload_warp(&fb.head) >= FQ) __nanosleep(32);
 #if NI_FILL_STATS
   if (lane == 0) NI_STAT(2, clock64() - tw0);
 #endif
@@ -1402,8 +1425,8 @@ __device__ void worker_loop(const FillArgs& a, unsigned char* ring, Mailbox& mb,
 #endif
   for (;;) {
     if (!have) {
-      if (mbh == vload(&mb.tail)) {
-        if (vload(&sh.done)) break;
+      if (mbh == vload_warp(&mb.tail)) {
+        if (vload_warp(&sh.done)) break;
 #if NI_FILL_STATS
         const long long ti = clock64();
         __nanosleep(NI_IDLE_NS);
@@ -1633,7 +1656,7 @@ struct FillWs {
       *active_items;
   int32_t *parent, *isroot, *gid, *cgrp, *gsize, *gstart, *gcnt, *gdone, *gchg, *gactive, *ngroups;
   unsigned long long *gtk, *ring;
-  uint32_t *ring_tail, *ring_hint;
+  uint32_t *ring_tail, *ring_hint, *gseq;
   int32_t* gnext;
   uint32_t R;
   double *partial, *rho, *alpha, *beta, *tol;
@@ -1703,6 +1726,7 @@ static void carve_fill(Carver& c, FillWs& w, int64_t npix, int rows, int W, int 
   w.gdone = c.take<int32_t>(C + 1);
   w.gchg = c.take<int32_t>(C + 1);
   w.gtk = c.take<unsigned long long>(C + 1);
+  w.gseq = c.take<uint32_t>(C + 1);
   w.R = ring_cap(C);
   w.ring = c.take<unsigned long long>(w.R);
   w.ring_tail = c.take<uint32_t>(1);
@@ -1859,6 +1883,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.gdone, 0, sizeof(int32_t) * (G + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.gchg, 0, sizeof(int32_t) * (G + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.gtk, 0, sizeof(unsigned long long) * (G + 1), s));
+  NI_CUDA_TRY(cudaMemsetAsync(w.gseq, 0xff, sizeof(uint32_t) * (G + 1), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.ring, 0xff, sizeof(unsigned long long) * w.R, s));
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_tail, 0, sizeof(uint32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_hint, 0, sizeof(uint32_t), s));
@@ -1895,8 +1920,18 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   a.R = w.R;
   a.ring_tail = w.ring_tail;
   a.ring_hint = w.ring_hint;
+  a.gseq = w.gseq;
   a.gactive = w.gactive;
   a.window = window;
+  // One queued item per worker keeps a few large components (single maps,
+  // unpaired items) spread over more workers; with many lockstep groups two
+  // queued items keep every worker's row stream continuous.
+  {
+    const char* me = getenv("NI_FILL_MB");
+    a.mb = me ? atoi(me) : (per > 1 ? MB : 1);
+    if (a.mb < 1) a.mb = 1;
+    if (a.mb > MB) a.mb = MB;
+  }
   a.gnext = w.gnext;
   a.rho = w.rho;
   a.alpha = w.alpha;
