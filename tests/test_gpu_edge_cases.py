@@ -1,0 +1,169 @@
+"""GPU known-answer and edge-case tests: the reference's own small exact
+cases mirrored on the CUDA path, ragged and degenerate
+shapes the strip decomposition of the fill must handle (maps narrower or
+shorter than one 30 x 30 strip, widths that are not a multiple of 30, holes,
+isolated pixels), and the scheduler under its non-default claim patterns.
+
+Every case runs the CUDA path through the C ABI and the CPU oracle on the
+same inputs: labels bit-exact, same outer iterations and merged partition,
+depth within the north-star tolerance (tests/parity.py).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.parity import assert_depth_close
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2510_11508_b200 as nb  # noqa: E402
+from paper_2510_11508_b200 import scenes  # noqa: E402
+from oracle import normint_oracle as O  # noqa: E402
+
+
+def _tilted(deg, azimuth=0.0):
+    t, a = np.deg2rad(deg), np.deg2rad(azimuth)
+    return np.array([np.sin(t) * np.cos(a), np.sin(t) * np.sin(a), -np.cos(t)])
+
+
+def run_both(normals, mask, intr, theta_deg=3.5, connectivity=8, model="milano",
+             merge_freq=None):
+    """GPU and oracle on identical fp32 normals; returns (gpu, oracle)."""
+    normals = np.ascontiguousarray(normals, np.float32)
+    mask = np.ascontiguousarray(mask, bool)
+    theta = None if theta_deg is None else float(np.deg2rad(theta_deg))
+    nm = nb.NormalMap.create(normals, mask)
+    r = nb.run_pipeline(nm, nb.CameraIntrinsics(*intr), theta,
+                        nb.SolveSettings(freq_merging=merge_freq), None, connectivity, model)
+    ref = O.run_pipeline(normals.astype(np.float64), mask, intr, theta,
+                         O.Settings(freq_merging=merge_freq), connectivity, model)
+    return r, ref
+
+
+def assert_parity(r, ref, mask, intr):
+    assert np.array_equal(r.partition0.labels, ref.labels0)
+    assert r.partition0.component_count == ref.count0
+    assert r.iterations == ref.iterations
+    assert np.array_equal(r.partition.labels, ref.labels)
+    assert_depth_close(r.log_depth.values, ref.log_depth, mask, float(intr[0]))
+
+
+def test_two_halves_two_components():
+    """test_graph.py:153-166: a 4x4 map whose halves differ by 10 degrees at
+    theta_c = 5 degrees -> 2 components, the first pixel's labelled 0."""
+    n = np.zeros((4, 4, 3))
+    n[:, :2] = _tilted(0.0)
+    n[:, 2:] = _tilted(10.0)
+    mask = np.ones((4, 4), bool)
+    intr = (32.0, 32.0, 1.5, 1.5)
+    r, ref = run_both(n, mask, intr, theta_deg=5.0)
+    assert r.partition0.component_count == 2
+    assert r.partition0.labels[0] == 0
+    assert_parity(r, ref, mask, intr)
+
+
+def test_uniform_map_one_component():
+    """test_graph.py:135-140: a uniform map is one component."""
+    n = np.broadcast_to(_tilted(20.0, 30.0), (9, 13, 3)).copy()
+    mask = np.ones((9, 13), bool)
+    intr = (104.0, 104.0, 6.0, 4.0)
+    r, ref = run_both(n, mask, intr)
+    assert r.partition0.component_count == 1
+    assert_parity(r, ref, mask, intr)
+
+
+def test_theta_none_one_pixel_per_component():
+    """graph.py:153-155 / test_graph.py:143-150: theta_c = None puts every
+    valid pixel in its own component."""
+    rng = np.random.default_rng(5)
+    sc = scenes.voronoi_ortho("t", 6, 7, 3, 5, 0.2)
+    mask = rng.random((6, 7)) < 0.8
+    r, ref = run_both(sc.normals, mask, sc.intrinsics(), theta_deg=None)
+    assert r.partition0.component_count == int(mask.sum())
+    assert_parity(r, ref, mask, sc.intrinsics())
+
+
+def test_fronto_parallel_plane_is_flat():
+    """test_pipeline.py:14-23: a fronto-parallel plane integrates to a
+    constant depth (every residual below 1e-8)."""
+    n = np.broadcast_to(_tilted(0.0), (24, 40, 3)).copy()
+    mask = np.ones((24, 40), bool)
+    intr = (320.0, 320.0, 19.5, 11.5)
+    r, ref = run_both(n, mask, intr)
+    z = r.log_depth.values[mask]
+    assert float(z.max() - z.min()) < 1e-8
+    assert_parity(r, ref, mask, intr)
+
+
+@pytest.mark.parametrize("shape", [(1, 7), (7, 1), (2, 2), (3, 31), (29, 61), (31, 33),
+                                   (33, 97), (45, 130)])
+def test_ragged_shapes(shape):
+    """Maps narrower or shorter than one strip and widths that are not a
+    multiple of the 30-column strip, with holes in the mask."""
+    h, w = shape
+    rng = np.random.default_rng(h * 1000 + w)
+    cells = max(2, min(6, h * w // 40))
+    sc = scenes.voronoi_ortho("ragged", h, w, cells, h + w, 0.2)
+    mask = rng.random((h, w)) < 0.9
+    if mask.sum() < 2:
+        mask[:] = True
+    r, ref = run_both(sc.normals, mask, sc.intrinsics())
+    assert_parity(r, ref, mask, sc.intrinsics())
+
+
+def test_single_valid_pixel():
+    """One valid pixel: one singleton component, no edges, nothing to fill."""
+    sc = scenes.voronoi_ortho("one", 5, 5, 2, 9, 0.2)
+    mask = np.zeros((5, 5), bool)
+    mask[2, 3] = True
+    r, ref = run_both(sc.normals, mask, sc.intrinsics())
+    assert r.partition0.component_count == 1
+    assert_parity(r, ref, mask, sc.intrinsics())
+
+
+def test_isolated_pixels_4conn():
+    """A checkerboard mask at 4-connectivity has no edges: every pixel is a
+    singleton component and the fill skips all of them (solver.py:220)."""
+    sc = scenes.voronoi_ortho("checker", 20, 23, 3, 4, 0.2)
+    v, u = np.mgrid[:20, :23]
+    mask = (u + v) % 2 == 0
+    r, ref = run_both(sc.normals, mask, sc.intrinsics(), connectivity=4)
+    assert r.partition0.component_count == int(mask.sum())
+    assert_parity(r, ref, mask, sc.intrinsics())
+
+
+def test_bini_model_4conn_ragged():
+    """The BiNI continuity model (4-connectivity only) on a ragged map."""
+    sc = scenes.voronoi_ortho("bini", 37, 53, 5, 12, 0.2)
+    r, ref = run_both(sc.normals, sc.mask, sc.intrinsics(), connectivity=4, model="bini")
+    assert_parity(r, ref, sc.mask, sc.intrinsics())
+
+
+@pytest.mark.parametrize("env", [{"NI_FILL_MB": "1"}, {"NI_FILL_MB": "2"},
+                                 {"NI_FILL_PAIR": "2"}, {"NI_FILL_PAIR": "1"}])
+def test_scheduler_claim_patterns(env, monkeypatch):
+    """The fill's batch scheduler under each mailbox depth and item pairing:
+    the batch completes, a different mailbox depth (pure scheduling) gives
+    bit-identical results, a different pairing the same iterations and depth
+    within tolerance."""
+    maps = [scenes.voronoi_ortho(f"s{i}", 70, 95, 5, 40 + i, 0.2) for i in range(12)]
+    nms = [nb.NormalMap.create(m.normals, m.mask) for m in maps]
+    intr = [nb.CameraIntrinsics(*m.intrinsics()) for m in maps]
+    theta = float(np.deg2rad(3.5))
+    base = nb.run_pipeline_batch(nb.stack(nms), intr, theta)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    other = nb.run_pipeline_batch(nb.stack(nms), intr, theta)
+    for m, a, b in zip(maps, base, other):
+        assert a.iterations == b.iterations
+        assert np.array_equal(a.partition.labels, b.partition.labels)
+        if "NI_FILL_MB" in env:
+            assert np.array_equal(a.log_depth.values, b.log_depth.values)
+        else:
+            assert_depth_close(b.log_depth.values, a.log_depth.values, m.mask, m.fx)
