@@ -1,0 +1,145 @@
+"""How many iterations would a multigrid-preconditioned fill need?
+
+CPU prototype for the round-2 plan: for the components of a
+C5 map, build the fill system exactly as the oracle does (oracle.fill: the
+pair normal system A^T W A x = A^T W b at z = 0), then solve it
+
+* with scipy-semantics CG (rtol 1e-6, x0 = 0) -- what the GPU fill does now;
+* with CG preconditioned by one V-cycle of an aggregation multigrid whose
+  levels are 2x2 pixel blocks *inside the component* (piecewise-constant
+  prolongation P, Galerkin coarse operator P^T A P, so coarse conductances
+  are sums of fine ones), damped-Jacobi pre/post smoothing, and a direct
+  solve on the coarsest level.
+
+Reports per component: size, CG iterations, MG-PCG iterations, and the
+relative difference of the two solutions after removing the mean (the
+null space).  Work per MG-PCG iteration is about 3-4 fine-level sweeps.
+
+    python scripts/mg_pcg_study.py [map index] [nu (smoothing steps)]
+"""
+import sys
+import time
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+sys.path.insert(0, ".")
+from oracle import normint_oracle as O  # noqa: E402
+from paper_2510_11508_b200 import scenes  # noqa: E402
+
+
+def component_systems(sc):
+    n64, m = O.normalize_normals(sc.normals.astype(np.float64), sc.mask)
+    edges, _ = O.pixel_edges(m, 8)
+    labels, count = O.components(n64, m, edges, float(np.deg2rad(3.5)))
+    co = O.edge_coefficients(n64, m, edges, sc.intrinsics())
+    z = np.zeros(labels.size)
+    la = labels[edges[:, 0]]
+    intra = np.flatnonzero(la == labels[edges[:, 1]])
+    wa, wb = O.edge_weights(co, edges, z, 2.0, intra)
+    out = []
+    h, w = m.shape
+    for c in range(count):
+        sel = la[intra] == c
+        eids = intra[sel]
+        pix = np.flatnonzero(labels == c)
+        if len(pix) < 2:
+            continue
+        ca = np.searchsorted(pix, edges[eids, 0])
+        cb = np.searchsorted(pix, edges[eids, 1])
+        mat, rhs = O.pair_normal_system(ca, cb, co.omega_a[eids], co.omega_b[eids],
+                                        wa[sel], wb[sel], len(pix))
+        out.append((c, pix, mat.tocsr(), rhs, w))
+    return out
+
+
+def aggregate(pix_u, pix_v):
+    """2x2 block aggregates of a pixel set: (aggregate id per pixel, coarse coords)."""
+    bu, bv = pix_u // 2, pix_v // 2
+    key = bv.astype(np.int64) * (1 << 20) + bu
+    uniq, agg = np.unique(key, return_inverse=True)
+    return agg, (uniq % (1 << 20)).astype(np.int64), (uniq >> 20).astype(np.int64)
+
+
+def hierarchy(A, pu, pv, min_size=400):
+    levels = [A]
+    Ps = []
+    while levels[-1].shape[0] > min_size:
+        agg, cu, cv = aggregate(pu, pv)
+        n, nc = len(agg), int(agg.max()) + 1
+        P = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
+        Ac = (P.T @ levels[-1] @ P).tocsr()
+        Ps.append(P)
+        levels.append(Ac)
+        pu, pv = cu, cv
+        if nc == n:
+            break
+    # coarsest: direct solve of the singular (Neumann) system via pinv-free trick:
+    # ground one node per connected part is overkill here; use lstsq on dense
+    Ad = levels[-1].toarray()
+    coarse_pinv = np.linalg.pinv(Ad)
+    return levels, Ps, coarse_pinv
+
+
+def vcycle(levels, Ps, coarse_pinv, b, nu=2, omega=0.8, lvl=0):
+    A = levels[lvl]
+    if lvl == len(levels) - 1:
+        return coarse_pinv @ b
+    d = A.diagonal()
+    dinv = np.where(d > 0, 1.0 / np.where(d > 0, d, 1.0), 0.0)
+    x = omega * dinv * b
+    for _ in range(nu - 1):
+        x += omega * dinv * (b - A @ x)
+    r = b - A @ x
+    P = Ps[lvl]
+    x += P @ vcycle(levels, Ps, coarse_pinv, P.T @ r, nu, omega, lvl + 1)
+    for _ in range(nu):  # symmetric: same number of post-smoothing steps
+        x += omega * dinv * (b - A @ x)
+    return x
+
+
+def pcg(A, b, M, rtol=1e-6, maxiter=5000):
+    bn = np.linalg.norm(b)
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = M(r)
+    p = z.copy()
+    rz = r @ z
+    for it in range(maxiter):
+        if np.linalg.norm(r) < rtol * bn:
+            return x, it
+        q = A @ p
+        alpha = rz / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        z = M(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, maxiter
+
+
+if __name__ == "__main__":
+    idx = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    nu = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    sc = scenes.config5_map(idx)
+    systems = component_systems(sc)
+    tot_cg = tot_mg = 0
+    for c, pix, A, b, w in sorted(systems, key=lambda s: -len(s[1]))[:8]:
+        if not np.any(b):
+            continue
+        t0 = time.perf_counter()
+        x_cg, ok, it_cg = O.conjugate_gradient(A.dot, b, 1e-6, max(5000, len(pix)))
+        t1 = time.perf_counter()
+        levels, Ps, cp = hierarchy(A, pix % w, pix // w)
+        x_mg, it_mg = pcg(A, b, lambda r: vcycle(levels, Ps, cp, r, nu), 1e-6)
+        t2 = time.perf_counter()
+        d = (x_mg - x_mg.mean()) - (x_cg - x_cg.mean())
+        rel = np.linalg.norm(d) / max(np.linalg.norm(x_cg - x_cg.mean()), 1e-300)
+        tot_cg += it_cg * len(pix)
+        tot_mg += it_mg * len(pix)
+        print(f"component {c}: {len(pix)} px, levels {len(levels)}, CG {it_cg} it ({t1 - t0:.1f} s), "
+              f"MG-PCG {it_mg} it ({t2 - t1:.1f} s), rel diff {rel:.2e}", flush=True)
+    print(f"px-weighted iterations: CG {tot_cg:.3e}, MG-PCG {tot_mg:.3e} "
+          f"(ratio {tot_cg / max(tot_mg, 1):.1f}x)")
