@@ -193,3 +193,74 @@ def map_level_study(idx=0, nu=1):
 
 if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "map":
     map_level_study(int(sys.argv[1]), int(sys.argv[2]))
+
+
+def grid_label_study(idx=0, nu=1, min_cells=64):
+    """GPU-friendly component-aware variant: every level is a regular grid
+    whose cells carry ONE label -- a 2x2 block takes the label of the most
+    pixels of the block (ties: the smallest label) and pixels of any other
+    label in the block are left out of the aggregation (they are only
+    smoothed).  One PCG per component (the preconditioner is block-diagonal
+    by component because aggregates never mix labels)."""
+    sc = scenes.config5_map(idx)
+    systems = component_systems(sc)
+    h, w = sc.mask.shape
+    n = h * w
+    lab = np.full(n, -1)
+    for c, pix, A, bc, _ in systems:
+        lab[pix] = c
+    # level hierarchy over the grid: label per cell, P maps fine cell -> coarse cell or -1
+    levels_lab = [lab.reshape(h, w)]
+    while min(levels_lab[-1].shape) > 8 and levels_lab[-1].size > min_cells:
+        L = levels_lab[-1]
+        hh, ww = (L.shape[0] + 1) // 2, (L.shape[1] + 1) // 2
+        Lp = np.full((2 * hh, 2 * ww), -1)
+        Lp[:L.shape[0], :L.shape[1]] = L
+        blocks = Lp.reshape(hh, 2, ww, 2).transpose(0, 2, 1, 3).reshape(hh, ww, 4)
+        coarse = np.full((hh, ww), -1)
+        for i in range(4):  # majority label (ties: smallest)
+            cand = blocks[..., i]
+            cnt = (blocks == cand[..., None]).sum(-1)
+            best = (cand >= 0) & ((coarse < 0) | (cnt > (blocks == coarse[..., None]).sum(-1)) |
+                                  ((cnt == (blocks == coarse[..., None]).sum(-1)) & (cand < coarse)))
+            coarse = np.where(best, cand, coarse)
+        levels_lab.append(coarse)
+    tot_cg = tot_mg = 0
+    for c, pix, A, b, _ in sorted(systems, key=lambda s: -len(s[1]))[:8]:
+        if not np.any(b):
+            continue
+        # per-level membership of component c and the aggregation maps
+        Ps = []
+        ids = np.full(n, -1)
+        ids[pix] = np.arange(len(pix))
+        fine_ids, fh, fw = ids.reshape(h, w), h, w
+        mats = [A]
+        for lv in range(1, len(levels_lab)):
+            L = levels_lab[lv]
+            ch, cw = L.shape
+            cids = np.full((ch, cw), -1)
+            mem = L == c
+            cids[mem] = np.arange(int(mem.sum()))
+            v, u = np.nonzero(fine_ids >= 0)
+            src = fine_ids[v, u]
+            dst = cids[v // 2, u // 2]
+            keep = dst >= 0
+            nf, nc = int((fine_ids >= 0).sum()), int(mem.sum())
+            if nc == 0:
+                break
+            P = sp.csr_matrix((np.ones(int(keep.sum())), (src[keep], dst[keep])), shape=(nf, nc))
+            Ps.append(P)
+            mats.append((P.T @ mats[-1] @ P).tocsr())
+            fine_ids = cids
+        cp = np.linalg.pinv(mats[-1].toarray())
+        x_cg, ok, it_cg = O.conjugate_gradient(A.dot, b, 1e-6, max(5000, len(pix)))
+        x_mg, it_mg = pcg(A, b, lambda r: vcycle(mats, Ps, cp, r, nu), 1e-6)
+        tot_cg += it_cg * len(pix)
+        tot_mg += it_mg * len(pix)
+        print(f"component {c}: {len(pix)} px, {len(mats)} levels, CG {it_cg}, grid-label MG-PCG {it_mg}",
+              flush=True)
+    print(f"grid-label aggregation: px-weighted iterations ratio {tot_cg / max(tot_mg, 1):.1f}x")
+
+
+if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "grid":
+    grid_label_study(int(sys.argv[1]), int(sys.argv[2]))
