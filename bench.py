@@ -183,7 +183,6 @@ def run_ours(args, rank, world, local_rank):
     m_dev = torch.from_numpy(masks_h).to(dev)
     n_pin = torch.from_numpy(normals_h).pin_memory()
     m_pin = torch.from_numpy(masks_h).pin_memory()
-    out_pin = torch.empty((B, normals_h.shape[1] * normals_h.shape[2]), dtype=torch.float64).pin_memory()
 
     def step_device():
         nm = nb.NormalMap.create(n_dev, m_dev)
@@ -191,15 +190,14 @@ def run_ours(args, rank, world, local_rank):
             return [nb.run_pipeline(nm, intr[0], theta, settings)]
         return nb.run_pipeline_batch(nm, intr, theta, settings)
 
-    def step_e2e():
-        nd = n_pin.to(dev, non_blocking=True)
-        md = m_pin.to(dev, non_blocking=True)
-        nm = nb.NormalMap.create(nd, md)
-        res = nb.run_pipeline_batch(nm, intr, theta, settings) if B > 1 else [
-            nb.run_pipeline(nm, intr[0], theta, settings)]
-        for i, r in enumerate(res):
-            out_pin[i].copy_(r.log_depth.values_t, non_blocking=True)
-        return res
+    def run_e2e(k):
+        """k steps through the serving API: every step copies its pinned host
+        inputs to the device and reads every map's log-depth back into pinned
+        host memory; run_pipeline_stream overlaps the next step's upload and
+        the previous step's read-back with the current step's compute."""
+        for _ in nb.run_pipeline_stream(((n_pin, m_pin) for _ in range(k)), intr, theta,
+                                        settings, device=dev):
+            pass  # each step's log-depth is already in pinned host memory
 
     def barrier():
         if world > 1:
@@ -242,9 +240,10 @@ def run_ours(args, rank, world, local_rank):
     clocks = clk.summary()
 
     # e2e through host buffers
-    step_e2e()
+    run_e2e(3)  # warms the pinned-host and device caching allocators
     torch.cuda.synchronize()
-    e2e_ms = timed(step_e2e, max(1, min(args.steps, 3)), lambda r: None)
+    e2e_steps = max(2, min(args.steps, 5))
+    e2e_ms = timed(lambda: run_e2e(e2e_steps), 1, lambda r: None) / e2e_steps
 
     from paper_2510_11508_b200.shard import aggregate
     valid_total, _ = aggregate(valid_local, ms, dev)
@@ -282,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         h2d = int(n_pin.numel() * n_pin.element_size() + m_pin.numel() * m_pin.element_size())
-        d2h = int(out_pin.numel() * out_pin.element_size())
+        d2h = int(B * normals_h.shape[1] * normals_h.shape[2] * 8)  # float64 log-depth per map
         line = {
             "metric": "valid pixels/s end-to-end (component normal integration, run_pipeline)",
             "value": round(valid_total / (ms * 1e-3), 1),

@@ -11,7 +11,8 @@ there is no CPU fallback.
 from .errors import (DegenerateEdge, DeviceError, EmptyMask, NoInterEdges, NormintError)
 from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, depth_from_logdepth, stack
 from .pipeline import (BaselineResult, Partition, PipelineResult, dot_cutoff, run_pipeline,
-                       run_pipeline_batch, run_pixel_baseline, run_pixel_baseline_batch)
+                       run_pipeline_batch, run_pipeline_stream, run_pixel_baseline,
+                       run_pixel_baseline_batch)
 from .settings import SolveSettings, WeightParams
 
 __version__ = "0.1.0"
@@ -34,6 +35,7 @@ __all__ = [
     "dot_cutoff",
     "run_pipeline",
     "run_pipeline_batch",
+    "run_pipeline_stream",
     "run_pixel_baseline",
     "run_pixel_baseline_batch",
     "stack",

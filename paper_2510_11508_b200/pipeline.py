@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .errors import EmptyMask
-from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _stream
+from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _device, _stream
 from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
 
 ENERGY_FLOOR = 1e-300  # pipeline.py:55
@@ -548,6 +548,77 @@ def run_pipeline_batch(
             fill_report=report,
         ))
     return out
+
+
+def run_pipeline_stream(
+    batches,
+    intrinsics,
+    theta_c: float | None,
+    settings: SolveSettings | None = None,
+    weights: WeightParams | None = None,
+    connectivity: int = 8,
+    model: str = "milano",
+    gauge_depth: float | None = None,
+    device=None,
+):
+    """Serve a stream of host batches through :func:`run_pipeline_batch`.
+
+    ``batches`` yields ``(normals, mask)`` CPU tensors of shape (B, H, W, 3) /
+    (B, H, W) (pinned memory lets the copies run asynchronously); every batch
+    uses ``intrinsics`` (one per map).  Yields ``(results, log_depth_host)``
+    per batch: the list of :class:`PipelineResult` and a pinned (B, H*W)
+    float64 CPU tensor with every map's log-depth (0 outside the mask).
+
+    The next batch's host->device copy and the previous batch's log-depth
+    read-back run on a copy stream while the current batch computes, so a
+    stream of batches pays for the transfers only at its two ends.  The
+    results are those of ``run_pipeline_batch`` on each batch.
+    """
+    dev = _device(device)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    it = iter(batches)
+
+    def upload():
+        try:
+            n_h, m_h = next(it)
+        except StopIteration:
+            return None
+        with torch.cuda.stream(copy):
+            n_d = n_h.to(dev, non_blocking=True)
+            m_d = m_h.to(dev, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(copy)
+        return n_d, m_d, ready
+
+    nxt = upload()
+    pending = None
+    while nxt is not None:
+        n_d, m_d, ready = nxt
+        comp.wait_event(ready)
+        n_d.record_stream(comp)
+        m_d.record_stream(comp)
+        nxt = upload()  # prefetch the next batch while this one computes
+        res = run_pipeline_batch(NormalMap.create(n_d, m_d, device=dev), intrinsics, theta_c,
+                                 settings, weights, connectivity, model, gauge_depth)
+        done = torch.cuda.Event()
+        done.record(comp)
+        out = torch.empty((len(res), res[0].log_depth.height * res[0].log_depth.width),
+                          dtype=torch.float64, pin_memory=True)
+        with torch.cuda.stream(copy):
+            copy.wait_event(done)
+            for i, r in enumerate(res):
+                r.log_depth.values_t.record_stream(copy)
+                out[i].copy_(r.log_depth.values_t, non_blocking=True)
+            fetched = torch.cuda.Event()
+            fetched.record(copy)
+        if pending is not None:
+            pending[2].synchronize()
+            yield pending[0], pending[1]
+        pending = (res, out, fetched)
+    if pending is not None:
+        pending[2].synchronize()
+        yield pending[0], pending[1]
 
 
 def _per_map_edge_stats(g: _Grid, eflags: torch.Tensor, records):

@@ -167,3 +167,22 @@ def test_scheduler_claim_patterns(env, monkeypatch):
             assert np.array_equal(a.log_depth.values, b.log_depth.values)
         else:
             assert_depth_close(b.log_depth.values, a.log_depth.values, m.mask, m.fx)
+
+
+def test_stream_matches_batch():
+    """run_pipeline_stream (overlapped upload / read-back) returns exactly
+    run_pipeline_batch's results for every batch of the stream."""
+    maps = [scenes.voronoi_ortho(f"st{i}", 48, 64, 4, 70 + i, 0.2) for i in range(3)]
+    n = torch.from_numpy(np.stack([m.normals for m in maps])).pin_memory()
+    mk = torch.from_numpy(np.stack([m.mask for m in maps])).pin_memory()
+    intr = [nb.CameraIntrinsics(*m.intrinsics()) for m in maps]
+    theta = float(np.deg2rad(3.5))
+    ref = nb.run_pipeline_batch(nb.NormalMap.create(n, mk), intr, theta)
+    outs = list(nb.run_pipeline_stream(((n, mk) for _ in range(3)), intr, theta))
+    assert len(outs) == 3
+    for res, host in outs:
+        assert host.is_pinned() and tuple(host.shape) == (3, 48 * 64)
+        for i, (a, b) in enumerate(zip(ref, res)):
+            assert a.iterations == b.iterations
+            assert np.array_equal(a.log_depth.values, b.log_depth.values)
+            assert np.array_equal(host[i].numpy(), a.log_depth.values_t.cpu().numpy())
