@@ -250,6 +250,39 @@ __global__ void __launch_bounds__(NT) strip_comps_kernel(const int32_t* __restri
     key[e] = lab < 0 ? INT32_MAX : lab;
   }
   __syncthreads();
+  // fast path: most strips hold a single component (or none) -- no sort
+  {
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (int e = tid; e < SPX; e += NT) {
+      const int32_t k = key[e];
+      if (k != INT32_MAX) {
+        lo = min(lo, k);
+        hi = max(hi, k);
+      }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    __shared__ int32_t wlo[WPB], whi[WPB];
+    if ((tid & 31) == 0) {
+      wlo[tid >> 5] = lo;
+      whi[tid >> 5] = hi;
+    }
+    __syncthreads();
+    lo = wlo[0];
+    hi = whi[0];
+#pragma unroll
+    for (int w = 1; w < WPB; ++w) {
+      lo = min(lo, wlo[w]);
+      hi = max(hi, whi[w]);
+    }
+    if (lo == INT32_MAX || lo == hi) {  // block-uniform branch
+      if (tid == 0) {
+        if (lo != INT32_MAX) strip_comps[int64_t(strip) * SPX] = lo;
+        nslots[strip] = lo == INT32_MAX ? 0 : 1;
+      }
+      return;
+    }
+  }
   for (int k = 2; k <= SPX; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int e = tid; e < SPX; e += NT) {
