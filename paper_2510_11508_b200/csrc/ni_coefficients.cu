@@ -36,6 +36,16 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
       const double a0 = n[i], a1 = n[npix + i], a2 = n[2 * npix + i];
       const double ua = double(u), va = double(vloc);
       const double ta0 = (ua - cx) / fx, ta1 = (va - cy) / fy;
+      // ray components at the neighbours' coordinates and at the edge
+      // midpoints, each divided once per pixel (same operands and operation
+      // order as per edge, so the values are bit-identical)
+      const double tbx_p = (ua + 1.0 - cx) / fx, tbx_m = (ua + -1.0 - cx) / fx;
+      const double tby_p = (va + 1.0 - cy) / fy;
+      const double tmx_p = (0.5 * (ua + (ua + 1.0)) - cx) / fx;
+      const double tmx_m = (0.5 * (ua + (ua + -1.0)) - cx) / fx;
+      const double tmy_p = (0.5 * (va + (va + 1.0)) - cy) / fy;
+      const double tmy_0 = (0.5 * (va + va) - cy) / fy;
+      const double tmx_0 = (0.5 * (ua + ua) - cx) / fx;
       // gamma = mean_focal * |n . tau / ||tau|| |
       const double tn = sqrt(ta0 * ta0 + ta1 * ta1 + 1.0);
       g = 0.5 * (fx + fy) * fabs(a0 * (ta0 / tn) + a1 * (ta1 / tn) + a2 * (1.0 / tn));
@@ -50,8 +60,11 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
         const double ub = ua + du, vb = va + dv;
         bool ok;
         if (MODEL == 0) {  // milano, continuity.py:232-247
-          const double tb0 = (ub - cx) / fx, tb1 = (vb - cy) / fy;
-          const double tm0 = (0.5 * (ua + ub) - cx) / fx, tm1 = (0.5 * (va + vb) - cy) / fy;
+          // = (ub - cx) / fx, (vb - cy) / fy, (0.5 (ua + ub) - cx) / fx, (0.5 (va + vb) - cy) / fy
+          const double tb0 = du > 0 ? tbx_p : (du < 0 ? tbx_m : ta0);
+          const double tb1 = dv > 0 ? tby_p : ta1;
+          const double tm0 = du > 0 ? tmx_p : (du < 0 ? tmx_m : tmx_0);
+          const double tm1 = dv > 0 ? tmy_p : tmy_0;
           const double pa = a0 * ta0 + a1 * ta1 + a2;
           const double pb = b0 * tb0 + b1 * tb1 + b2;
           const double ma = a0 * tm0 + a1 * tm1 + a2;
