@@ -171,19 +171,39 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
     atomicAdd((unsigned long long*)&st->edges, (unsigned long long)nedges);
 }
 
-// kept edges that leave their tile, unioned in global memory
+// kept edges that leave their tile, unioned in global memory.  Only pixels
+// on a tile's left / right column or bottom row have such edges (forward
+// offsets point right or down): the grid enumerates those 3 * UT - 2
+// positions per tile instead of every pixel.
+constexpr int UT_BORDER = 3 * UT - 2;
+
 template <int CONN>
 __global__ void __launch_bounds__(256) uf_border_kernel(const double* __restrict__ n,
                                                         const uint8_t* __restrict__ valid, int H,
-                                                        int W, int64_t npix, double cutoff,
+                                                        int W, int64_t rows, int tiles_x,
+                                                        int64_t nslots, double cutoff,
                                                         int theta_none, int32_t* parent) {
   constexpr int KF = CONN == 8 ? 4 : 2;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int x = int(i % W);
-    const int64_t y = i / W;
-    const int lx = x % UT, ly = int(y % UT);
-    if (lx != 0 && lx != UT - 1 && ly != UT - 1) continue;  // no edge of i leaves the tile
+  const int64_t npix = rows * W;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nslots;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t tile = t / UT_BORDER;
+    const int pos = int(t - tile * UT_BORDER);
+    int lx, ly;
+    if (pos < UT) {  // left column
+      lx = 0;
+      ly = pos;
+    } else if (pos < 2 * UT) {  // right column
+      lx = UT - 1;
+      ly = pos - UT;
+    } else {  // bottom row between the corners
+      lx = pos - 2 * UT + 1;
+      ly = UT - 1;
+    }
+    const int x = int(tile % tiles_x) * UT + lx;
+    const int64_t y = (tile / tiles_x) * UT + ly;
+    if (x >= W || y >= rows) continue;
+    const int64_t i = y * W + x;
     if (!valid[i]) continue;
     const int vloc = int(y % H);
 #pragma unroll
@@ -322,13 +342,15 @@ extern "C" int ni_components(const double* n, const uint8_t* valid, int B, int H
   if (connectivity == 8) {
     NI_COUNT_LAUNCH(), uf_tile_kernel<8><<<int(tiles), 256, 0, s>>>(
                            n, valid, H, W, rows, tiles_x, dot_cutoff, theta_none, parent, stats);
-    NI_COUNT_LAUNCH(), uf_border_kernel<8><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff,
-                                                                  theta_none, parent);
+    NI_COUNT_LAUNCH(), uf_border_kernel<8><<<grid_blocks(tiles * UT_BORDER), 256, 0, s>>>(
+                           n, valid, H, W, rows, tiles_x, tiles * UT_BORDER, dot_cutoff, theta_none,
+                           parent);
   } else {
     NI_COUNT_LAUNCH(), uf_tile_kernel<4><<<int(tiles), 256, 0, s>>>(
                            n, valid, H, W, rows, tiles_x, dot_cutoff, theta_none, parent, stats);
-    NI_COUNT_LAUNCH(), uf_border_kernel<4><<<blocks, 256, 0, s>>>(n, valid, H, W, npix, dot_cutoff,
-                                                                  theta_none, parent);
+    NI_COUNT_LAUNCH(), uf_border_kernel<4><<<grid_blocks(tiles * UT_BORDER), 256, 0, s>>>(
+                           n, valid, H, W, rows, tiles_x, tiles * UT_BORDER, dot_cutoff, theta_none,
+                           parent);
   }
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), uf_flatten_kernel<<<blocks, 256, 0, s>>>(parent, npix, flags);
