@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
                                                       ni_stats* __restrict__ st) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   __shared__ int p[UT * UT];
+  __shared__ double sn[3][UT * UT];  // the tile's normals: in-tile edges read only these
   const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
   const int x0 = tx * UT;
   const int64_t y0 = int64_t(ty) * UT;
@@ -129,7 +130,14 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
   for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
     const int x = x0 + (l % UT);
     const int64_t y = y0 + l / UT;
-    p[l] = (x < W && y < rows && valid[y * W + x]) ? l : -1;
+    const bool in = x < W && y < rows;
+    const int64_t gi = y * W + x;
+    p[l] = (in && valid[gi]) ? l : -1;
+    if (in) {
+      sn[0][l] = n[gi];
+      sn[1][l] = n[npix + gi];
+      sn[2][l] = n[2 * npix + gi];
+    }
   }
   __syncthreads();
   long long nedges = 0;
@@ -149,7 +157,11 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
       ++nedges;
       const int jx = lx + du, jy = ly + dv;
       if (jx < 0 || jx >= UT || jy >= UT) continue;  // crosses the tile: second pass
-      if (kept_edge(n, npix, i, j, cutoff, theta_none)) sm_union(p, l, jy * UT + jx);
+      const int lj = jy * UT + jx;
+      if (!theta_none &&
+          add_rn(add_rn(mul_rn(sn[0][l], sn[0][lj]), mul_rn(sn[1][l], sn[1][lj])),
+                 mul_rn(sn[2][l], sn[2][lj])) >= cutoff)  // = kept_edge(n, npix, i, j, ...)
+        sm_union(p, l, lj);
     }
   }
   __syncthreads();
