@@ -444,7 +444,8 @@ def run_pipeline_batch(
     fill_ms = _ms(t0)
     for m in range(B):
         records[m].append({"stage": "fill", "wall_ms": fill_ms})
-    filled = z.clone()
+    # the filled state (a copy: the outer loop updates z in place), 0 outside the mask
+    filled = torch.where(g.nmap.valid_t.bool(), z, torch.zeros((), dtype=z.dtype, device=g.dev))
     fit = fill_iters.cpu().numpy()
 
     valid = g.nmap.valid_t
@@ -536,8 +537,7 @@ def run_pipeline_batch(
         vm = valid[sl]
         out.append(PipelineResult(
             log_depth=LogDepthMap(z[sl], vm, g.H, g.W),
-            filled=LogDepthMap(torch.where(vm.bool(), filled[sl], torch.zeros_like(filled[sl])), vm,
-                               g.H, g.W),
+            filled=LogDepthMap(filled[sl], vm, g.H, g.W),
             partition0=Partition(labels0[sl], counts[m], 0, int(first[m])),
             partition=Partition(labels[sl], int(loop.count[m]), int(version[m]), int(first[m])),
             records=records[m],
