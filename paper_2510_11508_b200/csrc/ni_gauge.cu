@@ -36,13 +36,28 @@ __global__ void __launch_bounds__(256) select_hist_kernel(const double* __restri
   const unsigned long long hi_mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
   const unsigned long long p0 = st[m].prefix[0] & hi_mask, p1 = st[m].prefix[1] & hi_mask;
   const int64_t base = int64_t(m) * per_map;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_map;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    if (!valid[base + i]) continue;
-    const unsigned long long key = okey(z[base + i]);
-    const unsigned d = unsigned(key >> shift) & 255u;
-    if ((key & hi_mask) == p0) atomicAdd(&h[0][d], 1u);
-    if ((key & hi_mask) == p1) atomicAdd(&h[1][d], 1u);
+  // U independent loads in flight per thread (the pass is latency-bound
+  // with one outstanding load per thread)
+  constexpr int U = 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < per_map;
+       i0 += U * stride) {
+    bool v[U];
+    double zz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      v[u] = i < per_map && valid[base + i] != 0;
+      zz[u] = i < per_map ? z[base + i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!v[u]) continue;
+      const unsigned long long key = okey(zz[u]);
+      const unsigned d = unsigned(key >> shift) & 255u;
+      if ((key & hi_mask) == p0) atomicAdd(&h[0][d], 1u);
+      if ((key & hi_mask) == p1) atomicAdd(&h[1][d], 1u);
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < 512; t += blockDim.x) {
