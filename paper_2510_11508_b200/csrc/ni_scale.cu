@@ -627,14 +627,24 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const d
 }
 
 // K7b: z[valid] += s[label] on the active maps' pixels (pipeline.py:181-182)
+// grid.y = active map; U independent label/scale/z chains per thread.
 __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__ labels,
                              const double* __restrict__ s, const int32_t* __restrict__ active,
-                             int64_t per_map, int64_t n) {
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = int64_t(active[j / per_map]) * per_map + j % per_map;
-    const int32_t l = labels[i];
-    if (l >= 0) z[i] += s[l];
+                             int64_t per_map) {
+  constexpr int U = 4;
+  const int64_t base = int64_t(active[blockIdx.y]) * per_map;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j0 < per_map;
+       j0 += U * stride) {
+    int32_t l[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * stride;
+      l[u] = j < per_map ? labels[base + j] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (l[u] >= 0) z[base + j0 + u * stride] += s[l[u]];
   }
 }
 
@@ -1084,8 +1094,12 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                                                                      energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  NI_COUNT_LAUNCH(), apply_kernel<<<blocks_for(nact * per_map), 256, 0, s>>>(
-                         z, labels, scales, w.mp.active, per_map, nact * per_map);
+  {
+    const int bx = int(std::max<int64_t>(
+        1, std::min<int64_t>((per_map + 1023) / 1024, int64_t(kSMs) * 16 / nact + 1)));
+    NI_COUNT_LAUNCH(), apply_kernel<<<dim3(bx, nact), 256, 0, s>>>(z, labels, scales,
+                                                                  w.mp.active, per_map);
+  }
   NI_LAUNCH_CHECK();
   return NI_OK;
 }
