@@ -310,7 +310,11 @@ def run_ours(args, rank, world, local_rank):
             },
             "e2e": {"value": round(valid_total / (e2e_ms * 1e-3), 1), "unit": "valid_px/s",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "api": "run_pipeline_stream over pinned host batches: each step uploads its "
+                           "normals + mask and reads every map's log-depth back; the next "
+                           "step's upload and the previous step's read-back overlap the "
+                           "current step's compute"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
