@@ -624,14 +624,13 @@ def run_pipeline_stream(
 def _per_map_edge_stats(g: _Grid, eflags: torch.Tensor, records):
     """Per-map edge / degenerate counts for batched runs (records of
     pipeline.py:137-159 are per map)."""
-    ef = eflags.view(g.B, -1).to(torch.int32)
+    ef = eflags.view(g.B, -1)  # uint8 throughout: byte-sized temporaries
     ex = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
     dg = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
     for k in range(g.kf):
         e = (ef >> k) & 1
-        v = (ef >> (4 + k)) & 1
-        ex += e.sum(dim=1)
-        dg += (e * (1 - v)).sum(dim=1)
+        ex += e.sum(dim=1, dtype=torch.int64)
+        dg += (e & ~(ef >> (4 + k))).sum(dim=1, dtype=torch.int64)
     ex = ex.cpu().numpy()
     dg = dg.cpu().numpy()
     for m in range(g.B):
