@@ -359,12 +359,13 @@ __global__ void pair_sum_kernel(Quot q, StepWs w, const int32_t* __restrict__ nU
 // edge order (solver.py:108-111).  One warp per component.  A map whose
 // A^T W b vanishes (solver.py:112-113) needs no special case: its CG starts
 // from b = 0 and stops at once with s = 0.
-__global__ void comp_sum_kernel(Quot q, StepWs w) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < q.C; c += warps) {
+__global__ void __launch_bounds__(256) comp_sum_kernel(Quot q, StepWs w) {
+  // one block per component: thread-strided partial sums over its incident
+  // entries in edge order, then a fixed-order block tree (deterministic)
+  __shared__ double red[32];
+  for (int c = blockIdx.x; c < q.C; c += gridDim.x) {
     double d = 0.0, r = 0.0;
-    for (int j = q.cstart[c] + lane; j < q.cstart[c + 1]; j += 32) {
+    for (int j = q.cstart[c] + threadIdx.x; j < q.cstart[c + 1]; j += blockDim.x) {
       const int ent = q.cent[j];
       const int e = ent >> 1;
       const double wa = w.wa[e], wb = w.wb[e];
@@ -372,9 +373,9 @@ __global__ void comp_sum_kernel(Quot q, StepWs w) {
       d += wa + wb;
       r += (ent & 1) ? -t : t;
     }
-    d = warp_sum(d);
-    r = warp_sum(r);
-    if (lane == 0) {
+    d = block_sum(d, red);
+    r = block_sum(r, red);
+    if (threadIdx.x == 0) {
       w.diag[c] = d;
       w.rhs[c] = r;
     }
@@ -1049,7 +1050,7 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                            q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
-  NI_COUNT_LAUNCH(), comp_sum_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(q, w);
+  NI_COUNT_LAUNCH(), comp_sum_kernel<<<int(std::min<int64_t>(C, int64_t(kSMs) * 8)), 256, 0, s>>>(q, w);
   NI_LAUNCH_CHECK();
   // remove the roundoff null-space component of A^T W b
   NI_COUNT_LAUNCH(), part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
