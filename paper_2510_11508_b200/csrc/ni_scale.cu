@@ -324,7 +324,11 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
                                const double* __restrict__ gamma,
                                const uint8_t* __restrict__ eflags, int H, int W, int64_t npix,
                                WeightArgs wp, StepWs w) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < q.K; e += gridDim.x * blockDim.x) {
+  // grid.y = active map: only the edges of maps still in the loop
+  const int m = w.mp.active[blockIdx.y];
+  const int e1 = q.estart[m + 1];
+  for (int e = q.estart[m] + blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += gridDim.x * blockDim.x) {
     const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
     double wa, wb;
     edge_weights_at<CONN, MODEL>(z, omega_a, omega_b, gamma, eflags, H, W, npix, a, k, wp, wa, wb);
@@ -1039,14 +1043,20 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   wp.lt = log10(outlier_low);
   wp.ut = log10(outlier_high);
   wp.hi = outlier_high;
+  // one thread per inter edge, all in flight: each edge's weight gathers a
+  // few scattered pixels (latency-bound with fewer threads)
+  const dim3 wblocks(unsigned(std::max<int64_t>(
+                         1, std::min<int64_t>((int64_t(K) / std::max(B, 1) + 255) / 256 + 1,
+                                              int64_t(kSMs) * 64 / nact + 1))),
+                     unsigned(nact));
   if (connectivity == 8)
-    NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<blocks_for(K), 256, 0, s>>>(
+    NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<wblocks, 256, 0, s>>>(
                            q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else if (model == 0)
-    NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<blocks_for(K), 256, 0, s>>>(
+    NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<wblocks, 256, 0, s>>>(
                            q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else
-    NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<blocks_for(K), 256, 0, s>>>(
+    NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<wblocks, 256, 0, s>>>(
                            q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
