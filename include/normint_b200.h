@@ -120,6 +120,29 @@ int ni_fill(const int32_t* labels, int count, const double* omega_a, const doubl
             double* z_out, int32_t* comp_iters, int32_t* comp_status, void* workspace,
             size_t workspace_bytes, ni_stream_t stream);
 
+/* K3 (default fill) -- fill_components (solver.py:195-239) at z = 0 as ONE
+ * batched multigrid-preconditioned CG over every solve unit of every map
+ * (csrc/ni_mg.cu): the same systems as ni_fill (w_a = w_b = NULL), solved
+ * to the reference's relative residual per unit (||r_u|| < cg_tol ||b_u||,
+ * which implies the component's ||r_c|| < cg_tol ||b_c||; cap
+ * max(cg_max_iters, n_c) iterations), then the null-space component removed
+ * per unit -- the gauge of CG from x0 = 0.  Same outputs as ni_fill:
+ * z_out (float64, npix), comp_iters[count] (PCG iterations, max over the
+ * component's units) and comp_status[count] (1 = cap).  The hierarchy's size
+ * depends on the data: if `workspace_bytes` is too small the call returns
+ * NI_ERR_WORKSPACE and writes the bytes it needs to *needed_bytes (the
+ * caller retries); on success *needed_bytes holds the bytes used.
+ * SYNCHRONOUS. */
+int ni_fill_mg_workspace_size(int B, int H, int W, int connectivity, int count, size_t* bytes);
+int ni_fill_mg(const int32_t* labels, int count, const double* omega_a, const double* omega_b,
+               const double* gamma, const uint8_t* eflags, int B, int H, int W, int connectivity,
+               int model, double cg_tol, int cg_max_iters, double* z_out, int32_t* comp_iters,
+               int32_t* comp_status, void* workspace, size_t workspace_bytes,
+               size_t* needed_bytes, ni_stream_t stream);
+/* Multigrid statistics of the last ni_fill_mg on the calling thread: coarse
+ * levels, V-cycles run, unknowns per level (n_per_level[16], index 1..levels). */
+int ni_fill_mg_last_report(int* levels, int* vcycles, int* n_per_level);
+
 /* Directed weights of every forward pixel edge at log-depth state z
  * (continuity.py:292-331, solver.py:253-278): wmode 0 = valid (uniform,
  * t < alignment_iters), 1 = valid * gamma^2 * bilateral(z) (edge_weights,

@@ -45,6 +45,10 @@ SIGNATURES = {
     "ni_fill_workspace_size": ([_I, _I, _I, _I, _I, _I, _PSZ], _I),
     "ni_fill": ([_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ,
                  _P], _I),
+    "ni_fill_mg_workspace_size": ([_I, _I, _I, _I, _I, _PSZ], _I),
+    "ni_fill_mg": ([_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ, _PSZ,
+                    _P], _I),
+    "ni_fill_mg_last_report": ([_PI32, _PI32, _PI32], _I),
     "ni_edge_weights": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D, _P, _P, _P],
                         _I),
     "ni_pair_energy_workspace_size": ([_I, _PSZ], _I),
@@ -117,6 +121,14 @@ def size_query(fn, *args) -> int:
 def launch_count() -> int:
     """Kernels this library has launched so far (host-side counter)."""
     return int(load().ni_launch_count())
+
+
+def mg_report() -> dict:
+    """Multigrid statistics of the last ni_fill_mg on this thread."""
+    lv, vc = C.c_int32(0), C.c_int32(0)
+    n = (C.c_int32 * 16)()
+    load().ni_fill_mg_last_report(C.byref(lv), C.byref(vc), n)
+    return {"levels": lv.value, "vcycles": vc.value, "unknowns": [n[i] for i in range(1, lv.value + 1)]}
 
 
 def fill_report() -> dict:

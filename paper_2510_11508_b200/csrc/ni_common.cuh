@@ -28,6 +28,9 @@ struct FillReport {
   int grid;            // CTAs of the cooperative launch
   int ntiles;          // 32x32 tiles of the grid
   int npartials;       // (tile, component) partial slots
+  int mg_levels;       // multigrid fill: coarse levels used
+  int mg_vcycles;      // multigrid fill: V-cycles (PCG iterations + 1 of the longest unit)
+  int mg_n[16];        // multigrid fill: unknowns per level (index 1..levels)
 };
 extern thread_local FillReport g_fill_report;
 

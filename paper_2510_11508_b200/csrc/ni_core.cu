@@ -61,3 +61,12 @@ extern "C" int ni_fill_last_report(double* cg_ms, long long* px_iters, int* max_
   if (npartials) *npartials = r.npartials;
   return NI_OK;
 }
+
+extern "C" int ni_fill_mg_last_report(int* levels, int* vcycles, int* n_per_level) {
+  const ni::FillReport& r = ni::g_fill_report;
+  if (levels) *levels = r.mg_levels;
+  if (vcycles) *vcycles = r.mg_vcycles;
+  if (n_per_level)
+    for (int l = 0; l < 16; ++l) n_per_level[l] = r.mg_n[l];
+  return NI_OK;
+}

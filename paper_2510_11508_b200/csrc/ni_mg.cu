@@ -1,0 +1,1737 @@
+// K3 -- fill_components (solver.py:195-239) as ONE batched,
+// multigrid-preconditioned conjugate-gradient solve over every component of
+// every map of the batch.
+//
+// What the reference computes.  Per component c, scipy's CG on the normal
+// equations (A^T W A) x = A^T W b from x0 = 0, stopped when ||r|| <
+// rtol ||b|| (cap max(cg_max_iters, n_c); solver.py:97-122).  At the fill
+// state z = 0 every bilateral factor is 1/2 (continuity.py:302-308), so
+// A^T W A is the graph Laplacian of the component's valid edges with
+// conductance c_ab = gamma_a^2/2 + gamma_b^2/2.  CG
+// from 0 keeps x in range(A): the solution is mean-free on every connected
+// part of the positive-conductance graph (a "solve unit"; a component is one
+// unit unless degenerate edges split it).
+//
+// What this file computes.  The same systems solved to the same relative
+// residual (per unit ||r_u|| < rtol ||b_u||, which implies the component's
+// ||r_c|| < rtol ||b_c||), with the fewest passes over HBM: CG preconditioned
+// by one V-cycle of a component-aware aggregation multigrid, then the
+// null-space component removed per unit (the unpreconditioned CG's gauge).
+// A tightly converged solve stays within ~1e-7 of scipy's iterate, five
+// orders of magnitude inside the parity bound (scripts/
+// solver_tolerance_study.py); the CG needs ~1,000-2,600 sweeps per component
+// of a 1024^2 map, the MG-PCG ~20 V-cycles.
+//
+// Hierarchy (built once per call, all maps at once).  Level 0 is the pixel
+// grid.  A level-l unknown is a (2^l x 2^l block, unit) aggregate: the
+// pixels of one unit inside one block, so aggregates never mix units and the
+// preconditioner is block-diagonal over units.  Unknowns are sorted by
+// (map, block row, block column, unit) and found through a per-level block
+// table; each has 8 neighbour links (same unit in the 8 adjacent blocks),
+// Galerkin conductances (fixed-order sums of the finer links crossing the
+// two aggregates: P^T A P of the piecewise-constant prolongation), its
+// parent and (l >= 2) up to 4 children.  Coarsening stops when no link is
+// left (every unit is one aggregate).
+//
+// V-cycle (symmetric, so plain PCG applies): damped Jacobi from zero
+// (omega = 0.8), residual, restriction (sum over children), recursion,
+// prolongation scaled by 1.6 (over-correction, the standard fix for
+// piecewise-constant prolongation), one damped-Jacobi post-sweep.
+//
+// PCG in the Chronopoulos-Gear form: one fine "down" pass (vector updates
+// p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s fused with the
+// pre-smoothing, residual and restriction of the new r) and one fine "up"
+// pass (prolongation, post-smoothing -> u = M r, w = A u and the three dot
+// products (r,u), (w,u), (r,r) per unit) per iteration, so each iteration
+// has exactly one reduction point.  The stop test is scipy's, evaluated on
+// the recursive residual at the top of the iteration.
+//
+// Fine-level planes (padded: pixel (y, x) of the stacked B*H rows at
+// (y + RM) * P + x + XM, zero margins): x, r, p, s, u, w (f32), hw =
+// gamma^2/2 (f32), dinv (f32), imask (u8: bit k = forward edge k, bit 4+k =
+// backward edge k, set iff intra-component, valid and c > 0), par0 (i32:
+// the level-1 aggregate), slot (u16: index of the pixel's unit in its
+// tile's unit list).  Tiles of 64 x 32 pixels never straddle two maps; a CTA
+// stages a tile plus a 1- or 2-pixel halo of the planes it stencils in
+// shared memory.
+//
+// Reductions are deterministic: per (tile, unit) slot a fixed-order f64 sum,
+// per unit its slots in slot order (a stable radix sort gives the order).
+// Coarse conductances, restrictions and counts are fixed-order gathers.  No
+// floating-point atomics: reruns are bit-identical.
+#include <stdlib.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "ni_common.cuh"
+
+namespace ni {
+namespace mg {
+
+constexpr int TX = 64;  // tile width (pixels)
+constexpr int TY = 32;  // tile height
+constexpr int TPX = TX * TY;
+constexpr int NT = 256;  // threads per tile CTA: 2 x 2-pixel blocks each
+constexpr int XM = 16;   // left / right margin (columns)
+constexpr int RM = 2;    // top margin (rows)
+constexpr int RB = TY + 4;  // bottom margin (rows)
+constexpr int MAXLEV = 24;
+constexpr uint16_t NOSLOT = 0xFFFF;
+constexpr int NPART = 6;  // per-slot partials: (r,u) (w,u) (r,r) sum u, sum r, sum w
+#ifndef NI_MG_OMEGA
+#define NI_MG_OMEGA 0.8f
+#endif
+#ifndef NI_MG_OC
+#define NI_MG_OC 1.6f
+#endif
+constexpr float OM = NI_MG_OMEGA;  // damped-Jacobi weight
+constexpr float OC = NI_MG_OC;     // coarse-correction scale
+
+enum : uint8_t { U_ACTIVE = 0, U_CONV = 1, U_CAPPED = 2, U_IDLE = 3 };
+
+struct Geo {
+  int B, H, W, P, nTX, nTY, ntiles, rows;
+  int64_t npix, npad;
+};
+
+static Geo make_geo(int B, int H, int W) {
+  Geo g;
+  g.B = B;
+  g.H = H;
+  g.W = W;
+  g.nTX = div_up(W, TX);
+  g.nTY = div_up(H, TY);
+  g.P = g.nTX * TX + 2 * XM;
+  g.ntiles = B * g.nTX * g.nTY;
+  g.rows = B * H;
+  g.npix = int64_t(B) * H * W;
+  g.npad = int64_t(g.rows + RM + RB) * g.P;
+  return g;
+}
+
+__host__ __device__ __forceinline__ int64_t pidx(int P, int y, int x) {
+  return int64_t(y + RM) * P + x + XM;
+}
+
+// direction of a neighbouring block (dx, dy in -1..1, not both 0) -> 0..7;
+// opposite(d) = 7 - d
+__host__ __device__ __forceinline__ int dir_of(int dx, int dy) {
+  const int i = (dy + 1) * 3 + (dx + 1);
+  return i < 4 ? i : i - 1;
+}
+__host__ __device__ __forceinline__ int dir_dx(int d) {
+  const int i = d < 4 ? d : d + 1;
+  return i % 3 - 1;
+}
+__host__ __device__ __forceinline__ int dir_dy(int d) {
+  const int i = d < 4 ? d : d + 1;
+  return i / 3 - 1;
+}
+
+// W_a = gamma_a^2 / 2 at the fill state (continuity.py:302-308), as stored
+__device__ __forceinline__ float hw_of(double g) { return float(0.5 * (g * g)); }
+
+struct Tile {
+  int m, y0, y1, x0, x1;
+};
+
+__device__ __forceinline__ Tile tile_of(int t, int H, int W, int nTX, int nTY) {
+  Tile T;
+  const int per = nTX * nTY;
+  T.m = t / per;
+  const int r = t - T.m * per;
+  const int ty = r / nTX, tx = r - ty * nTX;
+  T.y0 = T.m * H + ty * TY;
+  T.y1 = min(T.y0 + TY, (T.m + 1) * H);
+  T.x0 = tx * TX;
+  T.x1 = min(T.x0 + TX, W);
+  return T;
+}
+
+// ------------------------------------------------------------ fine setup
+
+// hw, b (into r), imask per pixel; component sizes; count of same-label
+// edges that carry no conductance (then units != components).
+template <int CONN, int MODEL>
+__global__ void __launch_bounds__(256) prep_kernel(
+    const int32_t* __restrict__ labels, const double* __restrict__ omega_a,
+    const double* __restrict__ omega_b, const double* __restrict__ gamma,
+    const uint8_t* __restrict__ eflags, int H, int W, int P, int64_t npix,
+    float* __restrict__ hw, float* __restrict__ rvec, uint8_t* __restrict__ imask,
+    int32_t* __restrict__ comp_size, int32_t* __restrict__ missing) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  int miss = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t lab = labels[i];
+    if (lab < 0) continue;
+    const int u = int(i % W);
+    const int64_t row = i / W;
+    const int vloc = int(row % H);
+    const int64_t o = pidx(P, int(row), u);
+    {
+      const unsigned peers = __match_any_sync(__activemask(), lab);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(comp_size + lab, __popc(peers));
+    }
+    const double wself = 0.5 * (gamma[i] * gamma[i]);
+    const float hself = hw_of(gamma[i]);
+    hw[o] = hself;
+    const uint8_t ef = eflags[i];
+    uint8_t m = 0;
+    double b = 0.0;
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+      if ((ef >> k) & 1) {  // forward edge i -> j exists
+        const int64_t j = i + int64_t(dv) * W + du;
+        if (labels[j] == lab) {
+          const bool ok = ((ef >> (4 + k)) & 1) && (hself + hw_of(gamma[j])) > 0.f;
+          if (ok) {
+            m |= uint8_t(1u << k);
+            const double wb = 0.5 * (gamma[j] * gamma[j]);
+            const double oa = omega_a[k * npix + i];
+            const double ob = MODEL == 0 ? -oa : omega_b[k * npix + i];
+            b += wself * oa - wb * ob;  // A^T W b of rows 2e, 2e+1 (solver.py:83-93)
+          } else {
+            ++miss;
+          }
+        }
+      }
+      const int uj = u - du, vj = vloc - dv;
+      if (uj >= 0 && uj < W && vj >= 0) {  // backward edge j -> i
+        const int64_t j = i - int64_t(dv) * W - du;
+        const uint8_t efj = eflags[j];
+        if (((efj >> k) & 1) && labels[j] == lab && ((efj >> (4 + k)) & 1) &&
+            (hself + hw_of(gamma[j])) > 0.f) {
+          m |= uint8_t(1u << (4 + k));
+          const double wj = 0.5 * (gamma[j] * gamma[j]);
+          const double oa = omega_a[k * npix + j];
+          const double ob = MODEL == 0 ? -oa : omega_b[k * npix + j];
+          b += wself * ob - wj * oa;
+        }
+      }
+    }
+    imask[o] = m;
+    rvec[o] = float(b);
+  }
+  if (miss) atomicAdd(missing, miss);
+}
+
+// neighbour offset of imask bit `bit` in a row-major array of pitch S
+template <int CONN>
+__device__ __forceinline__ int nb_off(int bit, int S) {
+  const int k = bit & 3;
+  const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+  return bit < 4 ? dv * S + du : -(dv * S + du);
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(256) dinv_kernel(int H, int W, int P, int64_t npix,
+                                                   const float* __restrict__ hw,
+                                                   const uint8_t* __restrict__ imask,
+                                                   float* __restrict__ dinv) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = pidx(P, int(i / W), int(i % W));
+    const uint8_t m = imask[o];
+    if (!m) continue;
+    const float h = hw[o];
+    float d = 0.f;
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      if ((m >> k) & 1) d += h + hw[o + nb_off<CONN>(k, P)];
+      if ((m >> (4 + k)) & 1) d += h + hw[o + nb_off<CONN>(4 + k, P)];
+    }
+    dinv[o] = 1.0f / d;
+  }
+}
+
+// ---- solve units.  Fast path (every same-label edge carries conductance):
+// units are the components.  General path: union-find over the imask graph.
+__global__ void unit_from_label_kernel(const int32_t* __restrict__ labels, int H, int W, int P,
+                                       int64_t npix, const uint8_t* __restrict__ imask,
+                                       int32_t* __restrict__ unit) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = pidx(P, int(i / W), int(i % W));
+    if (imask[o]) unit[o] = labels[i];
+  }
+}
+
+__global__ void cc_init_kernel(int W, int P, int64_t npix, const uint8_t* __restrict__ imask,
+                               int32_t* __restrict__ parent) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x)
+    parent[i] = imask[pidx(P, int(i / W), int(i % W))] ? int32_t(i) : -1;
+}
+
+template <int CONN>
+__global__ void cc_union_kernel(int W, int P, int64_t npix, const uint8_t* __restrict__ imask,
+                                int32_t* __restrict__ parent) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t m = imask[pidx(P, int(i / W), int(i % W))];
+#pragma unroll
+    for (int k = 0; k < KF; ++k)
+      if ((m >> k) & 1)
+        uf_union(parent, int32_t(i), int32_t(i + int64_t(fwd_dv(CONN, k)) * W + fwd_du(CONN, k)));
+  }
+}
+
+__global__ void cc_flatten_kernel(int64_t npix, int32_t* __restrict__ parent,
+                                  int32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int32_t r = parent[i];
+    if (r >= 0) {
+      r = uf_find(parent, int32_t(i));
+      parent[i] = r;
+    }
+    flag[i] = r == int32_t(i);
+  }
+}
+
+__global__ void cc_label_kernel(const int32_t* __restrict__ labels, int W, int P, int64_t npix,
+                                const int32_t* __restrict__ parent,
+                                const int32_t* __restrict__ rank, int32_t* __restrict__ unit,
+                                int32_t* __restrict__ unit_comp) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = parent[i];
+    if (r < 0) continue;
+    unit[pidx(P, int(i / W), int(i % W))] = rank[r];
+    if (r == int32_t(i)) unit_comp[rank[r]] = labels[i];
+  }
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+// ---- block-wide helpers (NT threads)
+
+// exclusive scan of one int per thread; returns the total in every thread
+__device__ __forceinline__ int block_excl_scan(int v, int* sw, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  __syncthreads();
+  if (lane == 31) sw[wid] = inc;
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    const int s = sw[w];
+    if (w < wid) base += s;
+    tot += s;
+  }
+  total = tot;
+  return base + inc - v;
+}
+
+// ---- tile plan: per tile the sorted distinct units (its slots), per pixel
+// its slot
+__global__ void __launch_bounds__(NT) plan_tile_kernel(int H, int W, int P, int nTX, int nTY,
+                                                       const int32_t* __restrict__ unit,
+                                                       uint16_t* __restrict__ slot,
+                                                       int32_t* __restrict__ nslots,
+                                                       int32_t* __restrict__ tmp) {
+  __shared__ int32_t key[TPX];
+  __shared__ int sw[NT / 32];
+  const int t = blockIdx.x;
+  const Tile T = tile_of(t, H, W, nTX, nTY);
+  for (int e = threadIdx.x; e < TPX; e += NT) {
+    const int y = T.y0 + e / TX, x = T.x0 + e % TX;
+    int32_t k = INT32_MAX;
+    if (y < T.y1 && x < T.x1) {
+      const int32_t u = unit[pidx(P, y, x)];
+      if (u >= 0) k = u;
+    }
+    key[e] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= TPX; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < TPX; i += NT) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int32_t a = key[i], b = key[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            key[i] = b;
+            key[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // distinct values: thread owns 8 consecutive sorted entries
+  constexpr int PER = TPX / NT;
+  int32_t mine[PER];
+  int cnt = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = threadIdx.x * PER + q;
+    mine[q] = key[e];
+    const bool f = mine[q] != INT32_MAX && (e == 0 || mine[q] != key[e - 1]);
+    cnt += f;
+  }
+  int total = 0;
+  int pos = block_excl_scan(cnt, sw, total);
+  __syncthreads();  // every key read before the distinct list overwrites the front
+  // recompute the flags against the previous entry (held by this thread or
+  // the previous one) without re-reading the overwritten array
+  const int32_t prev_last = __shfl_up_sync(0xffffffffu, mine[PER - 1], 1);
+  __shared__ int32_t wlast[NT / 32];
+  if ((threadIdx.x & 31) == 31) wlast[threadIdx.x >> 5] = mine[PER - 1];
+  __syncthreads();
+  int32_t before = (threadIdx.x & 31) ? prev_last
+                                      : (threadIdx.x ? wlast[(threadIdx.x >> 5) - 1] : INT32_MIN);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int32_t v = mine[q];
+    if (v != INT32_MAX && v != before) {
+      key[pos] = v;
+      tmp[int64_t(t) * TPX + pos] = v;
+      ++pos;
+    }
+    before = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) nslots[t] = total;
+  for (int e = threadIdx.x; e < TPX; e += NT) {
+    const int y = T.y0 + e / TX, x = T.x0 + e % TX;
+    if (y >= T.y1 || x >= T.x1) continue;
+    const int64_t o = pidx(P, y, x);
+    const int32_t u = unit[o];
+    if (u < 0) continue;
+    int lo = 0, hi = total - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (key[mid] < u) lo = mid + 1;
+      else hi = mid;
+    }
+    slot[o] = uint16_t(lo);
+  }
+}
+
+__global__ void plan_copy_kernel(int ntiles, const int32_t* __restrict__ nslots,
+                                 const int32_t* __restrict__ base, const int32_t* __restrict__ tmp,
+                                 int32_t* __restrict__ slot_unit, int32_t* __restrict__ tile_flag) {
+  const int t = blockIdx.x;
+  if (t >= ntiles) return;
+  const int n = nslots[t];
+  if (threadIdx.x == 0) tile_flag[t] = n > 0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    slot_unit[base[t] + k] = tmp[int64_t(t) * TPX + k];
+}
+
+__global__ void tile_list_kernel(int ntiles, const int32_t* __restrict__ flag,
+                                 const int32_t* __restrict__ pos, int32_t* __restrict__ list) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+    if (flag[t]) list[pos[t]] = t;
+}
+
+// unit_pstart[u] = first position of unit u in the sorted slot keys
+__global__ void unit_bounds_kernel(const int32_t* __restrict__ skeys, int ns, int nu,
+                                   int32_t* __restrict__ pstart) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= nu; u += gridDim.x * blockDim.x) {
+    int lo = 0, hi = ns;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (skeys[mid] < u) lo = mid + 1;
+      else hi = mid;
+    }
+    pstart[u] = lo;
+  }
+}
+
+__global__ void unit_init_kernel(int nu, const int32_t* __restrict__ unit_comp,
+                                 const int32_t* __restrict__ comp_size,
+                                 const int32_t* __restrict__ pstart, int cg_max_iters,
+                                 uint8_t* __restrict__ status, uint8_t* __restrict__ upd,
+                                 int32_t* __restrict__ iters, int32_t* __restrict__ cap,
+                                 float* __restrict__ alpha_f, float* __restrict__ beta_f) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
+    const int c = unit_comp ? unit_comp[u] : u;
+    const int n = comp_size[c];
+    status[u] = pstart[u + 1] > pstart[u] ? U_ACTIVE : U_IDLE;
+    upd[u] = 0;
+    iters[u] = 0;
+    cap[u] = n > cg_max_iters ? n : cg_max_iters;
+    alpha_f[u] = 0.f;
+    beta_f[u] = 0.f;
+  }
+}
+
+// ------------------------------------------------------ level construction
+
+struct Level {
+  int n = 0;        // unknowns
+  int nact = 0;     // unknowns with a link (diag > 0)
+  int Hb = 0, Wb = 0;  // block grid per map
+  int64_t nblk = 0;
+  int32_t* bstart = nullptr;  // [nblk + 1]
+  int32_t* blk = nullptr;     // [n] block id
+  int32_t* unit = nullptr;    // [n]
+  int32_t* nbr = nullptr;     // [8][n]
+  float* cond = nullptr;      // [8][n]
+  float* dinv = nullptr;      // [n]
+  int32_t* parent = nullptr;  // [n] (-1: no coarser aggregate)
+  int32_t* child = nullptr;   // [4][n] (levels >= 2)
+  float* b = nullptr;         // [n]
+  float* e = nullptr;         // [n]
+  int32_t* cnt = nullptr;     // [nblk + 1] scratch (count per block)
+};
+
+// distinct values of up to 4 entries (-1 = none), ascending; returns count
+__device__ __forceinline__ int distinct4(int32_t v[4], int32_t out[4]) {
+  int n = 0;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    int32_t best = INT32_MAX;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (v[q] >= 0 && v[q] < best && (n == 0 || v[q] > out[n - 1])) best = v[q];
+    if (best == INT32_MAX) break;
+    out[n++] = best;
+  }
+  return n;
+}
+
+// level 1 from the pixel grid: count units per 2x2 block
+__global__ void l1_count_kernel(int B, int H, int W, int P, int Hb, int Wb,
+                                const int32_t* __restrict__ unit, int32_t* __restrict__ cnt) {
+  const int64_t nblk = int64_t(B) * Hb * Wb;
+  for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
+       bi += int64_t(gridDim.x) * blockDim.x) {
+    const int bx = int(bi % Wb);
+    const int64_t br = bi / Wb;
+    const int by = int(br % Hb), m = int(br / Hb);
+    int32_t v[4], d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int yy = 2 * by + (q >> 1), xx = 2 * bx + (q & 1);
+      v[q] = (yy < H && xx < W) ? unit[pidx(P, m * H + yy, xx)] : -1;
+    }
+    cnt[bi] = distinct4(v, d);
+  }
+}
+
+__global__ void l1_assign_kernel(int B, int H, int W, int P, int Hb, int Wb,
+                                 const int32_t* __restrict__ unit,
+                                 const int32_t* __restrict__ bstart, int32_t* __restrict__ blk,
+                                 int32_t* __restrict__ lunit, int32_t* __restrict__ par0) {
+  const int64_t nblk = int64_t(B) * Hb * Wb;
+  for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
+       bi += int64_t(gridDim.x) * blockDim.x) {
+    const int bx = int(bi % Wb);
+    const int64_t br = bi / Wb;
+    const int by = int(br % Hb), m = int(br / Hb);
+    int32_t v[4], d[4];
+    int64_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int yy = 2 * by + (q >> 1), xx = 2 * bx + (q & 1);
+      const bool in = yy < H && xx < W;
+      o[q] = in ? pidx(P, m * H + yy, xx) : -1;
+      v[q] = in ? unit[o[q]] : -1;
+    }
+    const int n = distinct4(v, d);
+    const int32_t s0 = bstart[bi];
+    for (int k = 0; k < n; ++k) {
+      blk[s0 + k] = int32_t(bi);
+      lunit[s0 + k] = d[k];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (v[q] < 0) continue;
+      int k = 0;
+      while (d[k] != v[q]) ++k;
+      par0[o[q]] = s0 + k;
+    }
+  }
+}
+
+// unknown of unit u in block bi of a level (-1 if none)
+__device__ __forceinline__ int32_t find_in_block(const int32_t* __restrict__ bstart,
+                                                 const int32_t* __restrict__ lunit, int64_t bi,
+                                                 int32_t u) {
+  const int32_t a = bstart[bi], b = bstart[bi + 1];
+  for (int32_t k = a; k < b; ++k) {
+    const int32_t v = lunit[k];
+    if (v == u) return k;
+    if (v > u) break;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void find_neighbours(const int32_t* __restrict__ bstart,
+                                                const int32_t* __restrict__ lunit, int32_t bi,
+                                                int Hb, int Wb, int32_t u, int32_t* __restrict__ nbr,
+                                                int n, int i) {
+  const int bx = bi % Wb;
+  const int br = bi / Wb;
+  const int by = br % Hb;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const int nx = bx + dir_dx(d), ny = by + dir_dy(d);
+    int32_t j = -1;
+    if (nx >= 0 && nx < Wb && ny >= 0 && ny < Hb)
+      j = find_in_block(bstart, lunit, int64_t(bi) + int64_t(dir_dy(d)) * Wb + dir_dx(d), u);
+    nbr[int64_t(d) * n + i] = j;
+  }
+}
+
+// level-1 links: neighbours + Galerkin conductances from the pixel stencil
+template <int CONN>
+__global__ void l1_links_kernel(int n, int H, int W, int P, int Hb, int Wb,
+                                const int32_t* __restrict__ bstart,
+                                const int32_t* __restrict__ blk, const int32_t* __restrict__ lunit,
+                                const int32_t* __restrict__ unit, const float* __restrict__ hw,
+                                const uint8_t* __restrict__ imask, int32_t* __restrict__ nbr,
+                                float* __restrict__ cond, float* __restrict__ dinv,
+                                int32_t* __restrict__ nact) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  int act = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t bi = blk[i], u = lunit[i];
+    find_neighbours(bstart, lunit, bi, Hb, Wb, u, nbr, n, i);
+    const int bx = bi % Wb;
+    const int br = bi / Wb;
+    const int by = br % Hb, m = br / Hb;
+    float c[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) c[d] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int yy = 2 * by + (q >> 1), xx = 2 * bx + (q & 1);
+      if (yy >= H || xx >= W) continue;
+      const int64_t o = pidx(P, m * H + yy, xx);
+      if (unit[o] != u) continue;
+      const uint8_t mk = imask[o];
+      const float h = hw[o];
+#pragma unroll
+      for (int bit = 0; bit < 8; ++bit) {
+        if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+        const int k = bit & 3;
+        const int du = bit < 4 ? fwd_du(CONN, k) : -fwd_du(CONN, k);
+        const int dv = bit < 4 ? fwd_dv(CONN, k) : -fwd_dv(CONN, k);
+        const int jy = yy + dv, jx = xx + du;
+        const int dbx = (jx >> 1) - bx, dby = (jy >> 1) - by;  // jx, jy >= 0 (edge inside the map)
+        if (dbx == 0 && dby == 0) continue;
+        c[dir_of(dbx, dby)] += h + hw[o + int64_t(dv) * P + du];
+      }
+    }
+    float diag = 0.f;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      cond[int64_t(d) * n + i] = c[d];
+      diag += c[d];
+    }
+    dinv[i] = diag > 0.f ? 1.0f / diag : 0.f;
+    act += diag > 0.f;
+  }
+  act = warp_sum_int(act);
+  if ((threadIdx.x & 31) == 0 && act) atomicAdd(nact, act);
+}
+
+// level l+1 from level l: count units (with links) over the 2x2 child blocks
+__device__ __forceinline__ int merge_children(const int32_t* __restrict__ bstart,
+                                              const int32_t* __restrict__ lunit,
+                                              const float* __restrict__ dinv, int64_t cb[4],
+                                              int32_t* __restrict__ out_units, int out_cap) {
+  // 4-way merge of the children blocks' sorted unit lists; only unknowns
+  // with a link take part (isolated ones have no coarser aggregate)
+  int32_t h[4], e[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    h[q] = cb[q] >= 0 ? bstart[cb[q]] : 0;
+    e[q] = cb[q] >= 0 ? bstart[cb[q] + 1] : 0;
+  }
+  int n = 0;
+  while (true) {
+    int32_t best = INT32_MAX;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      while (h[q] < e[q] && dinv[h[q]] == 0.f) ++h[q];
+      if (h[q] < e[q]) best = min(best, lunit[h[q]]);
+    }
+    if (best == INT32_MAX) break;
+    if (n < out_cap) out_units[n] = best;
+    ++n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (h[q] < e[q] && lunit[h[q]] == best) ++h[q];
+  }
+  return n;
+}
+
+__device__ __forceinline__ void child_blocks(int64_t bi, int Hb, int Wb, int Hc, int Wc,
+                                             int64_t cb[4]) {
+  const int bx = int(bi % Wb);
+  const int64_t br = bi / Wb;
+  const int by = int(br % Hb), m = int(br / Hb);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int cy = 2 * by + (q >> 1), cx = 2 * bx + (q & 1);
+    cb[q] = (cy < Hc && cx < Wc) ? (int64_t(m) * Hc + cy) * Wc + cx : -1;
+  }
+}
+
+__global__ void lc_count_kernel(int64_t nblk, int Hb, int Wb, int Hc, int Wc,
+                                const int32_t* __restrict__ cbstart,
+                                const int32_t* __restrict__ clunit,
+                                const float* __restrict__ cdinv, int32_t* __restrict__ cnt) {
+  for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
+       bi += int64_t(gridDim.x) * blockDim.x) {
+    int64_t cb[4];
+    child_blocks(bi, Hb, Wb, Hc, Wc, cb);
+    cnt[bi] = merge_children(cbstart, clunit, cdinv, cb, nullptr, 0);
+  }
+}
+
+__global__ void lc_assign_kernel(int64_t nblk, int Hb, int Wb, int Hc, int Wc,
+                                 const int32_t* __restrict__ cbstart,
+                                 const int32_t* __restrict__ clunit,
+                                 const float* __restrict__ cdinv,
+                                 const int32_t* __restrict__ bstart, int n,
+                                 int32_t* __restrict__ blk, int32_t* __restrict__ lunit,
+                                 int32_t* __restrict__ child, int32_t* __restrict__ cparent) {
+  for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
+       bi += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t s0 = bstart[bi], s1 = bstart[bi + 1];
+    if (s0 == s1) continue;
+    int64_t cb[4];
+    child_blocks(bi, Hb, Wb, Hc, Wc, cb);
+    int32_t h[4], e[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = cb[q] >= 0 ? cbstart[cb[q]] : 0;
+      e[q] = cb[q] >= 0 ? cbstart[cb[q] + 1] : 0;
+    }
+    for (int32_t k = s0; k < s1; ++k) {
+      int32_t best = INT32_MAX;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        while (h[q] < e[q] && cdinv[h[q]] == 0.f) ++h[q];
+        if (h[q] < e[q]) best = min(best, clunit[h[q]]);
+      }
+      blk[k] = int32_t(bi);
+      lunit[k] = best;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int32_t c = -1;
+        if (h[q] < e[q] && clunit[h[q]] == best) {
+          c = h[q];
+          cparent[c] = k;
+          ++h[q];
+        }
+        child[int64_t(q) * n + k] = c;
+      }
+    }
+  }
+}
+
+__global__ void lc_links_kernel(int n, int Hb, int Wb, const int32_t* __restrict__ bstart,
+                                const int32_t* __restrict__ blk,
+                                const int32_t* __restrict__ lunit,
+                                const int32_t* __restrict__ child, int nc,
+                                const int32_t* __restrict__ cnbr,
+                                const float* __restrict__ ccond,
+                                const int32_t* __restrict__ cparent, int32_t* __restrict__ nbr,
+                                float* __restrict__ cond, float* __restrict__ dinv,
+                                int32_t* __restrict__ nact) {
+  int act = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t bi = blk[i], u = lunit[i];
+    find_neighbours(bstart, lunit, bi, Hb, Wb, u, nbr, n, i);
+    const int bx = bi % Wb, by = (bi / Wb) % Hb;
+    float c[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) c[d] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t ch = child[int64_t(q) * n + i];
+      if (ch < 0) continue;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int32_t nb = cnbr[int64_t(k) * nc + ch];
+        if (nb < 0) continue;
+        const float ck = ccond[int64_t(k) * nc + ch];
+        if (ck == 0.f) continue;
+        const int32_t pj = cparent[nb];
+        if (pj < 0 || pj == i) continue;
+        const int32_t bj = blk[pj];
+        const int dbx = bj % Wb - bx, dby = (bj / Wb) % Hb - by;
+        c[dir_of(dbx, dby)] += ck;
+      }
+    }
+    float diag = 0.f;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      cond[int64_t(d) * n + i] = c[d];
+      diag += c[d];
+    }
+    dinv[i] = diag > 0.f ? 1.0f / diag : 0.f;
+    act += diag > 0.f;
+  }
+  act = warp_sum_int(act);
+  if ((threadIdx.x & 31) == 0 && act) atomicAdd(nact, act);
+}
+
+// ------------------------------------------------------------ V-cycle
+
+// down: b_{l+1}[P] = sum over children c of (b_c - A x1)_c, x1 = OM dinv b
+__global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __restrict__ child,
+                                                   int n, const int32_t* __restrict__ nbr,
+                                                   const float* __restrict__ cond,
+                                                   const float* __restrict__ dinv,
+                                                   const float* __restrict__ b,
+                                                   float* __restrict__ b1) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += gridDim.x * blockDim.x) {
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t c = child[int64_t(q) * n1 + i];
+      if (c < 0) continue;
+      const float bc = b[c];
+      const float x1 = OM * dinv[c] * bc;
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int32_t j = nbr[int64_t(k) * n + c];
+        if (j < 0) continue;
+        acc += cond[int64_t(k) * n + c] * (x1 - OM * dinv[j] * b[j]);
+      }
+      sum += bc - acc;
+    }
+    b1[i] = sum;
+  }
+}
+
+// up: e = x2 + OM dinv (b - A x2), x2 = OM dinv b + OC e_{l+1}[parent]
+template <bool COARSE>
+__global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restrict__ nbr,
+                                                 const float* __restrict__ cond,
+                                                 const float* __restrict__ dinv,
+                                                 const float* __restrict__ b,
+                                                 const int32_t* __restrict__ parent,
+                                                 const float* __restrict__ e1,
+                                                 float* __restrict__ e) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float di = dinv[i];
+    if (di == 0.f) {
+      e[i] = 0.f;
+      continue;
+    }
+    auto x2 = [&](int j) {
+      float v = OM * dinv[j] * b[j];
+      if (COARSE) {
+        const int32_t pj = parent[j];
+        if (pj >= 0) v += OC * e1[pj];
+      }
+      return v;
+    };
+    const float xi = x2(i);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int32_t j = nbr[int64_t(k) * n + i];
+      if (j < 0) continue;
+      acc += cond[int64_t(k) * n + i] * (xi - x2(j));
+    }
+    e[i] = xi + OM * di * (b[i] - acc);
+  }
+}
+
+// ---- fine passes
+
+struct FineArgs {
+  int H, W, P, nTX, nTY;
+  const int32_t* tiles;  // active tiles
+  float *x, *r, *p, *s, *u, *w;
+  const float *hw, *dinv;
+  const uint8_t* imask;
+  const int32_t* par0;
+  const uint16_t* slot;
+  const int32_t* slot_base;  // [ntiles]
+  const int32_t* slot_unit;  // [NS]
+  const uint8_t* status;
+  const uint8_t* upd;
+  const float *alpha, *beta;
+  float* b1;       // level-1 right-hand side
+  const float* e1; // level-1 correction
+  double* partial; // [NS][NPART]
+  const float* umean;  // per unit: mean of u (removed from p: the preconditioned
+                       // direction is kept orthogonal to the unit's null space)
+};
+
+// stage a (TY + 2h) x (TX + 2h) window of a padded plane into shared memory
+template <int HALO, class T>
+__device__ __forceinline__ void stage(T* __restrict__ sm, const T* __restrict__ g, int P, int y0,
+                                      int x0) {
+  constexpr int SWD = TX + 2 * HALO, SHT = TY + 2 * HALO;
+  for (int e = threadIdx.x; e < SWD * SHT; e += NT) {
+    const int ry = e / SWD, rx = e - ry * SWD;
+    sm[e] = g[pidx(P, y0 - HALO + ry, x0 - HALO + rx)];
+  }
+}
+
+// is every unit of the tile finished?  (then its passes are skipped)
+__device__ __forceinline__ bool tile_done(const FineArgs& a, int t) {
+  const int s0 = a.slot_base[t], s1 = a.slot_base[t + 1];
+  for (int k = s0; k < s1; ++k)
+    if (a.status[a.slot_unit[k]] == U_ACTIVE) return false;
+  return true;
+}
+
+// r after the pending update of its unit: r - alpha (w + beta s)
+__device__ __forceinline__ float r_new(float r, float w, float s, float al, float bt) {
+  return r - al * (w + bt * s);
+}
+
+// Pass A: pending CG update, pre-smoothing of the new r, residual,
+// restriction to level 1.
+template <int CONN>
+__global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ FineArgs a) {
+  constexpr int H1 = 1, S1 = TX + 2 * H1, N1 = S1 * (TY + 2 * H1);
+  __shared__ float sR[N1], sW[N1], sS[N1], sD[N1], sH[N1];
+  const int t = a.tiles[blockIdx.x];
+  if (tile_done(a, t)) return;
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
+  stage<H1>(sR, a.r, a.P, T.y0, T.x0);
+  stage<H1>(sW, a.w, a.P, T.y0, T.x0);
+  stage<H1>(sS, a.s, a.P, T.y0, T.x0);
+  stage<H1>(sD, a.dinv, a.P, T.y0, T.x0);
+  stage<H1>(sH, a.hw, a.P, T.y0, T.x0);
+  __syncthreads();
+  const int base = a.slot_base[t];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int by = wid + half * (NT / 32);  // block row 0..15
+    const int bx = lane;                    // block column 0..31
+    float res[4];
+    int32_t par[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ly = 2 * by + (q >> 1), lx = 2 * bx + (q & 1);
+      const int y = T.y0 + ly, x = T.x0 + lx;
+      res[q] = 0.f;
+      par[q] = -1;
+      if (y >= T.y1 || x >= T.x1) continue;
+      const int64_t o = pidx(a.P, y, x);
+      const uint16_t sl = a.slot[o];
+      if (sl == NOSLOT) continue;
+      const int32_t un = a.slot_unit[base + sl];
+      const bool up = a.upd[un] != 0;
+      const float al = a.alpha[un], bt = a.beta[un];
+      const int c = (ly + H1) * S1 + lx + H1;
+      float ri = sR[c];
+      if (up) {
+        const float si = sW[c] + bt * sS[c];
+        const float pi = (a.u[o] - a.umean[un]) + bt * a.p[o];
+        a.p[o] = pi;
+        a.s[o] = si;
+        a.x[o] = a.x[o] + al * pi;
+        ri = r_new(ri, sW[c], sS[c], al, bt);
+        a.r[o] = ri;
+      }
+      const float x1i = OM * sD[c] * ri;
+      const float hi = sH[c];
+      const uint8_t mk = a.imask[o];
+      float acc = 0.f;
+#pragma unroll
+      for (int bit = 0; bit < 8; ++bit) {
+        if ((bit & 3) >= (CONN == 8 ? 4 : 2) || !((mk >> bit) & 1)) continue;
+        const int j = c + nb_off<CONN>(bit, S1);
+        float rj = sR[j];
+        if (up) rj = r_new(rj, sW[j], sS[j], al, bt);
+        acc += (hi + sH[j]) * (x1i - OM * sD[j] * rj);
+      }
+      res[q] = ri - acc;
+      par[q] = a.par0[o];
+    }
+    // restriction: one write per distinct level-1 aggregate of the block
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (par[q] < 0) continue;
+      bool first = true;
+#pragma unroll
+      for (int q2 = 0; q2 < q; ++q2)
+        if (par[q2] == par[q]) first = false;
+      if (!first) continue;
+      float sum = 0.f;
+#pragma unroll
+      for (int q2 = q; q2 < 4; ++q2)
+        if (par[q2] == par[q]) sum += res[q2];
+      a.b1[par[q]] = sum;
+    }
+  }
+}
+
+// Pass B: prolongation + post-smoothing -> u = M r; w = A u; per-slot dots
+// (r,u), (w,u), (r,r).
+constexpr int PB_S2 = TX + 4, PB_N2 = PB_S2 * (TY + 4);
+constexpr int PB_S1 = TX + 2, PB_N1 = PB_S1 * (TY + 2);
+constexpr size_t kPassBSmem = size_t(PB_N2) * 4 * sizeof(float) + size_t(PB_N1) * sizeof(float) +
+                              size_t(TPX) * sizeof(float) + size_t(TPX) * sizeof(uint16_t) +
+                              size_t(PB_N1) * sizeof(uint8_t);
+
+template <int CONN>
+__global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ FineArgs a) {
+  constexpr int H2 = 2, S2 = PB_S2, N2 = PB_N2;
+  constexpr int H1 = 1, S1 = PB_S1, N1 = PB_N1;
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* sR = reinterpret_cast<float*>(smem_raw);
+  float* sD = sR + N2;
+  float* sH = sD + N2;
+  float* sX2 = sH + N2;
+  float* sX3 = sX2 + N2;
+  float* sWv = sX3 + N1;
+  uint16_t* sSl = reinterpret_cast<uint16_t*>(sWv + TPX);
+  uint8_t* sM = reinterpret_cast<uint8_t*>(sSl + TPX);
+  const int t = a.tiles[blockIdx.x];
+  if (tile_done(a, t)) return;
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
+  // 2-pixel halo: r, dinv, hw and the prolongated pre-smoothed state
+  // x2 = OM dinv r + OC e1[par0]
+  for (int e = threadIdx.x; e < N2; e += NT) {
+    const int ry = e / S2, rx = e - ry * S2;
+    const int64_t o = pidx(a.P, T.y0 - H2 + ry, T.x0 - H2 + rx);
+    const float rv = a.r[o], dv = a.dinv[o];
+    const int32_t pj = a.par0[o];
+    sR[e] = rv;
+    sD[e] = dv;
+    sH[e] = a.hw[o];
+    sX2[e] = OM * dv * rv + (pj >= 0 ? OC * a.e1[pj] : 0.f);
+  }
+  stage<H1>(sM, a.imask, a.P, T.y0, T.x0);
+  __syncthreads();
+  // post-smoothing on the tile + 1-pixel ring
+  for (int e = threadIdx.x; e < N1; e += NT) {
+    const int ry = e / S1, rx = e - ry * S1;
+    const int c = (ry + 1) * S2 + rx + 1;  // same pixel in the 2-halo arrays
+    const uint8_t mk = sM[e];
+    float v = sX2[c];
+    if (mk) {
+      const float hi = sH[c];
+      float acc = 0.f;
+#pragma unroll
+      for (int bit = 0; bit < 8; ++bit) {
+        if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+        const int j = c + nb_off<CONN>(bit, S2);
+        acc += (hi + sH[j]) * (v - sX2[j]);
+      }
+      v += OM * sD[c] * (sR[c] - acc);
+    } else {
+      v = 0.f;
+    }
+    sX3[e] = v;
+  }
+  __syncthreads();
+  // u, w on the tile
+  for (int e = threadIdx.x; e < TPX; e += NT) {
+    const int ly = e / TX, lx = e - ly * TX;
+    const int y = T.y0 + ly, x = T.x0 + lx;
+    uint16_t sl = NOSLOT;
+    float wv = 0.f;
+    if (y < T.y1 && x < T.x1) {
+      const int64_t o = pidx(a.P, y, x);
+      sl = a.slot[o];
+      if (sl != NOSLOT) {
+        const int c1 = (ly + 1) * S1 + lx + 1;
+        const int c2 = (ly + 2) * S2 + lx + 2;
+        const uint8_t mk = sM[c1];
+        const float ui = sX3[c1], hi = sH[c2];
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {
+          if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+          wv += (hi + sH[c2 + nb_off<CONN>(bit, S2)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S1)]);
+        }
+        a.u[o] = ui;
+        a.w[o] = wv;
+      }
+    }
+    sSl[e] = sl;
+    sWv[e] = wv;
+  }
+  __syncthreads();
+  // per-slot dots in a fixed order: warp w sums slots w, w+8, ... over the
+  // tile's pixels lane-strided, then a fixed xor tree
+  const int nsl = a.slot_base[t + 1] - a.slot_base[t];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int sl = wid; sl < nsl; sl += NT / 32) {
+    double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int e = lane; e < TPX; e += 32) {
+      if (sSl[e] != sl) continue;
+      const int ly = e / TX, lx = e - ly * TX;
+      const double ui = double(sX3[(ly + 1) * S1 + lx + 1]);
+      const double ri = double(sR[(ly + 2) * S2 + lx + 2]);
+      const double wi = double(sWv[e]);
+      d[0] += ri * ui;
+      d[1] += wi * ui;
+      d[2] += ri * ri;
+      d[3] += ui;
+      d[4] += ri;
+      d[5] += wi;
+    }
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) d[k] = warp_sum(d[k]);
+    if (lane == 0) {
+      double* pp = a.partial + NPART * int64_t(a.slot_base[t] + sl);
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) pp[k] = d[k];
+    }
+  }
+}
+
+// ---- per-unit scalars (warp per unit): scipy's stop test on the recursive
+// residual, then the Chronopoulos-Gear alpha / beta
+struct ScalarArgs {
+  int nu;
+  const int32_t* pstart;
+  const int32_t* plist;
+  const double* partial;
+  const double* unit_n;  // pixels per unit
+  double rtol;
+  uint8_t* status;
+  uint8_t* upd;
+  int32_t* iters;
+  const int32_t* cap;
+  double* tol2;
+  double* gprev;
+  double* aprev;
+  float* alpha;
+  float* beta;
+  float* umean;
+  int32_t* nactive;
+  int trace_unit;  // debug: print this unit's scalars every iteration (-1: off)
+};
+
+// The unit's Laplacian is singular (constants); float32 roundoff leaves
+// O(eps) null-space components in r and, amplified by the smoother, in
+// u = M r.  They carry no information (CG from 0 lives in range(A)) but
+// would stall / destabilise the recursion once ||r|| nears 1e-6 ||b||, so
+// the preconditioned vector is projected on range(A): u' = u - mean(u)
+// (w = A u' = A u in difference form), and the stop test uses the range
+// part of r -- the residual float64 arithmetic (the reference) would have.
+__global__ void __launch_bounds__(256) scalar_kernel(const __grid_constant__ ScalarArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  int act = 0;
+  for (int u = gw; u < a.nu; u += nw) {
+    if (a.status[u] != U_ACTIVE) continue;  // warp-uniform
+    double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = a.pstart[u] + lane; k < a.pstart[u + 1]; k += 32) {
+      const double* pp = a.partial + NPART * int64_t(a.plist[k]);
+#pragma unroll
+      for (int q = 0; q < NPART; ++q) d[q] += pp[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NPART; ++q) d[q] = warp_sum(d[q]);
+    if (lane == 0) {
+      const double n = a.unit_n[u];
+      const double cu = d[3] / n;
+      const double g = d[0] - cu * d[4];
+      const double dl = d[1] - cu * d[5];
+      const double rr = fmax(d[2] - d[4] * d[4] / n, 0.0);
+      const int it = a.iters[u];
+      if (u == a.trace_unit)
+        printf("mg unit %d it %d (r,u')=%.6e (w,u')=%.6e |r|=%.6e |r_range|=%.6e mean u=%.3e\n",
+               u, it, g, dl, sqrt(d[2]), sqrt(rr), cu);
+      if (it == 0) a.tol2[u] = rr;  // ||b||^2 (r = b before the first update)
+      const double tol = a.rtol * sqrt(a.tol2[u]);
+      uint8_t st = U_ACTIVE, up = 0;
+      if (it >= a.cap[u]) {  // scipy: no test after the last allowed update
+        st = U_CAPPED;
+      } else if (rr == 0.0 || sqrt(rr) < tol) {
+        st = U_CONV;
+      } else {
+        double al, bt;
+        if (it == 0) {
+          bt = 0.0;
+          al = g / dl;
+        } else {
+          bt = g / a.gprev[u];
+          al = g / (dl - bt * g / a.aprev[u]);
+        }
+        if (!(al > 0.0) || !isfinite(al) || !isfinite(bt)) {
+          st = U_CAPPED;  // breakdown (never seen): report like a cap
+        } else {
+          a.gprev[u] = g;
+          a.aprev[u] = al;
+          a.alpha[u] = float(al);
+          a.beta[u] = float(bt);
+          a.umean[u] = float(cu);
+          a.iters[u] = it + 1;
+          up = 1;
+          ++act;
+        }
+      }
+      a.status[u] = st;
+      a.upd[u] = up;
+    }
+  }
+  act = warp_sum_int(act);
+  if (lane == 0 && act) atomicAdd(a.nactive, act);
+}
+
+// ---- output: x minus its per-unit mean (the gauge of CG from x0 = 0)
+__global__ void __launch_bounds__(NT) xsum_kernel(const __grid_constant__ FineArgs a) {
+  __shared__ uint16_t sSl[TPX];
+  __shared__ float sX[TPX];
+  const int t = a.tiles[blockIdx.x];
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
+  for (int e = threadIdx.x; e < TPX; e += NT) {
+    const int y = T.y0 + e / TX, x = T.x0 + e % TX;
+    uint16_t sl = NOSLOT;
+    float xv = 0.f;
+    if (y < T.y1 && x < T.x1) {
+      const int64_t o = pidx(a.P, y, x);
+      sl = a.slot[o];
+      xv = a.x[o];
+    }
+    sSl[e] = sl;
+    sX[e] = xv;
+  }
+  __syncthreads();
+  const int nsl = a.slot_base[t + 1] - a.slot_base[t];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int sl = wid; sl < nsl; sl += NT / 32) {
+    double sx = 0.0, sn = 0.0;
+    for (int e = lane; e < TPX; e += 32) {
+      if (sSl[e] != sl) continue;
+      sx += double(sX[e]);
+      sn += 1.0;
+    }
+    sx = warp_sum(sx);
+    sn = warp_sum(sn);
+    if (lane == 0) {
+      double* pp = a.partial + NPART * int64_t(a.slot_base[t] + sl);
+      pp[0] = sx;
+      pp[1] = sn;
+    }
+  }
+}
+
+// per unit: mean of x (pp[0] / pp[1]) and, if n_out, its pixel count
+__global__ void unit_mean_kernel(int nu, const int32_t* __restrict__ pstart,
+                                 const int32_t* __restrict__ plist,
+                                 const double* __restrict__ partial, double* __restrict__ mean,
+                                 double* __restrict__ n_out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int u = gw; u < nu; u += nw) {
+    double sx = 0.0, sn = 0.0;
+    for (int k = pstart[u] + lane; k < pstart[u + 1]; k += 32) {
+      const double* pp = partial + NPART * int64_t(plist[k]);
+      sx += pp[0];
+      sn += pp[1];
+    }
+    sx = warp_sum(sx);
+    sn = warp_sum(sn);
+    if (lane == 0) {
+      mean[u] = sn > 0.0 ? sx / sn : 0.0;
+      if (n_out) n_out[u] = sn;
+    }
+  }
+}
+
+__global__ void output_kernel(int W, int P, int64_t npix, const float* __restrict__ x,
+                              const int32_t* __restrict__ unit, const double* __restrict__ mean,
+                              double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = pidx(P, int(i / W), int(i % W));
+    const int32_t u = unit[o];
+    z[i] = u >= 0 ? double(x[o]) - mean[u] : 0.0;
+  }
+}
+
+__global__ void comp_out_kernel(int nu, const int32_t* __restrict__ unit_comp,
+                                const uint8_t* __restrict__ status,
+                                const int32_t* __restrict__ iters,
+                                const int32_t* __restrict__ pstart,
+                                int32_t* __restrict__ comp_iters, int32_t* __restrict__ comp_status,
+                                int32_t* __restrict__ max_iters) {
+  int mx = 0;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
+    if (pstart[u + 1] == pstart[u]) continue;
+    const int c = unit_comp ? unit_comp[u] : u;
+    const int it = iters[u];
+    atomicMax(comp_iters + c, it);
+    if (status[u] == U_CAPPED) atomicMax(comp_status + c, 1);
+    mx = max(mx, it);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_iters, mx);
+}
+
+}  // namespace mg
+}  // namespace ni
+
+// ================================================================== host
+
+using namespace ni;
+using namespace ni::mg;
+
+namespace {
+
+struct MgFixed {
+  float *x, *r, *p, *s, *u, *w, *hw, *dinv;
+  uint8_t* imask;
+  int32_t *par0, *unit;
+  uint16_t* slot;
+  int32_t *comp_size, *nslots, *slot_base, *tile_flag, *tile_pos, *tiles, *tmp;
+  int32_t *cc_parent, *cc_flag, *cc_rank, *unit_comp;
+  int32_t* counters;  // [0] missing, [1] NS, [2] NA, [3] NU, [4] level n, [5] nact, [6] active,
+                      // [7] max iters
+  void* scan_ws;
+};
+
+void carve_fixed(Carver& c, MgFixed& f, const Geo& g, int count) {
+  const int64_t npad = g.npad;
+  f.x = c.take<float>(npad);
+  f.r = c.take<float>(npad);
+  f.p = c.take<float>(npad);
+  f.s = c.take<float>(npad);
+  f.u = c.take<float>(npad);
+  f.w = c.take<float>(npad);
+  f.hw = c.take<float>(npad);
+  f.dinv = c.take<float>(npad);
+  f.imask = c.take<uint8_t>(npad);
+  f.par0 = c.take<int32_t>(npad);
+  f.unit = c.take<int32_t>(npad);
+  f.slot = c.take<uint16_t>(npad);
+  f.comp_size = c.take<int32_t>(count + 1);
+  f.nslots = c.take<int32_t>(g.ntiles + 1);
+  f.slot_base = c.take<int32_t>(g.ntiles + 1);
+  f.tile_flag = c.take<int32_t>(g.ntiles + 1);
+  f.tile_pos = c.take<int32_t>(g.ntiles + 1);
+  f.tiles = c.take<int32_t>(g.ntiles + 1);
+  f.tmp = c.take<int32_t>(int64_t(g.ntiles) * TPX);
+  f.cc_parent = c.take<int32_t>(g.npix);
+  f.cc_flag = c.take<int32_t>(g.npix + 1);
+  f.cc_rank = c.take<int32_t>(g.npix + 1);
+  f.unit_comp = c.take<int32_t>(g.npix + 1);
+  f.counters = c.take<int32_t>(16);
+  const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(g.npix + 1, g.ntiles + 1),
+                                           int64_t(count) + 1);
+  f.scan_ws = c.take<char>(scan_ws_bytes(scan_n));
+}
+
+// bytes of one coarse unknown: blk, unit, nbr[8], cond[8], dinv, parent,
+// child[4], b, e + its share of the block table
+constexpr int64_t kBytesPerUnknown = 4 * (2 + 8 + 8 + 1 + 1 + 4 + 2);
+
+int64_t level_estimate(const Geo& g) {
+  // ~ npix/4 * 4/3 over all levels, + boundary aggregates and block tables
+  return g.npix / 2 + 65536;
+}
+
+void carve_level(Carver& c, Level& L, int n, bool children) {
+  L.blk = c.take<int32_t>(n + 1);
+  L.unit = c.take<int32_t>(n + 1);
+  L.nbr = c.take<int32_t>(8 * int64_t(n) + 1);
+  L.cond = c.take<float>(8 * int64_t(n) + 1);
+  L.dinv = c.take<float>(n + 1);
+  L.parent = c.take<int32_t>(n + 1);
+  L.child = children ? c.take<int32_t>(4 * int64_t(n) + 1) : nullptr;
+  L.b = c.take<float>(n + 1);
+  L.e = c.take<float>(n + 1);
+}
+
+int grid_for(int64_t n, int per = 256) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, int64_t(kSMs) * 32)));
+}
+
+}  // namespace
+
+extern "C" int ni_fill_mg_workspace_size(int B, int H, int W, int connectivity, int count,
+                                         size_t* bytes) {
+  NI_CHECK_ARG(bytes, "null pointer");
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  const Geo g = make_geo(B, H, W);
+  Sizer s;
+  MgFixed f;
+  carve_fixed(s, f, g, count);
+  // slot / unit arrays (estimates; ni_fill_mg reports the exact need)
+  const int64_t ns = int64_t(g.ntiles) * 4 + 1024;
+  s.take<int32_t>(ns * 4);
+  s.take<double>(ns * 3);
+  s.take<char>(int64_t(count + 1) * 64);
+  s.take<char>(level_estimate(g) * kBytesPerUnknown + g.npix * 2 + (1 << 20));
+  *bytes = s.used;
+  return NI_OK;
+}
+
+extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_a,
+                          const double* omega_b, const double* gamma, const uint8_t* eflags,
+                          int B, int H, int W, int connectivity, int model, double cg_tol,
+                          int cg_max_iters, double* z_out, int32_t* comp_iters,
+                          int32_t* comp_status, void* workspace, size_t workspace_bytes,
+                          size_t* needed_bytes, ni_stream_t stream) {
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  NI_CHECK_ARG(model == 0 || (model == 1 && connectivity == 4), "bad model/connectivity");
+  NI_CHECK_ARG(cg_tol > 0, "cg_tol must be positive");
+  NI_CHECK_ARG(count >= 0, "count must be non-negative");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo g = make_geo(B, H, W);
+  Carver cv(workspace, workspace_bytes);
+  MgFixed f;
+  carve_fixed(cv, f, g, count);
+  auto too_small = [&](size_t extra) {
+    if (needed_bytes) *needed_bytes = cv.used + extra;
+    set_error("ni_fill_mg: workspace too small (%zu < %zu)", workspace_bytes, cv.used + extra);
+    return NI_ERR_WORKSPACE;
+  };
+  if (!workspace || !cv.ok())
+    return too_small(size_t(level_estimate(g) * kBytesPerUnknown + g.npix * 2));
+  cudaEvent_t e0, e1;
+  NI_CUDA_TRY(cudaEventCreateWithFlags(&e0, cudaEventDefault));
+  NI_CUDA_TRY(cudaEventCreateWithFlags(&e1, cudaEventDefault));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evg{e0, e1};
+  const int npb = grid_for(g.npix);
+  const size_t npad = size_t(g.npad);
+  // ---- fine planes
+  for (float* pl : {f.x, f.r, f.p, f.s, f.u, f.w, f.hw, f.dinv})
+    NI_CUDA_TRY(cudaMemsetAsync(pl, 0, npad * sizeof(float), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.imask, 0, npad, st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.par0, 0xff, npad * sizeof(int32_t), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.unit, 0xff, npad * sizeof(int32_t), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.slot, 0xff, npad * sizeof(uint16_t), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.comp_size, 0, sizeof(int32_t) * (count + 1), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.counters, 0, sizeof(int32_t) * 16, st));
+#define NI_MG_PREP(CONN, MODEL)                                                                  \
+  NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<npb, 256, 0, st>>>(                             \
+                         labels, omega_a, omega_b, gamma, eflags, H, W, g.P, g.npix, f.hw, f.r, \
+                         f.imask, f.comp_size, f.counters + 0)
+  if (connectivity == 8) NI_MG_PREP(8, 0);
+  else if (model == 0) NI_MG_PREP(4, 0);
+  else NI_MG_PREP(4, 1);
+#undef NI_MG_PREP
+  NI_LAUNCH_CHECK();
+  if (connectivity == 8)
+    NI_COUNT_LAUNCH(), dinv_kernel<8><<<npb, 256, 0, st>>>(H, W, g.P, g.npix, f.hw, f.imask, f.dinv);
+  else
+    NI_COUNT_LAUNCH(), dinv_kernel<4><<<npb, 256, 0, st>>>(H, W, g.P, g.npix, f.hw, f.imask, f.dinv);
+  NI_LAUNCH_CHECK();
+  int32_t hc[16];
+  NI_CUDA_TRY(cudaMemcpyAsync(hc, f.counters, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  NI_CUDA_TRY(cudaStreamSynchronize(st));
+  // ---- solve units
+  int NU = count;
+  const int32_t* unit_comp = nullptr;
+  if (hc[0] == 0) {
+    NI_COUNT_LAUNCH(), unit_from_label_kernel<<<npb, 256, 0, st>>>(labels, H, W, g.P, g.npix,
+                                                                  f.imask, f.unit);
+    NI_LAUNCH_CHECK();
+  } else {
+    NI_COUNT_LAUNCH(), cc_init_kernel<<<npb, 256, 0, st>>>(W, g.P, g.npix, f.imask, f.cc_parent);
+    NI_LAUNCH_CHECK();
+    if (connectivity == 8)
+      NI_COUNT_LAUNCH(), cc_union_kernel<8><<<npb, 256, 0, st>>>(W, g.P, g.npix, f.imask, f.cc_parent);
+    else
+      NI_COUNT_LAUNCH(), cc_union_kernel<4><<<npb, 256, 0, st>>>(W, g.P, g.npix, f.imask, f.cc_parent);
+    NI_LAUNCH_CHECK();
+    NI_COUNT_LAUNCH(), cc_flatten_kernel<<<npb, 256, 0, st>>>(g.npix, f.cc_parent, f.cc_flag);
+    NI_LAUNCH_CHECK();
+    NI_TRY(exclusive_scan_i32(f.cc_flag, f.cc_rank, g.npix, f.counters + 3, f.scan_ws, st));
+    NI_COUNT_LAUNCH(), cc_label_kernel<<<npb, 256, 0, st>>>(labels, W, g.P, g.npix, f.cc_parent,
+                                                           f.cc_rank, f.unit, f.unit_comp);
+    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemcpyAsync(&NU, f.counters + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    NI_CUDA_TRY(cudaStreamSynchronize(st));
+    unit_comp = f.unit_comp;
+  }
+  // ---- tile plan (the scans run over n + 1 entries: the last count is 0)
+  NI_CUDA_TRY(cudaMemsetAsync(f.nslots + g.ntiles, 0, sizeof(int32_t), st));
+  NI_COUNT_LAUNCH(), plan_tile_kernel<<<g.ntiles, NT, 0, st>>>(H, W, g.P, g.nTX, g.nTY, f.unit,
+                                                              f.slot, f.nslots, f.tmp);
+  NI_LAUNCH_CHECK();
+  NI_TRY(exclusive_scan_i32(f.nslots, f.slot_base, g.ntiles + 1, f.counters + 1, f.scan_ws, st));
+  NI_CUDA_TRY(cudaMemcpyAsync(hc + 1, f.counters + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  NI_CUDA_TRY(cudaStreamSynchronize(st));
+  const int NS = hc[1];
+  // slot / unit arrays
+  int32_t* slot_unit = cv.take<int32_t>(NS + 1);
+  int32_t* slot_idx = cv.take<int32_t>(NS + 1);
+  int32_t* skeys = cv.take<int32_t>(NS + 1);
+  int32_t* plist = cv.take<int32_t>(NS + 1);
+  double* partial = cv.take<double>(NPART * int64_t(NS) + NPART);
+  int32_t* pstart = cv.take<int32_t>(NU + 2);
+  uint8_t* ustatus = cv.take<uint8_t>(NU + 1);
+  uint8_t* uupd = cv.take<uint8_t>(NU + 1);
+  int32_t* uiters = cv.take<int32_t>(NU + 1);
+  int32_t* ucap = cv.take<int32_t>(NU + 1);
+  double* utol2 = cv.take<double>(NU + 1);
+  double* ugprev = cv.take<double>(NU + 1);
+  double* uaprev = cv.take<double>(NU + 1);
+  double* umean = cv.take<double>(NU + 1);
+  float* ualpha = cv.take<float>(NU + 1);
+  float* ubeta = cv.take<float>(NU + 1);
+  float* uumean = cv.take<float>(NU + 1);
+  double* unit_n = cv.take<double>(NU + 1);
+  size_t sort_bytes = 0;
+  NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, std::max(NS, 1)));
+  void* sort_ws = cv.take<char>(sort_bytes + 256);
+  if (!cv.ok())
+    return too_small(size_t(level_estimate(g) * kBytesPerUnknown + g.npix * 2));
+  NI_COUNT_LAUNCH(), plan_copy_kernel<<<g.ntiles, 128, 0, st>>>(g.ntiles, f.nslots, f.slot_base,
+                                                               f.tmp, slot_unit, f.tile_flag);
+  NI_LAUNCH_CHECK();
+  NI_TRY(exclusive_scan_i32(f.tile_flag, f.tile_pos, g.ntiles, f.counters + 2, f.scan_ws, st));
+  NI_COUNT_LAUNCH(), tile_list_kernel<<<grid_for(g.ntiles), 256, 0, st>>>(g.ntiles, f.tile_flag,
+                                                                         f.tile_pos, f.tiles);
+  NI_LAUNCH_CHECK();
+  if (NS > 0) {
+    NI_COUNT_LAUNCH(), iota_kernel<<<grid_for(NS), 256, 0, st>>>(slot_idx, NS);
+    NI_LAUNCH_CHECK();
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) <= NU) ++end_bit;
+    size_t sb = sort_bytes;
+    NI_CUDA_TRY(cub::DeviceRadixSort::SortPairs(sort_ws, sb, slot_unit, skeys, slot_idx, plist,
+                                                NS, 0, end_bit, st));
+  }
+  NI_COUNT_LAUNCH(), unit_bounds_kernel<<<grid_for(NU + 1), 256, 0, st>>>(skeys, NS, NU, pstart);
+  NI_LAUNCH_CHECK();
+  if (NU > 0) {
+    NI_COUNT_LAUNCH(), unit_init_kernel<<<grid_for(NU), 256, 0, st>>>(
+                           NU, unit_comp, f.comp_size, pstart, cg_max_iters, ustatus, uupd,
+                           uiters, ucap, ualpha, ubeta);
+    NI_LAUNCH_CHECK();
+  }
+  NI_CUDA_TRY(cudaMemcpyAsync(hc + 2, f.counters + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  NI_CUDA_TRY(cudaStreamSynchronize(st));
+  const int NA = hc[2];
+  // ---- hierarchy
+  Level lev[MAXLEV + 1];
+  int L = 0;
+  if (NA > 0) {
+    Level& L1 = lev[1];
+    L1.Hb = div_up(H, 2);
+    L1.Wb = div_up(W, 2);
+    L1.nblk = int64_t(B) * L1.Hb * L1.Wb;
+    L1.bstart = cv.take<int32_t>(L1.nblk + 1);
+    L1.cnt = cv.take<int32_t>(L1.nblk + 1);
+    if (!cv.ok()) return too_small(size_t(level_estimate(g) * kBytesPerUnknown));
+    NI_CUDA_TRY(cudaMemsetAsync(L1.cnt + L1.nblk, 0, sizeof(int32_t), st));
+    NI_COUNT_LAUNCH(), l1_count_kernel<<<grid_for(L1.nblk), 256, 0, st>>>(B, H, W, g.P, L1.Hb,
+                                                                         L1.Wb, f.unit, L1.cnt);
+    NI_LAUNCH_CHECK();
+    NI_TRY(exclusive_scan_i32(L1.cnt, L1.bstart, L1.nblk + 1, f.counters + 4, f.scan_ws, st));
+    NI_CUDA_TRY(cudaMemcpyAsync(&L1.n, f.counters + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    NI_CUDA_TRY(cudaStreamSynchronize(st));
+    carve_level(cv, L1, L1.n, false);
+    if (!cv.ok()) return too_small(size_t(level_estimate(g) * kBytesPerUnknown));
+    NI_COUNT_LAUNCH(), l1_assign_kernel<<<grid_for(L1.nblk), 256, 0, st>>>(
+                           B, H, W, g.P, L1.Hb, L1.Wb, f.unit, L1.bstart, L1.blk, L1.unit, f.par0);
+    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemsetAsync(L1.parent, 0xff, sizeof(int32_t) * (L1.n + 1), st));
+    NI_CUDA_TRY(cudaMemsetAsync(f.counters + 5, 0, sizeof(int32_t), st));
+    if (connectivity == 8)
+      NI_COUNT_LAUNCH(), l1_links_kernel<8><<<grid_for(L1.n), 256, 0, st>>>(
+                             L1.n, H, W, g.P, L1.Hb, L1.Wb, L1.bstart, L1.blk, L1.unit, f.unit,
+                             f.hw, f.imask, L1.nbr, L1.cond, L1.dinv, f.counters + 5);
+    else
+      NI_COUNT_LAUNCH(), l1_links_kernel<4><<<grid_for(L1.n), 256, 0, st>>>(
+                             L1.n, H, W, g.P, L1.Hb, L1.Wb, L1.bstart, L1.blk, L1.unit, f.unit,
+                             f.hw, f.imask, L1.nbr, L1.cond, L1.dinv, f.counters + 5);
+    NI_LAUNCH_CHECK();
+    NI_CUDA_TRY(cudaMemcpyAsync(&L1.nact, f.counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    NI_CUDA_TRY(cudaStreamSynchronize(st));
+    L = 1;
+    while (L < MAXLEV && lev[L].nact > 0) {
+      Level& C = lev[L];
+      Level& N = lev[L + 1];
+      N.Hb = div_up(C.Hb, 2);
+      N.Wb = div_up(C.Wb, 2);
+      N.nblk = int64_t(B) * N.Hb * N.Wb;
+      N.bstart = cv.take<int32_t>(N.nblk + 1);
+      N.cnt = cv.take<int32_t>(N.nblk + 1);
+      if (!cv.ok()) return too_small(size_t(C.n) * kBytesPerUnknown * 2);
+      NI_CUDA_TRY(cudaMemsetAsync(N.cnt + N.nblk, 0, sizeof(int32_t), st));
+      NI_COUNT_LAUNCH(), lc_count_kernel<<<grid_for(N.nblk), 256, 0, st>>>(
+                             N.nblk, N.Hb, N.Wb, C.Hb, C.Wb, C.bstart, C.unit, C.dinv, N.cnt);
+      NI_LAUNCH_CHECK();
+      NI_TRY(exclusive_scan_i32(N.cnt, N.bstart, N.nblk + 1, f.counters + 4, f.scan_ws, st));
+      NI_CUDA_TRY(cudaMemcpyAsync(&N.n, f.counters + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      NI_CUDA_TRY(cudaStreamSynchronize(st));
+      if (N.n == 0) break;
+      carve_level(cv, N, N.n, true);
+      if (!cv.ok()) return too_small(size_t(N.n) * kBytesPerUnknown * 2);
+      NI_COUNT_LAUNCH(), lc_assign_kernel<<<grid_for(N.nblk), 256, 0, st>>>(
+                             N.nblk, N.Hb, N.Wb, C.Hb, C.Wb, C.bstart, C.unit, C.dinv, N.bstart,
+                             N.n, N.blk, N.unit, N.child, C.parent);
+      NI_LAUNCH_CHECK();
+      NI_CUDA_TRY(cudaMemsetAsync(N.parent, 0xff, sizeof(int32_t) * (N.n + 1), st));
+      NI_CUDA_TRY(cudaMemsetAsync(f.counters + 5, 0, sizeof(int32_t), st));
+      NI_COUNT_LAUNCH(), lc_links_kernel<<<grid_for(N.n), 256, 0, st>>>(
+                             N.n, N.Hb, N.Wb, N.bstart, N.blk, N.unit, N.child, C.n, C.nbr,
+                             C.cond, C.parent, N.nbr, N.cond, N.dinv, f.counters + 5);
+      NI_LAUNCH_CHECK();
+      NI_CUDA_TRY(cudaMemcpyAsync(&N.nact, f.counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      NI_CUDA_TRY(cudaStreamSynchronize(st));
+      ++L;
+    }
+    // the coarsest level used is the last one with a link
+    while (L > 1 && lev[L].nact == 0) --L;
+  }
+  if (needed_bytes) *needed_bytes = cv.used;
+  // ---- PCG
+  FineArgs fa;
+  fa.H = H;
+  fa.W = W;
+  fa.P = g.P;
+  fa.nTX = g.nTX;
+  fa.nTY = g.nTY;
+  fa.tiles = f.tiles;
+  fa.x = f.x;
+  fa.r = f.r;
+  fa.p = f.p;
+  fa.s = f.s;
+  fa.u = f.u;
+  fa.w = f.w;
+  fa.hw = f.hw;
+  fa.dinv = f.dinv;
+  fa.imask = f.imask;
+  fa.par0 = f.par0;
+  fa.slot = f.slot;
+  fa.slot_base = f.slot_base;
+  fa.slot_unit = slot_unit;
+  fa.status = ustatus;
+  fa.upd = uupd;
+  fa.alpha = ualpha;
+  fa.beta = ubeta;
+  fa.b1 = lev[1].b;
+  fa.e1 = lev[1].e;
+  fa.partial = partial;
+  fa.umean = uumean;
+  if (NA > 0) {  // pixels per unit (x = 0 here: the sums are the counts)
+    NI_CUDA_TRY(cudaMemsetAsync(uumean, 0, sizeof(float) * (NU + 1), st));
+    NI_COUNT_LAUNCH(), xsum_kernel<<<NA, NT, 0, st>>>(fa);
+    NI_LAUNCH_CHECK();
+    NI_COUNT_LAUNCH(), unit_mean_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(
+                           NU, pstart, plist, partial, umean, unit_n);
+    NI_LAUNCH_CHECK();
+  }
+  ScalarArgs sa;
+  sa.nu = NU;
+  sa.pstart = pstart;
+  sa.plist = plist;
+  sa.partial = partial;
+  sa.unit_n = unit_n;
+  sa.umean = uumean;
+  sa.rtol = cg_tol;
+  sa.status = ustatus;
+  sa.upd = uupd;
+  sa.iters = uiters;
+  sa.cap = ucap;
+  sa.tol2 = utol2;
+  sa.gprev = ugprev;
+  sa.aprev = uaprev;
+  sa.alpha = ualpha;
+  sa.beta = ubeta;
+  sa.nactive = f.counters + 6;
+  {
+    const char* tr = getenv("NI_MG_TRACE");
+    sa.trace_unit = tr ? atoi(tr) : -1;
+  }
+  int vcycles = 0;
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassBSmem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassBSmem)));
+  NI_CUDA_TRY(cudaEventRecord(e0, st));
+  if (NA > 0) {
+    while (true) {
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a_kernel<8><<<NA, NT, 0, st>>>(fa);
+      else NI_COUNT_LAUNCH(), pass_a_kernel<4><<<NA, NT, 0, st>>>(fa);
+      NI_LAUNCH_CHECK();
+      for (int l = 1; l < L; ++l) {
+        const Level& C = lev[l];
+        const Level& N = lev[l + 1];
+        NI_COUNT_LAUNCH(), down_kernel<<<grid_for(N.n), 256, 0, st>>>(N.n, N.child, C.n, C.nbr,
+                                                                     C.cond, C.dinv, C.b, N.b);
+        NI_LAUNCH_CHECK();
+      }
+      for (int l = L; l >= 1; --l) {
+        const Level& C = lev[l];
+        if (l == L)
+          NI_COUNT_LAUNCH(), up_kernel<false><<<grid_for(C.n), 256, 0, st>>>(
+                                 C.n, C.nbr, C.cond, C.dinv, C.b, nullptr, nullptr, C.e);
+        else
+          NI_COUNT_LAUNCH(), up_kernel<true><<<grid_for(C.n), 256, 0, st>>>(
+                                 C.n, C.nbr, C.cond, C.dinv, C.b, C.parent, lev[l + 1].e, C.e);
+        NI_LAUNCH_CHECK();
+      }
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b_kernel<8><<<NA, NT, kPassBSmem, st>>>(fa);
+      else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa);
+      NI_LAUNCH_CHECK();
+      NI_CUDA_TRY(cudaMemsetAsync(f.counters + 6, 0, sizeof(int32_t), st));
+      NI_COUNT_LAUNCH(), scalar_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(sa);
+      NI_LAUNCH_CHECK();
+      ++vcycles;
+      int32_t nact = 0;
+      NI_CUDA_TRY(cudaMemcpyAsync(&nact, f.counters + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      NI_CUDA_TRY(cudaStreamSynchronize(st));
+      if (nact == 0) break;
+    }
+  }
+  NI_CUDA_TRY(cudaEventRecord(e1, st));
+  // ---- output: x minus its per-unit mean
+  if (NA > 0) {
+    NI_COUNT_LAUNCH(), xsum_kernel<<<NA, NT, 0, st>>>(fa);
+    NI_LAUNCH_CHECK();
+    NI_COUNT_LAUNCH(), unit_mean_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(
+                           NU, pstart, plist, partial, umean, nullptr);
+    NI_LAUNCH_CHECK();
+  }
+  NI_COUNT_LAUNCH(), output_kernel<<<npb, 256, 0, st>>>(W, g.P, g.npix, f.x, f.unit, umean, z_out);
+  NI_LAUNCH_CHECK();
+  NI_CUDA_TRY(cudaMemsetAsync(comp_iters, 0, sizeof(int32_t) * std::max(count, 1), st));
+  NI_CUDA_TRY(cudaMemsetAsync(comp_status, 0, sizeof(int32_t) * std::max(count, 1), st));
+  NI_CUDA_TRY(cudaMemsetAsync(f.counters + 7, 0, sizeof(int32_t), st));
+  if (NU > 0) {
+    NI_COUNT_LAUNCH(), comp_out_kernel<<<grid_for(NU), 256, 0, st>>>(
+                           NU, unit_comp, ustatus, uiters, pstart, comp_iters, comp_status,
+                           f.counters + 7);
+    NI_LAUNCH_CHECK();
+  }
+  int32_t mx = 0;
+  NI_CUDA_TRY(cudaMemcpyAsync(&mx, f.counters + 7, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  NI_CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  NI_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  FillReport& rep = g_fill_report;
+  rep.cg_ms = ms;
+  rep.px_iters = 0;
+  rep.max_iters = mx;
+  rep.grid = NA;
+  rep.ntiles = g.ntiles;
+  rep.npartials = NS;
+  rep.mg_levels = L;
+  rep.mg_vcycles = vcycles;
+  for (int l = 0; l < 16; ++l) rep.mg_n[l] = l >= 1 && l <= L ? lev[l].n : 0;
+  return NI_OK;
+}

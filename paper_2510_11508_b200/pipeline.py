@@ -17,6 +17,7 @@ import concurrent.futures as cf
 import ctypes as C
 import hashlib
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -29,6 +30,9 @@ from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _device, _stream
 from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
 
 ENERGY_FLOOR = 1e-300  # pipeline.py:55
+# fill solver: "mg" (multigrid-preconditioned CG, default) or "cg" (the
+# round-1 unpreconditioned single-sweep CG kernel; experiments only)
+_FILL_SOLVER = os.environ.get("NI_FILL_SOLVER", "mg")
 
 
 def _ptr(t: torch.Tensor | None) -> C.c_void_p:
@@ -248,9 +252,37 @@ def _pair_energy(g: _Grid, co, x: torch.Tensor, wts) -> torch.Tensor:
     return out
 
 
+def _fill_mg(g: _Grid, labels, count, co, settings: SolveSettings):
+    """The fill at z = 0 (solver.py:195-239) as one batched multigrid-
+    preconditioned CG over every solve unit of the batch (ni_fill_mg)."""
+    lib = g.lib
+    omega_a, omega_b, gamma, eflags = co
+    z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
+    iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    nbytes = _lib.size_query(lib.ni_fill_mg_workspace_size, g.B, g.H, g.W, g.conn, count)
+    for _ in range(3):  # the hierarchy's size depends on the data: retry with what it needs
+        ws = _ws(nbytes, g.dev)
+        need = C.c_size_t(0)
+        st = lib.ni_fill_mg(_ptr(labels), count, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
+                            _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
+                            C.c_double(settings.cg_tol), int(settings.cg_max_iters), _ptr(z),
+                            _ptr(iters), _ptr(status), _ptr(ws), ws.numel(), C.byref(need),
+                            g.s())
+        if st != _lib.NI_ERR_WORKSPACE:
+            break
+        del ws
+        nbytes = max(int(need.value), nbytes + 1)
+    _lib.check(st, "fill_components")
+    return z, iters[:count], status[:count]
+
+
 def _fill(g: _Grid, labels, count, co, settings: SolveSettings, wts=None):
     """Batched per-component CG (solver.py:195-239); ``wts`` = per-edge weights
-    (w_a, w_b) for the refill pass / the pixel baseline, None for the fill."""
+    (w_a, w_b) for the refill pass / the pixel baseline, None for the fill
+    (which runs the multigrid-preconditioned solve unless NI_FILL_SOLVER=cg)."""
+    if wts is None and _FILL_SOLVER != "cg":
+        return _fill_mg(g, labels, count, co, settings)
     lib = g.lib
     omega_a, omega_b, gamma, eflags = co
     z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
@@ -441,6 +473,8 @@ def run_pipeline_batch(
             m = int(np.searchsorted(first, c, side="right") - 1)
             warnings[m].append(f"component {int(c - first[m])}: cg hit iteration cap")
     report = _lib.fill_report()
+    if _FILL_SOLVER != "cg":
+        report["mg"] = _lib.mg_report()
     fill_ms = _ms(t0)
     for m in range(B):
         records[m].append({"stage": "fill", "wall_ms": fill_ms})
