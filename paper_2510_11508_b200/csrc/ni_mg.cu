@@ -61,6 +61,9 @@
 // floating-point atomics: reruns are bit-identical.
 #include <stdlib.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ni_common.cuh"
@@ -82,7 +85,7 @@ constexpr int NPART = 6;  // per-slot partials: (r,u) (w,u) (r,r) sum u, sum r, 
 #define NI_MG_OMEGA 0.8f
 #endif
 #ifndef NI_MG_OC
-#define NI_MG_OC 1.6f
+#define NI_MG_OC 1.9f
 #endif
 constexpr float OM = NI_MG_OMEGA;  // damped-Jacobi weight
 constexpr float OC = NI_MG_OC;     // coarse-correction scale
@@ -486,7 +489,9 @@ struct Level {
   int32_t* parent = nullptr;  // [n] (-1: no coarser aggregate)
   int32_t* child = nullptr;   // [4][n] (levels >= 2)
   float* b = nullptr;         // [n]
-  float* e = nullptr;         // [n]
+  float* x1 = nullptr;        // [n] pre-smoothed OM dinv b
+  float* x2 = nullptr;        // [n] x1 + OC * parent's correction
+  float* e = nullptr;         // [n] (level 1 only)
   int32_t* cnt = nullptr;     // [nblk + 1] scratch (count per block)
 };
 
@@ -788,75 +793,117 @@ __global__ void lc_links_kernel(int n, int Hb, int Wb, const int32_t* __restrict
 
 // ------------------------------------------------------------ V-cycle
 
-// down: b_{l+1}[P] = sum over children c of (b_c - A x1)_c, x1 = OM dinv b
+// down: b_{l+1}[P] = sum over children c of (b - A x1)_c with x1 = OM dinv b
+// precomputed at level l; also x1 at level l+1
 __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __restrict__ child,
                                                    int n, const int32_t* __restrict__ nbr,
                                                    const float* __restrict__ cond,
-                                                   const float* __restrict__ dinv,
+                                                   const float* __restrict__ x1,
                                                    const float* __restrict__ b,
-                                                   float* __restrict__ b1) {
+                                                   const float* __restrict__ dinv1,
+                                                   float* __restrict__ b1,
+                                                   float* __restrict__ x1n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += gridDim.x * blockDim.x) {
     float sum = 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int32_t c = child[int64_t(q) * n1 + i];
       if (c < 0) continue;
-      const float bc = b[c];
-      const float x1 = OM * dinv[c] * bc;
+      const float xc = x1[c];
       float acc = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int32_t j = nbr[int64_t(k) * n + c];
         if (j < 0) continue;
-        acc += cond[int64_t(k) * n + c] * (x1 - OM * dinv[j] * b[j]);
+        acc += cond[int64_t(k) * n + c] * (xc - x1[j]);
       }
-      sum += bc - acc;
+      sum += b[c] - acc;
     }
     b1[i] = sum;
+    x1n[i] = OM * dinv1[i] * sum;
   }
 }
 
-// up: e = x2 + OM dinv (b - A x2), x2 = OM dinv b + OC e_{l+1}[parent]
-template <bool COARSE>
+// up: e = xs + OM dinv (b - A xs), xs = x2 = x1 + OC e_{l+1}[parent] (x1 on
+// the coarsest level); levels >= 2 hand x2 = x1 + OC e to their children.
+template <bool SCATTER>
 __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restrict__ nbr,
                                                  const float* __restrict__ cond,
                                                  const float* __restrict__ dinv,
                                                  const float* __restrict__ b,
-                                                 const int32_t* __restrict__ parent,
-                                                 const float* __restrict__ e1,
-                                                 float* __restrict__ e) {
+                                                 const float* __restrict__ xs,
+                                                 float* __restrict__ e_out,
+                                                 const int32_t* __restrict__ child,
+                                                 const float* __restrict__ x1c,
+                                                 float* __restrict__ x2c, int nc) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const float di = dinv[i];
-    if (di == 0.f) {
-      e[i] = 0.f;
-      continue;
-    }
-    auto x2 = [&](int j) {
-      float v = OM * dinv[j] * b[j];
-      if (COARSE) {
-        const int32_t pj = parent[j];
-        if (pj >= 0) v += OC * e1[pj];
-      }
-      return v;
-    };
-    const float xi = x2(i);
-    float acc = 0.f;
+    float e = 0.f;
+    if (di != 0.f) {
+      const float xi = xs[i];
+      float acc = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int32_t j = nbr[int64_t(k) * n + i];
-      if (j < 0) continue;
-      acc += cond[int64_t(k) * n + i] * (xi - x2(j));
+      for (int k = 0; k < 8; ++k) {
+        const int32_t j = nbr[int64_t(k) * n + i];
+        if (j < 0) continue;
+        acc += cond[int64_t(k) * n + i] * (xi - xs[j]);
+      }
+      e = xi + OM * di * (b[i] - acc);
     }
-    e[i] = xi + OM * di * (b[i] - acc);
+    if (SCATTER) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int32_t c = child[int64_t(q) * n + i];
+        if (c >= 0) x2c[c] = x1c[c] + OC * e;
+      }
+    } else {
+      e_out[i] = e;
+    }
   }
 }
 
 // ---- fine passes
+//
+// A CTA owns one 64 x 32 tile.  The planes it stencils are staged in shared
+// memory as dense boxes (row stride BW, 16-B multiple): by the Tensor Memory
+// Accelerator (cp.async.bulk.tensor, one elected thread, an mbarrier with
+// the expected byte count; out-of-range rows/columns zero-filled) or, in the
+// NI_MG_TMA=0 build, by cp.async (LDGSTS) element copies -- the two variants
+// compared in DESIGN.md.  Warp w owns tile rows {2w, 2w+1, 2w+16, 2w+17} and
+// lane l the columns l and l+32: consecutive lanes touch consecutive shared
+// addresses (no bank conflicts) and every global access is a 128-B row
+// segment.  A 2 x 2 block (restriction) is split over lanes l, l^1.
+#ifndef NI_MG_TMA
+#define NI_MG_TMA 1
+#endif
+
+// TMA boxes must start on a 16-byte-aligned column (measured: an unaligned
+// start raises an illegal-instruction fault), so every f32 box starts 4
+// columns left of the tile (CX) and every uint8 box 16 columns left (CXM).
+constexpr int CX = 4;
+constexpr int BW = TX + 2 * CX;  // f32 box width (72: covers a 1- and a 2-pixel halo)
+constexpr int BH1 = TY + 2;      // rows with a 1-pixel halo
+constexpr int BH2 = TY + 4;      // rows with a 2-pixel halo
+constexpr int CXM = 16;
+constexpr int BWM = 96;          // uint8 imask box width (x0-16 .. x0+79)
+constexpr int S3 = TX + 2;       // x3 array (computed, not a box): 1-pixel halo
+constexpr int BOX1 = BW * BH1, BOX2 = BW * BH2;
+
+__host__ __device__ constexpr int al128(int b) { return (b + 127) & ~127; }
+
+struct TmaMaps {
+  CUtensorMap r[2], s[2], w, dinv, hw;  // f32, BW x BH1 boxes (pass A)
+  CUtensorMap rB[2], dinvB, hwB, parB;  // BW x BH2 boxes (pass B)
+  CUtensorMap imB;                      // uint8 imask, BWM x BH1 box (pass B)
+};
 
 struct FineArgs {
   int H, W, P, nTX, nTY;
+  int par;  // which r / s buffer holds the values before this iteration's update
   const int32_t* tiles;  // active tiles
-  float *x, *r, *p, *s, *u, *w;
+  float *x, *p, *u, *w;
+  float* rbuf[2];  // r, s ping-pong: neighbouring tiles read the old values as halo
+  float* sbuf[2];
   const float *hw, *dinv;
   const uint8_t* imask;
   const int32_t* par0;
@@ -867,21 +914,55 @@ struct FineArgs {
   const uint8_t* upd;
   const float *alpha, *beta;
   float* b1;       // level-1 right-hand side
+  float* x1_1;     // level-1 pre-smoothed state OM dinv b
+  const float* dinv1;
   const float* e1; // level-1 correction
   double* partial; // [NS][NPART]
   const float* umean;  // per unit: mean of u (removed from p: the preconditioned
                        // direction is kept orthogonal to the unit's null space)
 };
 
-// stage a (TY + 2h) x (TX + 2h) window of a padded plane into shared memory
-template <int HALO, class T>
-__device__ __forceinline__ void stage(T* __restrict__ sm, const T* __restrict__ g, int P, int y0,
-                                      int x0) {
-  constexpr int SWD = TX + 2 * HALO, SHT = TY + 2 * HALO;
-  for (int e = threadIdx.x; e < SWD * SHT; e += NT) {
-    const int ry = e / SWD, rx = e - ry * SWD;
-    sm[e] = g[pidx(P, y0 - HALO + ry, x0 - HALO + rx)];
-  }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+// cp.async staging of a BWxBH box of a 4-byte plane (NI_MG_TMA=0 variant);
+// box rows/columns beyond the padded plane never occur (margins cover them)
+template <int BWX, int BHX, class T>
+__device__ __forceinline__ void stage_cp(T* sm, const T* g, int P, int ys, int xs) {
+  for (int ry = threadIdx.x >> 5; ry < BHX; ry += NT / 32)
+    for (int rx = threadIdx.x & 31; rx < BWX; rx += 32)
+      cp_async4(sm + ry * BWX + rx, g + pidx(P, ys + ry, xs + rx));
 }
 
 // is every unit of the tile finished?  (then its passes are skipped)
@@ -897,199 +978,353 @@ __device__ __forceinline__ float r_new(float r, float w, float s, float al, floa
   return r - al * (w + bt * s);
 }
 
+constexpr int kMaxSlotSm = 16;  // per-tile unit scalars kept in shared memory
+
+constexpr size_t kPassASmem = 5 * size_t(al128(BOX1 * 4)) + 128;
+
 // Pass A: pending CG update, pre-smoothing of the new r, residual,
 // restriction to level 1.
 template <int CONN>
-__global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ FineArgs a) {
-  constexpr int H1 = 1, S1 = TX + 2 * H1, N1 = S1 * (TY + 2 * H1);
-  __shared__ float sR[N1], sW[N1], sS[N1], sD[N1], sH[N1];
+__global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ FineArgs a,
+                                                    const __grid_constant__ TmaMaps tm) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sR = reinterpret_cast<float*>(smem_raw);
+  float* sW = sR + al128(BOX1 * 4) / 4;
+  float* sS = sW + al128(BOX1 * 4) / 4;
+  float* sD = sS + al128(BOX1 * 4) / 4;
+  float* sH = sD + al128(BOX1 * 4) / 4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sH + al128(BOX1 * 4) / 4);
+  __shared__ float s_al[kMaxSlotSm], s_bt[kMaxSlotSm], s_um[kMaxSlotSm];
+  __shared__ int s_un[kMaxSlotSm];
+  __shared__ uint8_t s_up[kMaxSlotSm];
   const int t = a.tiles[blockIdx.x];
   if (tile_done(a, t)) return;
   const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
-  stage<H1>(sR, a.r, a.P, T.y0, T.x0);
-  stage<H1>(sW, a.w, a.P, T.y0, T.x0);
-  stage<H1>(sS, a.s, a.P, T.y0, T.x0);
-  stage<H1>(sD, a.dinv, a.P, T.y0, T.x0);
-  stage<H1>(sH, a.hw, a.P, T.y0, T.x0);
-  __syncthreads();
+  const int xs = T.x0 - CX + XM, ys = T.y0 - 1 + RM;  // box origin (padded coordinates)
+#if NI_MG_TMA
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 5u * BOX1 * 4u);
+    tma_2d(sR, a.par ? &tm.r[1] : &tm.r[0], bar, xs, ys);
+    tma_2d(sW, &tm.w, bar, xs, ys);
+    tma_2d(sS, a.par ? &tm.s[1] : &tm.s[0], bar, xs, ys);
+    tma_2d(sD, &tm.dinv, bar, xs, ys);
+    tma_2d(sH, &tm.hw, bar, xs, ys);
+  }
+#else
+  stage_cp<BW, BH1>(sR, a.rbuf[a.par], a.P, T.y0 - 1, T.x0 - CX);
+  stage_cp<BW, BH1>(sW, (const float*)a.w, a.P, T.y0 - 1, T.x0 - CX);
+  stage_cp<BW, BH1>(sS, a.sbuf[a.par], a.P, T.y0 - 1, T.x0 - CX);
+  stage_cp<BW, BH1>(sD, a.dinv, a.P, T.y0 - 1, T.x0 - CX);
+  stage_cp<BW, BH1>(sH, a.hw, a.P, T.y0 - 1, T.x0 - CX);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
   const int base = a.slot_base[t];
+  const int nsl = a.slot_base[t + 1] - base;
+  if (threadIdx.x < nsl && threadIdx.x < kMaxSlotSm) {
+    const int un = a.slot_unit[base + threadIdx.x];
+    s_un[threadIdx.x] = un;
+    s_up[threadIdx.x] = a.upd[un];
+    s_al[threadIdx.x] = a.alpha[un];
+    s_bt[threadIdx.x] = a.beta[un];
+    s_um[threadIdx.x] = a.umean[un];
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    const int by = wid + half * (NT / 32);  // block row 0..15
-    const int bx = lane;                    // block column 0..31
-    float res[4];
-    int32_t par[4];
+  float* rout = a.rbuf[a.par ^ 1];
+  float* sout = a.sbuf[a.par ^ 1];
+  // per-pixel operands from global (issued before the wait)
+  uint16_t slv[2][2][2];
+  float uv[2][2][2], pv[2][2][2], xv[2][2][2];
+  int32_t pav[2][2][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int ly = 2 * by + (q >> 1), lx = 2 * bx + (q & 1);
-      const int y = T.y0 + ly, x = T.x0 + lx;
-      res[q] = 0.f;
-      par[q] = -1;
-      if (y >= T.y1 || x >= T.x1) continue;
-      const int64_t o = pidx(a.P, y, x);
-      const uint16_t sl = a.slot[o];
-      if (sl == NOSLOT) continue;
-      const int32_t un = a.slot_unit[base + sl];
-      const bool up = a.upd[un] != 0;
-      const float al = a.alpha[un], bt = a.beta[un];
-      const int c = (ly + H1) * S1 + lx + H1;
-      float ri = sR[c];
-      if (up) {
-        const float si = sW[c] + bt * sS[c];
-        const float pi = (a.u[o] - a.umean[un]) + bt * a.p[o];
-        a.p[o] = pi;
-        a.s[o] = si;
-        a.x[o] = a.x[o] + al * pi;
-        ri = r_new(ri, sW[c], sS[c], al, bt);
-        a.r[o] = ri;
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int ly = 2 * wid + 16 * h + j, lx = lane + 32 * c;
+        const int y = T.y0 + ly, x = T.x0 + lx;
+        slv[h][j][c] = NOSLOT;
+        if (y < T.y1 && x < T.x1) {
+          const int64_t o = pidx(a.P, y, x);
+          slv[h][j][c] = a.slot[o];
+          uv[h][j][c] = a.u[o];
+          pv[h][j][c] = a.p[o];
+          xv[h][j][c] = a.x[o];
+          pav[h][j][c] = a.par0[o];
+        }
       }
-      const float x1i = OM * sD[c] * ri;
-      const float hi = sH[c];
-      const uint8_t mk = a.imask[o];
-      float acc = 0.f;
+#if NI_MG_TMA
+  __syncthreads();  // barrier init visible; slot scalars staged
+  mbar_wait(bar, 0);
+#else
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+#endif
 #pragma unroll
-      for (int bit = 0; bit < 8; ++bit) {
-        if ((bit & 3) >= (CONN == 8 ? 4 : 2) || !((mk >> bit) & 1)) continue;
-        const int j = c + nb_off<CONN>(bit, S1);
-        float rj = sR[j];
-        if (up) rj = r_new(rj, sW[j], sS[j], al, bt);
-        acc += (hi + sH[j]) * (x1i - OM * sD[j] * rj);
+  for (int h = 0; h < 2; ++h) {
+    float res[2][2];
+    int32_t par[2][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        res[j][c] = 0.f;
+        par[j][c] = -1;
+        const uint16_t sl = slv[h][j][c];
+        if (sl == NOSLOT) continue;
+        const int ly = 2 * wid + 16 * h + j, lx = lane + 32 * c;
+        const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx);
+        int un;
+        bool up;
+        float al, bt, um;
+        if (sl < kMaxSlotSm) {
+          un = s_un[sl];
+          up = s_up[sl] != 0;
+          al = s_al[sl];
+          bt = s_bt[sl];
+          um = s_um[sl];
+        } else {
+          un = a.slot_unit[base + sl];
+          up = a.upd[un] != 0;
+          al = a.alpha[un];
+          bt = a.beta[un];
+          um = a.umean[un];
+        }
+        (void)un;
+        const int cc = (ly + 1) * BW + lx + CX;
+        float ri = sR[cc], si = sS[cc];
+        if (up) {
+          si = sW[cc] + bt * sS[cc];
+          const float pi = (uv[h][j][c] - um) + bt * pv[h][j][c];
+          a.p[o] = pi;
+          a.x[o] = xv[h][j][c] + al * pi;
+          ri = r_new(ri, sW[cc], sS[cc], al, bt);
+        }
+        rout[o] = ri;
+        sout[o] = si;
+        const float x1i = OM * sD[cc] * ri;
+        const float hi = sH[cc];
+        const uint8_t mk = a.imask[o];
+        float acc = 0.f;
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {
+          if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+          const int jn = cc + nb_off<CONN>(bit, BW);
+          float rj = sR[jn];
+          if (up) rj = r_new(rj, sW[jn], sS[jn], al, bt);
+          acc += (hi + sH[jn]) * (x1i - OM * sD[jn] * rj);
+        }
+        res[j][c] = ri - acc;
+        par[j][c] = pav[h][j][c];
       }
-      res[q] = ri - acc;
-      par[q] = a.par0[o];
-    }
-    // restriction: one write per distinct level-1 aggregate of the block
+    // restriction: lanes 2k (left column) and 2k+1 (right column) share a
+    // 2 x 2 block per column half; the even lane writes each distinct
+    // level-1 aggregate once, summing in pixel order (top-left, top-right,
+    // bottom-left, bottom-right)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (par[q] < 0) continue;
-      bool first = true;
+    for (int c = 0; c < 2; ++c) {
+      const float r01 = __shfl_xor_sync(0xffffffffu, res[0][c], 1);
+      const float r11 = __shfl_xor_sync(0xffffffffu, res[1][c], 1);
+      const int32_t p01 = __shfl_xor_sync(0xffffffffu, par[0][c], 1);
+      const int32_t p11 = __shfl_xor_sync(0xffffffffu, par[1][c], 1);
+      if (lane & 1) continue;
+      const float rq[4] = {res[0][c], r01, res[1][c], r11};
+      const int32_t pq[4] = {par[0][c], p01, par[1][c], p11};
 #pragma unroll
-      for (int q2 = 0; q2 < q; ++q2)
-        if (par[q2] == par[q]) first = false;
-      if (!first) continue;
-      float sum = 0.f;
+      for (int q = 0; q < 4; ++q) {
+        if (pq[q] < 0) continue;
+        bool first = true;
 #pragma unroll
-      for (int q2 = q; q2 < 4; ++q2)
-        if (par[q2] == par[q]) sum += res[q2];
-      a.b1[par[q]] = sum;
+        for (int q2 = 0; q2 < q; ++q2)
+          if (pq[q2] == pq[q]) first = false;
+        if (!first) continue;
+        float sum = 0.f;
+#pragma unroll
+        for (int q2 = q; q2 < 4; ++q2)
+          if (pq[q2] == pq[q]) sum += rq[q2];
+        a.b1[pq[q]] = sum;
+        a.x1_1[pq[q]] = OM * a.dinv1[pq[q]] * sum;
+      }
     }
   }
 }
 
 // Pass B: prolongation + post-smoothing -> u = M r; w = A u; per-slot dots
-// (r,u), (w,u), (r,r).
-constexpr int PB_S2 = TX + 4, PB_N2 = PB_S2 * (TY + 4);
-constexpr int PB_S1 = TX + 2, PB_N1 = PB_S1 * (TY + 2);
-constexpr size_t kPassBSmem = size_t(PB_N2) * 4 * sizeof(float) + size_t(PB_N1) * sizeof(float) +
-                              size_t(TPX) * sizeof(float) + size_t(TPX) * sizeof(uint16_t) +
-                              size_t(PB_N1) * sizeof(uint8_t);
+// (r,u), (w,u), (r,r), sum u, sum r, sum w.
+constexpr size_t kPassBSmem = 4 * size_t(al128(BOX2 * 4)) + size_t(al128(S3 * BH1 * 4)) +
+                              size_t(al128(BWM * BH1)) + size_t(TPX) * 4 + size_t(TPX) * 2 + 128;
 
 template <int CONN>
-__global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ FineArgs a) {
-  constexpr int H2 = 2, S2 = PB_S2, N2 = PB_N2;
-  constexpr int H1 = 1, S1 = PB_S1, N1 = PB_N1;
+__global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ FineArgs a,
+                                                    const __grid_constant__ TmaMaps tm) {
   constexpr int KF = CONN == 8 ? 4 : 2;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sR = reinterpret_cast<float*>(smem_raw);
-  float* sD = sR + N2;
-  float* sH = sD + N2;
-  float* sX2 = sH + N2;
-  float* sX3 = sX2 + N2;
-  float* sWv = sX3 + N1;
+  float* sD = sR + al128(BOX2 * 4) / 4;
+  float* sH = sD + al128(BOX2 * 4) / 4;
+  float* sX2 = sH + al128(BOX2 * 4) / 4;  // par0 lands here, then x2 replaces it
+  float* sX3 = sX2 + al128(BOX2 * 4) / 4;
+  uint8_t* sM = reinterpret_cast<uint8_t*>(sX3 + al128(S3 * BH1 * 4) / 4);
+  float* sWv = reinterpret_cast<float*>(sM + al128(BWM * BH1));
   uint16_t* sSl = reinterpret_cast<uint16_t*>(sWv + TPX);
-  uint8_t* sM = reinterpret_cast<uint8_t*>(sSl + TPX);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sSl + TPX);
+  __shared__ double sred[NT / 32][NPART];
   const int t = a.tiles[blockIdx.x];
   if (tile_done(a, t)) return;
   const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
-  // 2-pixel halo: r, dinv, hw and the prolongated pre-smoothed state
-  // x2 = OM dinv r + OC e1[par0]
-  for (int e = threadIdx.x; e < N2; e += NT) {
-    const int ry = e / S2, rx = e - ry * S2;
-    const int64_t o = pidx(a.P, T.y0 - H2 + ry, T.x0 - H2 + rx);
-    const float rv = a.r[o], dv = a.dinv[o];
-    const int32_t pj = a.par0[o];
-    sR[e] = rv;
-    sD[e] = dv;
-    sH[e] = a.hw[o];
-    sX2[e] = OM * dv * rv + (pj >= 0 ? OC * a.e1[pj] : 0.f);
+  const float* rcur = a.rbuf[a.par];
+#if NI_MG_TMA
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 4u * BOX2 * 4u + uint32_t(BWM * BH1));
+    const int xs2 = T.x0 - CX + XM, ys2 = T.y0 - 2 + RM;
+    tma_2d(sR, a.par ? &tm.rB[1] : &tm.rB[0], bar, xs2, ys2);
+    tma_2d(sD, &tm.dinvB, bar, xs2, ys2);
+    tma_2d(sH, &tm.hwB, bar, xs2, ys2);
+    tma_2d(sX2, &tm.parB, bar, xs2, ys2);
+    tma_2d(sM, &tm.imB, bar, T.x0 - CXM + XM, T.y0 - 1 + RM);
   }
-  stage<H1>(sM, a.imask, a.P, T.y0, T.x0);
-  __syncthreads();
-  // post-smoothing on the tile + 1-pixel ring
-  for (int e = threadIdx.x; e < N1; e += NT) {
-    const int ry = e / S1, rx = e - ry * S1;
-    const int c = (ry + 1) * S2 + rx + 1;  // same pixel in the 2-halo arrays
-    const uint8_t mk = sM[e];
-    float v = sX2[c];
-    if (mk) {
-      const float hi = sH[c];
-      float acc = 0.f;
+#else
+  stage_cp<BW, BH2>(sR, rcur, a.P, T.y0 - 2, T.x0 - CX);
+  stage_cp<BW, BH2>(sD, a.dinv, a.P, T.y0 - 2, T.x0 - CX);
+  stage_cp<BW, BH2>(sH, a.hw, a.P, T.y0 - 2, T.x0 - CX);
+  stage_cp<BW, BH2>(reinterpret_cast<int32_t*>(sX2), a.par0, a.P, T.y0 - 2, T.x0 - CX);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int e = threadIdx.x; e < BWM * BH1; e += NT) {
+    const int ry = e / BWM, rx = e - ry * BWM;
+    sM[e] = a.imask[pidx(a.P, T.y0 - 1 + ry, T.x0 - CXM + rx)];
+  }
+#endif
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // slots of the tile (interior), read while the boxes land
+  uint16_t slv[2][2][2];
 #pragma unroll
-      for (int bit = 0; bit < 8; ++bit) {
-        if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
-        const int j = c + nb_off<CONN>(bit, S2);
-        acc += (hi + sH[j]) * (v - sX2[j]);
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int ly = 2 * wid + 16 * h + j, lx = lane + 32 * c;
+        const int y = T.y0 + ly, x = T.x0 + lx;
+        slv[h][j][c] = (y < T.y1 && x < T.x1) ? a.slot[pidx(a.P, y, x)] : NOSLOT;
       }
-      v += OM * sD[c] * (sR[c] - acc);
-    } else {
-      v = 0.f;
-    }
-    sX3[e] = v;
+#if NI_MG_TMA
+  __syncthreads();
+  mbar_wait(bar, 0);
+#else
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+#endif
+  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box (in place of par0)
+  for (int e = threadIdx.x; e < BOX2; e += NT) {
+    const int32_t pj = __float_as_int(sX2[e]);
+    sX2[e] = OM * sD[e] * sR[e] + (pj >= 0 ? OC * a.e1[pj] : 0.f);
   }
   __syncthreads();
-  // u, w on the tile
-  for (int e = threadIdx.x; e < TPX; e += NT) {
-    const int ly = e / TX, lx = e - ly * TX;
-    const int y = T.y0 + ly, x = T.x0 + lx;
-    uint16_t sl = NOSLOT;
-    float wv = 0.f;
-    if (y < T.y1 && x < T.x1) {
-      const int64_t o = pidx(a.P, y, x);
-      sl = a.slot[o];
-      if (sl != NOSLOT) {
-        const int c1 = (ly + 1) * S1 + lx + 1;
-        const int c2 = (ly + 2) * S2 + lx + 2;
-        const uint8_t mk = sM[c1];
-        const float ui = sX3[c1], hi = sH[c2];
+  // post-smoothing on the tile + 1-pixel ring: x3 = x2 + OM dinv (r - A x2)
+  for (int ry = wid; ry < BH1; ry += NT / 32) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int rx = lane + 32 * k;  // pixel (ry - 1, rx - 1) of the tile
+      if (rx >= TX + 2) continue;
+      const int c2 = (ry + 1) * BW + rx - 1 + CX;
+      const uint8_t mk = sM[ry * BWM + rx - 1 + CXM];
+      float v = 0.f;
+      if (mk) {
+        v = sX2[c2];
+        const float hi = sH[c2];
+        float acc = 0.f;
 #pragma unroll
         for (int bit = 0; bit < 8; ++bit) {
           if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
-          wv += (hi + sH[c2 + nb_off<CONN>(bit, S2)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S1)]);
+          const int jn = c2 + nb_off<CONN>(bit, BW);
+          acc += (hi + sH[jn]) * (v - sX2[jn]);
         }
-        a.u[o] = ui;
-        a.w[o] = wv;
+        v += OM * sD[c2] * (sR[c2] - acc);
       }
+      sX3[ry * S3 + rx] = v;
     }
-    sSl[e] = sl;
-    sWv[e] = wv;
   }
   __syncthreads();
-  // per-slot dots in a fixed order: warp w sums slots w, w+8, ... over the
-  // tile's pixels lane-strided, then a fixed xor tree
+  // u = x3, w = A u on the tile; per-thread partial dots for the tile's
+  // first slot, the other slots' pixels staged for the per-slot pass
   const int nsl = a.slot_base[t + 1] - a.slot_base[t];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int sl = wid; sl < nsl; sl += NT / 32) {
-    double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int ly = 2 * wid + 16 * h + j, lx = lane + 32 * c;
+        const uint16_t sl = slv[h][j][c];
+        float wv = 0.f;
+        if (sl != NOSLOT) {
+          const int c1 = (ly + 1) * S3 + lx + 1;
+          const int c2 = (ly + 2) * BW + lx + CX;
+          const uint8_t mk = sM[(ly + 1) * BWM + lx + CXM];
+          const float ui = sX3[c1], hi = sH[c2];
+#pragma unroll
+          for (int bit = 0; bit < 8; ++bit) {
+            if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+            wv += (hi + sH[c2 + nb_off<CONN>(bit, BW)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S3)]);
+          }
+          const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx);
+          a.u[o] = ui;
+          a.w[o] = wv;
+          if (sl == 0) {
+            const double du = double(ui), dr = double(sR[c2]), dw = double(wv);
+            d[0] += dr * du;
+            d[1] += dw * du;
+            d[2] += dr * dr;
+            d[3] += du;
+            d[4] += dr;
+            d[5] += dw;
+          }
+        }
+        if (nsl > 1) {
+          sSl[ly * TX + lx] = sl;
+          sWv[ly * TX + lx] = wv;
+        }
+      }
+  // slot 0: fixed-order block reduction
+#pragma unroll
+  for (int k = 0; k < NPART; ++k) d[k] = warp_sum(d[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) sred[wid][k] = d[k];
+  __syncthreads();
+  if (threadIdx.x < NPART) {
+    double v = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < NT / 32; ++w8) v += sred[w8][threadIdx.x];
+    a.partial[NPART * int64_t(a.slot_base[t]) + threadIdx.x] = v;
+  }
+  if (nsl <= 1) return;
+  // slots 1..: warp w sums slots w+1, w+1+8, ... over the tile lane-strided
+  for (int sl = wid + 1; sl < nsl; sl += NT / 32) {
+    double q[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int e = lane; e < TPX; e += 32) {
       if (sSl[e] != sl) continue;
       const int ly = e / TX, lx = e - ly * TX;
-      const double ui = double(sX3[(ly + 1) * S1 + lx + 1]);
-      const double ri = double(sR[(ly + 2) * S2 + lx + 2]);
+      const double ui = double(sX3[(ly + 1) * S3 + lx + 1]);
+      const double ri = double(sR[(ly + 2) * BW + lx + CX]);
       const double wi = double(sWv[e]);
-      d[0] += ri * ui;
-      d[1] += wi * ui;
-      d[2] += ri * ri;
-      d[3] += ui;
-      d[4] += ri;
-      d[5] += wi;
+      q[0] += ri * ui;
+      q[1] += wi * ui;
+      q[2] += ri * ri;
+      q[3] += ui;
+      q[4] += ri;
+      q[5] += wi;
     }
 #pragma unroll
-    for (int k = 0; k < NPART; ++k) d[k] = warp_sum(d[k]);
+    for (int k = 0; k < NPART; ++k) q[k] = warp_sum(q[k]);
     if (lane == 0) {
       double* pp = a.partial + NPART * int64_t(a.slot_base[t] + sl);
 #pragma unroll
-      for (int k = 0; k < NPART; ++k) pp[k] = d[k];
+      for (int k = 0; k < NPART; ++k) pp[k] = q[k];
     }
   }
 }
@@ -1290,7 +1525,7 @@ using namespace ni::mg;
 namespace {
 
 struct MgFixed {
-  float *x, *r, *p, *s, *u, *w, *hw, *dinv;
+  float *x, *r, *r2, *p, *s, *s2, *u, *w, *hw, *dinv;
   uint8_t* imask;
   int32_t *par0, *unit;
   uint16_t* slot;
@@ -1305,8 +1540,10 @@ void carve_fixed(Carver& c, MgFixed& f, const Geo& g, int count) {
   const int64_t npad = g.npad;
   f.x = c.take<float>(npad);
   f.r = c.take<float>(npad);
+  f.r2 = c.take<float>(npad);
   f.p = c.take<float>(npad);
   f.s = c.take<float>(npad);
+  f.s2 = c.take<float>(npad);
   f.u = c.take<float>(npad);
   f.w = c.take<float>(npad);
   f.hw = c.take<float>(npad);
@@ -1334,7 +1571,7 @@ void carve_fixed(Carver& c, MgFixed& f, const Geo& g, int count) {
 
 // bytes of one coarse unknown: blk, unit, nbr[8], cond[8], dinv, parent,
 // child[4], b, e + its share of the block table
-constexpr int64_t kBytesPerUnknown = 4 * (2 + 8 + 8 + 1 + 1 + 4 + 2);
+constexpr int64_t kBytesPerUnknown = 4 * (2 + 8 + 8 + 1 + 1 + 4 + 4 + 2);
 
 int64_t level_estimate(const Geo& g) {
   // ~ npix/4 * 4/3 over all levels, + boundary aggregates and block tables
@@ -1350,11 +1587,59 @@ void carve_level(Carver& c, Level& L, int n, bool children) {
   L.parent = c.take<int32_t>(n + 1);
   L.child = children ? c.take<int32_t>(4 * int64_t(n) + 1) : nullptr;
   L.b = c.take<float>(n + 1);
+  L.x1 = c.take<float>(n + 1);
+  L.x2 = c.take<float>(n + 1);
   L.e = c.take<float>(n + 1);
 }
 
 int grid_for(int64_t n, int per = 256) {
   return int(std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, int64_t(kSMs) * 32)));
+}
+
+// Tensor maps of the padded planes for the fine passes' TMA boxes.
+int make_tma_maps(TmaMaps& tm, const Geo& g, const MgFixed& f) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    NI_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return NI_ERR_CUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const cuuint64_t rows = cuuint64_t(g.rows + RM + RB);
+  auto mk = [&](CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esz, int bw,
+                int bh) -> int {
+    const cuuint64_t dims[2] = {cuuint64_t(g.P), rows};
+    const cuuint64_t strides[1] = {cuuint64_t(g.P) * esz};
+    const cuuint32_t box[2] = {cuuint32_t(bw), cuuint32_t(bh)};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
+      return NI_ERR_CUDA;
+    }
+    return NI_OK;
+  };
+  const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  NI_TRY(mk(&tm.r[0], f.r, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.r[1], f.r2, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.s[0], f.s, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.s[1], f.s2, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.w, f.w, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.dinv, f.dinv, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.hw, f.hw, F32, 4, BW, BH1));
+  NI_TRY(mk(&tm.rB[0], f.r, F32, 4, BW, BH2));
+  NI_TRY(mk(&tm.rB[1], f.r2, F32, 4, BW, BH2));
+  NI_TRY(mk(&tm.dinvB, f.dinv, F32, 4, BW, BH2));
+  NI_TRY(mk(&tm.hwB, f.hw, F32, 4, BW, BH2));
+  NI_TRY(mk(&tm.parB, f.par0, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, BW, BH2));
+  NI_TRY(mk(&tm.imB, f.imask, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, BWM, BH1));
+  return NI_OK;
 }
 
 }  // namespace
@@ -1412,7 +1697,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   const int npb = grid_for(g.npix);
   const size_t npad = size_t(g.npad);
   // ---- fine planes
-  for (float* pl : {f.x, f.r, f.p, f.s, f.u, f.w, f.hw, f.dinv})
+  for (float* pl : {f.x, f.r, f.r2, f.p, f.s, f.s2, f.u, f.w, f.hw, f.dinv})
     NI_CUDA_TRY(cudaMemsetAsync(pl, 0, npad * sizeof(float), st));
   NI_CUDA_TRY(cudaMemsetAsync(f.imask, 0, npad, st));
   NI_CUDA_TRY(cudaMemsetAsync(f.par0, 0xff, npad * sizeof(int32_t), st));
@@ -1544,6 +1829,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
     NI_CUDA_TRY(cudaStreamSynchronize(st));
     carve_level(cv, L1, L1.n, false);
     if (!cv.ok()) return too_small(size_t(level_estimate(g) * kBytesPerUnknown));
+    NI_CUDA_TRY(cudaMemsetAsync(L1.x2, 0, sizeof(float) * (L1.n + 1), st));
     NI_COUNT_LAUNCH(), l1_assign_kernel<<<grid_for(L1.nblk), 256, 0, st>>>(
                            B, H, W, g.P, L1.Hb, L1.Wb, f.unit, L1.bstart, L1.blk, L1.unit, f.par0);
     NI_LAUNCH_CHECK();
@@ -1580,6 +1866,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
       if (N.n == 0) break;
       carve_level(cv, N, N.n, true);
       if (!cv.ok()) return too_small(size_t(N.n) * kBytesPerUnknown * 2);
+      NI_CUDA_TRY(cudaMemsetAsync(N.x2, 0, sizeof(float) * (N.n + 1), st));
       NI_COUNT_LAUNCH(), lc_assign_kernel<<<grid_for(N.nblk), 256, 0, st>>>(
                              N.nblk, N.Hb, N.Wb, C.Hb, C.Wb, C.bstart, C.unit, C.dinv, N.bstart,
                              N.n, N.blk, N.unit, N.child, C.parent);
@@ -1607,9 +1894,12 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   fa.nTY = g.nTY;
   fa.tiles = f.tiles;
   fa.x = f.x;
-  fa.r = f.r;
+  fa.par = 0;
+  fa.rbuf[0] = f.r;
+  fa.rbuf[1] = f.r2;
+  fa.sbuf[0] = f.s;
+  fa.sbuf[1] = f.s2;
   fa.p = f.p;
-  fa.s = f.s;
   fa.u = f.u;
   fa.w = f.w;
   fa.hw = f.hw;
@@ -1624,6 +1914,8 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   fa.alpha = ualpha;
   fa.beta = ubeta;
   fa.b1 = lev[1].b;
+  fa.x1_1 = lev[1].x1;
+  fa.dinv1 = lev[1].dinv;
   fa.e1 = lev[1].e;
   fa.partial = partial;
   fa.umean = uumean;
@@ -1662,31 +1954,42 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                                    int(kPassBSmem)));
   NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kPassBSmem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassASmem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassASmem)));
+  TmaMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  NI_TRY(make_tma_maps(tm, g, f));
   NI_CUDA_TRY(cudaEventRecord(e0, st));
   if (NA > 0) {
     while (true) {
-      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a_kernel<8><<<NA, NT, 0, st>>>(fa);
-      else NI_COUNT_LAUNCH(), pass_a_kernel<4><<<NA, NT, 0, st>>>(fa);
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a_kernel<8><<<NA, NT, kPassASmem, st>>>(fa, tm);
+      else NI_COUNT_LAUNCH(), pass_a_kernel<4><<<NA, NT, kPassASmem, st>>>(fa, tm);
+      fa.par ^= 1;  // pass B and the next pass A read the r / s pass A wrote
       NI_LAUNCH_CHECK();
       for (int l = 1; l < L; ++l) {
         const Level& C = lev[l];
         const Level& N = lev[l + 1];
-        NI_COUNT_LAUNCH(), down_kernel<<<grid_for(N.n), 256, 0, st>>>(N.n, N.child, C.n, C.nbr,
-                                                                     C.cond, C.dinv, C.b, N.b);
+        NI_COUNT_LAUNCH(), down_kernel<<<grid_for(N.n), 256, 0, st>>>(
+                               N.n, N.child, C.n, C.nbr, C.cond, C.x1, C.b, N.dinv, N.b, N.x1);
         NI_LAUNCH_CHECK();
       }
       for (int l = L; l >= 1; --l) {
         const Level& C = lev[l];
-        if (l == L)
-          NI_COUNT_LAUNCH(), up_kernel<false><<<grid_for(C.n), 256, 0, st>>>(
-                                 C.n, C.nbr, C.cond, C.dinv, C.b, nullptr, nullptr, C.e);
-        else
+        const float* xs = l == L ? C.x1 : C.x2;
+        if (l >= 2)
           NI_COUNT_LAUNCH(), up_kernel<true><<<grid_for(C.n), 256, 0, st>>>(
-                                 C.n, C.nbr, C.cond, C.dinv, C.b, C.parent, lev[l + 1].e, C.e);
+                                 C.n, C.nbr, C.cond, C.dinv, C.b, xs, nullptr, C.child,
+                                 lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
+        else
+          NI_COUNT_LAUNCH(), up_kernel<false><<<grid_for(C.n), 256, 0, st>>>(
+                                 C.n, C.nbr, C.cond, C.dinv, C.b, xs, C.e, nullptr, nullptr,
+                                 nullptr, 0);
         NI_LAUNCH_CHECK();
       }
-      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b_kernel<8><<<NA, NT, kPassBSmem, st>>>(fa);
-      else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa);
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b_kernel<8><<<NA, NT, kPassBSmem, st>>>(fa, tm);
+      else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa, tm);
       NI_LAUNCH_CHECK();
       NI_CUDA_TRY(cudaMemsetAsync(f.counters + 6, 0, sizeof(int32_t), st));
       NI_COUNT_LAUNCH(), scalar_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(sa);

@@ -60,14 +60,20 @@ def main():
         scs = [scenes.config5_map(i) for i in range(n)]
         nm = nb.NormalMap.create(np.stack([s.normals for s in scs]), np.stack([s.mask for s in scs]))
         intr = [nb.CameraIntrinsics(*s.intrinsics()) for s in scs]
-        for rep in range(2):
+        prev = None
+        for rep in range(3):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             rs = nb.run_pipeline_batch(nm, intr, THETA)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            its = [int(r.fill_iterations.max()) for r in rs]
+            filled = torch.cat([r.filled.values_t for r in rs])
+            same = None if prev is None else bool(torch.equal(prev, filled))
+            prev = filled
             print(f"batch {n}: step {dt*1e3:.1f} ms fill-loop {rs[0].fill_report['cg_ms']:.2f} ms "
-                  f"mg {rs[0].fill_report.get('mg')} -> {n * 1048576 / dt / 1e6:.1f} M px/s",
+                  f"mg {rs[0].fill_report.get('mg')} -> {n * 1048576 / dt / 1e6:.1f} M px/s "
+                  f"fill iters max {max(its)} mean {np.mean(its):.1f} rerun-identical {same}",
                   flush=True)
 
 
