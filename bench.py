@@ -41,10 +41,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_PX_ITER = 37  # paper_2510_11508_b200/csrc/ni_fill.cu header (single-sweep CG)
-# canonical bytes per px-iteration of a two-sweep PCG at 8-conn
-# (56 + 4 K_f); the single-sweep kernel needs only BYTES_PER_PX_ITER of them.
-SURVEY_BYTES_PER_PX_ITER = 72
+# Algorithmic HBM bytes per active unit pixel per V-cycle of the two fine
+# passes of the multigrid-preconditioned CG (8-connectivity):
+#  pass A reads r, s, w, dinv, hw, u, p, x (8 x f32), slot (u16), par0 (i32),
+#         imask (u8) = 39 B, writes p, x, r', s' = 16 B, and the level-1
+#         restriction b1, x1 (2 x f32 per 2x2 block) + its dinv1 read = 3 B;
+#  pass B reads r, dinv, hw, par0 (4 x 4 B), imask, slot = 19 B and the
+#         level-1 correction e1 (1 B), writes u, w = 8 B.
+PASS_A_BYTES = 58
+PASS_B_BYTES = 28
 SURVEY_PEAK_GBS = 8000.0  # SURVEY.md 8(d) north-star denominator
 THETA_DEG = 3.5
 
@@ -157,6 +162,51 @@ def traffic_from_profile():
         return None
 
 
+def mg_roofline(fills, step_ms):
+    """Roofline of the multigrid fill's dominant fine pass: algorithmic bytes
+    (PASS_*_BYTES x active unit pixels, summed over the V-cycles of every
+    timed step) over its CUDA-event time on the fill's stream."""
+    prof = [f["mg_profile"] for f in fills]
+    pxv = float(np.mean([p["px_vcycles"] for p in prof]))
+    vcyc = float(np.mean([f["mg"]["vcycles"] for f in fills]))
+    t = {k: float(np.mean([p[k] for p in prof]))
+         for k in ("pass_a_ms", "pass_b_ms", "coarse_ms", "scalar_ms")}
+    peak, peak_src = measured_peak()
+    passes = {}
+    for name, key, nbytes in (("pass_a_kernel<8>", "pass_a_ms", PASS_A_BYTES),
+                              ("pass_b_kernel<8>", "pass_b_ms", PASS_B_BYTES)):
+        ms_k = t[key]
+        ach = nbytes * pxv / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
+        passes[name] = {"ms_per_step": round(ms_k, 3), "bytes_per_px_vcycle": nbytes,
+                        "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4)}
+    top = max(passes, key=lambda k: passes[k]["ms_per_step"])
+    nbytes = passes[top]["bytes_per_px_vcycle"]
+    launches = max(vcyc, 1.0)
+    prof_traffic = traffic_from_profile()
+    traffic = None
+    if prof_traffic and top in prof_traffic:
+        traffic = round(prof_traffic[top]["dram_bytes_per_px"] * pxv / launches)
+    fine_ms = t["pass_a_ms"] + t["pass_b_ms"]
+    fine_ach = (PASS_A_BYTES + PASS_B_BYTES) * pxv / (fine_ms * 1e-3) / 1e9 if fine_ms else 0.0
+    return {
+        "kernel": top + " (fine pass of the multigrid-preconditioned CG fill)",
+        "bound": "hbm", "achieved": passes[top]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+        "frac": passes[top]["frac"], "peak_source": peak_src,
+        "traffic": traffic,
+        "traffic_note": (prof_traffic["source"] if prof_traffic else "no ncu capture committed"),
+        "alg_bytes_per_launch": round(nbytes * pxv / launches),
+        "bytes_per_px_vcycle": nbytes,
+        "px_vcycles_per_step": pxv, "vcycles_per_step": vcyc,
+        "kernel_ms_per_launch": round(passes[top]["ms_per_step"] / launches, 4),
+        "kernel_share_of_step": round(passes[top]["ms_per_step"] / step_ms, 4),
+        "passes": passes,
+        "fine_passes": {"achieved_gbs": round(fine_ach, 1), "frac": round(fine_ach / peak, 4),
+                        "frac_vs_8tbs": round(fine_ach / SURVEY_PEAK_GBS, 4),
+                        "share_of_step": round(fine_ms / step_ms, 4)},
+        "stage_ms_per_step": {k: round(v, 3) for k, v in t.items()},
+    }
+
+
 # ------------------------------------------------------------------ our arm
 
 
@@ -233,10 +283,12 @@ def run_ours(args, rank, world, local_rank):
         fills.append(res[0].fill_report)
         iters.append(max(r.iterations for r in res))
 
+    _lib.set_fill_profiling(True)
     launches0 = _lib.launch_count()
     with ClockSampler(local_rank) as clk:
         ms = timed(step_device, args.steps, rec)
     launches = _lib.launch_count() - launches0
+    _lib.set_fill_profiling(False)
     clocks = clk.summary()
 
     # e2e through host buffers
@@ -245,36 +297,12 @@ def run_ours(args, rank, world, local_rank):
     e2e_steps = max(2, min(args.steps, 5))
     e2e_ms = timed(lambda: run_e2e(e2e_steps), 1, lambda r: None) / e2e_steps
 
-    from paper_2510_11508_b200.shard import aggregate
-    valid_total, _ = aggregate(valid_local, ms, dev)
+    from paper_2510_11508_b200.shard import gather_stats, whole_job
+    stats = gather_stats(valid_local, ms, max(iters), B, dev)
+    valid_total, ms = whole_job(stats)
 
-    # roofline of the dominant kernel
-    cg_ms = float(np.mean([f["cg_ms"] for f in fills]))
-    px_iters = float(np.mean([f["px_iters"] for f in fills]))
-    alg_bytes = BYTES_PER_PX_ITER * px_iters
-    achieved = alg_bytes / (cg_ms * 1e-3) / 1e9
-    peak, peak_src = measured_peak()
-    prof = traffic_from_profile()
-    roofline = {
-        "kernel": "fill_cg_kernel (persistent batched CG, one launch per step)",
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "peak_source": peak_src,
-        "traffic": (round(prof["dram_bytes_per_px_iter"] * px_iters) if prof else None),
-        "traffic_note": ((prof["source"] + "; " + prof["note"]) if prof else
-                         "no ncu capture committed"),
-        "alg_bytes_per_launch": alg_bytes, "bytes_per_px_iter": BYTES_PER_PX_ITER,
-        "survey_units": {
-            "bytes_per_px_iter": SURVEY_BYTES_PER_PX_ITER,
-            "achieved": round(SURVEY_BYTES_PER_PX_ITER * px_iters / (cg_ms * 1e-3) / 1e9, 1),
-            "peak": SURVEY_PEAK_GBS,
-            "note": "px-iterations/s x the SURVEY 8(d) two-sweep figure (72 B at 8-conn); the "
-                    "single-sweep CG moves 37 B per px-iteration, so this exceeds what a "
-                    "two-sweep PCG could reach at the same HBM traffic"},
-        "px_iters_per_launch": px_iters, "kernel_ms": round(cg_ms, 3),
-        "kernel_share_of_step": round(cg_ms / ms, 4),
-        "fill_grid_ctas": fills[0]["grid"], "max_cg_iters": fills[0]["max_iters"],
-    }
-
+    # roofline of the dominant kernel: the fine passes of the multigrid fill
+    roofline = mg_roofline(fills, ms)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(normals_h[0], masks_h[0], intr_t[0], merge_freq)
@@ -296,17 +324,12 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f32 CG vectors / f64 coefficients, dots, scales",
             "data": "synthetic (seeded generators, paper_2510_11508_b200/scenes.py)",
             "config": {
-                "workload": desc,
-                "maps_total": total_maps,
+                **workload_config(args, world, merge_freq),
                 "maps_per_rank": B,
                 "valid_px_total": valid_total,
-                "theta_c_deg": THETA_DEG,
-                "connectivity": 8,
-                "model": "milano",
-                "reweighting": "soft",
-                "merge_freq": merge_freq,
-                "l2": "inputs larger than L2 (working set ~25 B/px x 67 M px)",
-                "parallelism": f"maps sharded over {world} rank(s), no data-path collective",
+                "per_rank": [{"maps": int(r["maps"]), "valid_px": int(r["valid_px"]),
+                              "ms_per_step": round(r["ms"], 3),
+                              "outer_iterations": int(r["outer_iters"])} for r in stats],
             },
             "e2e": {"value": round(valid_total / (e2e_ms * 1e-3), 1), "unit": "valid_px/s",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
@@ -344,35 +367,41 @@ def cpu_baseline(normals, mask, intr, merge_freq):
                       f"oracle/normint_oracle.py run_pipeline, {dt:.1f} s"}
 
 
+def _oracle_c5(index):
+    """One C5 map through the oracle port; the map is generated first, only
+    the pipeline is timed."""
+    return _oracle_one((*_gen_c5(index), None))
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     import concurrent.futures as cf
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     procs = max(1, min(ncpu, args.maps if args.config == "C5" else 1))
-    if args.config == "C5":
-        payloads = [(*_gen_c5(i), None) for i in range(procs)]
-    else:
-        n, m, i, mf = _gen_cfg(args.config)
-        payloads = [(n, m, i, mf)]
-    warm = min(args.warmup, 1)
-    times = []
+    warm = args.warmup
     # one single-threaded process per core: pin every BLAS / OpenMP pool
     # before the workers start (they are spawned, so they inherit this env)
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS",
                 "NUMEXPR_NUM_THREADS"):
         os.environ[var] = "1"
     import multiprocessing as mp
+    times, valids = [], []
     with cf.ProcessPoolExecutor(max_workers=procs, mp_context=mp.get_context("spawn")) as ex:
         for s in range(warm + args.steps):
-            t = time.perf_counter()
-            out = list(ex.map(_oracle_one, payloads))
-            dt = time.perf_counter() - t
+            if args.config == "C5":
+                # step s takes the next `procs` maps of the batch, so the
+                # timed steps sweep the whole 64-map workload in turn
+                idx = [(s * procs + k) % args.maps for k in range(procs)]
+                out = list(ex.map(_oracle_c5, idx))
+            else:
+                n, m, i, mf = _gen_cfg(args.config)
+                out = list(ex.map(_oracle_one, [(n, m, i, mf)]))
             if s >= warm:
-                times.append(dt)
-    valid = sum(v for _, v in out)
+                times.append(max(dt for dt, _ in out))  # the processes run side by side
+                valids.append(sum(v for _, v in out))
     ms = 1e3 * float(np.mean(times))
-    value = valid / (ms * 1e-3)
+    value = float(np.sum(valids)) / float(np.sum(times))
     line = {
         "impl": "reference",
         "metric": "valid pixels/s end-to-end (component normal integration, run_pipeline)",
@@ -380,22 +409,84 @@ def run_reference(args, rank, world):
         "warmup": warm, "ms_per_step": round(ms, 1), "higher_is_better": True,
         "scaling": "strong" if args.config == "C5" else "replicas", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generators, paper_2510_11508_b200/scenes.py)",
-        "config": {"workload": make_desc(args), "maps_per_step": procs},
+        "config": workload_config(args, world, None if args.config == "C5" else
+                                  _gen_cfg(args.config)[3]),
         "cpu_baseline": {"value": round(value, 1), "unit": "valid_px/s", "cores": procs,
                          "kind": "port",
                          "sample": f"{procs} map(s) per step, one process per core "
                                    f"(oracle/normint_oracle.py; the reference is pure Python and "
-                                   f"cannot be installed on the GPU box)"},
+                                   f"cannot be installed on the GPU box); step s runs maps "
+                                   f"s*{procs} .. s*{procs}+{procs - 1} (mod {args.maps}), so the "
+                                   f"warm-up + timed steps sweep the batch"},
         "e2e": {"value": round(value, 1), "unit": "valid_px/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def relaunch(nproc: int) -> int:
+    """`bench.py --gpus N` started without a launcher: re-run this command
+    under torch.distributed.run, one rank per GPU on this node."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world):
+    """The multi-rank plumbing of run_ours without a GPU: map split, one gloo
+    process group, the stats all_gather and the whole-job aggregate."""
+    import torch.distributed as dist
+
+    from paper_2510_11508_b200.shard import gather_stats, map_range, whole_job
+    if world > 1:
+        dist.init_process_group("gloo")
+    try:
+        lo, hi = map_range(rank, world, args.maps)
+        t = time.perf_counter()
+        valid = 0
+        for i in range(lo, hi):
+            _, m, _ = _gen_c5(i)
+            valid += int(m.sum())
+        ms = 1e3 * (time.perf_counter() - t)
+        stats = gather_stats(valid, ms, 1, hi - lo)
+        valid_total, ms_max = whole_job(stats)
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "value": valid_total / ms_max * 1e3,
+                              "config": {"maps_total": args.maps, "valid_px_total": valid_total,
+                                         "per_rank": [{"maps": int(r["maps"]),
+                                                       "valid_px": int(r["valid_px"])}
+                                                      for r in stats]}}), flush=True)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+def workload_config(args, world, merge_freq):
+    """The config keys both arms report for the same workload."""
+    return {
+        "workload": make_desc(args),
+        "maps_total": args.maps if args.config == "C5" else 1,
+        "theta_c_deg": THETA_DEG,
+        "connectivity": 8,
+        "model": "milano",
+        "reweighting": "soft",
+        "merge_freq": merge_freq,
+        "l2": ("inputs larger than L2 (working set ~25 B/px x 67 M px)" if args.config == "C5"
+               else "single-map config (a parity/latency line, not the bench workload)"),
+        "parallelism": f"maps sharded over {world} rank(s), no data-path collective",
+    }
+
+
 def make_desc(args):
     if args.config == "C5":
         return f"C5: {args.maps} x 1024x1024 orthographic maps (seeds 100..{99 + args.maps}), 16 Voronoi cells"
-    return args.config
+    return f"{args.config} (paper_2510_11508_b200/scenes.py)"
 
 
 def main():
@@ -407,13 +498,20 @@ def main():
     ap.add_argument("--config", default="C5", choices=("C1", "C2", "C3", "C4", "C5"))
     ap.add_argument("--maps", type=int, default=64, help="C5 batch size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / gather plumbing only: gloo, no GPU work (CPU tests)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.dry_run:
+        dry_run(args, rank, world)
         return
     if world > 1:
         import torch

@@ -142,6 +142,13 @@ int ni_fill_mg(const int32_t* labels, int count, const double* omega_a, const do
 /* Multigrid statistics of the last ni_fill_mg on the calling thread: coarse
  * levels, V-cycles run, unknowns per level (n_per_level[16], index 1..levels). */
 int ni_fill_mg_last_report(int* levels, int* vcycles, int* n_per_level);
+/* Measurement hook (not part of the reference interface): while on, ni_fill_mg
+ * brackets each V-cycle's pass A, coarse levels, pass B and scalar step with
+ * CUDA events on the call's stream and counts the active unit pixels of every
+ * V-cycle; ni_fill_mg_last_profile returns the four summed times (ms4[4]) and
+ * that pixel count.  Off by default; per calling thread. */
+int ni_set_fill_profiling(int on);
+int ni_fill_mg_last_profile(double* ms4, long long* px_vcycles);
 
 /* Directed weights of every forward pixel edge at log-depth state z
  * (continuity.py:292-331, solver.py:253-278): wmode 0 = valid (uniform,

@@ -13,12 +13,27 @@ from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, depth_from_logde
 from .pipeline import (BaselineResult, Partition, PipelineResult, dot_cutoff, run_pipeline,
                        run_pipeline_batch, run_pipeline_stream, run_pixel_baseline,
                        run_pixel_baseline_batch)
+from .seams import (EdgeCoefficients, PixelGraph, QuotientGraph, ScaleStep, apply_scales,
+                    build_edge_coefficients, build_pixel_graph, build_quotient, fill_components,
+                    form_components, merge_components, relative_scale_step)
 from .settings import SolveSettings, WeightParams
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BaselineResult",
+    "EdgeCoefficients",
+    "PixelGraph",
+    "QuotientGraph",
+    "ScaleStep",
+    "apply_scales",
+    "build_edge_coefficients",
+    "build_pixel_graph",
+    "build_quotient",
+    "fill_components",
+    "form_components",
+    "merge_components",
+    "relative_scale_step",
     "CameraIntrinsics",
     "DegenerateEdge",
     "DeviceError",

@@ -49,6 +49,8 @@ SIGNATURES = {
     "ni_fill_mg": ([_P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ, _PSZ,
                     _P], _I),
     "ni_fill_mg_last_report": ([_PI32, _PI32, _PI32], _I),
+    "ni_set_fill_profiling": ([_I], _I),
+    "ni_fill_mg_last_profile": ([C.POINTER(C.c_double), C.POINTER(C.c_longlong)], _I),
     "ni_edge_weights": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D, _P, _P, _P],
                         _I),
     "ni_pair_energy_workspace_size": ([_I, _PSZ], _I),
@@ -129,6 +131,22 @@ def mg_report() -> dict:
     n = (C.c_int32 * 16)()
     load().ni_fill_mg_last_report(C.byref(lv), C.byref(vc), n)
     return {"levels": lv.value, "vcycles": vc.value, "unknowns": [n[i] for i in range(1, lv.value + 1)]}
+
+
+def set_fill_profiling(on: bool) -> None:
+    """Bracket the multigrid fill's stages with CUDA events (measurement only)."""
+    check(load().ni_set_fill_profiling(int(bool(on))), "ni_set_fill_profiling")
+
+
+def mg_profile() -> dict:
+    """Per-stage device time of the last profiled ni_fill_mg on this thread:
+    pass A, coarse levels, pass B, scalar step (ms summed over V-cycles), and
+    the active unit pixels summed over V-cycles."""
+    ms = (C.c_double * 4)()
+    pxv = C.c_longlong(0)
+    load().ni_fill_mg_last_profile(ms, C.byref(pxv))
+    return {"pass_a_ms": ms[0], "coarse_ms": ms[1], "pass_b_ms": ms[2], "scalar_ms": ms[3],
+            "px_vcycles": pxv.value}
 
 
 def fill_report() -> dict:

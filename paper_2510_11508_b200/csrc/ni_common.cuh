@@ -31,7 +31,14 @@ struct FillReport {
   int mg_levels;       // multigrid fill: coarse levels used
   int mg_vcycles;      // multigrid fill: V-cycles (PCG iterations + 1 of the longest unit)
   int mg_n[16];        // multigrid fill: unknowns per level (index 1..levels)
+  // multigrid fill, filled only while profiling is on (ni_set_fill_profiling):
+  // CUDA-event time summed over the V-cycles of pass A, the coarse levels,
+  // pass B and the per-unit scalar step, and the active unit pixels summed
+  // over V-cycles (the algorithmic work of the fine passes)
+  double mg_ms[4];
+  long long mg_px_vcycles;
 };
+extern thread_local int g_fill_profile;
 extern thread_local FillReport g_fill_report;
 
 #define NI_CUDA_TRY(expr)                                                              \

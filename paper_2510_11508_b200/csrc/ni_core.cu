@@ -10,6 +10,7 @@ namespace ni {
 static thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 thread_local FillReport g_fill_report{};
+thread_local int g_fill_profile = 0;
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -68,5 +69,18 @@ extern "C" int ni_fill_mg_last_report(int* levels, int* vcycles, int* n_per_leve
   if (vcycles) *vcycles = r.mg_vcycles;
   if (n_per_level)
     for (int l = 0; l < 16; ++l) n_per_level[l] = r.mg_n[l];
+  return NI_OK;
+}
+
+extern "C" int ni_set_fill_profiling(int on) {
+  ni::g_fill_profile = on != 0;
+  return NI_OK;
+}
+
+extern "C" int ni_fill_mg_last_profile(double* ms4, long long* px_vcycles) {
+  const ni::FillReport& r = ni::g_fill_report;
+  if (ms4)
+    for (int k = 0; k < 4; ++k) ms4[k] = r.mg_ms[k];
+  if (px_vcycles) *px_vcycles = r.mg_px_vcycles;
   return NI_OK;
 }

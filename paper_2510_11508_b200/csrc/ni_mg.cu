@@ -1349,6 +1349,7 @@ struct ScalarArgs {
   float* beta;
   float* umean;
   int32_t* nactive;
+  unsigned long long* px_done;  // pixels of the units this V-cycle processed
   int trace_unit;  // debug: print this unit's scalars every iteration (-1: off)
 };
 
@@ -1364,8 +1365,10 @@ __global__ void __launch_bounds__(256) scalar_kernel(const __grid_constant__ Sca
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   int act = 0;
+  unsigned long long pxd = 0;
   for (int u = gw; u < a.nu; u += nw) {
     if (a.status[u] != U_ACTIVE) continue;  // warp-uniform
+    pxd += (unsigned long long)a.unit_n[u];
     double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int k = a.pstart[u] + lane; k < a.pstart[u + 1]; k += 32) {
       const double* pp = a.partial + NPART * int64_t(a.plist[k]);
@@ -1419,6 +1422,7 @@ __global__ void __launch_bounds__(256) scalar_kernel(const __grid_constant__ Sca
   }
   act = warp_sum_int(act);
   if (lane == 0 && act) atomicAdd(a.nactive, act);
+  if (lane == 0 && pxd) atomicAdd(a.px_done, pxd);  // lanes of a warp agree on pxd
 }
 
 // ---- output: x minus its per-unit mean (the gauge of CG from x0 = 0)
@@ -1642,6 +1646,27 @@ int make_tma_maps(TmaMaps& tm, const Geo& g, const MgFixed& f) {
   return NI_OK;
 }
 
+// Events of the calling thread, created once per device (not per call).
+struct EventPool {
+  int dev = -1;
+  cudaEvent_t ev[7];
+};
+thread_local EventPool g_events;
+
+int thread_events(cudaEvent_t** out) {
+  int dev = 0;
+  NI_CUDA_TRY(cudaGetDevice(&dev));
+  if (g_events.dev != dev) {
+    if (g_events.dev >= 0)
+      for (cudaEvent_t e : g_events.ev) cudaEventDestroy(e);
+    g_events.dev = -1;
+    for (cudaEvent_t& e : g_events.ev) NI_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDefault));
+    g_events.dev = dev;
+  }
+  *out = g_events.ev;
+  return NI_OK;
+}
+
 }  // namespace
 
 extern "C" int ni_fill_mg_workspace_size(int B, int H, int W, int connectivity, int count,
@@ -1684,16 +1709,12 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   };
   if (!workspace || !cv.ok())
     return too_small(size_t(level_estimate(g) * kBytesPerUnknown + g.npix * 2));
-  cudaEvent_t e0, e1;
-  NI_CUDA_TRY(cudaEventCreateWithFlags(&e0, cudaEventDefault));
-  NI_CUDA_TRY(cudaEventCreateWithFlags(&e1, cudaEventDefault));
-  struct EvGuard {
-    cudaEvent_t a, b;
-    ~EvGuard() {
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
-    }
-  } evg{e0, e1};
+  cudaEvent_t* ev = nullptr;  // [0], [1]: the PCG loop; [2..6]: one V-cycle's stages
+  NI_TRY(thread_events(&ev));
+  const cudaEvent_t e0 = ev[0], e1 = ev[1];
+  const bool prof = g_fill_profile != 0;
+  double stage_ms[4] = {0.0, 0.0, 0.0, 0.0};
+  long long px_vcycles = 0;
   const int npb = grid_for(g.npix);
   const size_t npad = size_t(g.npad);
   // ---- fine planes
@@ -1945,6 +1966,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   sa.alpha = ualpha;
   sa.beta = ubeta;
   sa.nactive = f.counters + 6;
+  sa.px_done = reinterpret_cast<unsigned long long*>(f.counters + 8);
   {
     const char* tr = getenv("NI_MG_TRACE");
     sa.trace_unit = tr ? atoi(tr) : -1;
@@ -1964,10 +1986,12 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   NI_CUDA_TRY(cudaEventRecord(e0, st));
   if (NA > 0) {
     while (true) {
+      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[2], st));
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a_kernel<8><<<NA, NT, kPassASmem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_a_kernel<4><<<NA, NT, kPassASmem, st>>>(fa, tm);
       fa.par ^= 1;  // pass B and the next pass A read the r / s pass A wrote
       NI_LAUNCH_CHECK();
+      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[3], st));
       for (int l = 1; l < L; ++l) {
         const Level& C = lev[l];
         const Level& N = lev[l + 1];
@@ -1988,17 +2012,31 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                                  nullptr, 0);
         NI_LAUNCH_CHECK();
       }
+      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b_kernel<8><<<NA, NT, kPassBSmem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa, tm);
       NI_LAUNCH_CHECK();
-      NI_CUDA_TRY(cudaMemsetAsync(f.counters + 6, 0, sizeof(int32_t), st));
+      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[5], st));
+      // counters [6] active units, [8..9] processed unit pixels (u64)
+      NI_CUDA_TRY(cudaMemsetAsync(f.counters + 6, 0, 4 * sizeof(int32_t), st));
       NI_COUNT_LAUNCH(), scalar_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(sa);
       NI_LAUNCH_CHECK();
+      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[6], st));
       ++vcycles;
-      int32_t nact = 0;
-      NI_CUDA_TRY(cudaMemcpyAsync(&nact, f.counters + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      int32_t hv[4] = {0, 0, 0, 0};
+      NI_CUDA_TRY(cudaMemcpyAsync(hv, f.counters + 6, sizeof(hv), cudaMemcpyDeviceToHost, st));
       NI_CUDA_TRY(cudaStreamSynchronize(st));
-      if (nact == 0) break;
+      if (prof) {
+        unsigned long long pxd;
+        memcpy(&pxd, hv + 2, sizeof(pxd));
+        px_vcycles += (long long)pxd;
+        for (int k = 0; k < 4; ++k) {
+          float t = 0.f;
+          NI_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 + k], ev[3 + k]));
+          stage_ms[k] += t;
+        }
+      }
+      if (hv[0] == 0) break;
     }
   }
   NI_CUDA_TRY(cudaEventRecord(e1, st));
@@ -2035,6 +2073,8 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   rep.npartials = NS;
   rep.mg_levels = L;
   rep.mg_vcycles = vcycles;
+  for (int k = 0; k < 4; ++k) rep.mg_ms[k] = prof ? stage_ms[k] : 0.0;
+  rep.mg_px_vcycles = prof ? px_vcycles : 0;
   for (int l = 0; l < 16; ++l) rep.mg_n[l] = l >= 1 && l <= L ? lev[l].n : 0;
   return NI_OK;
 }

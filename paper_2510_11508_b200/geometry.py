@@ -159,6 +159,23 @@ class NormalMap:
         _lib.check(st, "NormalMap.create")
         return cls(n_soa, valid, h, w, batch, int(stats[0].item()))
 
+    @classmethod
+    def from_unit(cls, normals, mask, device=None) -> "NormalMap":
+        """Upload normals that a reference ``NormalMap.create`` already
+        validated and renormalised, bit for bit (no second renormalisation:
+        n / |n| of a float64 unit vector can move its last bit)."""
+        dev = _device(device)
+        n = np.asarray(normals, dtype=np.float64)
+        m = np.asarray(mask, dtype=bool)
+        if n.ndim != 3 or n.shape[2] != 3 or m.shape != n.shape[:2]:
+            raise ValueError("normals must have shape (H, W, 3) and mask (H, W)")
+        h, w = m.shape
+        n_soa = torch.from_numpy(np.ascontiguousarray(n.reshape(-1, 3).T)).to(dev)
+        valid = torch.from_numpy(m.reshape(-1).astype(np.uint8)).to(dev)
+        n_soa = torch.where(valid.bool()[None, :], n_soa, torch.zeros((), dtype=torch.float64,
+                                                                       device=dev))
+        return cls(n_soa.contiguous(), valid, h, w, 1, int(m.sum()))
+
     def flipped(self) -> "NormalMap":
         """All valid normals negated (geometry.py:147-152)."""
         n = torch.where(self.valid_t.bool()[None, :], -self.n_soa, torch.zeros_like(self.n_soa))
@@ -169,6 +186,25 @@ class NormalMap:
         hw = self.height * self.width
         return NormalMap(self.n_soa[:, m * hw:(m + 1) * hw], self.valid_t[m * hw:(m + 1) * hw],
                          self.height, self.width, 1)
+
+
+def as_normal_map(nmap, device=None) -> NormalMap:
+    """This package's NormalMap, or a reference ``normint.NormalMap`` (any
+    object with ``.normals`` (H, W, 3) and ``.mask`` (H, W), geometry.py:96-113)
+    uploaded as is."""
+    if isinstance(nmap, NormalMap):
+        return nmap
+    if hasattr(nmap, "normals") and hasattr(nmap, "mask"):
+        return NormalMap.from_unit(nmap.normals, nmap.mask, device)
+    raise TypeError(f"expected a NormalMap, got {type(nmap).__name__}")
+
+
+def as_intrinsics(intr) -> CameraIntrinsics:
+    """This package's CameraIntrinsics, or any object with fx, fy, cx, cy
+    (a reference ``normint.CameraIntrinsics``, geometry.py:31-48)."""
+    if isinstance(intr, CameraIntrinsics):
+        return intr
+    return CameraIntrinsics(float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy))
 
 
 def stack(maps: list[NormalMap]) -> NormalMap:

@@ -26,8 +26,9 @@ import torch
 
 from . import _lib
 from .errors import EmptyMask
-from .geometry import CameraIntrinsics, LogDepthMap, NormalMap, _device, _stream
-from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams
+from .geometry import (CameraIntrinsics, LogDepthMap, NormalMap, _device, _stream, as_intrinsics,
+                       as_normal_map)
+from .settings import CONTINUITY_MODELS, SolveSettings, WeightParams, as_settings, as_weights
 
 ENERGY_FLOOR = 1e-300  # pipeline.py:55
 # fill solver: "mg" (multigrid-preconditioned CG, default) or "cg" (the
@@ -379,6 +380,7 @@ class _BatchLoop:
             C.c_double(wp.outlier_high), C.c_double(st.cg_tol), int(st.cg_max_iters), _ptr(z),
             _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
             ws.numel(), g.s()), "relative_scale_step")
+        self.last_scales = scales
         return residual, wts
 
     def merge(self, residual, wts, merging: np.ndarray):
@@ -419,11 +421,13 @@ def run_pipeline_batch(
     PipelineResult per map, each identical in content to what
     ``run_pipeline`` returns for that map alone.
     """
-    settings = settings or SolveSettings()
-    weights = weights or WeightParams()
+    settings = as_settings(settings) or SolveSettings()
+    weights = as_weights(weights) or WeightParams()
     _validate(model, connectivity)
+    nmap = as_normal_map(nmap)
     B = nmap.batch
     intr = list(intrinsics) if isinstance(intrinsics, (list, tuple)) else [intrinsics] * B
+    intr = [as_intrinsics(i) for i in intr]
     if len(intr) != B:
         raise ValueError("need one CameraIntrinsics per map")
     records = [[] for _ in range(B)]
@@ -475,6 +479,7 @@ def run_pipeline_batch(
     report = _lib.fill_report()
     if _FILL_SOLVER != "cg":
         report["mg"] = _lib.mg_report()
+        report["mg_profile"] = _lib.mg_profile()
     fill_ms = _ms(t0)
     for m in range(B):
         records[m].append({"stage": "fill", "wall_ms": fill_ms})
@@ -688,6 +693,7 @@ def run_pipeline(
     in radians (None = per-pixel components), output gauge-fixed to unit
     median depth unless ``gauge_depth`` is given.
     """
+    nmap = as_normal_map(nmap)
     if nmap.batch != 1:
         raise ValueError("run_pipeline takes a single map; use run_pipeline_batch")
     return run_pipeline_batch(nmap, [intr], theta_c, settings, weights, connectivity, model,
@@ -721,11 +727,13 @@ def run_pixel_baseline_batch(
     with the inter-system weight schedule (pipeline.py:261-285) -- in one
     batched weighted-fill launch, and the solutions replace z.
     """
-    settings = settings or SolveSettings()
-    weights = weights or WeightParams()
+    settings = as_settings(settings) or SolveSettings()
+    weights = as_weights(weights) or WeightParams()
     _validate(model, connectivity)
+    nmap = as_normal_map(nmap)
     B = nmap.batch
     intr = list(intrinsics) if isinstance(intrinsics, (list, tuple)) else [intrinsics] * B
+    intr = [as_intrinsics(i) for i in intr]
     if len(intr) != B:
         raise ValueError("need one CameraIntrinsics per map")
     run_start = time.perf_counter()
@@ -736,6 +744,8 @@ def run_pixel_baseline_batch(
     valid = g.nmap.valid_t
     vbool = valid.bool()
     nvalid = valid.view(B, -1).sum(dim=1, dtype=torch.int64).cpu().numpy()
+    if (nvalid == 0).any():  # every map raises like the reference (graph.py:65-66)
+        raise EmptyMask("normal map has no valid pixel")
     mapid = (torch.arange(g.npix, device=g.dev, dtype=torch.int64) // g.hw).to(torch.int32)
     z = torch.zeros(g.npix, dtype=torch.float64, device=g.dev)
     records = [[] for _ in range(B)]
@@ -799,6 +809,7 @@ def run_pixel_baseline(
     """Iteratively reweighted per-pixel log-depth integration
     (pipeline.py:297-369): same weight schedule and convergence test as
     ``run_pipeline``, but the full pixel system is re-solved every iteration."""
+    nmap = as_normal_map(nmap)
     if nmap.batch != 1:
         raise ValueError("run_pixel_baseline takes a single map; use run_pixel_baseline_batch")
     return run_pixel_baseline_batch(nmap, [intr], settings, weights, connectivity, model,

@@ -56,3 +56,22 @@ class WeightParams:
     @property
     def mode_code(self) -> int:
         return REWEIGHTING_MODES.index(self.reweighting_mode)
+
+
+def _coerce(cls, obj):
+    if obj is None or isinstance(obj, cls):
+        return obj
+    from dataclasses import fields
+    return cls(**{f.name: getattr(obj, f.name) for f in fields(cls) if hasattr(obj, f.name)})
+
+
+def as_settings(obj) -> SolveSettings | None:
+    """This package's SolveSettings from a reference ``normint.SolveSettings``
+    (same field names, solver.py:26-49), or None."""
+    return _coerce(SolveSettings, obj)
+
+
+def as_weights(obj) -> WeightParams | None:
+    """This package's WeightParams from a reference ``normint.WeightParams``
+    (continuity.py:42-57), or None."""
+    return _coerce(WeightParams, obj)

@@ -1,10 +1,12 @@
 """Map-level data parallelism for batched runs (BASELINE.json config 5).
 
 Independent normal maps are split across ranks in contiguous blocks; there is
-no data-path collective.  The only collectives are the result aggregation of
-bench.py: a sum of valid pixels and a max of the per-rank device step time
-(the whole job takes as long as its slowest rank).  Works with any
-torch.distributed backend (NCCL on the GPUs, gloo in the CPU tests).
+no data-path collective.  The only collective is the result gather of
+bench.py: one all_gather of every rank's (valid pixels, device step ms, outer
+iterations, maps) row, from which rank 0 forms the whole-job numbers (valid
+pixels summed, the step taking as long as its slowest rank).  Works with any
+torch.distributed backend (NCCL over NVLink on the GPUs, gloo in the CPU
+tests).
 """
 
 from __future__ import annotations
@@ -30,3 +32,26 @@ def aggregate(valid_local: int, ms_local: float, device=None) -> tuple[int, floa
     dist.all_reduce(v, op=dist.ReduceOp.SUM)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return int(v.item()), float(t.item())
+
+
+STAT_FIELDS = ("valid_px", "ms", "outer_iters", "maps")
+
+
+def gather_stats(valid_px: int, ms: float, outer_iters: int, maps: int, device=None) -> list[dict]:
+    """all_gather of each rank's step statistics; returns one dict per rank
+    (rank order).  A single process returns its own row."""
+    row = [float(valid_px), float(ms), float(outer_iters), float(maps)]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        rows = [row]
+    else:
+        dev = device if device is not None else torch.device("cpu")
+        mine = torch.tensor(row, dtype=torch.float64, device=dev)
+        out = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, mine)
+        rows = [o.cpu().tolist() for o in out]
+    return [dict(zip(STAT_FIELDS, r)) for r in rows]
+
+
+def whole_job(stats: list[dict]) -> tuple[int, float]:
+    """(valid pixels over all ranks, the slowest rank's step ms)."""
+    return int(sum(s["valid_px"] for s in stats)), float(max(s["ms"] for s in stats))

@@ -61,3 +61,35 @@ def test_two_rank_gloo_aggregation():
     for _, _, _, total, ms in out:
         assert total == expect_total
         assert ms == 20.0  # the slowest rank
+
+
+def test_gather_stats_single_process():
+    from paper_2510_11508_b200.shard import gather_stats, whole_job
+
+    st = gather_stats(123, 4.5, 7, 2)
+    assert st == [{"valid_px": 123.0, "ms": 4.5, "outer_iters": 7.0, "maps": 2.0}]
+    assert whole_job(st) == (123, 4.5)
+
+
+def test_bench_launcher_two_ranks_gloo():
+    """`bench.py --gpus 2` without WORLD_SIZE re-launches itself under
+    torch.distributed.run; the ranks split the maps, all_gather their stats
+    and rank 0 alone prints the whole-job line (gloo, no GPU work)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--maps", "4", "--dry-run"], capture_output=True, text=True,
+                         timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = lines[0]
+    assert line["n_gpus"] == 2
+    ranks = line["config"]["per_rank"]
+    assert [r["maps"] for r in ranks] == [2, 2]
+    assert line["config"]["valid_px_total"] == sum(r["valid_px"] for r in ranks)

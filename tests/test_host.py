@@ -129,3 +129,66 @@ def test_bench_reference_arm_line():
         assert key in line, key
     assert line["value"] > 0 and line["e2e"]["value"] == line["value"]
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_cli_flags_map_to_settings_like_the_reference():
+    """RunConfig mapping of `integrate` (cli.py:28-75, 104-128), no GPU needed."""
+    from paper_2510_11508_b200 import cli
+
+    ap = cli.build_parser()
+    a = ap.parse_args(["integrate", "--normals", "n.pfm", "--intrinsics", "i.json", "--output",
+                       "o.pfm", "--theta-c", "none", "--merge-freq", "4", "--reweighting", "hard",
+                       "--k", "3", "--max-iters", "9", "--alignment-iters", "1",
+                       "--delta-e-max", "1e-4", "--connectivity", "4",
+                       "--continuity-model", "bini", "--workers", "2"])
+    cfg = cli.RunConfig.from_args(a)
+    assert cfg.theta_c is None and cfg.connectivity == 4 and cfg.continuity_model == "bini"
+    st, wp = cfg.solve_settings(), cfg.weight_params()
+    assert (st.freq_merging, st.max_iters, st.alignment_iters, st.delta_e_max, st.worker_count) \
+        == (4, 9, 1, 1e-4, 2)
+    assert (wp.reweighting_mode, wp.k) == ("hard", 3.0)
+    d = cli.RunConfig.from_args(ap.parse_args(["integrate", "--normals", "n", "--intrinsics", "i",
+                                               "--output", "o", "--merge-freq", "off"]))
+    assert d.merge_freq is None and abs(d.theta_c - np.deg2rad(3.5)) == 0
+    assert cli.main(["integrate", "--normals", "n"]) == 2  # usage error
+    assert cli.main(["integrate", "--normals", "n", "--intrinsics", "i", "--output", "o",
+                     "--merge-freq", "0"]) == 2
+
+
+def test_reference_settings_objects_are_coerced():
+    from dataclasses import dataclass
+
+    from paper_2510_11508_b200.geometry import as_intrinsics
+    from paper_2510_11508_b200.settings import as_settings, as_weights
+
+    @dataclass(frozen=True)
+    class RefSettings:  # normint.solver.SolveSettings fields
+        cg_tol: float = 1e-7
+        cg_max_iters: int = 100
+        delta_e_max: float = 1e-3
+        max_iters: int = 7
+        alignment_iters: int = 2
+        freq_merging: int | None = 2
+        worker_count: int = 1
+        refill_reweighted: bool = True
+
+    st = as_settings(RefSettings())
+    assert (st.cg_tol, st.cg_max_iters, st.max_iters, st.freq_merging, st.refill_reweighted) == \
+        (1e-7, 100, 7, 2, True)
+
+    class W:
+        k, outlier_low, outlier_high, reweighting_mode = 1.5, 1e-6, 1e-2, "off"
+
+    assert as_weights(W()).mode_code == 0 and as_weights(None) is None
+
+    class I:
+        fx, fy, cx, cy = 10.0, 11.0, 3.0, 4.0
+
+    assert as_intrinsics(I()).as_tuple() == (10.0, 11.0, 3.0, 4.0)
+    try:
+        import normint  # the real reference, when importable (build container)
+    except ImportError:
+        return
+    ref = normint.SolveSettings(freq_merging=3)
+    assert as_settings(ref).freq_merging == 3
+    assert as_intrinsics(normint.CameraIntrinsics(5.0, 5.0, 1.0, 2.0)).cx == 1.0
