@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
     const int m = int(i / per_map);
     const double fx = intr[4 * m + 0], fy = intr[4 * m + 1];
     const double cx = intr[4 * m + 2], cy = intr[4 * m + 3];
-    const int u = int(i % W);
-    const int vloc = int((i / W) % H);
+    const int u = int(uint32_t(i) % uint32_t(W));
+    const int vloc = int((uint32_t(i) / uint32_t(W)) % uint32_t(H));
     uint8_t flags = 0;
     double g = 0.0;
     double om_a[KF], om_b[KF];

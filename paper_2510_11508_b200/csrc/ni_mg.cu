@@ -168,9 +168,9 @@ __global__ void __launch_bounds__(256) prep_kernel(
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t lab = labels[i];
     if (lab < 0) continue;
-    const int u = int(i % W);
-    const int64_t row = i / W;
-    const int vloc = int(row % H);
+    const int u = int(uint32_t(i) % uint32_t(W));
+    const int row = int(uint32_t(i) / uint32_t(W));
+    const int vloc = int(uint32_t(row) % uint32_t(H));
     const int64_t o = pidx(P, int(row), u);
     {
       const unsigned peers = __match_any_sync(__activemask(), lab);
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) dinv_kernel(int H, int W, int P, int64_t 
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t o = pidx(P, int(i / W), int(i % W));
+    const int64_t o = pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)));
     const uint8_t m = imask[o];
     if (!m) continue;
     const float h = hw[o];
@@ -257,7 +257,7 @@ __global__ void unit_from_label_kernel(const int32_t* __restrict__ labels, int H
                                        int32_t* __restrict__ unit) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t o = pidx(P, int(i / W), int(i % W));
+    const int64_t o = pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)));
     if (imask[o]) unit[o] = labels[i];
   }
 }
@@ -266,7 +266,7 @@ __global__ void cc_init_kernel(int W, int P, int64_t npix, const uint8_t* __rest
                                int32_t* __restrict__ parent) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x)
-    parent[i] = imask[pidx(P, int(i / W), int(i % W))] ? int32_t(i) : -1;
+    parent[i] = imask[pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)))] ? int32_t(i) : -1;
 }
 
 template <int CONN>
@@ -275,7 +275,7 @@ __global__ void cc_union_kernel(int W, int P, int64_t npix, const uint8_t* __res
   constexpr int KF = CONN == 8 ? 4 : 2;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const uint8_t m = imask[pidx(P, int(i / W), int(i % W))];
+    const uint8_t m = imask[pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)))];
 #pragma unroll
     for (int k = 0; k < KF; ++k)
       if ((m >> k) & 1)
@@ -304,7 +304,7 @@ __global__ void cc_label_kernel(const int32_t* __restrict__ labels, int W, int P
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t r = parent[i];
     if (r < 0) continue;
-    unit[pidx(P, int(i / W), int(i % W))] = rank[r];
+    unit[pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)))] = rank[r];
     if (r == int32_t(i)) unit_comp[rank[r]] = labels[i];
   }
 }
@@ -357,6 +357,46 @@ __global__ void __launch_bounds__(NT) plan_tile_kernel(int H, int W, int P, int 
       if (u >= 0) k = u;
     }
     key[e] = k;
+  }
+  // fast path: a tile holding at most one unit (most tiles) needs no sort
+  {
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (int e = threadIdx.x; e < TPX; e += NT) {
+      const int32_t k = key[e];
+      if (k != INT32_MAX) {
+        lo = min(lo, k);
+        hi = max(hi, k);
+      }
+    }
+    __shared__ int32_t s_lo, s_hi;
+    if (threadIdx.x == 0) {
+      s_lo = INT32_MAX;
+      s_hi = INT32_MIN;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_lo, lo);
+      atomicMax(&s_hi, hi);
+    }
+    __syncthreads();
+    lo = s_lo;
+    hi = s_hi;
+    if (lo == INT32_MAX || lo == hi) {
+      const int total = lo == INT32_MAX ? 0 : 1;
+      if (threadIdx.x == 0) {
+        nslots[t] = total;
+        if (total) tmp[int64_t(t) * TPX] = lo;
+      }
+      if (total)
+        for (int e = threadIdx.x; e < TPX; e += NT)
+          if (key[e] != INT32_MAX) slot[pidx(P, T.y0 + e / TX, T.x0 + e % TX)] = 0;
+      return;
+    }
   }
   __syncthreads();
   for (int k = 2; k <= TPX; k <<= 1)
@@ -516,8 +556,8 @@ __global__ void l1_count_kernel(int B, int H, int W, int P, int Hb, int Wb,
   const int64_t nblk = int64_t(B) * Hb * Wb;
   for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
        bi += int64_t(gridDim.x) * blockDim.x) {
-    const int bx = int(bi % Wb);
-    const int64_t br = bi / Wb;
+    const int bx = int(uint32_t(bi) % uint32_t(Wb));
+    const int br = int(uint32_t(bi) / uint32_t(Wb));
     const int by = int(br % Hb), m = int(br / Hb);
     int32_t v[4], d[4];
 #pragma unroll
@@ -536,8 +576,8 @@ __global__ void l1_assign_kernel(int B, int H, int W, int P, int Hb, int Wb,
   const int64_t nblk = int64_t(B) * Hb * Wb;
   for (int64_t bi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; bi < nblk;
        bi += int64_t(gridDim.x) * blockDim.x) {
-    const int bx = int(bi % Wb);
-    const int64_t br = bi / Wb;
+    const int bx = int(uint32_t(bi) % uint32_t(Wb));
+    const int br = int(uint32_t(bi) / uint32_t(Wb));
     const int by = int(br % Hb), m = int(br / Hb);
     int32_t v[4], d[4];
     int64_t o[4];
@@ -680,8 +720,8 @@ __device__ __forceinline__ int merge_children(const int32_t* __restrict__ bstart
 
 __device__ __forceinline__ void child_blocks(int64_t bi, int Hb, int Wb, int Hc, int Wc,
                                              int64_t cb[4]) {
-  const int bx = int(bi % Wb);
-  const int64_t br = bi / Wb;
+  const int bx = int(uint32_t(bi) % uint32_t(Wb));
+  const int br = int(uint32_t(bi) / uint32_t(Wb));
   const int by = int(br % Hb), m = int(br / Hb);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -1035,7 +1075,7 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
   float* sout = a.sbuf[a.par ^ 1];
   // per-pixel operands from global (issued before the wait)
   uint16_t slv[2][2][2];
-  float uv[2][2][2], pv[2][2][2], xv[2][2][2];
+  float uv[2][2][2], pv[2][2][2], xv[2][2][2], d1v[2][2][2];
   int32_t pav[2][2][2];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -1055,6 +1095,15 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
           pav[h][j][c] = a.par0[o];
         }
       }
+  // the level-1 diagonal of each pixel's aggregate, gathered while the boxes land
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        d1v[h][j][c] = (slv[h][j][c] != NOSLOT && pav[h][j][c] >= 0)
+                           ? __ldg(a.dinv1 + pav[h][j][c]) : 0.f;
 #if NI_MG_TMA
   __syncthreads();  // barrier init visible; slot scalars staged
   mbar_wait(bar, 0);
@@ -1129,9 +1178,12 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
       const float r11 = __shfl_xor_sync(0xffffffffu, res[1][c], 1);
       const int32_t p01 = __shfl_xor_sync(0xffffffffu, par[0][c], 1);
       const int32_t p11 = __shfl_xor_sync(0xffffffffu, par[1][c], 1);
+      const float d01 = __shfl_xor_sync(0xffffffffu, d1v[h][0][c], 1);
+      const float d11 = __shfl_xor_sync(0xffffffffu, d1v[h][1][c], 1);
       if (lane & 1) continue;
       const float rq[4] = {res[0][c], r01, res[1][c], r11};
       const int32_t pq[4] = {par[0][c], p01, par[1][c], p11};
+      const float dq[4] = {d1v[h][0][c], d01, d1v[h][1][c], d11};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (pq[q] < 0) continue;
@@ -1145,7 +1197,7 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
         for (int q2 = q; q2 < 4; ++q2)
           if (pq[q2] == pq[q]) sum += rq[q2];
         a.b1[pq[q]] = sum;
-        a.x1_1[pq[q]] = OM * a.dinv1[pq[q]] * sum;
+        a.x1_1[pq[q]] = OM * dq[q] * sum;
       }
     }
   }
@@ -1217,10 +1269,23 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 #endif
-  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box (in place of par0)
-  for (int e = threadIdx.x; e < BOX2; e += NT) {
-    const int32_t pj = __float_as_int(sX2[e]);
-    sX2[e] = OM * sD[e] * sR[e] + (pj >= 0 ? OC * a.e1[pj] : 0.f);
+  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box (in place of par0);
+  // the e1 gathers of a thread's box elements are all issued before any is
+  // used (one memory latency per thread instead of one per element)
+  {
+    constexpr int PER = (BOX2 + NT - 1) / NT;
+    float ev[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * NT;
+      const int32_t pj = e < BOX2 ? __float_as_int(sX2[e]) : -1;
+      ev[q] = pj >= 0 ? __ldg(a.e1 + pj) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * NT;
+      if (e < BOX2) sX2[e] = OM * sD[e] * sR[e] + OC * ev[q];
+    }
   }
   __syncthreads();
   // post-smoothing on the tile + 1-pixel ring: x3 = x2 + OM dinv (r - A x2)
@@ -1492,7 +1557,7 @@ __global__ void output_kernel(int W, int P, int64_t npix, const float* __restric
                               double* __restrict__ z) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t o = pidx(P, int(i / W), int(i % W));
+    const int64_t o = pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)));
     const int32_t u = unit[o];
     z[i] = u >= 0 ? double(x[o]) - mean[u] : 0.0;
   }

@@ -339,7 +339,7 @@ def build_quotient(g, p) -> QuotientGraph:
 def _loop_for(q: QuotientGraph, p: Partition, coeffs, settings, params, labels=None):
     g = q.graph
     grid = _grid_for(g, coeffs)
-    co = _planes(coeffs, g)
+    co = None if coeffs is None else _planes(coeffs, g)  # the merge reads no coefficients
     lab = p.labels_t if labels is None else labels
     loop = _BatchLoop(grid, lab, np.array([0, p.component_count]), [p.component_count], co,
                       settings, params)
