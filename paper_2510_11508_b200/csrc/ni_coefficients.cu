@@ -11,22 +11,60 @@ namespace ni {
 constexpr double kEpsDen = 1e-8;   // continuity.py:34
 constexpr double kEpsLog = 1e-12;  // continuity.py:35
 
+// A CTA covers a 32-column x CROWS-row tile of the stacked B*H rows: a
+// thread owns one column and walks the rows, so the ray components that
+// depend on the column only ((u - cx) / fx at u, u +- 1 and at the midpoints)
+// are divided once per column and those that depend on the row only once per
+// row (in shared memory).  Same operands and operation order as a per-edge
+// evaluation, so every value is bit-identical to the reference's.
+constexpr int CCOLS = 32, CTHR_Y = 8, CROWS = 32;
+
+struct ColRays {
+  int m = -1;
+  double t0, tp, tm, hp, hm;  // (u - cx)/fx at u, u+1, u-1 and the midpoints u+-1/2
+};
+
 template <int CONN, int MODEL>
-__global__ void __launch_bounds__(256) coefficients_kernel(
+__global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     const double* __restrict__ n, const uint8_t* __restrict__ valid,
     const double* __restrict__ intr, int H, int W, int64_t npix, double* __restrict__ omega_a,
     double* __restrict__ omega_b, double* __restrict__ gamma, uint8_t* __restrict__ eflags,
     ni_stats* __restrict__ st) {
   constexpr int KF = CONN == 8 ? 4 : 2;
+  __shared__ double s_t0[CROWS], s_tp[CROWS], s_hp[CROWS];  // (v - cy)/fy at v, v+1, v+1/2
+  const int rows = int(npix / W);
+  const int row0 = blockIdx.y * CROWS;
+  const int u = blockIdx.x * CCOLS + threadIdx.x;
+  const int tid = threadIdx.y * CCOLS + threadIdx.x;
+  if (tid < CROWS && row0 + tid < rows) {
+    const int r = row0 + tid;
+    const int m = r / H;
+    const double fy = intr[4 * m + 1], cy = intr[4 * m + 3];
+    const double va = double(r - m * H);
+    s_t0[tid] = (va - cy) / fy;
+    s_tp[tid] = (va + 1.0 - cy) / fy;
+    s_hp[tid] = (0.5 * (va + (va + 1.0)) - cy) / fy;
+  }
+  __syncthreads();
   long long ndegen = 0;
-  const int64_t per_map = int64_t(H) * W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int m = int(i / per_map);
+  ColRays cr;
+  for (int ry = threadIdx.y; ry < CROWS && u < W; ry += CTHR_Y) {
+    const int row = row0 + ry;
+    if (row >= rows) break;
+    const int m = row / H;
+    const int vloc = row - m * H;
+    const int64_t i = int64_t(row) * W + u;
     const double fx = intr[4 * m + 0], fy = intr[4 * m + 1];
-    const double cx = intr[4 * m + 2], cy = intr[4 * m + 3];
-    const int u = int(uint32_t(i) % uint32_t(W));
-    const int vloc = int((uint32_t(i) / uint32_t(W)) % uint32_t(H));
+    if (cr.m != m) {
+      const double cx = intr[4 * m + 2];
+      const double ua = double(u);
+      cr.m = m;
+      cr.t0 = (ua - cx) / fx;
+      cr.tp = (ua + 1.0 - cx) / fx;
+      cr.tm = (ua + -1.0 - cx) / fx;
+      cr.hp = (0.5 * (ua + (ua + 1.0)) - cx) / fx;
+      cr.hm = (0.5 * (ua + (ua + -1.0)) - cx) / fx;
+    }
     uint8_t flags = 0;
     double g = 0.0;
     double om_a[KF], om_b[KF];
@@ -34,19 +72,8 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
     for (int k = 0; k < KF; ++k) om_a[k] = om_b[k] = 0.0;
     if (valid[i]) {
       const double a0 = n[i], a1 = n[npix + i], a2 = n[2 * npix + i];
-      const double ua = double(u), va = double(vloc);
-      const double ta0 = (ua - cx) / fx, ta1 = (va - cy) / fy;
-      // ray components at the neighbours' coordinates and at the edge
-      // midpoints, each divided once per pixel (same operands and operation
-      // order as per edge, so the values are bit-identical)
-      const double tbx_p = (ua + 1.0 - cx) / fx, tbx_m = (ua + -1.0 - cx) / fx;
-      const double tby_p = (va + 1.0 - cy) / fy;
-      const double tmx_p = (0.5 * (ua + (ua + 1.0)) - cx) / fx;
-      const double tmx_m = (0.5 * (ua + (ua + -1.0)) - cx) / fx;
-      const double tmy_p = (0.5 * (va + (va + 1.0)) - cy) / fy;
-      const double tmy_0 = (0.5 * (va + va) - cy) / fy;
-      const double tmx_0 = (0.5 * (ua + ua) - cx) / fx;
-      // gamma = mean_focal * |n . tau / ||tau|| |
+      const double ta0 = cr.t0, ta1 = s_t0[ry];
+      // gamma = mean_focal * |n . tau / ||tau|| |   (continuity.py:270-274)
       const double tn = sqrt(ta0 * ta0 + ta1 * ta1 + 1.0);
       g = 0.5 * (fx + fy) * fabs(a0 * (ta0 / tn) + a1 * (ta1 / tn) + a2 * (1.0 / tn));
 #pragma unroll
@@ -57,14 +84,13 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
         if (!valid[j]) continue;
         flags |= uint8_t(1u << k);
         const double b0 = n[j], b1 = n[npix + j], b2 = n[2 * npix + j];
-        const double ub = ua + du, vb = va + dv;
         bool ok;
         if (MODEL == 0) {  // milano, continuity.py:232-247
-          // = (ub - cx) / fx, (vb - cy) / fy, (0.5 (ua + ub) - cx) / fx, (0.5 (va + vb) - cy) / fy
-          const double tb0 = du > 0 ? tbx_p : (du < 0 ? tbx_m : ta0);
-          const double tb1 = dv > 0 ? tby_p : ta1;
-          const double tm0 = du > 0 ? tmx_p : (du < 0 ? tmx_m : tmx_0);
-          const double tm1 = dv > 0 ? tmy_p : tmy_0;
+          // (ub - cx) / fx, (vb - cy) / fy, (0.5 (ua + ub) - cx) / fx, (0.5 (va + vb) - cy) / fy
+          const double tb0 = du > 0 ? cr.tp : (du < 0 ? cr.tm : ta0);
+          const double tb1 = dv > 0 ? s_tp[ry] : ta1;
+          const double tm0 = du > 0 ? cr.hp : (du < 0 ? cr.hm : ta0);
+          const double tm1 = dv > 0 ? s_hp[ry] : ta1;
           const double pa = a0 * ta0 + a1 * ta1 + a2;
           const double pb = b0 * tb0 + b1 * tb1 + b2;
           const double ma = a0 * tm0 + a1 * tm1 + a2;
@@ -77,6 +103,9 @@ __global__ void __launch_bounds__(256) coefficients_kernel(
             om_b[k] = -om_a[k];
           }
         } else {  // bini, continuity.py:248-268 (axis-aligned edges only)
+          const double cx = intr[4 * m + 2], cy = intr[4 * m + 3];
+          const double ua = double(u), va = double(vloc);
+          const double ub = ua + du, vb = va + dv;
           const bool horiz = dv == 0;
           const double f = horiz ? fx : fy;
           const double num_a = horiz ? du * a0 : dv * a1;
@@ -125,16 +154,16 @@ extern "C" int ni_coefficients(const double* n, const uint8_t* valid, const doub
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npix = int64_t(B) * H * W;
   NI_CUDA_TRY(cudaMemsetAsync(&stats->degenerate_edges, 0, sizeof(long long), s));
-  int64_t blocks64 = (npix + 255) / 256;
-  const int blocks = int(blocks64 < kSMs * 16 ? blocks64 : kSMs * 16);
+  const dim3 blocks(unsigned(div_up(W, CCOLS)), unsigned(div_up(B * H, CROWS)));
+  const dim3 threads(CCOLS, CTHR_Y);
   if (connectivity == 8)
-    NI_COUNT_LAUNCH(), coefficients_kernel<8, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<8, 0><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   else if (model == 0)
-    NI_COUNT_LAUNCH(), coefficients_kernel<4, 0><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<4, 0><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   else
-    NI_COUNT_LAUNCH(), coefficients_kernel<4, 1><<<blocks, 256, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
+    NI_COUNT_LAUNCH(), coefficients_kernel<4, 1><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
                                                      omega_b, gamma, eflags, stats);
   NI_LAUNCH_CHECK();
   return NI_OK;

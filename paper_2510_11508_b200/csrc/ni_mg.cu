@@ -154,7 +154,10 @@ __device__ __forceinline__ Tile tile_of(int t, int H, int W, int nTX, int nTY) {
 // ------------------------------------------------------------ fine setup
 
 // hw, b (into r), imask per pixel; component sizes; count of same-label
-// edges that carry no conductance (then units != components).
+// edges that carry no conductance (then units != components).  2-D launch
+// (x: column, y: stacked row); every neighbour's label / gamma / flags is
+// loaded before any is compared, so the 2 x KF gathers of a pixel are in
+// flight together instead of in dependent chains.
 template <int CONN, int MODEL>
 __global__ void __launch_bounds__(256) prep_kernel(
     const int32_t* __restrict__ labels, const double* __restrict__ omega_a,
@@ -163,55 +166,70 @@ __global__ void __launch_bounds__(256) prep_kernel(
     float* __restrict__ hw, float* __restrict__ rvec, uint8_t* __restrict__ imask,
     int32_t* __restrict__ comp_size, int32_t* __restrict__ missing) {
   constexpr int KF = CONN == 8 ? 4 : 2;
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int row = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const bool in = u < W && int64_t(row) * W < npix;
+  const int64_t i = int64_t(row) * W + u;
+  const int32_t lab = in ? labels[i] : -1;
   int miss = 0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int32_t lab = labels[i];
-    if (lab < 0) continue;
-    const int u = int(uint32_t(i) % uint32_t(W));
-    const int row = int(uint32_t(i) / uint32_t(W));
-    const int vloc = int(uint32_t(row) % uint32_t(H));
-    const int64_t o = pidx(P, int(row), u);
-    {
-      const unsigned peers = __match_any_sync(__activemask(), lab);
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(comp_size + lab, __popc(peers));
-    }
-    const double wself = 0.5 * (gamma[i] * gamma[i]);
-    const float hself = hw_of(gamma[i]);
-    hw[o] = hself;
+  {
+    const unsigned peers = __match_any_sync(0xffffffffu, lab);
+    if (lab >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(comp_size + lab, __popc(peers));
+  }
+  if (lab >= 0) {
+    const int vloc = row % H;
+    const int64_t o = pidx(P, row, u);
     const uint8_t ef = eflags[i];
+    const double gs = gamma[i];
+    // forward (k) and backward (4 + k) neighbours: existence, then all loads
+    bool fex[KF], bex[KF];
+    int32_t fl[KF], bl[KF];
+    double fg[KF], bg[KF], fo[KF], bo[KF], fob[KF], bob[KF];
+    uint8_t bef[KF];
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+      fex[k] = (ef >> k) & 1;
+      const int64_t jf = fex[k] ? i + int64_t(dv) * W + du : i;
+      fl[k] = labels[jf];
+      fg[k] = gamma[jf];
+      fo[k] = omega_a[k * npix + i];
+      fob[k] = MODEL == 0 ? 0.0 : omega_b[k * npix + i];
+      const int uj = u - du, vj = vloc - dv;
+      bex[k] = uj >= 0 && uj < W && vj >= 0;
+      const int64_t jb = bex[k] ? i - int64_t(dv) * W - du : i;
+      bl[k] = labels[jb];
+      bg[k] = gamma[jb];
+      bef[k] = eflags[jb];
+      bo[k] = omega_a[k * npix + jb];
+      bob[k] = MODEL == 0 ? 0.0 : omega_b[k * npix + jb];
+    }
+    const double wself = 0.5 * (gs * gs);
+    const float hself = hw_of(gs);
+    hw[o] = hself;
     uint8_t m = 0;
     double b = 0.0;
 #pragma unroll
     for (int k = 0; k < KF; ++k) {
-      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
-      if ((ef >> k) & 1) {  // forward edge i -> j exists
-        const int64_t j = i + int64_t(dv) * W + du;
-        if (labels[j] == lab) {
-          const bool ok = ((ef >> (4 + k)) & 1) && (hself + hw_of(gamma[j])) > 0.f;
-          if (ok) {
-            m |= uint8_t(1u << k);
-            const double wb = 0.5 * (gamma[j] * gamma[j]);
-            const double oa = omega_a[k * npix + i];
-            const double ob = MODEL == 0 ? -oa : omega_b[k * npix + i];
-            b += wself * oa - wb * ob;  // A^T W b of rows 2e, 2e+1 (solver.py:83-93)
-          } else {
-            ++miss;
-          }
+      if (fex[k] && fl[k] == lab) {  // forward edge i -> j inside the component
+        const bool ok = ((ef >> (4 + k)) & 1) && (hself + hw_of(fg[k])) > 0.f;
+        if (ok) {
+          m |= uint8_t(1u << k);
+          const double wb = 0.5 * (fg[k] * fg[k]);
+          const double oa = fo[k];
+          const double ob = MODEL == 0 ? -oa : fob[k];
+          b += wself * oa - wb * ob;  // A^T W b of rows 2e, 2e+1 (solver.py:83-93)
+        } else {
+          ++miss;
         }
       }
-      const int uj = u - du, vj = vloc - dv;
-      if (uj >= 0 && uj < W && vj >= 0) {  // backward edge j -> i
-        const int64_t j = i - int64_t(dv) * W - du;
-        const uint8_t efj = eflags[j];
-        if (((efj >> k) & 1) && labels[j] == lab && ((efj >> (4 + k)) & 1) &&
-            (hself + hw_of(gamma[j])) > 0.f) {
-          m |= uint8_t(1u << (4 + k));
-          const double wj = 0.5 * (gamma[j] * gamma[j]);
-          const double oa = omega_a[k * npix + j];
-          const double ob = MODEL == 0 ? -oa : omega_b[k * npix + j];
-          b += wself * ob - wj * oa;
-        }
+      if (bex[k] && ((bef[k] >> k) & 1) && bl[k] == lab && ((bef[k] >> (4 + k)) & 1) &&
+          (hself + hw_of(bg[k])) > 0.f) {  // backward edge j -> i
+        m |= uint8_t(1u << (4 + k));
+        const double wj = 0.5 * (bg[k] * bg[k]);
+        const double oa = bo[k];
+        const double ob = MODEL == 0 ? -oa : bob[k];
+        b += wself * ob - wj * oa;
       }
     }
     imask[o] = m;
@@ -835,6 +853,8 @@ __global__ void lc_links_kernel(int n, int Hb, int Wb, const int32_t* __restrict
 
 // down: b_{l+1}[P] = sum over children c of (b - A x1)_c with x1 = OM dinv b
 // precomputed at level l; also x1 at level l+1
+// Unknowns of units that already converged are skipped (the preconditioner is
+// block-diagonal over units, so their stale values never reach a live unit).
 __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __restrict__ child,
                                                    int n, const int32_t* __restrict__ nbr,
                                                    const float* __restrict__ cond,
@@ -842,8 +862,11 @@ __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __rest
                                                    const float* __restrict__ b,
                                                    const float* __restrict__ dinv1,
                                                    float* __restrict__ b1,
-                                                   float* __restrict__ x1n) {
+                                                   float* __restrict__ x1n,
+                                                   const int32_t* __restrict__ unit1,
+                                                   const uint8_t* __restrict__ status) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += gridDim.x * blockDim.x) {
+    if (status[unit1[i]] != U_ACTIVE) continue;
     float sum = 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -875,8 +898,11 @@ __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restric
                                                  float* __restrict__ e_out,
                                                  const int32_t* __restrict__ child,
                                                  const float* __restrict__ x1c,
-                                                 float* __restrict__ x2c, int nc) {
+                                                 float* __restrict__ x2c, int nc,
+                                                 const int32_t* __restrict__ unit,
+                                                 const uint8_t* __restrict__ status) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (status[unit[i]] != U_ACTIVE) continue;
     const float di = dinv[i];
     float e = 0.f;
     if (di != 0.f) {
@@ -1792,7 +1818,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   NI_CUDA_TRY(cudaMemsetAsync(f.comp_size, 0, sizeof(int32_t) * (count + 1), st));
   NI_CUDA_TRY(cudaMemsetAsync(f.counters, 0, sizeof(int32_t) * 16, st));
 #define NI_MG_PREP(CONN, MODEL)                                                                  \
-  NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<npb, 256, 0, st>>>(                             \
+  NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<dim3(div_up(W, 32), div_up(int64_t(B) * H, 8)), 256, 0, st>>>( \
                          labels, omega_a, omega_b, gamma, eflags, H, W, g.P, g.npix, f.hw, f.r, \
                          f.imask, f.comp_size, f.counters + 0)
   if (connectivity == 8) NI_MG_PREP(8, 0);
@@ -2061,7 +2087,8 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
         const Level& C = lev[l];
         const Level& N = lev[l + 1];
         NI_COUNT_LAUNCH(), down_kernel<<<grid_for(N.n), 256, 0, st>>>(
-                               N.n, N.child, C.n, C.nbr, C.cond, C.x1, C.b, N.dinv, N.b, N.x1);
+                               N.n, N.child, C.n, C.nbr, C.cond, C.x1, C.b, N.dinv, N.b, N.x1,
+                               N.unit, ustatus);
         NI_LAUNCH_CHECK();
       }
       for (int l = L; l >= 1; --l) {
@@ -2070,11 +2097,11 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
         if (l >= 2)
           NI_COUNT_LAUNCH(), up_kernel<true><<<grid_for(C.n), 256, 0, st>>>(
                                  C.n, C.nbr, C.cond, C.dinv, C.b, xs, nullptr, C.child,
-                                 lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
+                                 lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n, C.unit, ustatus);
         else
           NI_COUNT_LAUNCH(), up_kernel<false><<<grid_for(C.n), 256, 0, st>>>(
                                  C.n, C.nbr, C.cond, C.dinv, C.b, xs, C.e, nullptr, nullptr,
-                                 nullptr, 0);
+                                 nullptr, 0, C.unit, ustatus);
         NI_LAUNCH_CHECK();
       }
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));

@@ -60,9 +60,9 @@ def level0(sc):
     return lev, rhs, labels[pix]
 
 
-def coarsen(f):
+def coarsen(f, factor=2):
     """(block, label) aggregates of level f, their links and conductances."""
-    bu, bv, lab = f["u"] // 2, f["v"] // 2, f["lab"]
+    bu, bv, lab = f["u"] // factor, f["v"] // factor, f["lab"]
     key = (bv.astype(np.int64) << 40) | (bu.astype(np.int64) << 20) | lab
     uniq, parent = np.unique(key, return_inverse=True)
     nc = len(uniq)
@@ -155,8 +155,9 @@ if __name__ == "__main__":
     levels, parents = [lev0], []
     # coarsen until every component is (almost) one aggregate: the coarsest
     # system is then tiny and a few Jacobi sweeps solve it
+    first = int(__import__("os").environ.get("MG_FIRST", "2"))
     while len(levels) < 24:
-        c, par = coarsen(levels[-1])
+        c, par = coarsen(levels[-1], first if len(levels) == 1 else 2)
         if len(c["lab"]) >= len(levels[-1]["lab"]):
             break
         parents.append(par)
