@@ -201,7 +201,9 @@ int ni_quotient_build(const int32_t* keys, int K, const int32_t* labels, int cou
 /* K4-K7 -- relative_scale_step (solver.py:253-303) at 0-based iteration t for
  * the maps active[0..nact) of the batch, each solved as its own CG (one CTA
  * per map, a cooperative launch for maps above 8192 components), followed by
- * z[valid] += s[label] (pipeline.py:181-182) on those maps' pixels.
+ * z[valid] += s[label] (pipeline.py:181-182) on those maps' pixels -- or,
+ * when zshift != NULL, deferred: the state is z + zshift[label] throughout
+ * and only zshift[c] += s[c] is updated (ni_apply_shift folds it into z).
  * map_first[B+1], map_count[B] and active[nact] are HOST arrays (map m owns
  * component ids [map_first[m], map_first[m] + map_count[m])).  mode: 0 off,
  * 1 soft, 2 hard (continuity.py:140-158).  Outputs (device): scales[count],
@@ -216,9 +218,18 @@ int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, int 
                   const double* gamma, const uint8_t* eflags, int H, int W, int connectivity,
                   int model, int t, int alignment_iters, int mode, double k, double outlier_low,
                   double outlier_high, double cg_tol, int cg_max_iters, double* z,
-                  double* scales, double* residual, double* weights, double* energy_out,
-                  int32_t* cg_ok_out, void* workspace, size_t workspace_bytes,
-                  ni_stream_t stream);
+                  double* zshift, double* scales, double* residual, double* weights,
+                  double* energy_out, int32_t* cg_ok_out, void* workspace,
+                  size_t workspace_bytes, ni_stream_t stream);
+
+/* z[valid] += zshift[label] on the pixels of maps[0..nmaps) (a HOST list),
+ * then zshift = 0 on those maps' components: the deferred scales of
+ * ni_scale_step folded into the log-depth (pipeline.py:181-182), before a
+ * merge relabels the maps and at the end of the loop.  workspace: at least
+ * 4 * nmaps bytes.  Asynchronous. */
+int ni_apply_shift(double* z, double* zshift, const int32_t* labels, int B, int H, int W,
+                   const int32_t* maps, int nmaps, void* workspace, size_t workspace_bytes,
+                   ni_stream_t stream);
 
 /* K8 -- merge_components (graph.py:207-250) for the maps merging[0..nmerge)
  * with |residual[2e]| as the merge key, plus their energies restricted to

@@ -26,8 +26,17 @@ struct WeightArgs {
 
 // Weights (W_a, W_b) of the two directed rows of forward edge k at pixel a
 // (b = a + offset_k), at log-depth state z.  Invalid edges get 0.
+// Log-depth at pixel x: z[x], plus the pixel's component shift when the
+// caller defers the scale application (zs != nullptr: z_eff = z + zs[label]).
+__device__ __forceinline__ double z_at(const double* __restrict__ z, const double* __restrict__ zs,
+                                       const int32_t* __restrict__ labels, int64_t x) {
+  return zs ? z[x] + zs[labels[x]] : z[x];
+}
+
 template <int CONN, int MODEL>
 __device__ __forceinline__ void edge_weights_at(const double* __restrict__ z,
+                                                const double* __restrict__ zs,
+                                                const int32_t* __restrict__ zlab,
                                                 const double* __restrict__ omega_a,
                                                 const double* __restrict__ omega_b,
                                                 const double* __restrict__ gamma,
@@ -43,7 +52,7 @@ __device__ __forceinline__ void edge_weights_at(const double* __restrict__ z,
   }
   const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
   const int64_t b = a + int64_t(dv) * W + du;
-  const double za = z[a], zb = z[b];
+  const double za = z_at(z, zs, zlab, a), zb = z_at(z, zs, zlab, b);
   // opposite of b through a: a - off (continuity.py:196-207, 276)
   const int ua = int(a % W), va = int((a / W) % H);
   const int uo = ua - du, vo = va - dv;
@@ -53,11 +62,11 @@ __device__ __forceinline__ void edge_weights_at(const double* __restrict__ z,
     const int64_t o = a - int64_t(dv) * W - du;
     if ((eflags[o] >> k) & 1) {  // edge o -> a exists: o valid, same map
       has_a = true;
-      zoa = z[o];
+      zoa = z_at(z, zs, zlab, o);
     }
   }
   const bool has_b = (eflags[b] >> k) & 1;  // b + off exists
-  const double zob = has_b ? z[b + int64_t(dv) * W + du] : 0.0;
+  const double zob = has_b ? z_at(z, zs, zlab, b + int64_t(dv) * W + du) : 0.0;
   const double ga = gamma[a], gb = gamma[b];
   const double g2a = ga * ga, g2b = gb * gb;
   double bil_a = 0.5, bil_b = 0.5;

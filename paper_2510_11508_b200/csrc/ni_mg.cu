@@ -942,6 +942,18 @@ __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restric
 #ifndef NI_MG_TMA
 #define NI_MG_TMA 1
 #endif
+#ifndef NI_MG_V2
+#define NI_MG_V2 1  // register-blocked fine passes
+#endif
+#ifndef NI_MG_B_V2
+#define NI_MG_B_V2 0  // register-blocked pass B (slower: 128 registers, 2 CTAs / SM)
+#endif
+#ifndef NI_MG_B2_MINB
+#define NI_MG_B2_MINB 2
+#endif
+#ifndef NI_MG_A2_MINB
+#define NI_MG_A2_MINB 3  // resident pass-A CTAs per SM the register budget is cut for
+#endif
 
 // TMA boxes must start on a 16-byte-aligned column (measured: an unaligned
 // start raises an illegal-instruction fault), so every f32 box starts 4
@@ -961,6 +973,7 @@ struct TmaMaps {
   CUtensorMap r[2], s[2], w, dinv, hw;  // f32, BW x BH1 boxes (pass A)
   CUtensorMap rB[2], dinvB, hwB, parB;  // BW x BH2 boxes (pass B)
   CUtensorMap imB;                      // uint8 imask, BWM x BH1 box (pass B)
+  CUtensorMap uI, pI, xI;               // f32, TX x TY interior boxes (pass A v2)
 };
 
 struct FineArgs {
@@ -973,6 +986,7 @@ struct FineArgs {
   const float *hw, *dinv;
   const uint8_t* imask;
   const int32_t* par0;
+  const int32_t* unit;  // padded unit plane (-1 off the units)
   const uint16_t* slot;
   const int32_t* slot_base;  // [ntiles]
   const int32_t* slot_unit;  // [NS]
@@ -1137,6 +1151,50 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 #endif
+  // Box pass, in place, once per pixel of the tile + its 1-pixel ring: the
+  // pending update r' = r - alpha (w + beta s), s' = w + beta s of the
+  // pixel's own unit, and the pre-smoothed x1 = OM dinv r' (into sD).  The
+  // stencil below then reads x1 and hw only.  A ring pixel's unit is the
+  // tile's only unit on a single-slot tile; otherwise it is read from the
+  // unit plane (ring pixels of units outside the tile are never stencilled).
+  {
+    const bool single = nsl == 1;
+    const bool up0 = single && s_up[0] != 0;
+    const float al0 = single ? s_al[0] : 0.f, bt0 = single ? s_bt[0] : 0.f;
+    for (int e = threadIdx.x; e < BH1 * (TX + 2); e += NT) {
+      const int ry = e / (TX + 2), rx = e - ry * (TX + 2) + CX - 1;
+      const int cb = ry * BW + rx;
+      bool up = up0;
+      float al = al0, bt = bt0;
+      if (!single) {
+        const int32_t un = a.unit[pidx(a.P, T.y0 - 1 + ry, T.x0 - CX + rx)];
+        up = false;
+        if (un >= 0) {
+          int k = 0;
+          const int nk = nsl < kMaxSlotSm ? nsl : kMaxSlotSm;
+          while (k < nk && s_un[k] != un) ++k;
+          if (k < nk) {
+            up = s_up[k] != 0;
+            al = s_al[k];
+            bt = s_bt[k];
+          } else {
+            up = a.upd[un] != 0;
+            al = a.alpha[un];
+            bt = a.beta[un];
+          }
+        }
+      }
+      float r = sR[cb];
+      if (up) {
+        const float w = sW[cb], sv = sS[cb];
+        r = r_new(r, w, sv, al, bt);
+        sR[cb] = r;
+        sS[cb] = w + bt * sv;
+      }
+      sD[cb] = OM * sD[cb] * r;
+    }
+  }
+  __syncthreads();
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float res[2][2];
@@ -1151,35 +1209,30 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
         if (sl == NOSLOT) continue;
         const int ly = 2 * wid + 16 * h + j, lx = lane + 32 * c;
         const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx);
-        int un;
         bool up;
         float al, bt, um;
         if (sl < kMaxSlotSm) {
-          un = s_un[sl];
           up = s_up[sl] != 0;
           al = s_al[sl];
           bt = s_bt[sl];
           um = s_um[sl];
         } else {
-          un = a.slot_unit[base + sl];
+          const int un = a.slot_unit[base + sl];
           up = a.upd[un] != 0;
           al = a.alpha[un];
           bt = a.beta[un];
           um = a.umean[un];
         }
-        (void)un;
         const int cc = (ly + 1) * BW + lx + CX;
-        float ri = sR[cc], si = sS[cc];
+        const float ri = sR[cc];
         if (up) {
-          si = sW[cc] + bt * sS[cc];
           const float pi = (uv[h][j][c] - um) + bt * pv[h][j][c];
           a.p[o] = pi;
           a.x[o] = xv[h][j][c] + al * pi;
-          ri = r_new(ri, sW[cc], sS[cc], al, bt);
         }
         rout[o] = ri;
-        sout[o] = si;
-        const float x1i = OM * sD[cc] * ri;
+        sout[o] = sS[cc];
+        const float x1i = sD[cc];
         const float hi = sH[cc];
         const uint8_t mk = a.imask[o];
         float acc = 0.f;
@@ -1187,9 +1240,7 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
         for (int bit = 0; bit < 8; ++bit) {
           if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
           const int jn = cc + nb_off<CONN>(bit, BW);
-          float rj = sR[jn];
-          if (up) rj = r_new(rj, sW[jn], sS[jn], al, bt);
-          acc += (hi + sH[jn]) * (x1i - OM * sD[jn] * rj);
+          acc += (hi + sH[jn]) * (x1i - sD[jn]);
         }
         res[j][c] = ri - acc;
         par[j][c] = pav[h][j][c];
@@ -1256,19 +1307,17 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
 #if NI_MG_TMA
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, 4u * BOX2 * 4u + uint32_t(BWM * BH1));
+    mbar_expect_tx(bar, 3u * BOX2 * 4u + uint32_t(BWM * BH1));
     const int xs2 = T.x0 - CX + XM, ys2 = T.y0 - 2 + RM;
     tma_2d(sR, a.par ? &tm.rB[1] : &tm.rB[0], bar, xs2, ys2);
     tma_2d(sD, &tm.dinvB, bar, xs2, ys2);
     tma_2d(sH, &tm.hwB, bar, xs2, ys2);
-    tma_2d(sX2, &tm.parB, bar, xs2, ys2);
     tma_2d(sM, &tm.imB, bar, T.x0 - CXM + XM, T.y0 - 1 + RM);
   }
 #else
   stage_cp<BW, BH2>(sR, rcur, a.P, T.y0 - 2, T.x0 - CX);
   stage_cp<BW, BH2>(sD, a.dinv, a.P, T.y0 - 2, T.x0 - CX);
   stage_cp<BW, BH2>(sH, a.hw, a.P, T.y0 - 2, T.x0 - CX);
-  stage_cp<BW, BH2>(reinterpret_cast<int32_t*>(sX2), a.par0, a.P, T.y0 - 2, T.x0 - CX);
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int e = threadIdx.x; e < BWM * BH1; e += NT) {
     const int ry = e / BWM, rx = e - ry * BWM;
@@ -1276,6 +1325,21 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
   }
 #endif
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the level-1 correction OC e1[par0] of the thread's box elements: par0
+  // and the e1 gathers are issued while the boxes land (off the critical path)
+  constexpr int PER2 = (BOX2 + NT - 1) / NT;
+  float ev[PER2];
+  {
+    int32_t pj[PER2];
+#pragma unroll
+    for (int q = 0; q < PER2; ++q) {
+      const int e = threadIdx.x + q * NT;
+      const int ry = e / BW, rx = e - ry * BW;
+      pj[q] = e < BOX2 ? a.par0[pidx(a.P, T.y0 - 2 + ry, T.x0 - CX + rx)] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < PER2; ++q) ev[q] = pj[q] >= 0 ? __ldg(a.e1 + pj[q]) : 0.f;
+  }
   // slots of the tile (interior), read while the boxes land
   uint16_t slv[2][2][2];
 #pragma unroll
@@ -1295,23 +1359,11 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 #endif
-  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box (in place of par0);
-  // the e1 gathers of a thread's box elements are all issued before any is
-  // used (one memory latency per thread instead of one per element)
-  {
-    constexpr int PER = (BOX2 + NT - 1) / NT;
-    float ev[PER];
+  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = threadIdx.x + q * NT;
-      const int32_t pj = e < BOX2 ? __float_as_int(sX2[e]) : -1;
-      ev[q] = pj >= 0 ? __ldg(a.e1 + pj) : 0.f;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = threadIdx.x + q * NT;
-      if (e < BOX2) sX2[e] = OM * sD[e] * sR[e] + OC * ev[q];
-    }
+  for (int q = 0; q < PER2; ++q) {
+    const int e = threadIdx.x + q * NT;
+    if (e < BOX2) sX2[e] = OM * sD[e] * sR[e] + OC * ev[q];
   }
   __syncthreads();
   // post-smoothing on the tile + 1-pixel ring: x3 = x2 + OM dinv (r - A x2)
@@ -1416,6 +1468,546 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
       double* pp = a.partial + NPART * int64_t(a.slot_base[t] + sl);
 #pragma unroll
       for (int k = 0; k < NPART; ++k) pp[k] = q[k];
+    }
+  }
+}
+
+// ---- register-blocked fine passes (v2)
+//
+// Thread t of a tile CTA owns the 4 x 2 pixel block at tile columns
+// 4 (t & 15) .. +3 and rows 2 (t >> 4) .. +1: two whole 2 x 2 level-1 blocks,
+// so the restriction needs no shuffles, and the 4 x 6 window of a plane around
+// the block comes out of shared memory as 4 float4 + 8 scalars.  Neighbour
+// values then live in registers: every stencil weight and difference is a
+// compile-time register index (no per-neighbour shared-memory loads).
+// Per-lane global traffic is float4 / 8-byte / 4-byte vectors.
+
+struct Blk {
+  int lx0, ly0;  // tile column / row of the block's top-left pixel
+};
+__device__ __forceinline__ Blk blk_of() {
+  Blk b;
+  b.lx0 = 4 * (threadIdx.x & 15);
+  b.ly0 = 2 * (threadIdx.x >> 4);
+  return b;
+}
+
+// 4 x 6 window (rows ly0-1..ly0+2, columns lx0-1..lx0+4) of a box whose row 0
+// is tile row -ROW0 and whose column CX is tile column 0
+template <int ROW0>
+__device__ __forceinline__ void load_win(const float* box, const Blk& b, float (&v)[4][6]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float* q = box + (b.ly0 - 1 + r + ROW0) * BW + b.lx0 + CX;
+    const float4 m = *reinterpret_cast<const float4*>(q);
+    v[r][0] = q[-1];
+    v[r][1] = m.x;
+    v[r][2] = m.y;
+    v[r][3] = m.z;
+    v[r][4] = m.w;
+    v[r][5] = q[4];
+  }
+}
+
+// sum over the stencil edges of pixel (i, j) of the block: c_ij * (X_c - X_n),
+// c_ij = H_c + H_n; selects (not branches) on the edge bits, so a NaN-free
+// product is never needed for absent neighbours
+template <int CONN>
+__device__ __forceinline__ float stencil_at(const float (&X)[4][6], const float (&Hh)[4][6],
+                                            uint32_t mk, int i, int j) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  const float xc = X[i + 1][j + 1], hc = Hh[i + 1][j + 1];
+  float acc = 0.f;
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const int k = bit & 3;
+    if (k >= KF) continue;
+    const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+    const int r = i + 1 + (bit < 4 ? dv : -dv), c = j + 1 + (bit < 4 ? du : -du);
+    const float t = (hc + Hh[r][c]) * (xc - X[r][c]);
+    acc += ((mk >> bit) & 1u) ? t : 0.f;
+  }
+  return acc;
+}
+
+struct UnitScalars {
+  bool up;
+  float al, bt, um;
+};
+
+constexpr int IBOX = TX * TY;  // interior box (no halo)
+constexpr size_t kPassA2Smem = 5 * size_t(al128(BOX1 * 4)) + 3 * size_t(IBOX * 4) + 128;
+
+// Pass A (v2): pending CG update, pre-smoothing of the new r, residual,
+// restriction to level 1.  TMA brings the five halo boxes (r, w, s, dinv,
+// hw) and the three interior boxes (u, p, x).
+template <int CONN>
+__global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid_constant__ FineArgs a,
+                                                       const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sR = reinterpret_cast<float*>(smem_raw);
+  float* sW = sR + al128(BOX1 * 4) / 4;
+  float* sS = sW + al128(BOX1 * 4) / 4;
+  float* sD = sS + al128(BOX1 * 4) / 4;
+  float* sH = sD + al128(BOX1 * 4) / 4;
+  float* sU = sH + al128(BOX1 * 4) / 4;
+  float* sP = sU + IBOX;
+  float* sXv = sP + IBOX;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sXv + IBOX);
+  __shared__ float s_al[kMaxSlotSm], s_bt[kMaxSlotSm], s_um[kMaxSlotSm];
+  __shared__ int s_un[kMaxSlotSm];
+  __shared__ uint8_t s_up[kMaxSlotSm];
+  const int t = a.tiles[blockIdx.x];
+  if (tile_done(a, t)) return;
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
+  if (threadIdx.x == 0) {
+    const int xs = T.x0 - CX + XM, ys = T.y0 - 1 + RM;  // halo box origin (padded)
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 5u * BOX1 * 4u + 3u * IBOX * 4u);
+    tma_2d(sR, a.par ? &tm.r[1] : &tm.r[0], bar, xs, ys);
+    tma_2d(sW, &tm.w, bar, xs, ys);
+    tma_2d(sS, a.par ? &tm.s[1] : &tm.s[0], bar, xs, ys);
+    tma_2d(sD, &tm.dinv, bar, xs, ys);
+    tma_2d(sH, &tm.hw, bar, xs, ys);
+    tma_2d(sU, &tm.uI, bar, T.x0 + XM, T.y0 + RM);
+    tma_2d(sP, &tm.pI, bar, T.x0 + XM, T.y0 + RM);
+    tma_2d(sXv, &tm.xI, bar, T.x0 + XM, T.y0 + RM);
+  }
+  const int base = a.slot_base[t];
+  const int nsl = a.slot_base[t + 1] - base;
+  if (threadIdx.x < nsl && threadIdx.x < kMaxSlotSm) {
+    const int un = a.slot_unit[base + threadIdx.x];
+    s_un[threadIdx.x] = un;
+    s_up[threadIdx.x] = a.upd[un];
+    s_al[threadIdx.x] = a.alpha[un];
+    s_bt[threadIdx.x] = a.beta[un];
+    s_um[threadIdx.x] = a.umean[un];
+  }
+  const Blk b = blk_of();
+  // the block's slots, level-1 parents and edge masks (issued before the wait)
+  bool rowv[2];
+  uint16_t sl[2][4];
+  int32_t pa[2][4];
+  uint32_t mk[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int y = T.y0 + b.ly0 + i;
+    rowv[i] = y < T.y1;
+    const int64_t o = pidx(a.P, y, T.x0 + b.lx0);
+    const ushort4 s4 = *reinterpret_cast<const ushort4*>(a.slot + o);
+    const int4 p4 = *reinterpret_cast<const int4*>(a.par0 + o);
+    mk[i] = *reinterpret_cast<const uint32_t*>(a.imask + o);
+    sl[i][0] = s4.x;
+    sl[i][1] = s4.y;
+    sl[i][2] = s4.z;
+    sl[i][3] = s4.w;
+    pa[i][0] = p4.x;
+    pa[i][1] = p4.y;
+    pa[i][2] = p4.z;
+    pa[i][3] = p4.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (!rowv[i] || T.x0 + b.lx0 + j >= T.x1) sl[i][j] = NOSLOT;
+  }
+  __syncthreads();  // barrier init visible; slot scalars staged
+  mbar_wait(bar, 0);
+  // box pass, in place, float4-wide over the tile + 1-pixel ring (see pass A)
+  {
+    const bool single = nsl == 1;
+    const bool up0 = single && s_up[0] != 0;
+    const float al0 = single ? s_al[0] : 0.f, bt0 = single ? s_bt[0] : 0.f;
+    constexpr int Q = BW / 4;
+    for (int it = threadIdx.x; it < BH1 * Q; it += NT) {
+      const int ry = it / Q, q = it - ry * Q;
+      const int cb = ry * BW + 4 * q;
+      float4 r4 = *reinterpret_cast<float4*>(sR + cb);
+      bool up[4] = {up0, up0, up0, up0};
+      float al[4] = {al0, al0, al0, al0}, bt[4] = {bt0, bt0, bt0, bt0};
+      if (!single) {
+        const int4 u4 = *reinterpret_cast<const int4*>(
+            a.unit + pidx(a.P, T.y0 - 1 + ry, T.x0 - CX + 4 * q));
+        const int32_t uu[4] = {u4.x, u4.y, u4.z, u4.w};
+        const int nk = nsl < kMaxSlotSm ? nsl : kMaxSlotSm;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          up[e] = false;
+          if (uu[e] < 0) continue;
+          int k = 0;
+          while (k < nk && s_un[k] != uu[e]) ++k;
+          if (k < nk) {
+            up[e] = s_up[k] != 0;
+            al[e] = s_al[k];
+            bt[e] = s_bt[k];
+          } else {
+            up[e] = a.upd[uu[e]] != 0;
+            al[e] = a.alpha[uu[e]];
+            bt[e] = a.beta[uu[e]];
+          }
+        }
+      }
+      if (up[0] | up[1] | up[2] | up[3]) {
+        const float4 w4 = *reinterpret_cast<const float4*>(sW + cb);
+        float4 s4 = *reinterpret_cast<float4*>(sS + cb);
+        float* rr = &r4.x;
+        float* ss = &s4.x;
+        const float* ww = &w4.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (up[e]) {
+            rr[e] = r_new(rr[e], ww[e], ss[e], al[e], bt[e]);
+            ss[e] = ww[e] + bt[e] * ss[e];
+          }
+        *reinterpret_cast<float4*>(sR + cb) = r4;
+        *reinterpret_cast<float4*>(sS + cb) = s4;
+      }
+      float4 d4 = *reinterpret_cast<float4*>(sD + cb);
+      d4.x = OM * d4.x * r4.x;
+      d4.y = OM * d4.y * r4.y;
+      d4.z = OM * d4.z * r4.z;
+      d4.w = OM * d4.w * r4.w;
+      *reinterpret_cast<float4*>(sD + cb) = d4;
+    }
+  }
+  __syncthreads();
+  float* rout = a.rbuf[a.par ^ 1];
+  float* sout = a.sbuf[a.par ^ 1];
+  float res[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    // window rows i .. i + 2 of the 4 x 6 window (the stencil of output row i)
+    float X[4][6], Hh[4][6];
+#pragma unroll
+    for (int r = i; r < i + 3; ++r) {
+      const float* qx = sD + (b.ly0 + r) * BW + b.lx0 + CX;
+      const float* qh = sH + (b.ly0 + r) * BW + b.lx0 + CX;
+      const float4 mx = *reinterpret_cast<const float4*>(qx);
+      const float4 mh = *reinterpret_cast<const float4*>(qh);
+      X[r][0] = qx[-1];
+      X[r][1] = mx.x;
+      X[r][2] = mx.y;
+      X[r][3] = mx.z;
+      X[r][4] = mx.w;
+      X[r][5] = qx[4];
+      Hh[r][0] = qh[-1];
+      Hh[r][1] = mh.x;
+      Hh[r][2] = mh.y;
+      Hh[r][3] = mh.z;
+      Hh[r][4] = mh.w;
+      Hh[r][5] = qh[4];
+    }
+    const int cb = (b.ly0 + i + 1) * BW + b.lx0 + CX;
+    const int ci = (b.ly0 + i) * TX + b.lx0;
+    const float4 r4 = *reinterpret_cast<const float4*>(sR + cb);
+    const float4 s4 = *reinterpret_cast<const float4*>(sS + cb);
+    const float4 u4 = *reinterpret_cast<const float4*>(sU + ci);
+    float4 p4 = *reinterpret_cast<const float4*>(sP + ci);
+    float4 x4 = *reinterpret_cast<const float4*>(sXv + ci);
+    const float* rr = &r4.x;
+    const float* uu = &u4.x;
+    float* pp = &p4.x;
+    float* xx = &x4.x;
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      res[i][j] = 0.f;
+      const uint16_t q = sl[i][j];
+      if (q == NOSLOT) continue;
+      UnitScalars us;
+      if (q < kMaxSlotSm) {
+        us.up = s_up[q] != 0;
+        us.al = s_al[q];
+        us.bt = s_bt[q];
+        us.um = s_um[q];
+      } else {
+        const int un = a.slot_unit[base + q];
+        us.up = a.upd[un] != 0;
+        us.al = a.alpha[un];
+        us.bt = a.beta[un];
+        us.um = a.umean[un];
+      }
+      if (us.up) {
+        pp[j] = (uu[j] - us.um) + us.bt * pp[j];
+        xx[j] = xx[j] + us.al * pp[j];
+        any = true;
+      }
+      res[i][j] = rr[j] - stencil_at<CONN>(X, Hh, (mk[i] >> (8 * j)) & 0xffu, i, j);
+    }
+    if (rowv[i]) {
+      const int64_t o = pidx(a.P, T.y0 + b.ly0 + i, T.x0 + b.lx0);
+      *reinterpret_cast<float4*>(rout + o) = r4;
+      *reinterpret_cast<float4*>(sout + o) = s4;
+      if (any) {
+        *reinterpret_cast<float4*>(a.p + o) = p4;
+        *reinterpret_cast<float4*>(a.x + o) = x4;
+      }
+    }
+  }
+  // restriction: the two 2 x 2 blocks of the thread, each distinct level-1
+  // aggregate written once, summed in pixel order (TL, TR, BL, BR)
+#pragma unroll
+  for (int hb = 0; hb < 2; ++hb) {
+    const float rq[4] = {res[0][2 * hb], res[0][2 * hb + 1], res[1][2 * hb], res[1][2 * hb + 1]};
+    int32_t pq[4] = {pa[0][2 * hb], pa[0][2 * hb + 1], pa[1][2 * hb], pa[1][2 * hb + 1]};
+    const uint16_t sq[4] = {sl[0][2 * hb], sl[0][2 * hb + 1], sl[1][2 * hb], sl[1][2 * hb + 1]};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (sq[q] == NOSLOT) pq[q] = -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (pq[q] < 0) continue;
+      bool first = true;
+#pragma unroll
+      for (int q2 = 0; q2 < q; ++q2)
+        if (pq[q2] == pq[q]) first = false;
+      if (!first) continue;
+      float sum = 0.f;
+#pragma unroll
+      for (int q2 = q; q2 < 4; ++q2)
+        if (pq[q2] == pq[q]) sum += rq[q2];
+      a.b1[pq[q]] = sum;
+      a.x1_1[pq[q]] = OM * __ldg(a.dinv1 + pq[q]) * sum;
+    }
+  }
+}
+
+constexpr size_t kPassB2Smem = 4 * size_t(al128(BOX2 * 4)) + size_t(al128(BOX1 * 4)) +
+                               size_t(al128(BWM * BH1)) + size_t(TPX) * 4 + size_t(TPX) * 2 + 128;
+
+// 3 x 6 rows (i .. i + 2) of the 4 x 6 window of a box whose row 0 is tile row
+// -ROW0 (see load_win)
+template <int ROW0>
+__device__ __forceinline__ void load_rows3(const float* box, const Blk& b, int i,
+                                           float (&v)[4][6]) {
+#pragma unroll
+  for (int r = i; r < i + 3; ++r) {
+    const float* q = box + (b.ly0 - 1 + r + ROW0) * BW + b.lx0 + CX;
+    const float4 m = *reinterpret_cast<const float4*>(q);
+    v[r][0] = q[-1];
+    v[r][1] = m.x;
+    v[r][2] = m.y;
+    v[r][3] = m.z;
+    v[r][4] = m.w;
+    v[r][5] = q[4];
+  }
+}
+
+// Pass B (v2): prolongation + post-smoothing -> u = M r; w = A u; per-slot dots
+// (r,u), (w,u), (r,r), sum u, sum r, sum w.  Same staging as pass B; the
+// post-smoothing and A u of the tile interior are register-blocked, the
+// 1-pixel ring of x3 is one pixel per thread.
+template <int CONN>
+__global__ void __launch_bounds__(NT, NI_MG_B2_MINB) pass_b2_kernel(const __grid_constant__ FineArgs a,
+                                                       const __grid_constant__ TmaMaps tm) {
+  constexpr int KF = CONN == 8 ? 4 : 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sR = reinterpret_cast<float*>(smem_raw);
+  float* sD = sR + al128(BOX2 * 4) / 4;
+  float* sH = sD + al128(BOX2 * 4) / 4;
+  float* sX2 = sH + al128(BOX2 * 4) / 4;  // par0 lands here, then x2 replaces it
+  float* sX3 = sX2 + al128(BOX2 * 4) / 4;  // BW x BH1: row 0 = tile row -1
+  uint8_t* sM = reinterpret_cast<uint8_t*>(sX3 + al128(BOX1 * 4) / 4);
+  float* sWv = reinterpret_cast<float*>(sM + al128(BWM * BH1));
+  uint16_t* sSl = reinterpret_cast<uint16_t*>(sWv + TPX);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sSl + TPX);
+  __shared__ double sred[NT / 32][NPART];
+  const int t = a.tiles[blockIdx.x];
+  if (tile_done(a, t)) return;
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 3u * BOX2 * 4u + uint32_t(BWM * BH1));
+    const int xs2 = T.x0 - CX + XM, ys2 = T.y0 - 2 + RM;
+    tma_2d(sR, a.par ? &tm.rB[1] : &tm.rB[0], bar, xs2, ys2);
+    tma_2d(sD, &tm.dinvB, bar, xs2, ys2);
+    tma_2d(sH, &tm.hwB, bar, xs2, ys2);
+    tma_2d(sM, &tm.imB, bar, T.x0 - CXM + XM, T.y0 - 1 + RM);
+  }
+  // OC e1[par0] of the thread's float4 items of the 2-pixel halo box,
+  // gathered while the boxes land
+  constexpr int QB = BW / 4, NIT = (BH2 * QB + NT - 1) / NT;
+  float4 ev[NIT];
+#pragma unroll
+  for (int q = 0; q < NIT; ++q) {
+    const int it = threadIdx.x + q * NT;
+    int4 p4 = make_int4(-1, -1, -1, -1);
+    if (it < BH2 * QB) {
+      const int ry = it / QB, qq = it - ry * QB;
+      p4 = *reinterpret_cast<const int4*>(a.par0 + pidx(a.P, T.y0 - 2 + ry, T.x0 - CX + 4 * qq));
+    }
+    ev[q].x = p4.x >= 0 ? __ldg(a.e1 + p4.x) : 0.f;
+    ev[q].y = p4.y >= 0 ? __ldg(a.e1 + p4.y) : 0.f;
+    ev[q].z = p4.z >= 0 ? __ldg(a.e1 + p4.z) : 0.f;
+    ev[q].w = p4.w >= 0 ? __ldg(a.e1 + p4.w) : 0.f;
+  }
+  const Blk b = blk_of();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool rowv[2];
+  uint16_t sl[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int y = T.y0 + b.ly0 + i;
+    rowv[i] = y < T.y1;
+    const ushort4 s4 = *reinterpret_cast<const ushort4*>(a.slot + pidx(a.P, y, T.x0 + b.lx0));
+    sl[i][0] = s4.x;
+    sl[i][1] = s4.y;
+    sl[i][2] = s4.z;
+    sl[i][3] = s4.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (!rowv[i] || T.x0 + b.lx0 + j >= T.x1) sl[i][j] = NOSLOT;
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // x2 = OM dinv r + OC e1[par0] on the 2-pixel halo box, float4-wide
+#pragma unroll
+  for (int q = 0; q < NIT; ++q) {
+    const int it = threadIdx.x + q * NT;
+    if (it >= BH2 * QB) continue;
+    const int cb = it * 4;  // rows are BW = 4 QB floats: item it covers [4 it, 4 it + 4)
+    const float4 r4 = *reinterpret_cast<const float4*>(sR + cb);
+    const float4 d4 = *reinterpret_cast<const float4*>(sD + cb);
+    float4 x4;
+    x4.x = OM * d4.x * r4.x + OC * ev[q].x;
+    x4.y = OM * d4.y * r4.y + OC * ev[q].y;
+    x4.z = OM * d4.z * r4.z + OC * ev[q].z;
+    x4.w = OM * d4.w * r4.w + OC * ev[q].w;
+    *reinterpret_cast<float4*>(sX2 + cb) = x4;
+  }
+  __syncthreads();
+  // post-smoothing x3 = x2 + OM dinv (r - A x2): the 1-pixel ring, one pixel
+  // per thread (66 + 66 + 32 + 32 = 196 pixels)
+  if (threadIdx.x < 196) {
+    int ly, lx;
+    const int q = threadIdx.x;
+    if (q < 66) {
+      ly = -1;
+      lx = q - 1;
+    } else if (q < 132) {
+      ly = TY;
+      lx = q - 67;
+    } else if (q < 164) {
+      ly = q - 132;
+      lx = -1;
+    } else {
+      ly = q - 164;
+      lx = TX;
+    }
+    const int c2 = (ly + 2) * BW + lx + CX;
+    const uint8_t mk = sM[(ly + 1) * BWM + lx + CXM];
+    float v = 0.f;
+    if (mk) {
+      v = sX2[c2];
+      const float hi = sH[c2];
+      float acc = 0.f;
+#pragma unroll
+      for (int bit = 0; bit < 8; ++bit) {
+        if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+        const int jn = c2 + nb_off<CONN>(bit, BW);
+        acc += (hi + sH[jn]) * (v - sX2[jn]);
+      }
+      v += OM * sD[c2] * (sR[c2] - acc);
+    }
+    sX3[(ly + 1) * BW + lx + CX] = v;
+  }
+  // ... and the interior, register-blocked
+  uint32_t mk[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    mk[i] = *reinterpret_cast<const uint32_t*>(sM + (b.ly0 + i + 1) * BWM + b.lx0 + CXM);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float X[4][6], Hh[4][6];
+    load_rows3<2>(sX2, b, i, X);
+    load_rows3<2>(sH, b, i, Hh);
+    const int c2 = (b.ly0 + i + 2) * BW + b.lx0 + CX;
+    const float4 r4 = *reinterpret_cast<const float4*>(sR + c2);
+    const float4 d4 = *reinterpret_cast<const float4*>(sD + c2);
+    const float* rr = &r4.x;
+    const float* dd = &d4.x;
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t m = (mk[i] >> (8 * j)) & 0xffu;
+      const float acc = stencil_at<CONN>(X, Hh, m, i, j);
+      const float v = X[i + 1][j + 1] + OM * dd[j] * (rr[j] - acc);
+      o[j] = m ? v : 0.f;
+    }
+    *reinterpret_cast<float4*>(sX3 + (b.ly0 + i + 1) * BW + b.lx0 + CX) =
+        make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  // u = x3, w = A u on the interior; per-thread partial dots of slot 0
+  const int nsl = a.slot_base[t + 1] - a.slot_base[t];
+  double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float X[4][6], Hh[4][6];
+    load_rows3<1>(sX3, b, i, X);
+    load_rows3<2>(sH, b, i, Hh);
+    const float4 r4 = *reinterpret_cast<const float4*>(sR + (b.ly0 + i + 2) * BW + b.lx0 + CX);
+    const float* rr = &r4.x;
+    float wv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t m = (mk[i] >> (8 * j)) & 0xffu;
+      wv[j] = stencil_at<CONN>(X, Hh, m, i, j);
+      if (sl[i][j] == 0) {
+        const double du = double(X[i + 1][j + 1]), dr = double(rr[j]), dw = double(wv[j]);
+        d[0] += dr * du;
+        d[1] += dw * du;
+        d[2] += dr * dr;
+        d[3] += du;
+        d[4] += dr;
+        d[5] += dw;
+      }
+      if (nsl > 1) {
+        sSl[(b.ly0 + i) * TX + b.lx0 + j] = sl[i][j];
+        sWv[(b.ly0 + i) * TX + b.lx0 + j] = wv[j];
+      }
+    }
+    if (rowv[i]) {
+      const int64_t o = pidx(a.P, T.y0 + b.ly0 + i, T.x0 + b.lx0);
+      *reinterpret_cast<float4*>(a.u + o) =
+          make_float4(X[i + 1][1], X[i + 1][2], X[i + 1][3], X[i + 1][4]);
+      *reinterpret_cast<float4*>(a.w + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+    }
+  }
+  // slot 0: fixed-order block reduction
+#pragma unroll
+  for (int k = 0; k < NPART; ++k) d[k] = warp_sum(d[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) sred[wid][k] = d[k];
+  __syncthreads();
+  if (threadIdx.x < NPART) {
+    double v = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < NT / 32; ++w8) v += sred[w8][threadIdx.x];
+    a.partial[NPART * int64_t(a.slot_base[t]) + threadIdx.x] = v;
+  }
+  if (nsl <= 1) return;
+  // slots 1..: warp w sums slots w+1, w+1+8, ... over the tile lane-strided
+  for (int q = wid + 1; q < nsl; q += NT / 32) {
+    double qd[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int e = lane; e < TPX; e += 32) {
+      if (sSl[e] != q) continue;
+      const int ly = e / TX, lx = e - ly * TX;
+      const double ui = double(sX3[(ly + 1) * BW + lx + CX]);
+      const double ri = double(sR[(ly + 2) * BW + lx + CX]);
+      const double wi = double(sWv[e]);
+      qd[0] += ri * ui;
+      qd[1] += wi * ui;
+      qd[2] += ri * ri;
+      qd[3] += ui;
+      qd[4] += ri;
+      qd[5] += wi;
+    }
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) qd[k] = warp_sum(qd[k]);
+    if (lane == 0) {
+      double* pp = a.partial + NPART * int64_t(a.slot_base[t] + q);
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) pp[k] = qd[k];
     }
   }
 }
@@ -1734,6 +2326,9 @@ int make_tma_maps(TmaMaps& tm, const Geo& g, const MgFixed& f) {
   NI_TRY(mk(&tm.hwB, f.hw, F32, 4, BW, BH2));
   NI_TRY(mk(&tm.parB, f.par0, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, BW, BH2));
   NI_TRY(mk(&tm.imB, f.imask, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, BWM, BH1));
+  NI_TRY(mk(&tm.uI, f.u, F32, 4, TX, TY));
+  NI_TRY(mk(&tm.pI, f.p, F32, 4, TX, TY));
+  NI_TRY(mk(&tm.xI, f.x, F32, 4, TX, TY));
   return NI_OK;
 }
 
@@ -2018,6 +2613,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   fa.dinv = f.dinv;
   fa.imask = f.imask;
   fa.par0 = f.par0;
+  fa.unit = f.unit;
   fa.slot = f.slot;
   fa.slot_base = f.slot_base;
   fa.slot_unit = slot_unit;
@@ -2071,6 +2667,14 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                                    int(kPassASmem)));
   NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kPassASmem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassB2Smem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassB2Smem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassA2Smem)));
+  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kPassA2Smem)));
   TmaMaps tm;
   memset(&tm, 0, sizeof(tm));
   NI_TRY(make_tma_maps(tm, g, f));
@@ -2078,8 +2682,13 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   if (NA > 0) {
     while (true) {
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[2], st));
+#if NI_MG_V2
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a2_kernel<8><<<NA, NT, kPassA2Smem, st>>>(fa, tm);
+      else NI_COUNT_LAUNCH(), pass_a2_kernel<4><<<NA, NT, kPassA2Smem, st>>>(fa, tm);
+#else
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a_kernel<8><<<NA, NT, kPassASmem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_a_kernel<4><<<NA, NT, kPassASmem, st>>>(fa, tm);
+#endif
       fa.par ^= 1;  // pass B and the next pass A read the r / s pass A wrote
       NI_LAUNCH_CHECK();
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[3], st));
@@ -2105,8 +2714,13 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
         NI_LAUNCH_CHECK();
       }
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));
+#if NI_MG_V2 && NI_MG_B_V2
+      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b2_kernel<8><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
+      else NI_COUNT_LAUNCH(), pass_b2_kernel<4><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
+#else
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b_kernel<8><<<NA, NT, kPassBSmem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa, tm);
+#endif
       NI_LAUNCH_CHECK();
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[5], st));
       // counters [6] active units, [8..9] processed unit pixels (u64)

@@ -319,6 +319,7 @@ static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
 // K4: weights and row right-hand sides (solver.py:253-278, 170-180)
 template <int CONN, int MODEL>
 __global__ void weights_kernel(Quot q, const double* __restrict__ z,
+                               const double* __restrict__ zs, const int32_t* __restrict__ zlab,
                                const double* __restrict__ omega_a,
                                const double* __restrict__ omega_b,
                                const double* __restrict__ gamma,
@@ -331,8 +332,9 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
        e += gridDim.x * blockDim.x) {
     const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
     double wa, wb;
-    edge_weights_at<CONN, MODEL>(z, omega_a, omega_b, gamma, eflags, H, W, npix, a, k, wp, wa, wb);
-    const double za = z[a], zb = z[b];
+    edge_weights_at<CONN, MODEL>(z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W, npix, a, k,
+                                 wp, wa, wb);
+    const double za = z_at(z, zs, zlab, a), zb = z_at(z, zs, zlab, b);
     const double oa = omega_a[k * npix + a];
     const double ob = MODEL == 0 ? -oa : omega_b[k * npix + a];
     w.wa[e] = wa;
@@ -650,6 +652,29 @@ __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (l[u] >= 0) z[base + j0 + u * stride] += s[l[u]];
+  }
+}
+
+// deferred scales: zshift[c] += s[c] over the components of the active maps
+__global__ void shift_accumulate_kernel(double* __restrict__ zshift, const double* __restrict__ s,
+                                        const int32_t* __restrict__ first,
+                                        const int32_t* __restrict__ count,
+                                        const int32_t* __restrict__ active) {
+  const int m = active[blockIdx.y];
+  const int c0 = first[m], n = count[m];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    zshift[c0 + j] += s[c0 + j];
+}
+
+// zshift[label] = 0 for every labelled pixel of the listed maps (after the
+// shift was applied to z)
+__global__ void shift_clear_kernel(double* __restrict__ zshift, const int32_t* __restrict__ labels,
+                                   const int32_t* __restrict__ maps, int64_t per_map) {
+  const int64_t base = int64_t(maps[blockIdx.y]) * per_map;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < per_map;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t l = labels[base + j];
+    if (l >= 0) zshift[l] = 0.0;
   }
 }
 
@@ -1008,7 +1033,7 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                              const uint8_t* eflags, int H, int W, int connectivity, int model, int t,
                              int alignment_iters, int mode, double k, double outlier_low,
                              double outlier_high, double cg_tol, int cg_max_iters, double* z,
-                             double* scales, double* residual, double* weights,
+                             double* zshift, double* scales, double* residual, double* weights,
                              double* energy_out, int32_t* cg_ok_out, void* workspace,
                              size_t workspace_bytes, ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
@@ -1036,6 +1061,15 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     NI_CUDA_TRY(cudaMemsetAsync(scales, 0, sizeof(double) * C, s));
     return NI_OK;
   }
+  if (nact < B) {
+    // maps that left the loop keep their edges in the quotient; the pair and
+    // component sums read every edge, so theirs must hold zeros, not stale
+    // workspace (the active maps' systems are block-diagonal from them)
+    NI_CUDA_TRY(cudaMemsetAsync(w.wa, 0, sizeof(double) * K, s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.wb, 0, sizeof(double) * K, s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.ba, 0, sizeof(double) * K, s));
+    NI_CUDA_TRY(cudaMemsetAsync(w.bb, 0, sizeof(double) * K, s));
+  }
   WeightArgs wp;
   wp.wmode = t < alignment_iters ? EW_UNIFORM : EW_FULL;
   wp.mode = mode;
@@ -1051,13 +1085,13 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                      unsigned(nact));
   if (connectivity == 8)
     NI_COUNT_LAUNCH(), weights_kernel<8, 0><<<wblocks, 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
+                           q, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else if (model == 0)
     NI_COUNT_LAUNCH(), weights_kernel<4, 0><<<wblocks, 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
+                           q, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   else
     NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<wblocks, 256, 0, s>>>(
-                           q, z, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
+                           q, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
   NI_COUNT_LAUNCH(), comp_sum_kernel<<<int(std::min<int64_t>(C, int64_t(kSMs) * 8)), 256, 0, s>>>(q, w);
@@ -1105,12 +1139,39 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                                                                      energy_out);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  {
+  if (zshift) {  // deferred: zshift[c] += s[c] for the active maps' components
+    NI_COUNT_LAUNCH(), shift_accumulate_kernel<<<dim3(div_up(C, 256 * nact) + 1, nact), 256, 0, s>>>(
+                           zshift, scales, w.mp.first, w.mp.count, w.mp.active);
+  } else {
     const int bx = int(std::max<int64_t>(
         1, std::min<int64_t>((per_map + 1023) / 1024, int64_t(kSMs) * 16 / nact + 1)));
     NI_COUNT_LAUNCH(), apply_kernel<<<dim3(bx, nact), 256, 0, s>>>(z, labels, scales,
                                                                   w.mp.active, per_map);
   }
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}
+
+extern "C" int ni_apply_shift(double* z, double* zshift, const int32_t* labels, int B, int H, int W,
+                              const int32_t* maps, int nmaps, void* workspace,
+                              size_t workspace_bytes, ni_stream_t stream) {
+  NI_CHECK_ARG(z && zshift && labels && B >= 1 && nmaps >= 0 && nmaps <= B, "bad argument");
+  NI_CHECK_ARG(maps || nmaps == 0, "null map list");
+  NI_CHECK_ARG(workspace && workspace_bytes >= sizeof(int32_t) * size_t(std::max(nmaps, 1)),
+               "workspace too small");
+  if (nmaps == 0) return NI_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* dmaps = static_cast<int32_t*>(workspace);
+  NI_CUDA_TRY(cudaMemcpyAsync(dmaps, maps, sizeof(int32_t) * nmaps, cudaMemcpyHostToDevice, s));
+  const int64_t per_map = int64_t(H) * W;
+  const int bx = int(std::max<int64_t>(
+      1, std::min<int64_t>((per_map + 1023) / 1024, int64_t(kSMs) * 16 / nmaps + 1)));
+  NI_COUNT_LAUNCH(), apply_kernel<<<dim3(bx, nmaps), 256, 0, s>>>(z, labels, zshift, dmaps, per_map);
+  NI_LAUNCH_CHECK();
+  // the shift is now in z: clear it for every component (labels of these maps
+  // are the only ones that index their entries)
+  NI_COUNT_LAUNCH(), shift_clear_kernel<<<dim3(bx, nmaps), 256, 0, s>>>(zshift, labels, dmaps,
+                                                                       per_map);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) edge_weights_kernel(
     for (int k = 0; k < KF; ++k) {
       double wa = 0.0, wb = 0.0;
       if ((ef >> k) & 1)
-        edge_weights_at<CONN, MODEL>(z, omega_a, omega_b, gamma, eflags, H, W, npix, i, k, wp, wa,
+        edge_weights_at<CONN, MODEL>(z, nullptr, nullptr, omega_a, omega_b, gamma, eflags, H, W, npix, i, k, wp, wa,
                                      wb);
       w_a[k * npix + i] = wa;
       w_b[k * npix + i] = wb;

@@ -144,8 +144,9 @@ class NormalMap:
                 raise ValueError("mask shape does not match normals")
             m = mt.to(dev).to(torch.uint8).contiguous()
         npix = batch * h * w
-        n_soa = torch.empty((3, npix), dtype=torch.float64, device=dev)
-        valid = torch.empty(npix, dtype=torch.uint8, device=dev)
+        from . import devmem
+        n_soa = devmem.empty((3, npix), torch.float64, dev)
+        valid = devmem.empty(npix, torch.uint8, dev)
         stats = torch.zeros(6, dtype=torch.int64, device=dev)
         lib = _lib.load()
         st = lib.ni_normalize(C.c_void_p(t.data_ptr()), 0 if t.dtype == torch.float32 else 1,

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, devmem
 from .errors import EmptyMask
 from .geometry import (CameraIntrinsics, LogDepthMap, NormalMap, _device, _stream, as_intrinsics,
                        as_normal_map)
@@ -41,7 +41,7 @@ def _ptr(t: torch.Tensor | None) -> C.c_void_p:
 
 
 def _ws(nbytes: int, dev) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+    return devmem.empty(max(int(nbytes), 1), torch.uint8, dev)
 
 
 def _ms(start: float) -> float:
@@ -198,7 +198,7 @@ class _Grid:
 
 def _components(g: _Grid, theta_c):
     lib = g.lib
-    labels = torch.empty(g.npix, dtype=torch.int32, device=g.dev)
+    labels = devmem.empty(g.npix, torch.int32, g.dev)
     count = torch.zeros(1, dtype=torch.int32, device=g.dev)
     map_first = torch.zeros(g.B + 1, dtype=torch.int32, device=g.dev)
     ws = _ws(_lib.size_query(lib.ni_components_workspace_size, g.B, g.H, g.W), g.dev)
@@ -213,10 +213,10 @@ def _components(g: _Grid, theta_c):
 def _coefficients(g: _Grid, intrinsics: list[CameraIntrinsics]):
     lib = g.lib
     intr = torch.tensor([i.as_tuple() for i in intrinsics], dtype=torch.float64).to(g.dev)
-    omega_a = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
-    omega_b = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev) if g.model == 1 else None
-    gamma = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
-    eflags = torch.empty(g.npix, dtype=torch.uint8, device=g.dev)
+    omega_a = devmem.empty((g.kf, g.npix), torch.float64, g.dev)
+    omega_b = devmem.empty((g.kf, g.npix), torch.float64, g.dev) if g.model == 1 else None
+    gamma = devmem.empty(g.npix, torch.float64, g.dev)
+    eflags = devmem.empty(g.npix, torch.uint8, g.dev)
     _lib.check(lib.ni_coefficients(_ptr(g.nmap.n_soa), _ptr(g.nmap.valid_t), _ptr(intr), g.B, g.H,
                                    g.W, g.conn, g.model, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
                                    _ptr(eflags), _ptr(g.stats), g.s()), "build_edge_coefficients")
@@ -231,8 +231,8 @@ def _edge_weights(g: _Grid, co, z: torch.Tensor, wmode: int, weights: WeightPara
     """Directed weights of every forward pixel edge at state z (continuity.py:292-331,
     solver.py:253-278)."""
     omega_a, omega_b, gamma, eflags = co
-    w_a = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
-    w_b = torch.empty((g.kf, g.npix), dtype=torch.float64, device=g.dev)
+    w_a = devmem.empty((g.kf, g.npix), torch.float64, g.dev)
+    w_b = devmem.empty((g.kf, g.npix), torch.float64, g.dev)
     _lib.check(g.lib.ni_edge_weights(_ptr(z), _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
                                      _ptr(eflags), g.B, g.H, g.W, g.conn, g.model, wmode,
                                      weights.mode_code, C.c_double(weights.k),
@@ -245,7 +245,7 @@ def _edge_weights(g: _Grid, co, z: torch.Tensor, wmode: int, weights: WeightPara
 def _pair_energy(g: _Grid, co, x: torch.Tensor, wts) -> torch.Tensor:
     """Per-map energy of the pixel pair system at x (pipeline.py:336-337)."""
     omega_a, omega_b, _, eflags = co
-    out = torch.empty(g.B, dtype=torch.float64, device=g.dev)
+    out = devmem.empty(g.B, torch.float64, g.dev)
     ws = _ws(_lib.size_query(g.lib.ni_pair_energy_workspace_size, g.B), g.dev)
     _lib.check(g.lib.ni_pair_energy(_ptr(x), _ptr(omega_a), _ptr(omega_b), _ptr(wts[0]),
                                     _ptr(wts[1]), _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
@@ -258,7 +258,7 @@ def _fill_mg(g: _Grid, labels, count, co, settings: SolveSettings):
     preconditioned CG over every solve unit of the batch (ni_fill_mg)."""
     lib = g.lib
     omega_a, omega_b, gamma, eflags = co
-    z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
+    z = devmem.empty(g.npix, torch.float64, g.dev)
     iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
     status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
     nbytes = _lib.size_query(lib.ni_fill_mg_workspace_size, g.B, g.H, g.W, g.conn, count)
@@ -286,7 +286,7 @@ def _fill(g: _Grid, labels, count, co, settings: SolveSettings, wts=None):
         return _fill_mg(g, labels, count, co, settings)
     lib = g.lib
     omega_a, omega_b, gamma, eflags = co
-    z = torch.empty(g.npix, dtype=torch.float64, device=g.dev)
+    z = devmem.empty(g.npix, torch.float64, g.dev)
     iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
     status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
     ws = _ws(_lib.size_query(lib.ni_fill_workspace_size, g.B, g.H, g.W, g.conn, count,
@@ -324,6 +324,22 @@ class _BatchLoop:
         self.ok = torch.zeros(g.B, dtype=torch.int32, device=dev)
         self.merge_energy = torch.zeros(g.B, dtype=torch.float64, device=dev)
         self.new_count = torch.zeros(g.B, dtype=torch.int32, device=dev)
+        # deferred scales: the loop's state is z + zshift[label]; folded into
+        # z (ni_apply_shift) before a merge relabels a map and at the end
+        self.zshift = None
+        self._mapws = devmem.empty(4 * g.B, torch.uint8, dev)
+
+    def defer_scales(self):
+        self.zshift = torch.zeros(self.C, dtype=torch.float64, device=self.g.dev)
+
+    def fold_scales(self, z: torch.Tensor, maps: np.ndarray):
+        if self.zshift is None or len(maps) == 0:
+            return
+        g = self.g
+        mp = np.ascontiguousarray(maps, dtype=np.int32)
+        _lib.check(g.lib.ni_apply_shift(_ptr(z), _ptr(self.zshift), _ptr(self.labels), g.B, g.H,
+                                        g.W, self._hp(mp), len(mp), _ptr(self._mapws),
+                                        self._mapws.numel(), g.s()), "apply_scales")
 
     @staticmethod
     def _hp(a: np.ndarray) -> C.c_void_p:
@@ -331,7 +347,7 @@ class _BatchLoop:
 
     def initial_keys(self):
         g, lib = self.g, self.g.lib
-        out = torch.empty(g.npix * g.kf, dtype=torch.int32, device=g.dev)
+        out = devmem.empty(g.npix * g.kf, torch.int32, g.dev)
         n = torch.zeros(1, dtype=torch.int32, device=g.dev)
         ws = _ws(_lib.size_query(lib.ni_inter_edges_workspace_size, g.B, g.H, g.W, g.conn), g.dev)
         _lib.check(lib.ni_inter_edges(_ptr(self.labels), _ptr(self.co[3]), g.B, g.H, g.W, g.conn,
@@ -344,7 +360,7 @@ class _BatchLoop:
         """Drop edges of maps that left the loop and edges a merge made intra."""
         g, lib = self.g, self.g.lib
         mk = torch.from_numpy(keep.astype(np.uint8)).to(g.dev)
-        out = torch.empty(max(self.K, 1), dtype=torch.int32, device=g.dev)
+        out = devmem.empty(max(self.K, 1), torch.int32, g.dev)
         n = torch.zeros(1, dtype=torch.int32, device=g.dev)
         ws = _ws(_lib.size_query(lib.ni_keys_filter_workspace_size, self.K), g.dev)
         _lib.check(lib.ni_keys_filter(_ptr(self.keys), self.K, _ptr(self.labels), _ptr(mk), g.H,
@@ -368,9 +384,9 @@ class _BatchLoop:
         g, lib = self.g, self.g.lib
         st, wp = self.settings, self.weights
         omega_a, omega_b, gamma, eflags = self.co
-        scales = torch.empty(self.C, dtype=torch.float64, device=g.dev)
-        residual = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
-        wts = torch.empty(max(2 * self.K, 1), dtype=torch.float64, device=g.dev)
+        scales = devmem.empty(self.C, torch.float64, g.dev)
+        residual = devmem.empty(max(2 * self.K, 1), torch.float64, g.dev)
+        wts = devmem.empty(max(2 * self.K, 1), torch.float64, g.dev)
         ws = _ws(_lib.size_query(lib.ni_scale_step_workspace_size, self.K, self.C, g.B), g.dev)
         _lib.check(lib.ni_scale_step(
             _ptr(self.quot), self.quot.numel(), self.K, self.C, g.B, self._hp(self.first),
@@ -378,7 +394,7 @@ class _BatchLoop:
             _ptr(omega_a), _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.H, g.W, g.conn, g.model, t,
             st.alignment_iters, wp.mode_code, C.c_double(wp.k), C.c_double(wp.outlier_low),
             C.c_double(wp.outlier_high), C.c_double(st.cg_tol), int(st.cg_max_iters), _ptr(z),
-            _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
+            _ptr(self.zshift), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
             ws.numel(), g.s()), "relative_scale_step")
         self.last_scales = scales
         return residual, wts
@@ -489,6 +505,7 @@ def run_pipeline_batch(
 
     valid = g.nmap.valid_t
     loop = _BatchLoop(g, labels, first, counts, co, settings, weights)
+    loop.defer_scales()
     loop.initial_keys()
     loop.build()
     active = np.arange(B, dtype=np.int32)
@@ -510,6 +527,7 @@ def run_pipeline_batch(
         if len(merging):
             # merges relabel only, so z (and its digest) is the same before
             # and after; hash a device snapshot off the critical path
+            loop.fold_scales(z, merging)  # the digests and the relabel see the applied z
             if hasher is None:
                 hasher = cf.ThreadPoolExecutor(max_workers=4)
             snaps = {int(m): z[m * g.hw:(m + 1) * g.hw].clone() for m in merging}
@@ -556,6 +574,7 @@ def run_pipeline_batch(
             loop.build()
         active = np.array(still, dtype=np.int32)
 
+    loop.fold_scales(z, np.arange(B, dtype=np.int32))
     if hasher is not None:  # resolve the merge digests (pipeline.py:194-209)
         for recs in records:
             for r in recs:

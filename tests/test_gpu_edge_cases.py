@@ -145,28 +145,22 @@ def test_bini_model_4conn_ragged():
     assert_parity(r, ref, sc.mask, sc.intrinsics())
 
 
-@pytest.mark.parametrize("env", [{"NI_FILL_MB": "1"}, {"NI_FILL_MB": "2"},
-                                 {"NI_FILL_PAIR": "2"}, {"NI_FILL_PAIR": "1"}])
-def test_scheduler_claim_patterns(env, monkeypatch):
-    """The fill's batch scheduler under each mailbox depth and item pairing:
-    the batch completes, a different mailbox depth (pure scheduling) gives
-    bit-identical results, a different pairing the same iterations and depth
-    within tolerance."""
+def test_batch_bit_identical_to_single_maps():
+    """Every reduction of a map (fill slots, unit sums, scale CG, energies,
+    median) runs in an order that does not depend on the other maps of the
+    batch, so a 12-map batch reproduces each map's single run bit for bit."""
     maps = [scenes.voronoi_ortho(f"s{i}", 70, 95, 5, 40 + i, 0.2) for i in range(12)]
     nms = [nb.NormalMap.create(m.normals, m.mask) for m in maps]
     intr = [nb.CameraIntrinsics(*m.intrinsics()) for m in maps]
     theta = float(np.deg2rad(3.5))
-    base = nb.run_pipeline_batch(nb.stack(nms), intr, theta)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    other = nb.run_pipeline_batch(nb.stack(nms), intr, theta)
-    for m, a, b in zip(maps, base, other):
-        assert a.iterations == b.iterations
-        assert np.array_equal(a.partition.labels, b.partition.labels)
-        if "NI_FILL_MB" in env:
-            assert np.array_equal(a.log_depth.values, b.log_depth.values)
-        else:
-            assert_depth_close(b.log_depth.values, a.log_depth.values, m.mask, m.fx)
+    batch = nb.run_pipeline_batch(nb.stack(nms), intr, theta, nb.SolveSettings(freq_merging=3))
+    for m, nm, i, b in zip(maps, nms, intr, batch):
+        s = nb.run_pipeline(nm, i, theta, nb.SolveSettings(freq_merging=3))
+        assert b.iterations == s.iterations
+        assert np.array_equal(b.partition.labels, s.partition.labels)
+        assert np.array_equal(b.filled.values, s.filled.values)
+        assert np.array_equal(b.log_depth.values, s.log_depth.values)
+        assert b.energies == s.energies
 
 
 def test_stream_matches_batch():

@@ -75,8 +75,20 @@ def test_pipeline_vs_reference(name):
     fill_err = np.abs(r.filled.values - d["filled"])[mask]
     assert fill_err.max() < 2e-5, fill_err.max()
     if reference_drifted(d):
-        # reference trajectory is roundoff-driven (see oracle.project_range);
-        # compare with the oracle instead (test_pipeline_vs_oracle)
+        # The reference's own scale CG hit its cap here: its trajectory is
+        # driven by roundoff in the singular scale system (DESIGN.md,
+        # "Reference numerics"; oracle.project_range), so iterations and
+        # energies are not comparable and test_pipeline_vs_oracle holds the
+        # exact bar.  Against the drifted reference: the same initial
+        # partition and a depth divergence that stays bounded (measured
+        # 1.36e-3 = 13x the north-star bound on c5_voronoi48; asserted <= 20x).
+        # After the capped iteration the two trajectories reweight different
+        # iterates and settle on different energies (0.215 vs 0.170), so
+        # energies are not compared.
+        assert np.array_equal(r.partition0.labels, d["labels0"].astype(np.int64))
+        err, bound = depth_error(r.log_depth.values, d["log_depth"], mask, fx)
+        print(f"{name}: drifted reference, depth error {err:.3e} (bound {bound:.3e})")
+        assert err <= 20 * bound, (err, bound)
         return
     assert r.iterations == int(d["iterations"])
     assert r.partition.component_count == int(d["count"])
