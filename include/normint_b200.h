@@ -218,9 +218,23 @@ int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int count, int 
                   const double* gamma, const uint8_t* eflags, int H, int W, int connectivity,
                   int model, int t, int alignment_iters, int mode, double k, double outlier_low,
                   double outlier_high, double cg_tol, int cg_max_iters, double* z,
-                  double* zshift, double* scales, double* residual, double* weights,
-                  double* energy_out, int32_t* cg_ok_out, void* workspace,
+                  double* zshift, const int32_t* live, double* scales, double* residual,
+                  double* weights, double* energy_out, int32_t* cg_ok_out, void* workspace,
                   size_t workspace_bytes, ni_stream_t stream);
+
+/* The convergence test of the outer loop (pipeline.py:66-83) on the device,
+ * so a run of iterations without merges needs no host round trip: after the
+ * step at 1-based iteration t, every active map whose live[m] (device) is set
+ * records e_hist[m * hist_stride + t - 1] = energy[m] and ok_hist[...] =
+ * cg_ok[m], is tested against e_prev[m] (then overwritten) and, once
+ * converged, gets live[m] = 0 and iters[m] = t.  ni_scale_step skips maps
+ * whose live flag is 0 (pass live = NULL to run every active map).
+ * active[nact] is a DEVICE list here; nlive (device, nullable) is decremented
+ * once per map that converges.  Asynchronous. */
+int ni_loop_decide(const double* energy, const int32_t* cg_ok, const int32_t* active, int nact,
+                   int t, int max_iters, int alignment_iters, double delta_e_max,
+                   double* e_prev, int32_t* live, int32_t* iters, double* e_hist,
+                   int32_t* ok_hist, int hist_stride, int32_t* nlive, ni_stream_t stream);
 
 /* z[valid] += zshift[label] on the pixels of maps[0..nmaps) (a HOST list),
  * then zshift = 0 on those maps' components: the deferred scales of

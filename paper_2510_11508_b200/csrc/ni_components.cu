@@ -113,6 +113,15 @@ __device__ __forceinline__ void sm_union(int* p, int a, int b) {
   }
 }
 
+// One 32 x 32 tile per CTA (warp w owns rows w, w+8, w+16, w+24; lane =
+// column).  (1) The kept-edge bits of every in-tile forward edge.  (2) Row
+// runs: pixels joined by kept right edges share the run's first pixel as
+// parent, found with one warp ballot per row (no atomics).  (3) Union-find in
+// shared memory over the remaining edges, skipping every edge another pair of
+// kept edges already implies (a down edge whose left neighbour's down edge
+// joins the same two runs; a diagonal closed by a right + down pair): a
+// uniform region then needs one union per row instead of four per pixel.
+// Roots stay the smallest local id, i.e. the smallest pixel id.
 template <int CONN>
 __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__ n,
                                                       const uint8_t* __restrict__ valid, int H,
@@ -121,12 +130,16 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
                                                       int32_t* __restrict__ parent,
                                                       ni_stats* __restrict__ st) {
   constexpr int KF = CONN == 8 ? 4 : 2;
+  // edge bits: 0 right, 1 down, 2 down-left, 3 down-right (in-tile, kept)
+  constexpr uint8_t RT = 1, DN = 2, DL = 4, DR = 8;
   __shared__ int p[UT * UT];
+  __shared__ uint8_t kb[UT * UT];
   __shared__ double sn[3][UT * UT];  // the tile's normals: in-tile edges read only these
   const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
   const int x0 = tx * UT;
   const int64_t y0 = int64_t(ty) * UT;
   const int64_t npix = rows * W;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
     const int x = x0 + (l % UT);
     const int64_t y = y0 + l / UT;
@@ -141,27 +154,70 @@ __global__ void __launch_bounds__(256) uf_tile_kernel(const double* __restrict__
   }
   __syncthreads();
   long long nedges = 0;
-  for (int l = threadIdx.x; l < UT * UT; l += blockDim.x) {
-    if (p[l] < 0) continue;
-    const int lx = l % UT, ly = l / UT;
-    const int x = x0 + lx;
-    const int64_t y = y0 + ly;
-    const int64_t i = y * W + x;
-    const int vloc = int(y % H);
+  // (1) kept bits
 #pragma unroll
-    for (int k = 0; k < KF; ++k) {
-      const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
-      if (!fwd_inside(x, vloc, du, dv, W, H)) continue;
-      const int64_t j = i + int64_t(dv) * W + du;
-      if (!valid[j]) continue;
-      ++nedges;
-      const int jx = lx + du, jy = ly + dv;
-      if (jx < 0 || jx >= UT || jy >= UT) continue;  // crosses the tile: second pass
-      const int lj = jy * UT + jx;
-      if (!theta_none &&
-          add_rn(add_rn(mul_rn(sn[0][l], sn[0][lj]), mul_rn(sn[1][l], sn[1][lj])),
-                 mul_rn(sn[2][l], sn[2][lj])) >= cutoff)  // = kept_edge(n, npix, i, j, ...)
-        sm_union(p, l, lj);
+  for (int q = 0; q < UT / 8; ++q) {
+    const int ly = wid + 8 * q, lx = lane, l = ly * UT + lx;
+    uint8_t bits = 0;
+    if (p[l] >= 0) {
+      const int x = x0 + lx;
+      const int64_t y = y0 + ly;
+      const int64_t i = y * W + x;
+      const int vloc = int(uint32_t(y) % uint32_t(H));
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {
+        const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
+        if (!fwd_inside(x, vloc, du, dv, W, H)) continue;
+        const int64_t j = i + int64_t(dv) * W + du;
+        const int jx = lx + du, jy = ly + dv;
+        const bool inside = jx >= 0 && jx < UT && jy < UT;
+        if (inside ? p[jy * UT + jx] < 0 : !valid[j]) continue;
+        ++nedges;
+        if (!inside || theta_none) continue;  // crosses the tile: the border pass
+        const int lj = jy * UT + jx;
+        if (add_rn(add_rn(mul_rn(sn[0][l], sn[0][lj]), mul_rn(sn[1][l], sn[1][lj])),
+                   mul_rn(sn[2][l], sn[2][lj])) >= cutoff) {  // = kept_edge(n, npix, i, j, ...)
+          const uint8_t b = du == 1 && dv == 0 ? RT : (du == 0 ? DN : (du < 0 ? DL : DR));
+          bits |= b;
+        }
+      }
+    }
+    kb[l] = bits;
+  }
+  __syncwarp();
+  // (2) row runs: a pixel starts a run unless its left neighbour's right edge is kept
+#pragma unroll
+  for (int q = 0; q < UT / 8; ++q) {
+    const int ly = wid + 8 * q, l = ly * UT + lane;
+    const uint8_t left = __shfl_up_sync(0xffffffffu, kb[l], 1);
+    const bool start = lane == 0 || !(left & RT);
+    const unsigned starts = __ballot_sync(0xffffffffu, start);
+    const unsigned upto = starts & (0xffffffffu >> (31 - lane));
+    if (p[l] >= 0) p[l] = ly * UT + (31 - __clz(upto));
+  }
+  __syncthreads();
+  // (3) the remaining (non-implied) edges
+#pragma unroll
+  for (int q = 0; q < UT / 8; ++q) {
+    const int ly = wid + 8 * q, l = ly * UT + lane;
+    const uint8_t b = kb[l];
+    if (ly == UT - 1 || !(b & (DN | DL | DR))) continue;
+    const uint8_t bl = lane > 0 ? kb[l - 1] : 0;   // left neighbour
+    const uint8_t br = lane < UT - 1 ? kb[l + 1] : 0;  // right neighbour
+    const uint8_t dnb = kb[l + UT];                       // pixel below
+    const uint8_t dlb = lane > 0 ? kb[l + UT - 1] : 0;    // below-left
+    if (b & DN) {
+      // implied by the left neighbour's down edge when both row pairs are runs
+      const bool implied = (bl & RT) && (bl & DN) && (dlb & RT);
+      if (!implied) sm_union(p, l, l + UT);
+    }
+    if (b & DR) {  // (x, y) -> (x + 1, y + 1)
+      const bool implied = ((b & RT) && (br & DN)) || ((b & DN) && (dnb & RT));
+      if (!implied) sm_union(p, l, l + UT + 1);
+    }
+    if (b & DL) {  // (x, y) -> (x - 1, y + 1)
+      const bool implied = ((bl & RT) && (bl & DN)) || ((b & DN) && (dlb & RT));
+      if (!implied) sm_union(p, l, l + UT - 1);
     }
   }
   __syncthreads();

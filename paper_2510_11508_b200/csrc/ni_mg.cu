@@ -65,6 +65,7 @@
 #include <cudaTypedefs.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda_bf16.h>
 
 #include "ni_common.cuh"
 
@@ -533,6 +534,12 @@ __global__ void unit_init_kernel(int nu, const int32_t* __restrict__ unit_comp,
 
 // ------------------------------------------------------ level construction
 
+constexpr int16_t kNoLink = -32768;
+struct alignas(16) Link8 {
+  int16_t rel[8];
+  __nv_bfloat16 c[8];
+};
+
 struct Level {
   int n = 0;        // unknowns
   int nact = 0;     // unknowns with a link (diag > 0)
@@ -550,6 +557,8 @@ struct Level {
   float* x1 = nullptr;        // [n] pre-smoothed OM dinv b
   float* x2 = nullptr;        // [n] x1 + OC * parent's correction
   float* e = nullptr;         // [n] (level 1 only)
+  Link8* lnk = nullptr;       // [n] compact links (when cmp)
+  bool cmp = false;
   int32_t* cnt = nullptr;     // [nblk + 1] scratch (count per block)
 };
 
@@ -851,13 +860,73 @@ __global__ void lc_links_kernel(int n, int Hb, int Wb, const int32_t* __restrict
 
 // ------------------------------------------------------------ V-cycle
 
+// Compact coarse links: per unknown 32 contiguous bytes, 8 int16 offsets to
+// the neighbour (j - i; -32768 = no link) and 8 bf16 conductances (two
+// 16-byte loads instead of sixteen 4-byte ones; half the bytes of the
+// int32 index + fp32 conductance planes, which the next level's
+// construction still reads).  The preconditioner only has to be symmetric
+// positive definite, not exact: both directions of a link round the same
+// fp32 Galerkin sum.
+
+__global__ void compact_links_kernel(int n, const int32_t* __restrict__ nbr,
+                                     const float* __restrict__ cond, Link8* __restrict__ out,
+                                     int32_t* __restrict__ overflow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    Link8 l;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int32_t j = nbr[int64_t(k) * n + i];
+      const int32_t d = j - i;
+      l.rel[k] = kNoLink;
+      l.c[k] = __float2bfloat16_rn(0.f);
+      if (j < 0) continue;
+      if (d < -32767 || d > 32767) {
+        bad = true;
+        continue;
+      }
+      l.rel[k] = int16_t(d);
+      l.c[k] = __float2bfloat16_rn(cond[int64_t(k) * n + i]);
+    }
+    out[i] = l;
+    if (bad) atomicOr(overflow, 1);
+  }
+}
+
+// sum over the links of unknown i: cond * (xi - x[j])
+template <bool CMP>
+__device__ __forceinline__ float link_sum(int i, int n, const int32_t* __restrict__ nbr,
+                                          const float* __restrict__ cond,
+                                          const Link8* __restrict__ lnk, float xi,
+                                          const float* __restrict__ x) {
+  float acc = 0.f;
+  if (CMP) {
+    const Link8 l = lnk[i];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (l.rel[k] == kNoLink) continue;
+      acc += __bfloat162float(l.c[k]) * (xi - x[i + l.rel[k]]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int32_t j = nbr[int64_t(k) * n + i];
+      if (j < 0) continue;
+      acc += cond[int64_t(k) * n + i] * (xi - x[j]);
+    }
+  }
+  return acc;
+}
+
 // down: b_{l+1}[P] = sum over children c of (b - A x1)_c with x1 = OM dinv b
 // precomputed at level l; also x1 at level l+1
 // Unknowns of units that already converged are skipped (the preconditioner is
 // block-diagonal over units, so their stale values never reach a live unit).
+template <bool CMP>
 __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __restrict__ child,
                                                    int n, const int32_t* __restrict__ nbr,
                                                    const float* __restrict__ cond,
+                                                   const Link8* __restrict__ lnk,
                                                    const float* __restrict__ x1,
                                                    const float* __restrict__ b,
                                                    const float* __restrict__ dinv1,
@@ -873,14 +942,7 @@ __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __rest
       const int32_t c = child[int64_t(q) * n1 + i];
       if (c < 0) continue;
       const float xc = x1[c];
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int32_t j = nbr[int64_t(k) * n + c];
-        if (j < 0) continue;
-        acc += cond[int64_t(k) * n + c] * (xc - x1[j]);
-      }
-      sum += b[c] - acc;
+      sum += b[c] - link_sum<CMP>(c, n, nbr, cond, lnk, xc, x1);
     }
     b1[i] = sum;
     x1n[i] = OM * dinv1[i] * sum;
@@ -889,9 +951,10 @@ __global__ void __launch_bounds__(256) down_kernel(int n1, const int32_t* __rest
 
 // up: e = xs + OM dinv (b - A xs), xs = x2 = x1 + OC e_{l+1}[parent] (x1 on
 // the coarsest level); levels >= 2 hand x2 = x1 + OC e to their children.
-template <bool SCATTER>
+template <bool SCATTER, bool CMP>
 __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restrict__ nbr,
                                                  const float* __restrict__ cond,
+                                                 const Link8* __restrict__ lnk,
                                                  const float* __restrict__ dinv,
                                                  const float* __restrict__ b,
                                                  const float* __restrict__ xs,
@@ -907,14 +970,7 @@ __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restric
     float e = 0.f;
     if (di != 0.f) {
       const float xi = xs[i];
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int32_t j = nbr[int64_t(k) * n + i];
-        if (j < 0) continue;
-        acc += cond[int64_t(k) * n + i] * (xi - xs[j]);
-      }
-      e = xi + OM * di * (b[i] - acc);
+      e = xi + OM * di * (b[i] - link_sum<CMP>(i, n, nbr, cond, lnk, xi, xs));
     }
     if (SCATTER) {
 #pragma unroll
@@ -945,8 +1001,11 @@ __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restric
 #ifndef NI_MG_V2
 #define NI_MG_V2 1  // register-blocked fine passes
 #endif
+#ifndef NI_MG_CMP_LINKS
+#define NI_MG_CMP_LINKS 1  // int16 offsets + bf16 conductances on the coarse levels
+#endif
 #ifndef NI_MG_B_V2
-#define NI_MG_B_V2 0  // register-blocked pass B (slower: 128 registers, 2 CTAs / SM)
+#define NI_MG_B_V2 0  // register-blocked pass B (measured slower than the scalar pass B)
 #endif
 #ifndef NI_MG_B2_MINB
 #define NI_MG_B2_MINB 2
@@ -2258,7 +2317,7 @@ void carve_fixed(Carver& c, MgFixed& f, const Geo& g, int count) {
 
 // bytes of one coarse unknown: blk, unit, nbr[8], cond[8], dinv, parent,
 // child[4], b, e + its share of the block table
-constexpr int64_t kBytesPerUnknown = 4 * (2 + 8 + 8 + 1 + 1 + 4 + 4 + 2);
+constexpr int64_t kBytesPerUnknown = 4 * (2 + 8 + 8 + 1 + 1 + 4 + 4 + 2 + 8);
 
 int64_t level_estimate(const Geo& g) {
   // ~ npix/4 * 4/3 over all levels, + boundary aggregates and block tables
@@ -2277,6 +2336,7 @@ void carve_level(Carver& c, Level& L, int n, bool children) {
   L.x1 = c.take<float>(n + 1);
   L.x2 = c.take<float>(n + 1);
   L.e = c.take<float>(n + 1);
+  L.lnk = c.take<Link8>(n + 1);
 }
 
 int grid_for(int64_t n, int per = 256) {
@@ -2329,6 +2389,24 @@ int make_tma_maps(TmaMaps& tm, const Geo& g, const MgFixed& f) {
   NI_TRY(mk(&tm.uI, f.u, F32, 4, TX, TY));
   NI_TRY(mk(&tm.pI, f.p, F32, 4, TX, TY));
   NI_TRY(mk(&tm.xI, f.x, F32, 4, TX, TY));
+  return NI_OK;
+}
+
+// Compact links of a built level (counters[10]: offset overflow flag) and
+// its count of unknowns with a link (counters[5], written by the links
+// kernel): one read-back.
+int compact_level(Level& L, int32_t* counters, cudaStream_t st) {
+  NI_CUDA_TRY(cudaMemsetAsync(counters + 10, 0, sizeof(int32_t), st));
+  if (L.n > 0) {
+    NI_COUNT_LAUNCH(), compact_links_kernel<<<grid_for(L.n), 256, 0, st>>>(L.n, L.nbr, L.cond,
+                                                                          L.lnk, counters + 10);
+    NI_LAUNCH_CHECK();
+  }
+  int32_t h[6];
+  NI_CUDA_TRY(cudaMemcpyAsync(h, counters + 5, sizeof(h), cudaMemcpyDeviceToHost, st));
+  NI_CUDA_TRY(cudaStreamSynchronize(st));
+  L.nact = h[0];
+  L.cmp = h[5] == 0 && NI_MG_CMP_LINKS;
   return NI_OK;
 }
 
@@ -2551,8 +2629,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                              L1.n, H, W, g.P, L1.Hb, L1.Wb, L1.bstart, L1.blk, L1.unit, f.unit,
                              f.hw, f.imask, L1.nbr, L1.cond, L1.dinv, f.counters + 5);
     NI_LAUNCH_CHECK();
-    NI_CUDA_TRY(cudaMemcpyAsync(&L1.nact, f.counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    NI_CUDA_TRY(cudaStreamSynchronize(st));
+    NI_TRY(compact_level(L1, f.counters, st));
     L = 1;
     while (L < MAXLEV && lev[L].nact > 0) {
       Level& C = lev[L];
@@ -2584,8 +2661,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                              N.n, N.Hb, N.Wb, N.bstart, N.blk, N.unit, N.child, C.n, C.nbr,
                              C.cond, C.parent, N.nbr, N.cond, N.dinv, f.counters + 5);
       NI_LAUNCH_CHECK();
-      NI_CUDA_TRY(cudaMemcpyAsync(&N.nact, f.counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      NI_CUDA_TRY(cudaStreamSynchronize(st));
+      NI_TRY(compact_level(N, f.counters, st));
       ++L;
     }
     // the coarsest level used is the last one with a link
@@ -2695,22 +2771,31 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
       for (int l = 1; l < L; ++l) {
         const Level& C = lev[l];
         const Level& N = lev[l + 1];
-        NI_COUNT_LAUNCH(), down_kernel<<<grid_for(N.n), 256, 0, st>>>(
-                               N.n, N.child, C.n, C.nbr, C.cond, C.x1, C.b, N.dinv, N.b, N.x1,
-                               N.unit, ustatus);
+        if (C.cmp)
+          NI_COUNT_LAUNCH(), down_kernel<true><<<grid_for(N.n), 256, 0, st>>>(
+                                 N.n, N.child, C.n, C.nbr, C.cond, C.lnk, C.x1, C.b, N.dinv, N.b,
+                                 N.x1, N.unit, ustatus);
+        else
+          NI_COUNT_LAUNCH(), down_kernel<false><<<grid_for(N.n), 256, 0, st>>>(
+                                 N.n, N.child, C.n, C.nbr, C.cond, C.lnk, C.x1, C.b, N.dinv, N.b,
+                                 N.x1, N.unit, ustatus);
         NI_LAUNCH_CHECK();
       }
       for (int l = L; l >= 1; --l) {
         const Level& C = lev[l];
         const float* xs = l == L ? C.x1 : C.x2;
-        if (l >= 2)
-          NI_COUNT_LAUNCH(), up_kernel<true><<<grid_for(C.n), 256, 0, st>>>(
-                                 C.n, C.nbr, C.cond, C.dinv, C.b, xs, nullptr, C.child,
-                                 lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n, C.unit, ustatus);
-        else
-          NI_COUNT_LAUNCH(), up_kernel<false><<<grid_for(C.n), 256, 0, st>>>(
-                                 C.n, C.nbr, C.cond, C.dinv, C.b, xs, C.e, nullptr, nullptr,
-                                 nullptr, 0, C.unit, ustatus);
+#define NI_MG_UP(SC, CM, EOUT, CH, X1C, X2C, NC)                                               \
+  NI_COUNT_LAUNCH(), up_kernel<SC, CM><<<grid_for(C.n), 256, 0, st>>>(                           \
+                         C.n, C.nbr, C.cond, C.lnk, C.dinv, C.b, xs, EOUT, CH, X1C, X2C, NC, C.unit, \
+                         ustatus)
+        if (l >= 2) {
+          if (C.cmp) NI_MG_UP(true, true, nullptr, C.child, lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
+          else NI_MG_UP(true, false, nullptr, C.child, lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
+        } else {
+          if (C.cmp) NI_MG_UP(false, true, C.e, nullptr, nullptr, nullptr, 0);
+          else NI_MG_UP(false, false, C.e, nullptr, nullptr, nullptr, 0);
+        }
+#undef NI_MG_UP
         NI_LAUNCH_CHECK();
       }
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));

@@ -33,6 +33,8 @@ namespace cg = cooperative_groups;
 
 namespace ni {
 
+constexpr double kEnergyFloor = 1e-300;  // pipeline.py:55
+
 // ------------------------------------------------------------ inter edges
 
 template <int CONN>
@@ -259,7 +261,10 @@ struct Maps {
   int32_t* first;   // [B+1]
   int32_t* count;   // [B]
   int32_t* active;  // [nact] maps taking part in this call
+  const int32_t* live = nullptr;  // [B] device flags (nullable): a 0 makes the map sit the call out
 };
+
+__device__ __forceinline__ bool map_live(const Maps& mp, int m) { return !mp.live || mp.live[m]; }
 
 static void carve_maps(Carver& c, Maps& mp, int B) {
   mp.B = B;
@@ -328,8 +333,13 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
   // grid.y = active map: only the edges of maps still in the loop
   const int m = w.mp.active[blockIdx.y];
   const int e1 = q.estart[m + 1];
+  const bool live = map_live(w.mp, m);
   for (int e = q.estart[m] + blockIdx.x * blockDim.x + threadIdx.x; e < e1;
        e += gridDim.x * blockDim.x) {
+    if (!live) {  // a map that converged inside a chunk: its pair system stays zero
+      w.wa[e] = w.wb[e] = w.ba[e] = w.bb[e] = 0.0;
+      continue;
+    }
     const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
     double wa, wb;
     edge_weights_at<CONN, MODEL>(z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W, npix, a, k,
@@ -446,6 +456,7 @@ struct CgArgs {
   double rtol;
   double* s;     // the map's scales (global id space)
   int32_t* ok;   // the map's "converged" flag
+  int map;       // the map (cooperative launches: checked against the live flags)
 };
 
 // apply the Laplacian to p = r + beta pold for rows [c0, c1) with stride
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_block_kernel(Quot q, Step
   __shared__ double red[32];
   const int m = w.mp.active[blockIdx.x];
   const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
-  if (n > kBlockCgMax) return;  // solved by the cooperative kernel
+  if (n > kBlockCgMax || !map_live(w.mp, m)) return;  // cooperative kernel / sitting out
   const int tid = threadIdx.x, stride = blockDim.x;
   const int maxiter = cg_max_iters > n ? cg_max_iters : n;
   double rr = 0.0;
@@ -498,7 +509,7 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_block_kernel(Quot q, Step
   double* pold = w.p0;
   double* pnew = w.p1;
   int ok = 0;
-  CgArgs g{c0, c1, maxiter, rtol, s, ok_out};
+  CgArgs g{c0, c1, maxiter, rtol, s, ok_out, m};
   for (int it = 0; it < maxiter; ++it) {
     if (sqrt(rr) < atol) {
       ok = 1;
@@ -540,6 +551,7 @@ __device__ __forceinline__ double grid_sum(cg::grid_group& grid, double v, doubl
 }
 
 __global__ void __launch_bounds__(kCgThreads) scale_cg_kernel(Quot q, StepWs w, CgArgs g) {
+  if (!map_live(w.mp, g.map)) return;  // uniform over the grid: before any grid sync
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
   const int tid0 = g.c0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -602,9 +614,10 @@ __device__ __forceinline__ void chunk_range(int e0, int e1, int& c0, int& c1) {
 }
 
 __global__ void chunk_sum_kernel(const double* __restrict__ part, const int32_t* __restrict__ maps,
-                                 int n, double* __restrict__ out) {
+                                 int n, double* __restrict__ out,
+                                 const int32_t* __restrict__ live) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  if (j >= n || (live && !live[maps[j]])) return;
   double e = 0.0;
   for (int c = 0; c < kEChunks; ++c) e += part[j * kEChunks + c];
   out[maps[j]] = e;
@@ -616,6 +629,7 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const d
                                                        double* __restrict__ part) {
   __shared__ double red[32];
   const int m = w.mp.active[blockIdx.y];
+  if (!map_live(w.mp, m)) return;
   int c0, c1;
   chunk_range(q.estart[m], q.estart[m + 1], c0, c1);
   double en = 0.0;
@@ -637,8 +651,9 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const d
 // grid.y = active map; U independent label/scale/z chains per thread.
 __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__ labels,
                              const double* __restrict__ s, const int32_t* __restrict__ active,
-                             int64_t per_map) {
+                             int64_t per_map, const int32_t* __restrict__ live = nullptr) {
   constexpr int U = 4;
+  if (live && !live[active[blockIdx.y]]) return;
   const int64_t base = int64_t(active[blockIdx.y]) * per_map;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t j0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j0 < per_map;
@@ -659,8 +674,10 @@ __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__
 __global__ void shift_accumulate_kernel(double* __restrict__ zshift, const double* __restrict__ s,
                                         const int32_t* __restrict__ first,
                                         const int32_t* __restrict__ count,
-                                        const int32_t* __restrict__ active) {
+                                        const int32_t* __restrict__ active,
+                                        const int32_t* __restrict__ live) {
   const int m = active[blockIdx.y];
+  if (live && !live[m]) return;
   const int c0 = first[m], n = count[m];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     zshift[c0 + j] += s[c0 + j];
@@ -1033,9 +1050,10 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
                              const uint8_t* eflags, int H, int W, int connectivity, int model, int t,
                              int alignment_iters, int mode, double k, double outlier_low,
                              double outlier_high, double cg_tol, int cg_max_iters, double* z,
-                             double* zshift, double* scales, double* residual, double* weights,
-                             double* energy_out, int32_t* cg_ok_out, void* workspace,
-                             size_t workspace_bytes, ni_stream_t stream) {
+                             double* zshift, const int32_t* live, double* scales,
+                             double* residual, double* weights, double* energy_out,
+                             int32_t* cg_ok_out, void* workspace, size_t workspace_bytes,
+                             ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
   NI_CHECK_ARG(count >= 1 && K >= 0 && B >= 1 && nact >= 0 && nact <= B, "bad sizes");
   NI_CHECK_ARG(map_first && map_count && (active || nact == 0), "null map table");
@@ -1052,6 +1070,7 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   }
   if (nact == 0) return NI_OK;
   NI_TRY(upload_maps(w.mp, map_first, map_count, active, nact, s));
+  w.mp.live = live;
   const int C = count;
   const int64_t npix = int64_t(B) * H * W;
   if (K == 0) {  // solver.py:293-295: no inter edge anywhere in the batch
@@ -1127,7 +1146,7 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     if (g > G) g = G;
     if (g < 1) g = 1;
     CgArgs ca{map_first[m], map_first[m] + n, cg_max_iters > n ? cg_max_iters : n, cg_tol, scales,
-              cg_ok_out + m};
+              cg_ok_out + m, m};
     void* args[] = {&q, &w, &ca};
     NI_COUNT_LAUNCH();
     NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(g), dim3(kCgThreads), args,
@@ -1136,18 +1155,63 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   NI_COUNT_LAUNCH(), residual_kernel<<<dim3(kEChunks, nact), 256, 0, s>>>(q, w, scales, residual,
                                                                           weights, w.epart);
   NI_COUNT_LAUNCH(), chunk_sum_kernel<<<div_up(nact, 64), 64, 0, s>>>(w.epart, w.mp.active, nact,
-                                                                     energy_out);
+                                                                     energy_out, live);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
   if (zshift) {  // deferred: zshift[c] += s[c] for the active maps' components
     NI_COUNT_LAUNCH(), shift_accumulate_kernel<<<dim3(div_up(C, 256 * nact) + 1, nact), 256, 0, s>>>(
-                           zshift, scales, w.mp.first, w.mp.count, w.mp.active);
+                           zshift, scales, w.mp.first, w.mp.count, w.mp.active, live);
   } else {
     const int bx = int(std::max<int64_t>(
         1, std::min<int64_t>((per_map + 1023) / 1024, int64_t(kSMs) * 16 / nact + 1)));
     NI_COUNT_LAUNCH(), apply_kernel<<<dim3(bx, nact), 256, 0, s>>>(z, labels, scales,
-                                                                  w.mp.active, per_map);
+                                                                  w.mp.active, per_map, live);
   }
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}
+
+// pipeline.py:66-83 for every live map of the active list after the step at
+// 1-based iteration t: record E_t and the CG flag, then the convergence test
+// against the previous energy; a converged map drops its live flag.
+__global__ void loop_decide_kernel(const double* __restrict__ energy,
+                                   const int32_t* __restrict__ ok, const int32_t* __restrict__ active,
+                                   int nact, int t, int max_iters, int alignment_iters,
+                                   double delta_e_max, double* __restrict__ e_prev,
+                                   int32_t* __restrict__ live, int32_t* __restrict__ iters,
+                                   double* __restrict__ e_hist, int32_t* __restrict__ ok_hist,
+                                   int hist_stride, int32_t* __restrict__ nlive) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nact) return;
+  const int m = active[j];
+  if (!live[m]) return;
+  const double e = energy[m], ep = e_prev[m];
+  e_hist[int64_t(m) * hist_stride + t - 1] = e;
+  ok_hist[int64_t(m) * hist_stride + t - 1] = ok[m];
+  bool conv;
+  if (t >= max_iters || e <= kEnergyFloor) conv = true;
+  else if (t <= alignment_iters + 1 || ep <= kEnergyFloor) conv = false;
+  else conv = fabs(e - ep) / ep < delta_e_max;
+  e_prev[m] = e;
+  if (conv) {
+    live[m] = 0;
+    iters[m] = t;
+    if (nlive) atomicSub(nlive, 1);
+  }
+}
+
+extern "C" int ni_loop_decide(const double* energy, const int32_t* cg_ok, const int32_t* active,
+                              int nact, int t, int max_iters, int alignment_iters,
+                              double delta_e_max, double* e_prev, int32_t* live, int32_t* iters,
+                              double* e_hist, int32_t* ok_hist, int hist_stride,
+                              int32_t* nlive, ni_stream_t stream) {
+  NI_CHECK_ARG(energy && cg_ok && e_prev && live && iters && e_hist && ok_hist, "null pointer");
+  NI_CHECK_ARG(nact >= 0 && t >= 1 && t <= hist_stride, "bad iteration / sizes");
+  NI_CHECK_ARG(active || nact == 0, "null active list");
+  if (nact == 0) return NI_OK;
+  NI_COUNT_LAUNCH(), loop_decide_kernel<<<div_up(nact, 128), 128, 0, (cudaStream_t)stream>>>(
+                         energy, cg_ok, active, nact, t, max_iters, alignment_iters, delta_e_max,
+                         e_prev, live, iters, e_hist, ok_hist, hist_stride, nlive);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }
@@ -1218,7 +1282,7 @@ extern "C" int ni_merge(const void* quot_ws, size_t quot_bytes, int K, int count
   NI_COUNT_LAUNCH(), merge_energy_kernel<<<dim3(kEChunks, nmerge), 256, 0, s>>>(q, m, residual,
                                                                                  weights, m.epart);
   NI_COUNT_LAUNCH(), chunk_sum_kernel<<<div_up(nmerge, 64), 64, 0, s>>>(m.epart, m.mp.active,
-                                                                       nmerge, energy_out);
+                                                                       nmerge, energy_out, nullptr);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
   NI_COUNT_LAUNCH(), merge_relabel_kernel<<<blocks_for(nmerge * per_map), 256, 0, s>>>(

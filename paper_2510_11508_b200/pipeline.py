@@ -380,7 +380,7 @@ class _BatchLoop:
                                          C.byref(npairs), self._hp(self.map_edges), g.s()),
                    "build_quotient")
 
-    def step(self, z: torch.Tensor, t: int, active: np.ndarray):
+    def step(self, z: torch.Tensor, t: int, active: np.ndarray, live: torch.Tensor | None = None):
         g, lib = self.g, self.g.lib
         st, wp = self.settings, self.weights
         omega_a, omega_b, gamma, eflags = self.co
@@ -394,7 +394,7 @@ class _BatchLoop:
             _ptr(omega_a), _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.H, g.W, g.conn, g.model, t,
             st.alignment_iters, wp.mode_code, C.c_double(wp.k), C.c_double(wp.outlier_low),
             C.c_double(wp.outlier_high), C.c_double(st.cg_tol), int(st.cg_max_iters), _ptr(z),
-            _ptr(self.zshift), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
+            _ptr(self.zshift), _ptr(live), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy), _ptr(self.ok), _ptr(ws),
             ws.numel(), g.s()), "relative_scale_step")
         self.last_scales = scales
         return residual, wts
@@ -407,6 +407,101 @@ class _BatchLoop:
                                 len(merging), _ptr(self.labels), g.H, g.W, _ptr(residual),
                                 _ptr(wts), _ptr(self.new_count), _ptr(self.merge_energy),
                                 _ptr(ws), ws.numel(), g.s()), "merge_components")
+
+
+class _DeviceLoop:
+    """Chunks of outer iterations with the convergence test on the device
+    (ni_loop_decide): maps that converge inside a chunk sit the remaining
+    steps out (live flag 0); the host reads energies, cap flags and
+    convergence points back once per chunk and writes the same records as the
+    per-iteration loop.  A chunk never contains a merge step."""
+
+    MAX_CHUNK = 64
+    LAG = 3  # iterations enqueued ahead of the last one whose outcome the host has seen
+
+    def __init__(self, g: _Grid, settings: SolveSettings):
+        self.g, self.settings = g, settings
+        dev, B, T = g.dev, g.B, max(settings.max_iters, 1)
+        self.T = T
+        self.live = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.iters = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.e_hist = torch.zeros((B, T), dtype=torch.float64, device=dev)
+        self.ok_hist = torch.zeros((B, T), dtype=torch.int32, device=dev)
+        self.e_prev = torch.zeros(B, dtype=torch.float64, device=dev)
+        self.nlive = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.nlive_host = torch.zeros(self.MAX_CHUNK, dtype=torch.int32, pin_memory=True)
+        self.events = [torch.cuda.Event() for _ in range(self.MAX_CHUNK)]
+        self.t0 = 0
+        self.wall = 0.0
+
+    def length(self, t: int) -> int:
+        st = self.settings
+        k = st.max_iters - t
+        if st.freq_merging is not None:  # stop before the next step t' with (t' + 1) % f == 0
+            k = min(k, (st.freq_merging - 1 - t) % st.freq_merging)
+        return min(k, self.MAX_CHUNK)
+
+    def run(self, loop: "_BatchLoop", z, t: int, k: int, active: np.ndarray) -> int:
+        g, st = self.g, self.settings
+        start = time.perf_counter()
+        act = torch.from_numpy(np.ascontiguousarray(active, dtype=np.int32)).to(g.dev)
+        self.live.zero_()
+        self.live[act.long()] = 1
+        self.iters.zero_()
+        self.nlive.fill_(len(active))
+        self.t0 = t
+        stream = torch.cuda.current_stream(g.dev)
+        for i in range(k):
+            # stop once every map has converged, judged LAG iterations behind
+            # the queue head (at most LAG iterations run with no map left)
+            if i >= self.LAG:
+                self.events[i - self.LAG].synchronize()
+                if int(self.nlive_host[i - self.LAG]) == 0:
+                    break
+            loop.step(z, t, active, self.live)
+            t += 1
+            _lib.check(g.lib.ni_loop_decide(
+                _ptr(loop.energy), _ptr(loop.ok), _ptr(act), len(active), t, st.max_iters,
+                st.alignment_iters, C.c_double(st.delta_e_max), _ptr(self.e_prev),
+                _ptr(self.live), _ptr(self.iters), _ptr(self.e_hist), _ptr(self.ok_hist),
+                self.T, _ptr(self.nlive), g.s()), "convergence test")
+            self.nlive_host[i:i + 1].copy_(self.nlive, non_blocking=True)
+            self.events[i].record(stream)
+        self.wall = _ms(start) / max(t - self.t0, 1)
+        return t
+
+    def collect(self, loop, active, t, e_prev, energies, records, warnings, iters) -> list:
+        t0 = self.t0
+        host = torch.cat([self.e_hist[:, t0:t].reshape(-1),
+                          self.ok_hist[:, t0:t].reshape(-1).to(torch.float64),
+                          self.live.to(torch.float64), self.iters.to(torch.float64),
+                          self.e_prev]).cpu().numpy()
+        B, k = self.g.B, t - t0
+        eh = host[:B * k].reshape(B, k)
+        oh = host[B * k:2 * B * k].reshape(B, k)
+        live = host[2 * B * k:2 * B * k + B]
+        conv = host[2 * B * k + B:2 * B * k + 2 * B]
+        ep = host[2 * B * k + 2 * B:]
+        still = []
+        for m in active:
+            m = int(m)
+            last = int(conv[m]) if not live[m] else t
+            for tt in range(t0 + 1, last + 1):
+                e_t = float(eh[m, tt - 1 - t0])
+                if not oh[m, tt - 1 - t0]:
+                    warnings[m].append(f"iteration {tt - 1}: cg hit iteration cap")
+                energies[m].append(e_t)
+                records[m].append({"t": tt, "E_t": e_t, "component_count": int(loop.count[m]),
+                                   "merge_performed": False, "wall_ms": self.wall})
+            e_prev[m] = float(ep[m])
+            if live[m]:
+                still.append(m)
+            else:
+                iters[m] = last
+        return still
+
+    def sync_prev(self, e_prev: np.ndarray):
+        self.e_prev.copy_(torch.from_numpy(np.ascontiguousarray(e_prev, dtype=np.float64)))
 
 
 def _validate(model, connectivity):
@@ -514,8 +609,18 @@ def run_pipeline_batch(
     iters = np.zeros(B, dtype=np.int64)
     version = np.zeros(B, dtype=np.int64)
     hasher = None
+    chunk = _DeviceLoop(g, settings)
     t = 0
     while len(active):
+        # iterations that cannot merge run back to back with the convergence
+        # test on the device (one read-back per chunk instead of per iteration)
+        k = chunk.length(t)
+        if k >= 2:
+            chunk.sync_prev(e_prev)
+            t = chunk.run(loop, z, t, k, active)
+            still = chunk.collect(loop, active, t, e_prev, energies, records, warnings, iters)
+            active = np.array(still, dtype=np.int32)
+            continue
         it_start = time.perf_counter()
         residual, wts = loop.step(z, t, active)
         t_step = t
