@@ -153,8 +153,8 @@ def measured_peak():
 
 
 def traffic_from_profile():
-    """dram bytes per launch of fill_cg_kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "fill_cg_traffic.json")
+    """DRAM bytes per pixel of the fine passes from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "mg_traffic.json")
     try:
         with open(p) as f:
             return json.load(f)
@@ -173,7 +173,7 @@ def mg_roofline(fills, step_ms):
          for k in ("pass_a_ms", "pass_b_ms", "coarse_ms", "scalar_ms")}
     peak, peak_src = measured_peak()
     passes = {}
-    for name, key, nbytes in (("pass_a_kernel<8>", "pass_a_ms", PASS_A_BYTES),
+    for name, key, nbytes in (("pass_a2_kernel<8>", "pass_a_ms", PASS_A_BYTES),
                               ("pass_b_kernel<8>", "pass_b_ms", PASS_B_BYTES)):
         ms_k = t[key]
         ach = nbytes * pxv / (ms_k * 1e-3) / 1e9 if ms_k > 0 else 0.0
