@@ -236,6 +236,26 @@ int ni_loop_decide(const double* energy, const int32_t* cg_ok, const int32_t* ac
                    double* e_prev, int32_t* live, int32_t* iters, double* e_hist,
                    int32_t* ok_hist, int hist_stride, int32_t* nlive, ni_stream_t stream);
 
+/* k_iters outer iterations (0-based t .. t + k_iters - 1) for maps with
+ * small quotients (<= max_edges inter edges and <= max_comps components,
+ * ni_scale_fused_limits), one CTA per map of active[0..nact) (HOST list), in
+ * a single launch: each iteration is ni_scale_step with deferred scales
+ * (zshift) followed by ni_loop_decide; a map's CTA stops at its convergence.
+ * Same arguments and outputs as those calls.  Asynchronous. */
+int ni_scale_step_fused(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+                        const int32_t* map_first, const int32_t* map_count,
+                        const int32_t* active, int nact, const int32_t* labels,
+                        const double* omega_a, const double* omega_b, const double* gamma,
+                        const uint8_t* eflags, int H, int W, int connectivity, int model, int t,
+                        int k_iters, int alignment_iters, int mode, double k, double outlier_low,
+                        double outlier_high, double cg_tol, int cg_max_iters, const double* z,
+                        double* zshift, double* scales, double* residual, double* weights,
+                        double* energy_out, int32_t* cg_ok_out, int max_iters,
+                        double delta_e_max, double* e_prev, int32_t* live, int32_t* iters,
+                        double* e_hist, int32_t* ok_hist, int hist_stride, int32_t* nlive,
+                        void* workspace, size_t workspace_bytes, ni_stream_t stream);
+int ni_scale_fused_limits(int* max_edges, int* max_comps);
+
 /* z[valid] += zshift[label] on the pixels of maps[0..nmaps) (a HOST list),
  * then zshift = 0 on those maps' components: the deferred scales of
  * ni_scale_step folded into the log-depth (pipeline.py:181-182), before a

@@ -67,6 +67,10 @@ SIGNATURES = {
                        _P], _I),
     "ni_loop_decide": ([_P, _P, _P, _I, _I, _I, _I, _D, _P, _P, _P, _P, _P, _I, _P, _P], _I),
     "ni_apply_shift": ([_P, _P, _P, _I, _I, _I, _P, _I, _P, _SZ, _P], _I),
+    "ni_scale_step_fused": ([_P, _SZ, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _I,
+                             _I, _I, _I, _I, _I, _I, _D, _D, _D, _D, _I, _P, _P, _P, _P, _P,
+                             _P, _P, _I, _D, _P, _P, _P, _P, _P, _I, _P, _P, _SZ, _P], _I),
+    "ni_scale_fused_limits": ([_PI32, _PI32], _I),
     "ni_merge_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_merge": ([_P, _SZ, _I, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P, _P, _P, _P, _P, _SZ, _P],
                  _I),

@@ -59,6 +59,9 @@ extern thread_local FillReport g_fill_report;
     }                                                                                   \
   } while (0)
 
+// an environment knob read once per process (experiment switches; never per call)
+#define NI_ENV_ONCE(name) ([] { static const char* v_ = getenv(name); return v_; }())
+
 #define NI_CHECK_ARG(cond, msg)              \
   do {                                       \
     if (!(cond)) {                           \

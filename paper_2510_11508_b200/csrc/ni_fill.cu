@@ -1,28 +1,29 @@
-// K3 -- fill_components (solver.py:195-239) as ONE batched CG over every
-// component of the partition, matrix-free on the pixel grid, run by ONE
-// persistent cooperative kernel whose workers are independent warps.
+// Weighted fill passes -- the refill pass of solver.py:237-238 and the
+// pixel-level baseline of pipeline.py:297-369 -- as ONE batched,
+// unpreconditioned CG over every component of the partition, matrix-free on
+// the pixel grid, run by ONE persistent kernel of independent worker warps.
+// (The plain fill at z = 0 runs the multigrid-preconditioned solve of
+// ni_mg.cu; this kernel also serves it behind NI_FILL_SOLVER=cg.)
 //
 // Per component c the reference solves (A^T W A) x = A^T W b with scipy's
 // unpreconditioned CG (x0 = 0, stop when ||r|| < rtol ||b|| at the top of an
-// iteration, cap max(cg_max_iters, n_c); solver.py:97-122).  At the fill
-// state z = 0 every bilateral factor is 1/2 (continuity.py:302-308), so
-// W_a = gamma_a^2 / 2 and A^T W A is the graph Laplacian of the intra-
-// component valid edges with conductance c_ab = W_a + W_b (SURVEY.md
-// Appendix A).  All components iterate together; each keeps its own
-// alpha/beta/rho, stop test and cap, exactly like separate scipy solves.
-// The stencil is applied in difference form q_a = sum c_ab (p_a - p_b), so
-// constants stay an exact null vector in float32 (a rounded CSR Laplacian
-// loses that and doubles the iteration count).
+// iteration, cap max(cg_max_iters, n_c); solver.py:97-122).  Without edge
+// weights (the fill at z = 0) every bilateral factor is 1/2
+// (continuity.py:302-308): W_a = gamma_a^2 / 2 and A^T W A is the graph
+// Laplacian of the intra-component valid edges with conductance c_ab = W_a +
+// W_b; the EW variant takes per-edge weights (w_a, w_b) instead.  All
+// components iterate together; each keeps its own alpha/beta/rho, stop test
+// and cap, exactly like separate scipy solves.  The stencil is applied in
+// difference form q_a = sum c_ab (p_a - p_b), so constants stay an exact
+// null vector in float32.
 //
 // Data layout in HBM.  rows = B*H; pixel (y, x) lives at padded index
 // (y + RM) * P + (x + XM) with zeroed margins, so no access needs a bounds
-// check (RM = 2 rows top / RB rows bottom, XM = 16 columns left, >= 32
-// right):
+// check:
 //   v[2]  : float4 {r, q, p, x} per pixel, double-buffered by iteration
 //           parity (a sweep reads its neighbours' previous values while other
-//           warps write the new ones): one 16-B load and one 16-B store per
-//           pixel and iteration
-//   hw    : float32 W_a = gamma_a^2 / 2  (c_ab = hw_a + hw_b)
+//           warps write the new ones)
+//   hw    : float32 W_a = gamma_a^2 / 2 (EW: four forward conductances)
 //   imask : uint8, bit k = forward edge k intra-component and valid,
 //           bit 4+k = backward edge k (pixel - offset_k)
 //   lab   : int32 labels (read by mixed items only)
@@ -39,15 +40,17 @@
 // stops gets one last "flush" sweep that applies its pending x update; its
 // final x then lives in the buffer of that sweep's parity.
 //
-// Work decomposition: strips of 30 columns x 30 rows.  A warp processes a
-// strip ("item") by marching down its rows: raw rows are prefetched into a
-// 6-row register ring four rows ahead, each row's p' = r + beta p is formed
-// once and shuffled to the neighbouring lanes (lanes 0 and 31 hold the halo
-// columns), and the row loop is unrolled by the ring period so no register
-// moves wait on loads.  No block barrier anywhere in a sweep.  A strip
-// touching several multi-pixel components becomes ceil(n/2) "mixed" items of
-// <= 2 components that read labels; a strip with one component is a "pure"
-// item (singleton / invalid pixels carry r = q = p = x = 0 and stay 0).
+// Work decomposition: strips of 30 x 30 centre pixels, never straddling two
+// maps.  A warp processes a strip ("item") by streaming its 32 rows (lanes
+// and rows 0 / 31 are the halo) through a per-warp shared-memory ring of row
+// slots filled by cp.async several rows ahead, forming p' = r + beta p once
+// per row and taking the horizontal neighbours by shuffles.  A CTA (one per
+// SM) is 15 sweeping warps + 1 scheduler warp that claims items into
+// per-worker mailboxes and retires finished ones; components sharing items
+// iterate in lockstep "groups" whose batches are published through a ring
+// (DESIGN.md s5b).  A strip touching several multi-pixel components becomes
+// items of <= 2 components that read labels; a strip with one component is
+// a "pure" item (singleton / invalid pixels carry r = q = p = x = 0).
 //
 // Reductions are deterministic: each item writes float64 partials per
 // component (lane-local sums over rows, fixed xor tree over lanes); the last
@@ -1864,7 +1867,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   // components into one lockstep group.  With many maps the groups (about
   // one per map) overlap each other well and pairing saves re-reading mixed
   // strips; with few maps one group per component overlaps far better.
-  const char* pe = getenv("NI_FILL_PAIR");
+  const char* pe = NI_ENV_ONCE("NI_FILL_PAIR");
   const int per = pe ? (atoi(pe) > 1 ? SLOTS : 1) : (B >= kPairMaps ? SLOTS : 1);
   NI_COUNT_LAUNCH(), item_counts_kernel<<<div_up(nstrips, 256), 256, 0, s>>>(w.nslots, nstrips, per,
                                                                             w.nitems_strip);
@@ -1921,7 +1924,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_tail, 0, sizeof(uint32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.ring_hint, 0, sizeof(uint32_t), s));
   NI_CUDA_TRY(cudaMemsetAsync(w.gactive, 0, sizeof(int32_t), s));
-  const char* we = getenv("NI_FILL_WINDOW");
+  const char* we = NI_ENV_ONCE("NI_FILL_WINDOW");
   const int window = we ? atoi(we) : 0;
   NI_CUDA_TRY(cudaMemcpyAsync(w.gnext, &window, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   FillArgs a;
@@ -1960,7 +1963,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
   // unpaired items) spread over more workers; with many lockstep groups two
   // queued items keep every worker's row stream continuous.
   {
-    const char* me = getenv("NI_FILL_MB");
+    const char* me = NI_ENV_ONCE("NI_FILL_MB");
     a.mb = me ? atoi(me) : (per > 1 ? MB : 1);
     if (a.mb < 1) a.mb = 1;
     if (a.mb > MB) a.mb = MB;
@@ -2054,7 +2057,7 @@ extern "C" int ni_fill(const int32_t* labels, int count, const double* omega_a,
             "scheduler retire=%.1f%% claim=%.1f%% items/claim=%.2f\n",
             a.G, 100.0 * h[1] / h[0], 100.0 * h[2] / h[0], double(h[0]) / double(h[3]),
             100.0 * h[5] / h[4], 100.0 * h[6] / h[4], double(h[3]) / double(h[7]));
-    if (const char* tp = getenv("NI_FILL_TRACE")) {  // batch publish timeline per group
+    if (const char* tp = NI_ENV_ONCE("NI_FILL_TRACE")) {  // batch publish timeline per group
       static int hn[kTraceG];
       static unsigned long long ht[kTraceG * kTraceI];
       NI_CUDA_TRY(cudaMemcpyFromSymbol(hn, g_pub_n, sizeof(hn)));

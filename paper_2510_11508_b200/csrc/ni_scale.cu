@@ -1171,6 +1171,358 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   return NI_OK;
 }
 
+// ---------------------------------------------------- fused per-map step
+//
+// Maps whose quotient is small (<= kFusedMaxEdges inter edges, <=
+// kFusedMaxComps components) take the whole iteration -- weights, pair and
+// component sums, the null-space projection, the CG, residual rows, energy,
+// the deferred shift and the convergence test -- in ONE CTA: one launch per
+// iteration for every such map of the batch instead of ~15 small launches.
+// Same arithmetic as the multi-kernel step; the pair sums, component sums
+// and CG reduce in the same orders, the part means and the energy in other
+// fixed orders (a map's path depends only on its own sizes, so batched and
+// single-map runs stay bit-identical).
+constexpr int kFusedThreads = 512;
+constexpr int kFusedMaxEdges = 1 << 17;
+constexpr int kFusedMaxComps = 1024;
+
+struct DecideArgs {
+  int t;  // 1-based iteration after this step
+  int max_iters, alignment_iters;
+  double delta_e_max;
+  double* e_prev;
+  int32_t* live;
+  int32_t* iters;
+  double* e_hist;
+  int32_t* ok_hist;
+  int hist_stride;
+  int32_t* nlive;
+};
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One outer iteration of map m by the whole CTA (the body of the chunk loop).
+template <int CONN, int MODEL>
+__device__ void fused_iteration(
+    int m, const Quot& q, const StepWs& w, const double* __restrict__ z,
+    const double* __restrict__ zs, const int32_t* __restrict__ zlab,
+    const double* __restrict__ omega_a, const double* __restrict__ omega_b,
+    const double* __restrict__ gamma, const uint8_t* __restrict__ eflags, int H, int W,
+    int64_t npix, const WeightArgs& wp, double rtol, int cg_max_iters, double* __restrict__ s,
+    double* __restrict__ residual, double* __restrict__ weights, double* __restrict__ energy_out,
+    int32_t* __restrict__ ok_out, double* __restrict__ zshift, const DecideArgs& da, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int e0 = q.estart[m], e1 = q.estart[m + 1];
+  const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
+  // K4: weights and row right-hand sides (solver.py:253-278, 170-180)
+  for (int e = e0 + tid; e < e1; e += nt) {
+    const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
+    double wa, wb;
+    edge_weights_at<CONN, MODEL>(z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W, npix, a, k,
+                                 wp, wa, wb);
+    const double za = z_at(z, zs, zlab, a), zb = z_at(z, zs, zlab, b);
+    const double oa = omega_a[k * npix + a];
+    const double ob = MODEL == 0 ? -oa : omega_b[k * npix + a];
+    w.wa[e] = wa;
+    w.wb[e] = wb;
+    w.ba[e] = oa - (za - zb);
+    w.bb[e] = ob - (zb - za);
+  }
+  __syncthreads();
+  // K5a: pair conductances (the map's pairs are a contiguous run of the
+  // (min, max)-sorted pair list); a warp per pair, as pair_sum_kernel
+  const int U = q.nU[0];
+  const int u0 = lower_bound_i32(q.pp, U, c0), u1 = lower_bound_i32(q.pp, U, c1);
+  for (int u = u0 + wid; u < u1; u += nw) {
+    double sum = 0.0;
+    for (int j = q.pstart[u] + lane; j < q.pstart[u + 1]; j += 32) {
+      const int e = q.order[j];
+      sum += w.wa[e] + w.wb[e];
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) w.S[u] = sum;
+  }
+  __syncthreads();
+  // K5b: diagonal and A^T W b per component: a warp per component,
+  // lane-strided over its incident entries in edge order
+  for (int c = c0 + wid; c < c1; c += nw) {
+    double d = 0.0, r = 0.0;
+    for (int j = q.cstart[c] + lane; j < q.cstart[c + 1]; j += 32) {
+      const int ent = q.cent[j];
+      const int e = ent >> 1;
+      const double wa = w.wa[e], wb = w.wb[e];
+      const double t = wa * w.ba[e] - wb * w.bb[e];
+      d += wa + wb;
+      r += (ent & 1) ? -t : t;
+    }
+    d = warp_sum(d);
+    r = warp_sum(r);
+    if (lane == 0) {
+      w.diag[c] = d;
+      w.rhs[c] = r;
+    }
+  }
+  // roundoff null-space removal per part (components joined by S > 0)
+  for (int c = c0 + tid; c < c1; c += nt) w.parent[c] = c;
+  __syncthreads();
+  for (int u = u0 + tid; u < u1; u += nt)
+    if (w.S[u] > 0.0) uf_union(w.parent, q.pp[u], q.pq[u]);
+  __syncthreads();
+  for (int c = c0 + tid; c < c1; c += nt) w.pkey[c] = uf_find(w.parent, c);
+  __syncthreads();
+  // a warp per part root: its components in ascending id, lane-strided
+  for (int r0 = c0 + wid; r0 < c1; r0 += nw) {
+    if (w.pkey[r0] != r0) continue;  // warp-uniform
+    double sum = 0.0, cnt = 0.0;
+    for (int c = c0 + lane; c < c1; c += 32)
+      if (w.pkey[c] == r0) {
+        sum += w.rhs[c];
+        cnt += 1.0;
+      }
+    sum = warp_sum(sum);
+    cnt = warp_sum(cnt);
+    if (lane == 0) w.r[r0] = sum / cnt;  // the part's mean, stashed at its root
+  }
+  __syncthreads();
+  for (int c = c0 + tid; c < c1; c += nt) w.q[c] = w.rhs[c] - w.r[w.pkey[c]];
+  __syncthreads();
+  for (int c = c0 + tid; c < c1; c += nt) w.rhs[c] = w.q[c];
+  __syncthreads();
+  // K6: the map's CG.  Up to 32 components: one warp, a lane per component,
+  // shuffle reductions only (no block barrier per CG iteration).
+  if (n <= 32) {
+    if (wid == 0) {
+      const int maxiter = cg_max_iters > n ? cg_max_iters : n;
+      const int c = c0 + lane;
+      const bool own = lane < n;
+      const double b = own ? w.rhs[c] : 0.0;
+      double x = 0.0, r = b, p = 0.0;
+      double rr = warp_sum(b * b);
+      const double bnrm = sqrt(rr);
+      int ok = 1;
+      if (bnrm != 0.0) {
+        const double atol = rtol * bnrm;
+        double rho_prev = 0.0;
+        ok = 0;
+        for (int it = 0; it < maxiter; ++it) {
+          if (sqrt(rr) < atol) {
+            ok = 1;
+            break;
+          }
+          const double rho = rr;
+          const double beta = it == 0 ? 0.0 : rho / rho_prev;
+          p = r + beta * p;
+          // q = L p: the diagonal and the pair conductances of the lane's row,
+          // neighbours' p by shuffle (their lane = column - c0)
+          double aq = own ? w.diag[c] * p : 0.0;
+          const int j0 = own ? q.lstart[c] : 0, j1 = own ? q.lstart[c + 1] : 0;
+          int jmax = j1 - j0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+          for (int jj = 0; jj < jmax; ++jj) {
+            const bool has = jj < j1 - j0;
+            const int col = has ? q.lcol[j0 + jj] - c0 : 0;
+            const double pn = __shfl_sync(0xffffffffu, p, col);
+            if (has) aq -= w.S[q.lpair[j0 + jj]] * pn;
+          }
+          const double pq = warp_sum(p * aq);
+          const double alpha = rho / pq;
+          x += alpha * p;
+          r -= alpha * aq;
+          rr = warp_sum(r * r);
+          rho_prev = rho;
+        }
+      }
+      if (own) s[c] = x;
+      if (lane == 0) ok_out[m] = ok;
+    }
+    __syncthreads();
+  } else {
+    const int maxiter = cg_max_iters > n ? cg_max_iters : n;
+    double rr = 0.0;
+    for (int c = c0 + tid; c < c1; c += nt) {
+      const double b = w.rhs[c];
+      s[c] = 0.0;
+      w.r[c] = b;
+      w.p0[c] = 0.0;
+      rr += b * b;
+    }
+    rr = block_sum(rr, red);
+    const double bnrm = sqrt(rr);
+    int ok = 1;
+    if (bnrm != 0.0) {
+      const double atol = rtol * bnrm;
+      double rho_prev = 0.0;
+      double* pold = w.p0;
+      double* pnew = w.p1;
+      ok = 0;
+      CgArgs g{c0, c1, maxiter, rtol, s, ok_out, m};
+      for (int it = 0; it < maxiter; ++it) {
+        if (sqrt(rr) < atol) {
+          ok = 1;
+          break;
+        }
+        const double rho = rr;
+        const double beta = it == 0 ? 0.0 : rho / rho_prev;
+        __syncthreads();
+        double pq = cg_sweep<int>(q, w, g, tid, nt, beta, pold, pnew);
+        pq = block_sum(pq, red);
+        const double alpha = rho / pq;
+        double rn = 0.0;
+        for (int c = c0 + tid; c < c1; c += nt) {
+          s[c] += alpha * pnew[c];
+          const double r2 = w.r[c] - alpha * w.q[c];
+          w.r[c] = r2;
+          rn += r2 * r2;
+        }
+        rr = block_sum(rn, red);
+        rho_prev = rho;
+        double* tp = pold;
+        pold = pnew;
+        pnew = tp;
+      }
+    }
+    if (tid == 0) ok_out[m] = ok;
+  }
+  __syncthreads();
+  // K7a: residual rows and the map's energy (solver.py:301-302)
+  double en = 0.0;
+  for (int e = e0 + tid; e < e1; e += nt) {
+    const double sa = s[q.pa[e]], sb = s[q.pb[e]];
+    const double ra = sa - sb - w.ba[e];
+    const double rb = sb - sa - w.bb[e];
+    residual[2 * e] = ra;
+    residual[2 * e + 1] = rb;
+    weights[2 * e] = w.wa[e];
+    weights[2 * e + 1] = w.wb[e];
+    en += ra * (w.wa[e] * ra) + rb * (w.wb[e] * rb);
+  }
+  en = block_sum(en, red);
+  // K7b: deferred z += s[label]
+  for (int c = c0 + tid; c < c1; c += nt) zshift[c] += s[c];
+  // the convergence test of pipeline.py:66-83
+  if (tid == 0) {
+    energy_out[m] = en;
+    const double ep = da.e_prev[m];
+    const int t = da.t;
+    da.e_hist[int64_t(m) * da.hist_stride + t - 1] = en;
+    da.ok_hist[int64_t(m) * da.hist_stride + t - 1] = ok_out[m];
+    bool conv;
+    if (t >= da.max_iters || en <= kEnergyFloor) conv = true;
+    else if (t <= da.alignment_iters + 1 || ep <= kEnergyFloor) conv = false;
+    else conv = fabs(en - ep) / ep < da.delta_e_max;
+    da.e_prev[m] = en;
+    if (conv) {
+      da.live[m] = 0;
+      da.iters[m] = t;
+      atomicSub(da.nlive, 1);
+    }
+  }
+  __syncthreads();
+}
+
+// k outer iterations of each map (a CTA per map, its loop entirely inside the
+// CTA: maps never interact), stopping at the map's convergence.
+template <int CONN, int MODEL>
+__global__ void __launch_bounds__(kFusedThreads) scale_fused_kernel(
+    Quot q, StepWs w, const double* __restrict__ z, const double* __restrict__ zs,
+    const int32_t* __restrict__ zlab, const double* __restrict__ omega_a,
+    const double* __restrict__ omega_b, const double* __restrict__ gamma,
+    const uint8_t* __restrict__ eflags, int H, int W, int64_t npix, WeightArgs wp, int t0,
+    int k, int alignment_iters, double rtol, int cg_max_iters, double* __restrict__ s,
+    double* __restrict__ residual, double* __restrict__ weights,
+    double* __restrict__ energy_out, int32_t* __restrict__ ok_out,
+    double* __restrict__ zshift, DecideArgs da) {
+  __shared__ double red[32];
+  const int m = w.mp.active[blockIdx.x];
+  for (int i = 0; i < k; ++i) {
+    if (!da.live[m]) return;  // uniform: written by thread 0 before the previous barrier
+    WeightArgs wi = wp;
+    wi.wmode = t0 + i < alignment_iters ? EW_UNIFORM : EW_FULL;
+    DecideArgs di = da;
+    di.t = t0 + i + 1;
+    fused_iteration<CONN, MODEL>(m, q, w, z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W,
+                                 npix, wi, rtol, cg_max_iters, s, residual, weights, energy_out,
+                                 ok_out, zshift, di, red);
+  }
+}
+
+extern "C" int ni_scale_step_fused(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
+                                   const int32_t* map_first, const int32_t* map_count,
+                                   const int32_t* active, int nact, const int32_t* labels,
+                                   const double* omega_a, const double* omega_b,
+                                   const double* gamma, const uint8_t* eflags, int H, int W,
+                                   int connectivity, int model, int t, int k_iters,
+                                   int alignment_iters,
+                                   int mode, double k, double outlier_low, double outlier_high,
+                                   double cg_tol, int cg_max_iters, const double* z,
+                                   double* zshift, double* scales, double* residual,
+                                   double* weights, double* energy_out, int32_t* cg_ok_out,
+                                   int max_iters, double delta_e_max, double* e_prev,
+                                   int32_t* live, int32_t* iters, double* e_hist, int32_t* ok_hist,
+                                   int hist_stride, int32_t* nlive, void* workspace,
+                                   size_t workspace_bytes, ni_stream_t stream) {
+  NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
+  NI_CHECK_ARG(count >= 1 && K >= 1 && B >= 1 && nact >= 0 && nact <= B, "bad sizes");
+  NI_CHECK_ARG(map_first && map_count && (active || nact == 0), "null map table");
+  NI_CHECK_ARG(z && zshift && live && e_prev && iters && e_hist && ok_hist && nlive, "null pointer");
+  NI_CHECK_ARG(t >= 0 && k_iters >= 1 && t + k_iters <= hist_stride, "bad iteration range");
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver cq(const_cast<void*>(quot_ws), quot_bytes);
+  Quot q;
+  carve_quot(cq, q, K, count, B);
+  Carver c(workspace, workspace_bytes);
+  StepWs w;
+  carve_step(c, w, K, count, B);
+  if (!c.ok() || !workspace || !cq.ok()) {
+    set_error("ni_scale_step_fused: workspace too small");
+    return NI_ERR_WORKSPACE;
+  }
+  if (nact == 0) return NI_OK;
+  for (int j = 0; j < nact; ++j) {
+    const int mm = active[j];
+    NI_CHECK_ARG(mm >= 0 && mm < B && map_count[mm] <= kFusedMaxComps, "map too large to fuse");
+  }
+  NI_TRY(upload_maps(w.mp, map_first, map_count, active, nact, s));
+  w.mp.live = live;
+  WeightArgs wp;
+  wp.wmode = EW_FULL;  // per iteration in the kernel
+  wp.mode = mode;
+  wp.k = k;
+  wp.lt = log10(outlier_low);
+  wp.ut = log10(outlier_high);
+  wp.hi = outlier_high;
+  DecideArgs da{t + 1, max_iters, alignment_iters, delta_e_max, e_prev, live, iters,
+                e_hist, ok_hist, hist_stride, nlive};
+  const int64_t npix = int64_t(B) * H * W;
+#define NI_FUSED(CN, MD)                                                                       \
+  NI_COUNT_LAUNCH(), scale_fused_kernel<CN, MD><<<nact, kFusedThreads, 0, s>>>(                 \
+                         q, w, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, \
+                         wp, t, k_iters, alignment_iters, cg_tol, cg_max_iters, scales,        \
+                         residual, weights, energy_out, cg_ok_out, zshift, da)
+  if (connectivity == 8) NI_FUSED(8, 0);
+  else if (model == 0) NI_FUSED(4, 0);
+  else NI_FUSED(4, 1);
+#undef NI_FUSED
+  NI_LAUNCH_CHECK();
+  return NI_OK;
+}
+
+extern "C" int ni_scale_fused_limits(int* max_edges, int* max_comps) {
+  if (max_edges) *max_edges = kFusedMaxEdges;
+  if (max_comps) *max_comps = kFusedMaxComps;
+  return NI_OK;
+}
+
 // pipeline.py:66-83 for every live map of the active list after the step at
 // 1-based iteration t: record E_t and the CG flag, then the convergence test
 // against the previous energy; a converged map drops its live flag.

@@ -328,6 +328,7 @@ class _BatchLoop:
         # z (ni_apply_shift) before a merge relabels a map and at the end
         self.zshift = None
         self._mapws = devmem.empty(4 * g.B, torch.uint8, dev)
+        self._fused_bufs = None
 
     def defer_scales(self):
         self.zshift = torch.zeros(self.C, dtype=torch.float64, device=self.g.dev)
@@ -399,6 +400,40 @@ class _BatchLoop:
         self.last_scales = scales
         return residual, wts
 
+    def step_fused(self, z: torch.Tensor, t: int, k: int, maps: np.ndarray, dl: "_DeviceLoop"):
+        """Iterations t .. t + k - 1 with the convergence test of the
+        small-quotient maps ``maps``, a CTA per map, in one launch
+        (ni_scale_step_fused)."""
+        g, lib = self.g, self.g.lib
+        st, wp = self.settings, self.weights
+        omega_a, omega_b, gamma, eflags = self.co
+        if self._fused_bufs is None or self._fused_bufs[0].numel() < self.C:
+            self._fused_bufs = (devmem.empty(self.C, torch.float64, g.dev),
+                                devmem.empty(max(2 * self.K, 1), torch.float64, g.dev),
+                                devmem.empty(max(2 * self.K, 1), torch.float64, g.dev),
+                                _ws(_lib.size_query(lib.ni_scale_step_workspace_size, self.K,
+                                                    self.C, g.B), g.dev))
+        scales, residual, wts, ws = self._fused_bufs
+        mp = np.ascontiguousarray(maps, dtype=np.int32)
+        _lib.check(lib.ni_scale_step_fused(
+            _ptr(self.quot), self.quot.numel(), self.K, self.C, g.B, self._hp(self.first),
+            self._hp(self.count), self._hp(mp), len(mp), _ptr(self.labels), _ptr(omega_a),
+            _ptr(omega_b), _ptr(gamma), _ptr(eflags), g.H, g.W, g.conn, g.model, t, k,
+            st.alignment_iters, wp.mode_code, C.c_double(wp.k), C.c_double(wp.outlier_low),
+            C.c_double(wp.outlier_high), C.c_double(st.cg_tol), int(st.cg_max_iters), _ptr(z),
+            _ptr(self.zshift), _ptr(scales), _ptr(residual), _ptr(wts), _ptr(self.energy),
+            _ptr(self.ok), st.max_iters, C.c_double(st.delta_e_max), _ptr(dl.e_prev),
+            _ptr(dl.live), _ptr(dl.iters), _ptr(dl.e_hist), _ptr(dl.ok_hist), dl.T,
+            _ptr(dl.nlive), _ptr(ws), ws.numel(), g.s()), "relative_scale_step")
+
+    def fusable(self, active: np.ndarray) -> np.ndarray:
+        """Maps of ``active`` whose quotient fits one CTA (ni_scale_fused_limits)."""
+        if self.K == 0 or self.zshift is None:
+            return np.zeros(len(active), dtype=bool)
+        me, mc = C.c_int32(0), C.c_int32(0)
+        self.g.lib.ni_scale_fused_limits(C.byref(me), C.byref(mc))
+        return ((self.map_edges[active] <= me.value) & (self.count[active] <= mc.value))
+
     def merge(self, residual, wts, merging: np.ndarray):
         g, lib = self.g, self.g.lib
         ws = _ws(_lib.size_query(lib.ni_merge_workspace_size, self.K, self.C, g.B), g.dev)
@@ -451,6 +486,14 @@ class _DeviceLoop:
         self.nlive.fill_(len(active))
         self.t0 = t
         stream = torch.cuda.current_stream(g.dev)
+        fuse = loop.fusable(active)
+        fused, rest = active[fuse], active[~fuse]
+        if len(fused):  # their whole chunk in one launch
+            loop.step_fused(z, t, k, fused, self)
+        if not len(rest):
+            self.wall = _ms(start) / k
+            return t + k
+        act = torch.from_numpy(np.ascontiguousarray(rest, dtype=np.int32)).to(g.dev)
         for i in range(k):
             # stop once every map has converged, judged LAG iterations behind
             # the queue head (at most LAG iterations run with no map left)
@@ -458,10 +501,10 @@ class _DeviceLoop:
                 self.events[i - self.LAG].synchronize()
                 if int(self.nlive_host[i - self.LAG]) == 0:
                     break
-            loop.step(z, t, active, self.live)
+            loop.step(z, t, rest, self.live)
             t += 1
             _lib.check(g.lib.ni_loop_decide(
-                _ptr(loop.energy), _ptr(loop.ok), _ptr(act), len(active), t, st.max_iters,
+                _ptr(loop.energy), _ptr(loop.ok), _ptr(act), len(rest), t, st.max_iters,
                 st.alignment_iters, C.c_double(st.delta_e_max), _ptr(self.e_prev),
                 _ptr(self.live), _ptr(self.iters), _ptr(self.e_hist), _ptr(self.ok_hist),
                 self.T, _ptr(self.nlive), g.s()), "convergence test")

@@ -86,3 +86,43 @@ def test_png16_and_pfm_normals_decode_bit_exact():
     assert np.array_equal(nm2.mask, e["scene_mask"])
     assert [intr.fx, intr.fy, intr.cx, intr.cy] == list(e["scene_intr"])
     assert np.array_equal(gt, e["depth"])
+
+
+@pytest.mark.gpu
+def test_device_side_writers_match_the_host_formulas(tmp_path):
+    """The writers that do their per-pixel arithmetic on the GPU produce the
+    bytes the reference's host formulas produce: the normals PFM (rewriting
+    the reference's own file byte for byte), the PNG16 quantisation, the
+    depth PFM of a LogDepthMap, the label blob of a device Partition, and the
+    pinned-memory stream writer."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_11508_b200 as nb
+    from paper_2510_11508_b200 import fileio
+
+    pf = fileio.read_normals_pfm(os.path.join(FILES, "normals.pfm"))
+    fileio.write_normals_pfm(tmp_path / "n.pfm", pf)
+    assert (tmp_path / "n.pfm").read_bytes() == open(os.path.join(FILES, "normals.pfm"),
+                                                      "rb").read()
+    nm = fileio.read_png16_normals(os.path.join(FILES, "normals.png"))
+    fileio.write_png16_normals(tmp_path / "n.png", nm)
+    import cv2
+    got = cv2.imread(str(tmp_path / "n.png"), cv2.IMREAD_UNCHANGED)[..., ::-1]
+    want = np.rint(np.clip((nm.normals + 1.0) * 0.5, 0.0, 1.0) * 65535.0).astype(np.uint16)
+    want[~nm.mask] = 0
+    assert np.array_equal(got, want)
+    intr = fileio.load_intrinsics(os.path.join(FILES, "intrinsics.json"))
+    res = nb.run_pipeline(pf, intr, float(np.deg2rad(3.5)))
+    fileio.write_depth(tmp_path / "a.pfm", res.log_depth)
+    fileio.write_depth(tmp_path / "b.pfm", nb.depth_from_logdepth(res.log_depth), pf.mask)
+    assert (tmp_path / "a.pfm").read_bytes() == (tmp_path / "b.pfm").read_bytes()
+    h, w = pf.mask.shape
+    assert fileio.export_labels(res.partition0, w, h) == \
+        fileio.export_labels(res.partition0.labels, w, h)
+    host = torch.from_numpy(np.stack([res.log_depth.values.reshape(-1)] * 2)).pin_memory()
+    with fileio.DepthStreamWriter(h, w) as wr:
+        wr.submit([tmp_path / "s0.pfm", tmp_path / "s1.pfm"], host, np.stack([pf.mask] * 2))
+    fileio.write_depth(tmp_path / "c.pfm", np.exp(res.log_depth.values), pf.mask)
+    for p in ("s0.pfm", "s1.pfm"):
+        assert (tmp_path / p).read_bytes() == (tmp_path / "c.pfm").read_bytes()
