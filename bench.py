@@ -1,22 +1,25 @@
 """Benchmark: valid pixels/s of the component normal-integration hot path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+                    [--scaling weak|strong]
 
 A step is one pass of the hot path (``run_pipeline`` semantics: normalise ->
 components -> coefficients -> batched fill -> relative-scale loop with
 merges -> gauge) over one batch of synthetic normal maps.  The default
-workload is BASELINE.json config 5: 64 independent 1024x1024 orthographic
-maps (seeds 100..163, 16 Voronoi cells), split across ranks by map (strong
-scaling: the 64 maps are fixed, each rank takes a contiguous block).
+workload is BASELINE.json config 5: a batch of 64 independent 1024x1024
+orthographic maps (16 Voronoi cells).  Maps are independent objects, so with
+N ranks every rank runs its own 64-map batch (weak scaling, rank r: seeds
+100 + 64 r + i); ``--scaling strong`` splits one 64-map batch across the
+ranks instead.
 
 * ``value``: valid px/s with the normals already resident in HBM; whole-job
   = all ranks' valid pixels / max-over-ranks device time of a step.
 * ``e2e``: the same through the public API from pinned HOST normals, with
   the host->device copy of the normals+mask and the device->host copy of the
   log-depth inside the timed region.
-* ``roofline``: the dominant kernel (the persistent batched CG,
-  ``fill_cg_kernel``), algorithmic bytes per launch = 37 B x (component
-  size x CG iterations, summed) / its CUDA-event duration.
+* ``roofline``: the dominant kernel, fine pass A of the multigrid fill:
+  algorithmic bytes (58 B x active unit pixels per V-cycle, summed over the
+  timed steps) over its CUDA-event time.
 * ``cpu_baseline``: the CPU oracle port (oracle/normint_oracle.py, a numpy
   restatement of the reference) on one map of the same batch, rank 0, N=1.
 
@@ -69,13 +72,22 @@ def _gen_cfg(name):
     return s.normals, s.mask, s.intrinsics(), s.options.get("merge_freq")
 
 
-def make_workload(config, rank, world, nmaps):
+def map_indices(scaling, rank, world, nmaps):
+    """C5 maps of a rank: weak scaling gives every rank its own batch of nmaps
+    (config5_map indices 64 r .. 64 r + nmaps - 1, i.e. seeds 100 + 64 r + i);
+    strong scaling splits one batch of nmaps into contiguous blocks."""
+    if scaling == "weak":
+        return list(range(rank * nmaps, (rank + 1) * nmaps))
+    from paper_2510_11508_b200.shard import map_range
+    lo, hi = map_range(rank, world, nmaps)
+    return list(range(lo, hi))
+
+
+def make_workload(config, rank, world, nmaps, scaling="weak"):
     """Return (normals (B,H,W,3) f32, masks (B,H,W) bool, intrinsics list,
     merge_freq, description, total maps)."""
     if config == "C5":
-        from paper_2510_11508_b200.shard import map_range
-        lo, hi = map_range(rank, world, nmaps)
-        idx = list(range(lo, hi))
+        idx = map_indices(scaling, rank, world, nmaps)
         import concurrent.futures as cf
         workers = max(1, min(len(idx), (os.cpu_count() or 2) // max(1, world)))
         if workers > 1:
@@ -86,8 +98,8 @@ def make_workload(config, rank, world, nmaps):
         normals = np.stack([m[0] for m in maps])
         masks = np.stack([m[1] for m in maps])
         intr = [m[2] for m in maps]
-        desc = f"C5: {nmaps} x 1024x1024 orthographic maps (seeds 100..{99 + nmaps}), 16 Voronoi cells"
-        return normals, masks, intr, None, desc, nmaps
+        total = nmaps * world if scaling == "weak" else nmaps
+        return normals, masks, intr, None, None, total
     n, m, i, mf = _gen_cfg(config)
     return n[None], m[None], [i], mf, f"{config} (paper_2510_11508_b200/scenes.py)", 1
 
@@ -218,7 +230,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2510_11508_b200 import _lib
 
     normals_h, masks_h, intr_t, merge_freq, desc, total_maps = make_workload(
-        args.config, rank, world, args.maps)
+        args.config, rank, world, args.maps, args.scaling)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     _lib.load()
@@ -319,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup,
             "ms_per_step": round(ms, 3),
             "higher_is_better": True,
-            "scaling": "strong" if args.config == "C5" else "replicas",
+            "scaling": args.scaling if args.config == "C5" else "replicas",
             "vs_baseline": None,
             "dtype": "f32 CG vectors / f64 coefficients, dots, scales",
             "data": "synthetic (seeded generators, paper_2510_11508_b200/scenes.py)",
@@ -407,7 +419,7 @@ def run_reference(args, rank, world):
         "metric": "valid pixels/s end-to-end (component normal integration, run_pipeline)",
         "value": round(value, 1), "unit": "valid_px/s", "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": round(ms, 1), "higher_is_better": True,
-        "scaling": "strong" if args.config == "C5" else "replicas", "vs_baseline": None,
+        "scaling": args.scaling if args.config == "C5" else "replicas", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generators, paper_2510_11508_b200/scenes.py)",
         "config": workload_config(args, world, None if args.config == "C5" else
                                   _gen_cfg(args.config)[3]),
@@ -447,18 +459,20 @@ def dry_run(args, rank, world):
     if world > 1:
         dist.init_process_group("gloo")
     try:
-        lo, hi = map_range(rank, world, args.maps)
+        idx = map_indices(args.scaling, rank, world, args.maps)
         t = time.perf_counter()
         valid = 0
-        for i in range(lo, hi):
+        for i in idx:
             _, m, _ = _gen_c5(i)
             valid += int(m.sum())
         ms = 1e3 * (time.perf_counter() - t)
-        stats = gather_stats(valid, ms, 1, hi - lo)
+        stats = gather_stats(valid, ms, 1, len(idx))
         valid_total, ms_max = whole_job(stats)
         if rank == 0:
             print(json.dumps({"dry_run": True, "n_gpus": world, "value": valid_total / ms_max * 1e3,
-                              "config": {"maps_total": args.maps, "valid_px_total": valid_total,
+                              "scaling": args.scaling,
+                              "config": {"maps_total": sum(int(r["maps"]) for r in stats),
+                                         "valid_px_total": valid_total,
                                          "per_rank": [{"maps": int(r["maps"]),
                                                        "valid_px": int(r["valid_px"])}
                                                       for r in stats]}}), flush=True)
@@ -471,7 +485,8 @@ def workload_config(args, world, merge_freq):
     """The config keys both arms report for the same workload."""
     return {
         "workload": make_desc(args),
-        "maps_total": args.maps if args.config == "C5" else 1,
+        "maps_total": (args.maps * (world if args.scaling == "weak" else 1)
+                       if args.config == "C5" else 1),
         "theta_c_deg": THETA_DEG,
         "connectivity": 8,
         "model": "milano",
@@ -479,13 +494,19 @@ def workload_config(args, world, merge_freq):
         "merge_freq": merge_freq,
         "l2": ("inputs larger than L2 (working set ~25 B/px x 67 M px)" if args.config == "C5"
                else "single-map config (a parity/latency line, not the bench workload)"),
-        "parallelism": f"maps sharded over {world} rank(s), no data-path collective",
+        "parallelism": (f"{world} rank(s), each its own batch of {args.maps} maps (weak scaling), "
+                        "no data-path collective" if args.scaling == "weak" and args.config == "C5"
+                        else f"maps sharded over {world} rank(s), no data-path collective"),
     }
 
 
 def make_desc(args):
     if args.config == "C5":
-        return f"C5: {args.maps} x 1024x1024 orthographic maps (seeds 100..{99 + args.maps}), 16 Voronoi cells"
+        return (f"C5: {args.maps} x 1024x1024 orthographic maps per rank (BASELINE config 5; "
+                f"rank r: seeds 100 + {args.maps} r .. + {args.maps - 1}), 16 Voronoi cells"
+                if args.scaling == "weak" else
+                f"C5: {args.maps} x 1024x1024 orthographic maps (seeds 100..{99 + args.maps}) "
+                "split across the ranks, 16 Voronoi cells")
     return f"{args.config} (paper_2510_11508_b200/scenes.py)"
 
 
@@ -496,7 +517,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C5", choices=("C1", "C2", "C3", "C4", "C5"))
-    ap.add_argument("--maps", type=int, default=64, help="C5 batch size")
+    ap.add_argument("--maps", type=int, default=64, help="C5 batch size (per rank when weak)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every rank its own 64-map batch (independent maps, SURVEY 8(e)); "
+                         "strong: one 64-map batch split across the ranks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher / gather plumbing only: gloo, no GPU work (CPU tests)")

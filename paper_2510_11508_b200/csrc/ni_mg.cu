@@ -2071,258 +2071,6 @@ __global__ void __launch_bounds__(NT, NI_MG_B2_MINB) pass_b2_kernel(const __grid
   }
 }
 
-// ---- pass B (v3): 512 threads, one row of 4 pixels per thread
-//
-// Thread t owns tile row t >> 4, columns 4 (t & 15) .. +3; the 3 x 6 window
-// of a plane around its 4 pixels is 3 float4 shared-memory loads plus
-// shuffles from the neighbouring lanes (the two lanes at the tile edge read
-// the halo column themselves).  Twice the threads of pass B with a quarter of
-// the per-thread pixels keep the register count low enough for 2 CTAs (32
-// warps) per SM.
-constexpr int NT3 = 512;
-constexpr unsigned kFull3 = 0xffffffffu;
-
-template <int ROW0>
-__device__ __forceinline__ void win3b(const float* box, int ly, int lx0, float (&v)[3][6]) {
-  const int l16 = threadIdx.x & 15;
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const float* q = box + (ly - 1 + r + ROW0) * BW + lx0 + CX;
-    const float4 m = *reinterpret_cast<const float4*>(q);
-    float left = __shfl_up_sync(kFull3, m.w, 1);
-    float right = __shfl_down_sync(kFull3, m.x, 1);
-    if (l16 == 0) left = q[-1];
-    if (l16 == 15) right = q[4];
-    v[r][0] = left;
-    v[r][1] = m.x;
-    v[r][2] = m.y;
-    v[r][3] = m.z;
-    v[r][4] = m.w;
-    v[r][5] = right;
-  }
-}
-
-template <int CONN>
-__device__ __forceinline__ float stencil3b(const float (&X)[3][6], const float (&Hh)[3][6],
-                                           uint32_t mk, int j) {
-  constexpr int KF = CONN == 8 ? 4 : 2;
-  const float xc = X[1][j + 1], hc = Hh[1][j + 1];
-  float acc = 0.f;
-#pragma unroll
-  for (int bit = 0; bit < 8; ++bit) {
-    const int k = bit & 3;
-    if (k >= KF) continue;
-    const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
-    const int r = 1 + (bit < 4 ? dv : -dv), c = j + 1 + (bit < 4 ? du : -du);
-    const float t = (hc + Hh[r][c]) * (xc - X[r][c]);
-    acc += ((mk >> bit) & 1u) ? t : 0.f;
-  }
-  return acc;
-}
-
-template <int CONN>
-__global__ void __launch_bounds__(NT3, 2) pass_b3_kernel(const __grid_constant__ FineArgs a,
-                                                        const __grid_constant__ TmaMaps tm) {
-  constexpr int KF = CONN == 8 ? 4 : 2;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* sR = reinterpret_cast<float*>(smem_raw);
-  float* sD = sR + al128(BOX2 * 4) / 4;
-  float* sH = sD + al128(BOX2 * 4) / 4;
-  float* sX2 = sH + al128(BOX2 * 4) / 4;   // x2 on the 2-pixel halo box
-  float* sX3 = sX2 + al128(BOX2 * 4) / 4;  // BW x BH1: row 0 = tile row -1
-  uint8_t* sM = reinterpret_cast<uint8_t*>(sX3 + al128(BOX1 * 4) / 4);
-  float* sWv = reinterpret_cast<float*>(sM + al128(BWM * BH1));
-  uint16_t* sSl = reinterpret_cast<uint16_t*>(sWv + TPX);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sSl + TPX);
-  __shared__ double sred[NT3 / 32][NPART];
-  const int t = a.tiles[blockIdx.x];
-  if (tile_done(a, t)) return;
-  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 3u * BOX2 * 4u + uint32_t(BWM * BH1));
-    const int xs2 = T.x0 - CX + XM, ys2 = T.y0 - 2 + RM;
-    tma_2d(sR, a.par ? &tm.rB[1] : &tm.rB[0], bar, xs2, ys2);
-    tma_2d(sD, &tm.dinvB, bar, xs2, ys2);
-    tma_2d(sH, &tm.hwB, bar, xs2, ys2);
-    tma_2d(sM, &tm.imB, bar, T.x0 - CXM + XM, T.y0 - 1 + RM);
-  }
-  // OC e1[par0] of the thread's float4 items of the 2-pixel halo box,
-  // gathered while the boxes land
-  constexpr int QB = BW / 4, NIT = (BH2 * QB + NT3 - 1) / NT3;
-  float4 ev[NIT];
-#pragma unroll
-  for (int q = 0; q < NIT; ++q) {
-    const int it = threadIdx.x + q * NT3;
-    int4 p4 = make_int4(-1, -1, -1, -1);
-    if (it < BH2 * QB) {
-      const int ry = it / QB, qq = it - ry * QB;
-      p4 = *reinterpret_cast<const int4*>(a.par0 + pidx(a.P, T.y0 - 2 + ry, T.x0 - CX + 4 * qq));
-    }
-    ev[q].x = p4.x >= 0 ? __ldg(a.e1 + p4.x) : 0.f;
-    ev[q].y = p4.y >= 0 ? __ldg(a.e1 + p4.y) : 0.f;
-    ev[q].z = p4.z >= 0 ? __ldg(a.e1 + p4.z) : 0.f;
-    ev[q].w = p4.w >= 0 ? __ldg(a.e1 + p4.w) : 0.f;
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int lx0 = 4 * (threadIdx.x & 15), ly = threadIdx.x >> 4;
-  const bool rowv = T.y0 + ly < T.y1;
-  uint16_t sl[4];
-  {
-    const ushort4 s4 = *reinterpret_cast<const ushort4*>(a.slot + pidx(a.P, T.y0 + ly, T.x0 + lx0));
-    sl[0] = s4.x;
-    sl[1] = s4.y;
-    sl[2] = s4.z;
-    sl[3] = s4.w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (!rowv || T.x0 + lx0 + j >= T.x1) sl[j] = NOSLOT;
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-#pragma unroll
-  for (int q = 0; q < NIT; ++q) {
-    const int it = threadIdx.x + q * NT3;
-    if (it >= BH2 * QB) continue;
-    const int cb = it * 4;
-    const float4 r4 = *reinterpret_cast<const float4*>(sR + cb);
-    const float4 d4 = *reinterpret_cast<const float4*>(sD + cb);
-    float4 x4;
-    x4.x = OM * d4.x * r4.x + OC * ev[q].x;
-    x4.y = OM * d4.y * r4.y + OC * ev[q].y;
-    x4.z = OM * d4.z * r4.z + OC * ev[q].z;
-    x4.w = OM * d4.w * r4.w + OC * ev[q].w;
-    *reinterpret_cast<float4*>(sX2 + cb) = x4;
-  }
-  __syncthreads();
-  // post-smoothing x3 = x2 + OM dinv (r - A x2): the 1-pixel ring, one pixel
-  // per thread, and the interior, one 4-pixel row segment per thread
-  if (threadIdx.x < 196) {
-    int ry, rx;
-    const int q = threadIdx.x;
-    if (q < 66) {
-      ry = -1;
-      rx = q - 1;
-    } else if (q < 132) {
-      ry = TY;
-      rx = q - 67;
-    } else if (q < 164) {
-      ry = q - 132;
-      rx = -1;
-    } else {
-      ry = q - 164;
-      rx = TX;
-    }
-    const int c2 = (ry + 2) * BW + rx + CX;
-    const uint8_t m = sM[(ry + 1) * BWM + rx + CXM];
-    float v = 0.f;
-    if (m) {
-      v = sX2[c2];
-      const float hi = sH[c2];
-      float acc = 0.f;
-#pragma unroll
-      for (int bit = 0; bit < 8; ++bit) {
-        if ((bit & 3) >= KF || !((m >> bit) & 1)) continue;
-        const int jn = c2 + nb_off<CONN>(bit, BW);
-        acc += (hi + sH[jn]) * (v - sX2[jn]);
-      }
-      v += OM * sD[c2] * (sR[c2] - acc);
-    }
-    sX3[(ry + 1) * BW + rx + CX] = v;
-  }
-  const uint32_t mk = *reinterpret_cast<const uint32_t*>(sM + (ly + 1) * BWM + lx0 + CXM);
-  {
-    float X[3][6], Hh[3][6];
-    win3b<2>(sX2, ly, lx0, X);
-    win3b<2>(sH, ly, lx0, Hh);
-    const int c2 = (ly + 2) * BW + lx0 + CX;
-    const float4 r4 = *reinterpret_cast<const float4*>(sR + c2);
-    const float4 d4 = *reinterpret_cast<const float4*>(sD + c2);
-    const float* rr = &r4.x;
-    const float* dd = &d4.x;
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t m = (mk >> (8 * j)) & 0xffu;
-      const float acc = stencil3b<CONN>(X, Hh, m, j);
-      const float v = X[1][j + 1] + OM * dd[j] * (rr[j] - acc);
-      o[j] = m ? v : 0.f;
-    }
-    *reinterpret_cast<float4*>(sX3 + (ly + 1) * BW + lx0 + CX) =
-        make_float4(o[0], o[1], o[2], o[3]);
-  }
-  __syncthreads();
-  // u = x3, w = A u; per-lane partial dots of slot 0
-  const int nsl = a.slot_base[t + 1] - a.slot_base[t];
-  double d[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  {
-    float X[3][6], Hh[3][6];
-    win3b<1>(sX3, ly, lx0, X);
-    win3b<2>(sH, ly, lx0, Hh);
-    const float4 r4 = *reinterpret_cast<const float4*>(sR + (ly + 2) * BW + lx0 + CX);
-    const float* rr = &r4.x;
-    float wv[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      wv[j] = stencil3b<CONN>(X, Hh, (mk >> (8 * j)) & 0xffu, j);
-      if (sl[j] == 0) {
-        const double du = double(X[1][j + 1]), dr = double(rr[j]), dw = double(wv[j]);
-        d[0] += dr * du;
-        d[1] += dw * du;
-        d[2] += dr * dr;
-        d[3] += du;
-        d[4] += dr;
-        d[5] += dw;
-      }
-      if (nsl > 1) {
-        sSl[ly * TX + lx0 + j] = sl[j];
-        sWv[ly * TX + lx0 + j] = wv[j];
-      }
-    }
-    if (rowv) {
-      const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx0);
-      *reinterpret_cast<float4*>(a.u + o) = make_float4(X[1][1], X[1][2], X[1][3], X[1][4]);
-      *reinterpret_cast<float4*>(a.w + o) = make_float4(wv[0], wv[1], wv[2], wv[3]);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NPART; ++k) d[k] = warp_sum(d[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NPART; ++k) sred[wid][k] = d[k];
-  __syncthreads();
-  if (threadIdx.x < NPART) {
-    double v = 0.0;
-#pragma unroll
-    for (int w8 = 0; w8 < NT3 / 32; ++w8) v += sred[w8][threadIdx.x];
-    a.partial[NPART * int64_t(a.slot_base[t]) + threadIdx.x] = v;
-  }
-  if (nsl <= 1) return;
-  for (int q = wid + 1; q < nsl; q += NT3 / 32) {
-    double qd[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int e = lane; e < TPX; e += 32) {
-      if (sSl[e] != q) continue;
-      const int ey = e / TX, ex = e - ey * TX;
-      const double ui = double(sX3[(ey + 1) * BW + ex + CX]);
-      const double ri = double(sR[(ey + 2) * BW + ex + CX]);
-      const double wi = double(sWv[e]);
-      qd[0] += ri * ui;
-      qd[1] += wi * ui;
-      qd[2] += ri * ri;
-      qd[3] += ui;
-      qd[4] += ri;
-      qd[5] += wi;
-    }
-#pragma unroll
-    for (int k = 0; k < NPART; ++k) qd[k] = warp_sum(qd[k]);
-    if (lane == 0) {
-      double* pp = a.partial + NPART * int64_t(a.slot_base[t] + q);
-#pragma unroll
-      for (int k = 0; k < NPART; ++k) pp[k] = qd[k];
-    }
-  }
-}
-
 // ---- per-unit scalars (warp per unit): scipy's stop test on the recursive
 // residual, then the Chronopoulos-Gear alpha / beta
 struct ScalarArgs {
@@ -2995,10 +2743,6 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
                                    int(kPassASmem)));
   NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kPassASmem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b3_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassB2Smem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b3_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassB2Smem)));
   NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(kPassB2Smem)));
   NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3055,10 +2799,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
         NI_LAUNCH_CHECK();
       }
       if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));
-#if NI_MG_V2 && NI_MG_B_V2 == 3
-      if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b3_kernel<8><<<NA, NT3, kPassB2Smem, st>>>(fa, tm);
-      else NI_COUNT_LAUNCH(), pass_b3_kernel<4><<<NA, NT3, kPassB2Smem, st>>>(fa, tm);
-#elif NI_MG_V2 && NI_MG_B_V2
+#if NI_MG_V2 && NI_MG_B_V2
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b2_kernel<8><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_b2_kernel<4><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
 #else

@@ -71,10 +71,12 @@ def test_gather_stats_single_process():
     assert whole_job(st) == (123, 4.5)
 
 
-def test_bench_launcher_two_ranks_gloo():
+@pytest.mark.parametrize("scaling,maps,per_rank", [("weak", 2, [2, 2]), ("strong", 4, [2, 2])])
+def test_bench_launcher_two_ranks_gloo(scaling, maps, per_rank):
     """`bench.py --gpus 2` without WORLD_SIZE re-launches itself under
-    torch.distributed.run; the ranks split the maps, all_gather their stats
-    and rank 0 alone prints the whole-job line (gloo, no GPU work)."""
+    torch.distributed.run; the ranks take their maps (weak: each its own
+    batch; strong: halves of one batch), all_gather their stats and rank 0
+    alone prints the whole-job line (gloo, no GPU work)."""
     import json
     import subprocess
     import sys
@@ -83,13 +85,14 @@ def test_bench_launcher_two_ranks_gloo():
     env = {k: v for k, v in os.environ.items()
            if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
-                          "--maps", "4", "--dry-run"], capture_output=True, text=True,
-                         timeout=300, env=env, cwd=root)
+                          "--maps", str(maps), "--scaling", scaling, "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1  # rank 0 only
     line = lines[0]
-    assert line["n_gpus"] == 2
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling
     ranks = line["config"]["per_rank"]
-    assert [r["maps"] for r in ranks] == [2, 2]
+    assert [r["maps"] for r in ranks] == per_rank
+    assert line["config"]["maps_total"] == sum(per_rank)
     assert line["config"]["valid_px_total"] == sum(r["valid_px"] for r in ranks)
