@@ -93,11 +93,14 @@ int ni_components(const double* n, const uint8_t* valid, int B, int H, int W, in
  * float64 [B*4].  Outputs, per pixel a and forward edge k:
  *   omega_a[k*npix + a] (float64), omega_b[k*npix + a] (bini only; may be NULL
  *   for milano where omega_b = -omega_a), gamma[a] (float64),
+ *   map_counts (nullable, device int64 [2B]): per map, the edges and the
+ *   degenerate edges (the build_graph / edge_coefficients records);
  *   eflags[a]: bit k = edge exists (both endpoints valid), bit 4+k = its
  *   coefficient is valid (continuity.py:243-245, 266). */
 int ni_coefficients(const double* n, const uint8_t* valid, const double* intrinsics, int B, int H,
                     int W, int connectivity, int model, double* omega_a, double* omega_b,
-                    double* gamma, uint8_t* eflags, ni_stats* stats, ni_stream_t stream);
+                    double* gamma, uint8_t* eflags, ni_stats* stats, long long* map_counts,
+                    ni_stream_t stream);
 
 /* K3 -- fill_components (solver.py:195-239): per-component CG on the
  * weighted normal equations, all components in one batched solve.

@@ -41,7 +41,7 @@ SIGNATURES = {
     "ni_normalize": ([_P, _I, _P, _I, _I, _I, _P, _P, _P, _P], _I),
     "ni_components_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_components": ([_P, _P, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _SZ, _P], _I),
-    "ni_coefficients": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P], _I),
+    "ni_coefficients": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "ni_fill_workspace_size": ([_I, _I, _I, _I, _I, _I, _PSZ], _I),
     "ni_fill": ([_P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _SZ,
                  _P], _I),

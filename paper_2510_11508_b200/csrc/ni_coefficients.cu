@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     const double* __restrict__ n, const uint8_t* __restrict__ valid,
     const double* __restrict__ intr, int H, int W, int64_t npix, double* __restrict__ omega_a,
     double* __restrict__ omega_b, double* __restrict__ gamma, uint8_t* __restrict__ eflags,
-    ni_stats* __restrict__ st) {
+    ni_stats* __restrict__ st, long long* __restrict__ map_counts) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   __shared__ double s_t0[CROWS], s_tp[CROWS], s_hp[CROWS];  // (v - cy)/fy at v, v+1, v+1/2
   const int rows = int(npix / W);
@@ -45,6 +45,11 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     s_tp[tid] = (va + 1.0 - cy) / fy;
     s_hp[tid] = (0.5 * (va + (va + 1.0)) - cy) / fy;
   }
+  // per-map edge / degenerate-edge counts of this tile's rows (maps m0 ..),
+  // accumulated in shared memory, one global atomic per map and counter
+  __shared__ unsigned long long s_cnt[CROWS][2];
+  const int m0 = row0 / H;
+  if (tid < CROWS) s_cnt[tid][0] = s_cnt[tid][1] = 0ull;
   __syncthreads();
   long long ndegen = 0;
   ColRays cr;
@@ -124,6 +129,11 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     }
     gamma[i] = g;
     eflags[i] = flags;
+    if (map_counts && flags) {
+      const unsigned nex = __popc(flags & 0xfu), nok = __popc(flags >> 4);
+      atomicAdd(&s_cnt[m - m0][0], (unsigned long long)nex);
+      if (nex != nok) atomicAdd(&s_cnt[m - m0][1], (unsigned long long)(nex - nok));
+    }
 #pragma unroll
     for (int k = 0; k < KF; ++k) {
       omega_a[k * npix + i] = om_a[k];
@@ -134,6 +144,14 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
   for (int o = 16; o > 0; o >>= 1) ndegen += __shfl_xor_sync(0xffffffffu, ndegen, o);
   if ((threadIdx.x & 31) == 0 && ndegen)
     atomicAdd((unsigned long long*)&st->degenerate_edges, (unsigned long long)ndegen);
+  if (map_counts) {
+    __syncthreads();
+    if (tid < CROWS) {
+      const int m = m0 + tid;
+      if (s_cnt[tid][0]) atomicAdd((unsigned long long*)&map_counts[2 * m], s_cnt[tid][0]);
+      if (s_cnt[tid][1]) atomicAdd((unsigned long long*)&map_counts[2 * m + 1], s_cnt[tid][1]);
+    }
+  }
 }
 
 }  // namespace ni
@@ -143,7 +161,7 @@ using namespace ni;
 extern "C" int ni_coefficients(const double* n, const uint8_t* valid, const double* intrinsics, int B,
                                int H, int W, int connectivity, int model, double* omega_a,
                                double* omega_b, double* gamma, uint8_t* eflags, ni_stats* stats,
-                               ni_stream_t stream) {
+                               long long* map_counts, ni_stream_t stream) {
   NI_CHECK_ARG(connectivity == 4 || connectivity == 8, "connectivity must be 4 or 8");
   NI_CHECK_ARG(model == 0 || model == 1, "model must be 0 (milano) or 1 (bini)");
   NI_CHECK_ARG(!(model == 1 && connectivity == 8),
@@ -154,17 +172,18 @@ extern "C" int ni_coefficients(const double* n, const uint8_t* valid, const doub
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npix = int64_t(B) * H * W;
   NI_CUDA_TRY(cudaMemsetAsync(&stats->degenerate_edges, 0, sizeof(long long), s));
+  if (map_counts) NI_CUDA_TRY(cudaMemsetAsync(map_counts, 0, sizeof(long long) * 2 * B, s));
   const dim3 blocks(unsigned(div_up(W, CCOLS)), unsigned(div_up(B * H, CROWS)));
   const dim3 threads(CCOLS, CTHR_Y);
   if (connectivity == 8)
     NI_COUNT_LAUNCH(), coefficients_kernel<8, 0><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
-                                                     omega_b, gamma, eflags, stats);
+                                                     omega_b, gamma, eflags, stats, map_counts);
   else if (model == 0)
     NI_COUNT_LAUNCH(), coefficients_kernel<4, 0><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
-                                                     omega_b, gamma, eflags, stats);
+                                                     omega_b, gamma, eflags, stats, map_counts);
   else
     NI_COUNT_LAUNCH(), coefficients_kernel<4, 1><<<blocks, threads, 0, s>>>(n, valid, intrinsics, H, W, npix, omega_a,
-                                                     omega_b, gamma, eflags, stats);
+                                                     omega_b, gamma, eflags, stats, map_counts);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) prep_kernel(
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
     const uint8_t* __restrict__ eflags, int H, int W, int P, int64_t npix,
     float* __restrict__ hw, float* __restrict__ rvec, uint8_t* __restrict__ imask,
-    int32_t* __restrict__ comp_size, int32_t* __restrict__ missing) {
+    float* __restrict__ dinv, int32_t* __restrict__ comp_size, int32_t* __restrict__ missing) {
   constexpr int KF = CONN == 8 ? 4 : 2;
   const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   const int row = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -235,6 +235,17 @@ __global__ void __launch_bounds__(256) prep_kernel(
     }
     imask[o] = m;
     rvec[o] = float(b);
+    // the Jacobi diagonal sum of c_ab over the stencil edges, in the order
+    // the fine passes' stencil visits them (forward k, then backward k)
+    if (m) {
+      float d = 0.f;
+#pragma unroll
+      for (int k = 0; k < KF; ++k) {
+        if ((m >> k) & 1) d += hself + hw_of(fg[k]);
+        if ((m >> (4 + k)) & 1) d += hself + hw_of(bg[k]);
+      }
+      dinv[o] = 1.0f / d;
+    }
   }
   if (miss) atomicAdd(missing, miss);
 }
@@ -245,28 +256,6 @@ __device__ __forceinline__ int nb_off(int bit, int S) {
   const int k = bit & 3;
   const int du = fwd_du(CONN, k), dv = fwd_dv(CONN, k);
   return bit < 4 ? dv * S + du : -(dv * S + du);
-}
-
-template <int CONN>
-__global__ void __launch_bounds__(256) dinv_kernel(int H, int W, int P, int64_t npix,
-                                                   const float* __restrict__ hw,
-                                                   const uint8_t* __restrict__ imask,
-                                                   float* __restrict__ dinv) {
-  constexpr int KF = CONN == 8 ? 4 : 2;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npix;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t o = pidx(P, int(uint32_t(i) / uint32_t(W)), int(uint32_t(i) % uint32_t(W)));
-    const uint8_t m = imask[o];
-    if (!m) continue;
-    const float h = hw[o];
-    float d = 0.f;
-#pragma unroll
-    for (int k = 0; k < KF; ++k) {
-      if ((m >> k) & 1) d += h + hw[o + nb_off<CONN>(k, P)];
-      if ((m >> (4 + k)) & 1) d += h + hw[o + nb_off<CONN>(4 + k, P)];
-    }
-    dinv[o] = 1.0f / d;
-  }
 }
 
 // ---- solve units.  Fast path (every same-label edge carries conductance):
@@ -414,6 +403,46 @@ __global__ void __launch_bounds__(NT) plan_tile_kernel(int H, int W, int P, int 
       if (total)
         for (int e = threadIdx.x; e < TPX; e += NT)
           if (key[e] != INT32_MAX) slot[pidx(P, T.y0 + e / TX, T.x0 + e % TX)] = 0;
+      return;
+    }
+    // a few units: extract them in ascending order by repeated block minima
+    // (one pass over the tile each) instead of sorting the whole tile
+    constexpr int kQuick = 16;
+    __shared__ int32_t s_units[kQuick];
+    __shared__ int32_t s_next;
+    int total = 1;
+    int32_t prev = lo;
+    if (threadIdx.x == 0) s_units[0] = lo;
+    while (total <= kQuick) {
+      int32_t nx = INT32_MAX;
+      for (int e = threadIdx.x; e < TPX; e += NT) {
+        const int32_t k = key[e];
+        if (k > prev && k < nx) nx = k;  // INT32_MAX (no unit) never qualifies as < nx
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nx = min(nx, __shfl_xor_sync(0xffffffffu, nx, o));
+      __syncthreads();  // every thread is done with the previous s_next
+      if (threadIdx.x == 0) s_next = INT32_MAX;
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) atomicMin(&s_next, nx);
+      __syncthreads();
+      nx = s_next;
+      if (nx == INT32_MAX) break;
+      if (total < kQuick && threadIdx.x == 0) s_units[total] = nx;
+      ++total;
+      prev = nx;
+    }
+    if (total <= kQuick) {
+      __syncthreads();
+      if (threadIdx.x == 0) nslots[t] = total;
+      if (threadIdx.x < total) tmp[int64_t(t) * TPX + threadIdx.x] = s_units[threadIdx.x];
+      for (int e = threadIdx.x; e < TPX; e += NT) {
+        const int32_t k = key[e];
+        if (k == INT32_MAX) continue;
+        int q = 0;
+        while (s_units[q] != k) ++q;
+        slot[pidx(P, T.y0 + e / TX, T.x0 + e % TX)] = uint16_t(q);
+      }
       return;
     }
   }
@@ -1439,10 +1468,11 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
         const float hi = sH[c2];
         float acc = 0.f;
 #pragma unroll
-        for (int bit = 0; bit < 8; ++bit) {
-          if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+        for (int bit = 0; bit < 8; ++bit) {  // predicated, not branched
+          if ((bit & 3) >= KF) continue;
           const int jn = c2 + nb_off<CONN>(bit, BW);
-          acc += (hi + sH[jn]) * (v - sX2[jn]);
+          const float t = (hi + sH[jn]) * (v - sX2[jn]);
+          acc += ((mk >> bit) & 1) ? t : 0.f;
         }
         v += OM * sD[c2] * (sR[c2] - acc);
       }
@@ -1469,9 +1499,11 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
           const uint8_t mk = sM[(ly + 1) * BWM + lx + CXM];
           const float ui = sX3[c1], hi = sH[c2];
 #pragma unroll
-          for (int bit = 0; bit < 8; ++bit) {
-            if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
-            wv += (hi + sH[c2 + nb_off<CONN>(bit, BW)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S3)]);
+          for (int bit = 0; bit < 8; ++bit) {  // predicated, not branched
+            if ((bit & 3) >= KF) continue;
+            const float t =
+                (hi + sH[c2 + nb_off<CONN>(bit, BW)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S3)]);
+            wv += ((mk >> bit) & 1) ? t : 0.f;
           }
           const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx);
           a.u[o] = ui;
@@ -2493,16 +2525,11 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
 #define NI_MG_PREP(CONN, MODEL)                                                                  \
   NI_COUNT_LAUNCH(), prep_kernel<CONN, MODEL><<<dim3(div_up(W, 32), div_up(int64_t(B) * H, 8)), 256, 0, st>>>( \
                          labels, omega_a, omega_b, gamma, eflags, H, W, g.P, g.npix, f.hw, f.r, \
-                         f.imask, f.comp_size, f.counters + 0)
+                         f.imask, f.dinv, f.comp_size, f.counters + 0)
   if (connectivity == 8) NI_MG_PREP(8, 0);
   else if (model == 0) NI_MG_PREP(4, 0);
   else NI_MG_PREP(4, 1);
 #undef NI_MG_PREP
-  NI_LAUNCH_CHECK();
-  if (connectivity == 8)
-    NI_COUNT_LAUNCH(), dinv_kernel<8><<<npb, 256, 0, st>>>(H, W, g.P, g.npix, f.hw, f.imask, f.dinv);
-  else
-    NI_COUNT_LAUNCH(), dinv_kernel<4><<<npb, 256, 0, st>>>(H, W, g.P, g.npix, f.hw, f.imask, f.dinv);
   NI_LAUNCH_CHECK();
   int32_t hc[16];
   NI_CUDA_TRY(cudaMemcpyAsync(hc, f.counters, sizeof(hc), cudaMemcpyDeviceToHost, st));

@@ -1220,23 +1220,35 @@ __device__ void fused_iteration(
     int64_t npix, const WeightArgs& wp, double rtol, int cg_max_iters, double* __restrict__ s,
     double* __restrict__ residual, double* __restrict__ weights, double* __restrict__ energy_out,
     int32_t* __restrict__ ok_out, double* __restrict__ zshift, const DecideArgs& da, double* red) {
+  __shared__ double s_cnd[32][32];  // warp CG: row j of lane's Laplacian row (<= 31 entries)
+  __shared__ int8_t s_col[32][32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   const int e0 = q.estart[m], e1 = q.estart[m + 1];
   const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
-  // K4: weights and row right-hand sides (solver.py:253-278, 170-180)
+  // K4: weights and row right-hand sides (solver.py:253-278, 170-180); two
+  // edges per step so their gather chains overlap (restrict copies let the
+  // compiler hoist the second edge's loads over the first edge's stores)
+  const int32_t* __restrict__ qea = q.ea;
+  const int32_t* __restrict__ qeb = q.eb;
+  const int32_t* __restrict__ qek = q.ek;
+  double* __restrict__ wwa = w.wa;
+  double* __restrict__ wwb = w.wb;
+  double* __restrict__ wba = w.ba;
+  double* __restrict__ wbb = w.bb;
+#pragma unroll 2
   for (int e = e0 + tid; e < e1; e += nt) {
-    const int32_t a = q.ea[e], b = q.eb[e], k = q.ek[e];
+    const int32_t a = qea[e], b = qeb[e], k = qek[e];
     double wa, wb;
     edge_weights_at<CONN, MODEL>(z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W, npix, a, k,
                                  wp, wa, wb);
     const double za = z_at(z, zs, zlab, a), zb = z_at(z, zs, zlab, b);
     const double oa = omega_a[k * npix + a];
     const double ob = MODEL == 0 ? -oa : omega_b[k * npix + a];
-    w.wa[e] = wa;
-    w.wb[e] = wb;
-    w.ba[e] = oa - (za - zb);
-    w.bb[e] = ob - (zb - za);
+    wwa[e] = wa;
+    wwb[e] = wb;
+    wba[e] = oa - (za - zb);
+    wbb[e] = ob - (zb - za);
   }
   __syncthreads();
   // K5a: pair conductances (the map's pairs are a contiguous run of the
@@ -1306,6 +1318,18 @@ __device__ void fused_iteration(
       const int c = c0 + lane;
       const bool own = lane < n;
       const double b = own ? w.rhs[c] : 0.0;
+      // the lane's Laplacian row, read once: off-diagonal conductances and
+      // their columns (as lanes) into shared memory, the diagonal into a register
+      const double dg = own ? w.diag[c] : 0.0;
+      const int j0 = own ? q.lstart[c] : 0, deg = own ? q.lstart[c + 1] - j0 : 0;
+      for (int jj = 0; jj < deg; ++jj) {
+        s_col[jj][lane] = int8_t(q.lcol[j0 + jj] - c0);
+        s_cnd[jj][lane] = w.S[q.lpair[j0 + jj]];
+      }
+      int jmax = deg;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+      __syncwarp();
       double x = 0.0, r = b, p = 0.0;
       double rr = warp_sum(b * b);
       const double bnrm = sqrt(rr);
@@ -1324,22 +1348,26 @@ __device__ void fused_iteration(
           p = r + beta * p;
           // q = L p: the diagonal and the pair conductances of the lane's row,
           // neighbours' p by shuffle (their lane = column - c0)
-          double aq = own ? w.diag[c] * p : 0.0;
-          const int j0 = own ? q.lstart[c] : 0, j1 = own ? q.lstart[c + 1] : 0;
-          int jmax = j1 - j0;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+          double aq = dg * p;
           for (int jj = 0; jj < jmax; ++jj) {
-            const bool has = jj < j1 - j0;
-            const int col = has ? q.lcol[j0 + jj] - c0 : 0;
+            const bool has = jj < deg;
+            const int col = has ? int(s_col[jj][lane]) : 0;
             const double pn = __shfl_sync(0xffffffffu, p, col);
-            if (has) aq -= w.S[q.lpair[j0 + jj]] * pn;
+            if (has) aq -= s_cnd[jj][lane] * pn;
           }
-          const double pq = warp_sum(p * aq);
-          const double alpha = rho / pq;
+          // the three dots of the iteration in one set of shuffle rounds:
+          // <p,q>, <r,q>, <q,q>; then <r',r'> = <r,r> - 2 a <r,q> + a^2 <q,q>
+          double d0 = p * aq, d1 = r * aq, d2 = aq * aq;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+            d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+            d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+          }
+          const double alpha = rho / d0;
           x += alpha * p;
           r -= alpha * aq;
-          rr = warp_sum(r * r);
+          rr = fmax(rho - 2.0 * alpha * d1 + alpha * alpha * d2, 0.0);
           rho_prev = rho;
         }
       }

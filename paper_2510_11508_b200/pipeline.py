@@ -217,9 +217,11 @@ def _coefficients(g: _Grid, intrinsics: list[CameraIntrinsics]):
     omega_b = devmem.empty((g.kf, g.npix), torch.float64, g.dev) if g.model == 1 else None
     gamma = devmem.empty(g.npix, torch.float64, g.dev)
     eflags = devmem.empty(g.npix, torch.uint8, g.dev)
+    g.map_counts = torch.zeros(2 * g.B, dtype=torch.int64, device=g.dev)
     _lib.check(lib.ni_coefficients(_ptr(g.nmap.n_soa), _ptr(g.nmap.valid_t), _ptr(intr), g.B, g.H,
                                    g.W, g.conn, g.model, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
-                                   _ptr(eflags), _ptr(g.stats), g.s()), "build_edge_coefficients")
+                                   _ptr(eflags), _ptr(g.stats), _ptr(g.map_counts), g.s()),
+               "build_edge_coefficients")
     return omega_a, omega_b, gamma, eflags
 
 
@@ -829,16 +831,9 @@ def run_pipeline_stream(
 
 def _per_map_edge_stats(g: _Grid, eflags: torch.Tensor, records):
     """Per-map edge / degenerate counts for batched runs (records of
-    pipeline.py:137-159 are per map)."""
-    ef = eflags.view(g.B, -1)  # uint8 throughout: byte-sized temporaries
-    ex = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
-    dg = torch.zeros(g.B, dtype=torch.int64, device=g.dev)
-    for k in range(g.kf):
-        e = (ef >> k) & 1
-        ex += e.sum(dim=1, dtype=torch.int64)
-        dg += (e & ~(ef >> (4 + k))).sum(dim=1, dtype=torch.int64)
-    ex = ex.cpu().numpy()
-    dg = dg.cpu().numpy()
+    pipeline.py:137-159 are per map), counted by the coefficients kernel."""
+    cnt = g.map_counts.view(g.B, 2).cpu().numpy()
+    ex, dg = cnt[:, 0], cnt[:, 1]
     for m in range(g.B):
         records[m][0]["edges"] = int(ex[m])
         records[m][2]["degenerate_edges"] = int(dg[m])
