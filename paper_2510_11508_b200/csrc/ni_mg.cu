@@ -1468,11 +1468,10 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
         const float hi = sH[c2];
         float acc = 0.f;
 #pragma unroll
-        for (int bit = 0; bit < 8; ++bit) {  // predicated, not branched
-          if ((bit & 3) >= KF) continue;
+        for (int bit = 0; bit < 8; ++bit) {
+          if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
           const int jn = c2 + nb_off<CONN>(bit, BW);
-          const float t = (hi + sH[jn]) * (v - sX2[jn]);
-          acc += ((mk >> bit) & 1) ? t : 0.f;
+          acc += (hi + sH[jn]) * (v - sX2[jn]);
         }
         v += OM * sD[c2] * (sR[c2] - acc);
       }
@@ -1499,11 +1498,9 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
           const uint8_t mk = sM[(ly + 1) * BWM + lx + CXM];
           const float ui = sX3[c1], hi = sH[c2];
 #pragma unroll
-          for (int bit = 0; bit < 8; ++bit) {  // predicated, not branched
-            if ((bit & 3) >= KF) continue;
-            const float t =
-                (hi + sH[c2 + nb_off<CONN>(bit, BW)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S3)]);
-            wv += ((mk >> bit) & 1) ? t : 0.f;
+          for (int bit = 0; bit < 8; ++bit) {
+            if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+            wv += (hi + sH[c2 + nb_off<CONN>(bit, BW)]) * (ui - sX3[c1 + nb_off<CONN>(bit, S3)]);
           }
           const int64_t o = pidx(a.P, T.y0 + ly, T.x0 + lx);
           a.u[o] = ui;
@@ -1632,38 +1629,65 @@ constexpr size_t kPassA2Smem = 5 * size_t(al128(BOX1 * 4)) + 3 * size_t(IBOX * 4
 // Pass A (v2): pending CG update, pre-smoothing of the new r, residual,
 // restriction to level 1.  TMA brings the five halo boxes (r, w, s, dinv,
 // hw) and the three interior boxes (u, p, x).
-template <int CONN>
-__global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid_constant__ FineArgs a,
-                                                       const __grid_constant__ TmaMaps tm) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* sR = reinterpret_cast<float*>(smem_raw);
-  float* sW = sR + al128(BOX1 * 4) / 4;
-  float* sS = sW + al128(BOX1 * 4) / 4;
-  float* sD = sS + al128(BOX1 * 4) / 4;
-  float* sH = sD + al128(BOX1 * 4) / 4;
-  float* sU = sH + al128(BOX1 * 4) / 4;
-  float* sP = sU + IBOX;
-  float* sXv = sP + IBOX;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sXv + IBOX);
-  __shared__ float s_al[kMaxSlotSm], s_bt[kMaxSlotSm], s_um[kMaxSlotSm];
-  __shared__ int s_un[kMaxSlotSm];
-  __shared__ uint8_t s_up[kMaxSlotSm];
-  const int t = a.tiles[blockIdx.x];
-  if (tile_done(a, t)) return;
+// stage buffers of pass A (halo boxes r, w, s, dinv, hw; interior u, p, x)
+struct AStage {
+  float *sR, *sW, *sS, *sD, *sH, *sU, *sP, *sX;
+};
+__device__ __forceinline__ AStage astage(unsigned char* base) {
+  AStage g;
+  g.sR = reinterpret_cast<float*>(base);
+  g.sW = g.sR + al128(BOX1 * 4) / 4;
+  g.sS = g.sW + al128(BOX1 * 4) / 4;
+  g.sD = g.sS + al128(BOX1 * 4) / 4;
+  g.sH = g.sD + al128(BOX1 * 4) / 4;
+  g.sU = g.sH + al128(BOX1 * 4) / 4;
+  g.sP = g.sU + IBOX;
+  g.sX = g.sP + IBOX;
+  return g;
+}
+constexpr size_t kAStageBytes = 5 * size_t(al128(BOX1 * 4)) + 3 * size_t(IBOX * 4);
+
+// TMA copies of tile t's pass-A planes into a stage (one elected thread)
+__device__ __forceinline__ void a2_issue(const FineArgs& a, const TmaMaps& tm, int t,
+                                         const AStage& g, uint64_t* bar) {
   const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
-  if (threadIdx.x == 0) {
-    const int xs = T.x0 - CX + XM, ys = T.y0 - 1 + RM;  // halo box origin (padded)
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 5u * BOX1 * 4u + 3u * IBOX * 4u);
-    tma_2d(sR, a.par ? &tm.r[1] : &tm.r[0], bar, xs, ys);
-    tma_2d(sW, &tm.w, bar, xs, ys);
-    tma_2d(sS, a.par ? &tm.s[1] : &tm.s[0], bar, xs, ys);
-    tma_2d(sD, &tm.dinv, bar, xs, ys);
-    tma_2d(sH, &tm.hw, bar, xs, ys);
-    tma_2d(sU, &tm.uI, bar, T.x0 + XM, T.y0 + RM);
-    tma_2d(sP, &tm.pI, bar, T.x0 + XM, T.y0 + RM);
-    tma_2d(sXv, &tm.xI, bar, T.x0 + XM, T.y0 + RM);
-  }
+  const int xs = T.x0 - CX + XM, ys = T.y0 - 1 + RM;  // halo box origin (padded)
+  mbar_expect_tx(bar, 5u * BOX1 * 4u + 3u * IBOX * 4u);
+  tma_2d(g.sR, a.par ? &tm.r[1] : &tm.r[0], bar, xs, ys);
+  tma_2d(g.sW, &tm.w, bar, xs, ys);
+  tma_2d(g.sS, a.par ? &tm.s[1] : &tm.s[0], bar, xs, ys);
+  tma_2d(g.sD, &tm.dinv, bar, xs, ys);
+  tma_2d(g.sH, &tm.hw, bar, xs, ys);
+  tma_2d(g.sU, &tm.uI, bar, T.x0 + XM, T.y0 + RM);
+  tma_2d(g.sP, &tm.pI, bar, T.x0 + XM, T.y0 + RM);
+  tma_2d(g.sX, &tm.xI, bar, T.x0 + XM, T.y0 + RM);
+}
+
+struct ASlots {
+  float al[kMaxSlotSm], bt[kMaxSlotSm], um[kMaxSlotSm];
+  int un[kMaxSlotSm];
+  uint8_t up[kMaxSlotSm];
+};
+
+// Pass A on tile t whose planes land in stage g (mbarrier bar, parity
+// phase): everything after the TMA issue.
+template <int CONN>
+__device__ __forceinline__ void a2_tile(const FineArgs& a, int t, const AStage& g, uint64_t* bar,
+                                        uint32_t phase, ASlots& sc) {
+  float* sR = g.sR;
+  float* sS = g.sS;
+  float* sW = g.sW;
+  float* sD = g.sD;
+  float* sH = g.sH;
+  float* sU = g.sU;
+  float* sP = g.sP;
+  float* sXv = g.sX;
+  float* s_al = sc.al;
+  float* s_bt = sc.bt;
+  float* s_um = sc.um;
+  int* s_un = sc.un;
+  uint8_t* s_up = sc.up;
+  const Tile T = tile_of(t, a.H, a.W, a.nTX, a.nTY);
   const int base = a.slot_base[t];
   const int nsl = a.slot_base[t + 1] - base;
   if (threadIdx.x < nsl && threadIdx.x < kMaxSlotSm) {
@@ -1701,7 +1725,7 @@ __global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid
       if (!rowv[i] || T.x0 + b.lx0 + j >= T.x1) sl[i][j] = NOSLOT;
   }
   __syncthreads();  // barrier init visible; slot scalars staged
-  mbar_wait(bar, 0);
+  mbar_wait(bar, phase);
   // box pass, in place, float4-wide over the tile + 1-pixel ring (see pass A)
   {
     const bool single = nsl == 1;
@@ -1804,7 +1828,12 @@ __global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid
       const uint16_t q = sl[i][j];
       if (q == NOSLOT) continue;
       UnitScalars us;
-      if (q < kMaxSlotSm) {
+      if (nsl == 1) {  // most tiles: one unit, its scalars hoisted by the compiler
+        us.up = s_up[0] != 0;
+        us.al = s_al[0];
+        us.bt = s_bt[0];
+        us.um = s_um[0];
+      } else if (q < kMaxSlotSm) {
         us.up = s_up[q] != 0;
         us.al = s_al[q];
         us.bt = s_bt[q];
@@ -1843,6 +1872,13 @@ __global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (sq[q] == NOSLOT) pq[q] = -1;
+    if (pq[0] >= 0 && pq[1] == pq[0] && pq[2] == pq[0] && pq[3] == pq[0]) {
+      // the common case: one aggregate for the whole block (same order as below)
+      const float sum = ((rq[0] + rq[1]) + rq[2]) + rq[3];
+      a.b1[pq[0]] = sum;
+      a.x1_1[pq[0]] = OM * __ldg(a.dinv1 + pq[0]) * sum;
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (pq[q] < 0) continue;
@@ -1859,6 +1895,25 @@ __global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(const __grid
       a.x1_1[pq[q]] = OM * __ldg(a.dinv1 + pq[q]) * sum;
     }
   }
+}
+
+// Pass A (v2): pending CG update, pre-smoothing of the new r, residual,
+// restriction to level 1; one tile per CTA, TMA brings the five halo boxes
+// (r, w, s, dinv, hw) and the three interior boxes (u, p, x).
+template <int CONN>
+__global__ void __launch_bounds__(NT, NI_MG_A2_MINB) pass_a2_kernel(
+    const __grid_constant__ FineArgs a, const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const AStage g = astage(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + kAStageBytes);
+  __shared__ ASlots sc;
+  const int t = a.tiles[blockIdx.x];
+  if (tile_done(a, t)) return;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    a2_issue(a, tm, t, g, bar);
+  }
+  a2_tile<CONN>(a, t, g, bar, 0, sc);
 }
 
 constexpr size_t kPassB2Smem = 4 * size_t(al128(BOX2 * 4)) + size_t(al128(BOX1 * 4)) +

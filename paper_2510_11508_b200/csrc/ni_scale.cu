@@ -442,9 +442,24 @@ __global__ void part_mean_kernel(StepWs w, int C) {
   }
 }
 
+// maps of <= kWarpMaxComps components project their right-hand side inside
+// the CG kernel (one warp), so this pass leaves them alone: a map's arithmetic
+// never depends on which other maps share the batch
+constexpr int kWarpMaxComps = 32;
+
+__device__ __forceinline__ int map_of_comp(const Maps& mp, int c) {
+  int lo = 0, hi = mp.B - 1;  // last m with first[m] <= c
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (mp.first[mid] <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 __global__ void part_sub_kernel(StepWs w, int C) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x)
-    w.rhs[c] = w.rhs[c] - w.r[c];
+    if (w.mp.count[map_of_comp(w.mp, c)] > kWarpMaxComps) w.rhs[c] = w.rhs[c] - w.r[c];
 }
 
 // K6: scipy-equivalent CG on one map's component Laplacian (solver.py:97-122):
@@ -479,6 +494,102 @@ __device__ __forceinline__ double cg_sweep(const Quot& q, const StepWs& w, const
   return pq;
 }
 
+// scipy's CG from x0 = 0 (solver.py:97-122) for a map of n <= 32 components,
+// one warp, a lane per component: the lane's Laplacian row (diagonal dg,
+// off-diagonal conductances s_cnd[.][lane] at lanes s_col[.][lane], deg of
+// them, jmax = the warp's largest deg) and right-hand side b; neighbours' p
+// by shuffle, the iteration's three dots in one set of shuffle rounds
+// (<r',r'> = <r,r> - 2 a <r,q> + a^2 <q,q>).  Returns the lane's x.
+__device__ __forceinline__ double warp_cg(int lane, bool own, int deg, int jmax, double dg,
+                                          double b, int n, double rtol, int cg_max_iters,
+                                          const int8_t (*s_col)[32], const double (*s_cnd)[32],
+                                          int& ok) {
+  const int maxiter = cg_max_iters > n ? cg_max_iters : n;
+  double x = 0.0, r = b, pv = 0.0;
+  double rr = warp_sum(b * b);
+  const double bnrm = sqrt(rr);
+  ok = 1;
+  if (bnrm == 0.0) return 0.0;
+  const double atol = rtol * bnrm;
+  double rho_prev = 0.0;
+  ok = 0;
+  for (int it = 0; it < maxiter; ++it) {
+    if (sqrt(rr) < atol) {
+      ok = 1;
+      break;
+    }
+    const double rho = rr;
+    const double beta = it == 0 ? 0.0 : rho / rho_prev;
+    pv = r + beta * pv;
+    double aq = dg * pv;
+    for (int jj = 0; jj < jmax; ++jj) {
+      const bool has = jj < deg;
+      const double pn = __shfl_sync(0xffffffffu, pv, has ? int(s_col[jj][lane]) : lane);
+      if (has) aq -= s_cnd[jj][lane] * pn;
+    }
+    double d0 = pv * aq, d1 = r * aq, d2 = aq * aq;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+    }
+    const double alpha = rho / d0;
+    x += alpha * pv;
+    r -= alpha * aq;
+    rr = fmax(rho - 2.0 * alpha * d1 + alpha * alpha * d2, 0.0);
+    rho_prev = rho;
+  }
+  return own ? x : 0.0;
+}
+
+// the lane's Laplacian row of a small map into shared memory; returns its
+// length, jmax = the warp's largest
+__device__ __forceinline__ int warp_rows(const Quot& q, const StepWs& w, int c0, int lane,
+                                         bool own, int8_t (*s_col)[32], double (*s_cnd)[32],
+                                         int& jmax) {
+  const int c = c0 + lane;
+  const int j0 = own ? q.lstart[c] : 0, deg = own ? q.lstart[c + 1] - j0 : 0;
+  for (int jj = 0; jj < deg; ++jj) {
+    s_col[jj][lane] = int8_t(q.lcol[j0 + jj] - c0);
+    s_cnd[jj][lane] = w.S[q.lpair[j0 + jj]];
+  }
+  __syncwarp();
+  jmax = deg;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+  return deg;
+}
+
+// the right-hand side minus its mean over the lane's part (the components
+// joined by positive-conductance links: min-label propagation, < 32 rounds)
+__device__ __forceinline__ double warp_project(int lane, bool own, int deg, int jmax, int n,
+                                               double b0, const int8_t (*s_col)[32],
+                                               const double (*s_cnd)[32]) {
+  int part = own ? lane : 32 + lane;
+  for (int round = 0; round < 32; ++round) {
+    int nl = part;
+    for (int jj = 0; jj < jmax; ++jj) {  // every lane takes part in every shuffle
+      const bool link = jj < deg && s_cnd[jj][lane] > 0.0;
+      const int other = __shfl_sync(0xffffffffu, part, link ? int(s_col[jj][lane]) : lane);
+      if (link) nl = min(nl, other);
+    }
+    const bool changed = nl != part;
+    part = nl;
+    if (!__any_sync(0xffffffffu, changed)) break;
+  }
+  double psum = 0.0, pcnt = 0.0;
+  for (int l = 0; l < n; ++l) {
+    const int pl = __shfl_sync(0xffffffffu, part, l);
+    const double bl = __shfl_sync(0xffffffffu, b0, l);
+    if (pl == part) {
+      psum += bl;
+      pcnt += 1.0;
+    }
+  }
+  return own ? b0 - psum / pcnt : 0.0;
+}
+
 // One CTA per map (maps with <= kBlockCgMax components): every reduction is
 // a block reduction, so the whole solve runs without a grid barrier.
 __global__ void __launch_bounds__(kCgThreads) scale_cg_block_kernel(Quot q, StepWs w, double rtol,
@@ -488,6 +599,24 @@ __global__ void __launch_bounds__(kCgThreads) scale_cg_block_kernel(Quot q, Step
   const int m = w.mp.active[blockIdx.x];
   const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
   if (n > kBlockCgMax || !map_live(w.mp, m)) return;  // cooperative kernel / sitting out
+  if (n <= kWarpMaxComps) {  // one warp, a lane per component: projection + CG
+    __shared__ int8_t s_col[32][32];
+    __shared__ double s_cnd[32][32];
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const bool own = lane < n;
+    int jmax;
+    const int deg = warp_rows(q, w, c0, lane, own, s_col, s_cnd, jmax);
+    const double b = warp_project(lane, own, deg, jmax, n, own ? w.rhs[c0 + lane] : 0.0, s_col,
+                                  s_cnd);
+    if (own) w.rhs[c0 + lane] = b;
+    int ok;
+    const double x = warp_cg(lane, own, deg, jmax, own ? w.diag[c0 + lane] : 0.0, b, n, rtol,
+                             cg_max_iters, s_col, s_cnd, ok);
+    if (own) s[c0 + lane] = x;
+    if (lane == 0) ok_out[m] = ok;
+    return;
+  }
   const int tid = threadIdx.x, stride = blockDim.x;
   const int maxiter = cg_max_iters > n ? cg_max_iters : n;
   double rr = 0.0;
@@ -1115,7 +1244,11 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
   NI_COUNT_LAUNCH(), comp_sum_kernel<<<int(std::min<int64_t>(C, int64_t(kSMs) * 8)), 256, 0, s>>>(q, w);
   NI_LAUNCH_CHECK();
-  // remove the roundoff null-space component of A^T W b
+  // remove the roundoff null-space component of A^T W b; maps
+  // of <= kWarpMaxComps components do it in their CG warp
+  bool any_big = false;
+  for (int j = 0; j < nact; ++j) any_big |= map_count[active[j]] > kWarpMaxComps;
+  if (any_big) {
   NI_COUNT_LAUNCH(), part_init_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
   NI_COUNT_LAUNCH(), part_union_kernel<<<blocks_for(K), 256, 0, s>>>(q, w, q.nU);
   NI_COUNT_LAUNCH(), part_flatten_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
@@ -1126,6 +1259,7 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
   NI_COUNT_LAUNCH(), part_mean_kernel<<<blocks_for(32 * int64_t(C)), 256, 0, s>>>(w, C);
   NI_COUNT_LAUNCH(), part_sub_kernel<<<blocks_for(C), 256, 0, s>>>(w, C);
   NI_LAUNCH_CHECK();
+  }
   // K6: one CTA per map, and one cooperative launch per large map
   NI_COUNT_LAUNCH(), scale_cg_block_kernel<<<nact, kCgThreads, 0, s>>>(q, w, cg_tol, cg_max_iters,
                                                                       scales, cg_ok_out);
@@ -1220,7 +1354,7 @@ __device__ void fused_iteration(
     int64_t npix, const WeightArgs& wp, double rtol, int cg_max_iters, double* __restrict__ s,
     double* __restrict__ residual, double* __restrict__ weights, double* __restrict__ energy_out,
     int32_t* __restrict__ ok_out, double* __restrict__ zshift, const DecideArgs& da, double* red) {
-  __shared__ double s_cnd[32][32];  // warp CG: row j of lane's Laplacian row (<= 31 entries)
+  __shared__ double s_cnd[32][32];  // small maps: entry j of lane's Laplacian row (<= 31)
   __shared__ int8_t s_col[32][32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -1284,98 +1418,51 @@ __device__ void fused_iteration(
       w.rhs[c] = r;
     }
   }
-  // roundoff null-space removal per part (components joined by S > 0)
-  for (int c = c0 + tid; c < c1; c += nt) w.parent[c] = c;
-  __syncthreads();
-  for (int u = u0 + tid; u < u1; u += nt)
-    if (w.S[u] > 0.0) uf_union(w.parent, q.pp[u], q.pq[u]);
-  __syncthreads();
-  for (int c = c0 + tid; c < c1; c += nt) w.pkey[c] = uf_find(w.parent, c);
-  __syncthreads();
-  // a warp per part root: its components in ascending id, lane-strided
-  for (int r0 = c0 + wid; r0 < c1; r0 += nw) {
-    if (w.pkey[r0] != r0) continue;  // warp-uniform
-    double sum = 0.0, cnt = 0.0;
-    for (int c = c0 + lane; c < c1; c += 32)
-      if (w.pkey[c] == r0) {
-        sum += w.rhs[c];
-        cnt += 1.0;
-      }
-    sum = warp_sum(sum);
-    cnt = warp_sum(cnt);
-    if (lane == 0) w.r[r0] = sum / cnt;  // the part's mean, stashed at its root
-  }
-  __syncthreads();
-  for (int c = c0 + tid; c < c1; c += nt) w.q[c] = w.rhs[c] - w.r[w.pkey[c]];
-  __syncthreads();
-  for (int c = c0 + tid; c < c1; c += nt) w.rhs[c] = w.q[c];
-  __syncthreads();
-  // K6: the map's CG.  Up to 32 components: one warp, a lane per component,
-  // shuffle reductions only (no block barrier per CG iteration).
   if (n <= 32) {
+    // One warp, a lane per component: the parts (components joined by
+    // S > 0) by label propagation, the roundoff null-space projection of the
+    // right-hand side, and the CG.
     if (wid == 0) {
-      const int maxiter = cg_max_iters > n ? cg_max_iters : n;
       const int c = c0 + lane;
       const bool own = lane < n;
-      const double b = own ? w.rhs[c] : 0.0;
-      // the lane's Laplacian row, read once: off-diagonal conductances and
-      // their columns (as lanes) into shared memory, the diagonal into a register
-      const double dg = own ? w.diag[c] : 0.0;
-      const int j0 = own ? q.lstart[c] : 0, deg = own ? q.lstart[c + 1] - j0 : 0;
-      for (int jj = 0; jj < deg; ++jj) {
-        s_col[jj][lane] = int8_t(q.lcol[j0 + jj] - c0);
-        s_cnd[jj][lane] = w.S[q.lpair[j0 + jj]];
-      }
-      int jmax = deg;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
-      __syncwarp();
-      double x = 0.0, r = b, p = 0.0;
-      double rr = warp_sum(b * b);
-      const double bnrm = sqrt(rr);
+      int jmax;
+      const int deg = warp_rows(q, w, c0, lane, own, s_col, s_cnd, jmax);
+      const double b = warp_project(lane, own, deg, jmax, n, own ? w.rhs[c] : 0.0, s_col, s_cnd);
+      if (own) w.rhs[c] = b;
       int ok = 1;
-      if (bnrm != 0.0) {
-        const double atol = rtol * bnrm;
-        double rho_prev = 0.0;
-        ok = 0;
-        for (int it = 0; it < maxiter; ++it) {
-          if (sqrt(rr) < atol) {
-            ok = 1;
-            break;
-          }
-          const double rho = rr;
-          const double beta = it == 0 ? 0.0 : rho / rho_prev;
-          p = r + beta * p;
-          // q = L p: the diagonal and the pair conductances of the lane's row,
-          // neighbours' p by shuffle (their lane = column - c0)
-          double aq = dg * p;
-          for (int jj = 0; jj < jmax; ++jj) {
-            const bool has = jj < deg;
-            const int col = has ? int(s_col[jj][lane]) : 0;
-            const double pn = __shfl_sync(0xffffffffu, p, col);
-            if (has) aq -= s_cnd[jj][lane] * pn;
-          }
-          // the three dots of the iteration in one set of shuffle rounds:
-          // <p,q>, <r,q>, <q,q>; then <r',r'> = <r,r> - 2 a <r,q> + a^2 <q,q>
-          double d0 = p * aq, d1 = r * aq, d2 = aq * aq;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-            d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-            d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-          }
-          const double alpha = rho / d0;
-          x += alpha * p;
-          r -= alpha * aq;
-          rr = fmax(rho - 2.0 * alpha * d1 + alpha * alpha * d2, 0.0);
-          rho_prev = rho;
-        }
-      }
+      const double x = warp_cg(lane, own, deg, jmax, own ? w.diag[c] : 0.0, b, n, rtol,
+                               cg_max_iters, s_col, s_cnd, ok);
       if (own) s[c] = x;
       if (lane == 0) ok_out[m] = ok;
     }
     __syncthreads();
   } else {
+  // roundoff null-space removal per part (components joined by S > 0)
+    for (int c = c0 + tid; c < c1; c += nt) w.parent[c] = c;
+    __syncthreads();
+    for (int u = u0 + tid; u < u1; u += nt)
+      if (w.S[u] > 0.0) uf_union(w.parent, q.pp[u], q.pq[u]);
+    __syncthreads();
+    for (int c = c0 + tid; c < c1; c += nt) w.pkey[c] = uf_find(w.parent, c);
+    __syncthreads();
+    // a warp per part root: its components in ascending id, lane-strided
+    for (int r0 = c0 + wid; r0 < c1; r0 += nw) {
+      if (w.pkey[r0] != r0) continue;  // warp-uniform
+      double sum = 0.0, cnt = 0.0;
+      for (int c = c0 + lane; c < c1; c += 32)
+        if (w.pkey[c] == r0) {
+          sum += w.rhs[c];
+          cnt += 1.0;
+        }
+      sum = warp_sum(sum);
+      cnt = warp_sum(cnt);
+      if (lane == 0) w.r[r0] = sum / cnt;  // the part's mean, stashed at its root
+    }
+    __syncthreads();
+    for (int c = c0 + tid; c < c1; c += nt) w.q[c] = w.rhs[c] - w.r[w.pkey[c]];
+    __syncthreads();
+    for (int c = c0 + tid; c < c1; c += nt) w.rhs[c] = w.q[c];
+    __syncthreads();
     const int maxiter = cg_max_iters > n ? cg_max_iters : n;
     double rr = 0.0;
     for (int c = c0 + tid; c < c1; c += nt) {

@@ -574,8 +574,10 @@ def run_pipeline_batch(
     """``run_pipeline`` over the B maps of a batched NormalMap.
 
     ``intrinsics`` is one CameraIntrinsics or a list of B.  Returns one
-    PipelineResult per map, each identical in content to what
-    ``run_pipeline`` returns for that map alone.
+    PipelineResult per map, bit-identical in content to what
+    ``run_pipeline`` returns for that map alone (every reduction of a map
+    runs in an order that does not depend on the other maps;
+    tests/test_gpu_edge_cases.py::test_batch_bit_identical_to_single_maps).
     """
     settings = as_settings(settings) or SolveSettings()
     weights = as_weights(weights) or WeightParams()
@@ -778,13 +780,14 @@ def run_pipeline_stream(
     float64 CPU tensor with every map's log-depth (0 outside the mask).
 
     The next batch's host->device copy and the previous batch's log-depth
-    read-back run on a copy stream while the current batch computes, so a
+    read-back run on two copy streams while the current batch computes, so a
     stream of batches pays for the transfers only at its two ends.  The
     results are those of ``run_pipeline_batch`` on each batch.
     """
     dev = _device(device)
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    h2d = torch.cuda.Stream(dev)  # uploads and read-backs on separate streams: the
+    d2h = torch.cuda.Stream(dev)  # link is full duplex, so they overlap each other too
     it = iter(batches)
 
     def upload():
@@ -792,11 +795,11 @@ def run_pipeline_stream(
             n_h, m_h = next(it)
         except StopIteration:
             return None
-        with torch.cuda.stream(copy):
+        with torch.cuda.stream(h2d):
             n_d = n_h.to(dev, non_blocking=True)
             m_d = m_h.to(dev, non_blocking=True)
             ready = torch.cuda.Event()
-            ready.record(copy)
+            ready.record(h2d)
         return n_d, m_d, ready
 
     nxt = upload()
@@ -813,13 +816,13 @@ def run_pipeline_stream(
         done.record(comp)
         out = torch.empty((len(res), res[0].log_depth.height * res[0].log_depth.width),
                           dtype=torch.float64, pin_memory=True)
-        with torch.cuda.stream(copy):
-            copy.wait_event(done)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
             for i, r in enumerate(res):
-                r.log_depth.values_t.record_stream(copy)
+                r.log_depth.values_t.record_stream(d2h)
                 out[i].copy_(r.log_depth.values_t, non_blocking=True)
             fetched = torch.cuda.Event()
-            fetched.record(copy)
+            fetched.record(d2h)
         if pending is not None:
             pending[2].synchronize()
             yield pending[0], pending[1]
@@ -853,7 +856,12 @@ def run_pipeline(
 
     Same contract as normint.run_pipeline (pipeline.py:105-248): ``theta_c``
     in radians (None = per-pixel components), output gauge-fixed to unit
-    median depth unless ``gauge_depth`` is given.
+    median depth unless ``gauge_depth`` is given.  Numerical differences
+    (INTEGRATION.md): the fill is solved by a multigrid-preconditioned fp32
+    CG to scipy's tolerance, and the scale step removes the roundoff
+    null-space part of its right-hand side -- a no-op unless the reference's
+    own scale CG hits its cap, where the reference's records, warnings and
+    energies follow a roundoff-driven trajectory these do not reproduce.
     """
     nmap = as_normal_map(nmap)
     if nmap.batch != 1:

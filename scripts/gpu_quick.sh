@@ -5,7 +5,7 @@ tag=$1; tests=$2; mode=$3
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${tag}_build.log 2>&1 || true
 if [ -n "$tests" ]; then
-  timeout 1200 python -m pytest $tests -x -q > gpurun_out/${tag}_pytest.log 2>&1
+  timeout 1200 python -m pytest $tests -x -q --timeout 300 > gpurun_out/${tag}_pytest.log 2>&1
   echo "pytest exit $?" >> gpurun_out/${tag}_pytest.log
 fi
 timeout 600 python bench.py > gpurun_out/${tag}_bench.log 2>&1
