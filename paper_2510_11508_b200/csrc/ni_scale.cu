@@ -1317,8 +1317,10 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
 // fixed orders (a map's path depends only on its own sizes, so batched and
 // single-map runs stay bit-identical).
 constexpr int kFusedThreads = 512;
-constexpr int kFusedMaxEdges = 1 << 14;  // measured: 64 C5 maps (~50 k edges each) run faster
-                                          // as the multi-kernel step spread over every SM
+#ifndef NI_FUSED_MAX_EDGES
+#define NI_FUSED_MAX_EDGES (1 << 14)  // measured: 64 C5 maps (~50 k edges each) run faster as
+#endif                                // the multi-kernel step spread over every SM
+constexpr int kFusedMaxEdges = NI_FUSED_MAX_EDGES;
 constexpr int kFusedMaxComps = 1024;
 
 struct DecideArgs {
@@ -1418,6 +1420,7 @@ __device__ void fused_iteration(
       w.rhs[c] = r;
     }
   }
+  __syncthreads();  // every warp's diagonal / right-hand side is written
   if (n <= 32) {
     // One warp, a lane per component: the parts (components joined by
     // S > 0) by label propagation, the roundoff null-space projection of the
