@@ -286,6 +286,7 @@ static int upload_maps(Maps& mp, const int32_t* first, const int32_t* count, con
 struct StepWs {
   double *wa, *wb, *ba, *bb, *S, *diag, *rhs, *r, *p0, *p1, *q, *part, *epart;
   int32_t *parent, *pkey, *pkey_s, *pval, *pval_s;
+  int32_t* arrivals;  // [B] per-map block arrivals of residual_kernel
   Maps mp;
   void* sort_ws;
   size_t sort_bytes;
@@ -314,6 +315,7 @@ static void carve_step(Carver& c, StepWs& w, int K, int C, int B) {
   w.pkey_s = c.take<int32_t>(C + 1);
   w.pval = c.take<int32_t>(C + 1);
   w.pval_s = c.take<int32_t>(C + 1);
+  w.arrivals = c.take<int32_t>(B + 1);
   carve_maps(c, w.mp, B);
   w.sort_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, w.sort_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
@@ -354,32 +356,31 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
   }
 }
 
-// K5a: conductance per component pair, summed over its run in edge order.
-// One warp per pair: lane-strided partial sums then a fixed xor tree.
-__global__ void pair_sum_kernel(Quot q, StepWs w, const int32_t* __restrict__ nU_dev) {
-  const int U = nU_dev[0];
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += warps) {
-    double s = 0.0;
-    for (int j = q.pstart[u] + lane; j < q.pstart[u + 1]; j += 32) {
-      const int e = q.order[j];
-      s += w.wa[e] + w.wb[e];
-    }
-    s = warp_sum(s);
-    if (lane == 0) w.S[u] = s;
-  }
-}
-
-// K5b: diagonal and A^T W b per component, summed over its incident edges in
-// edge order (solver.py:108-111).  One warp per component.  A map whose
-// A^T W b vanishes (solver.py:112-113) needs no special case: its CG starts
-// from b = 0 and stops at once with s = 0.
-__global__ void __launch_bounds__(256) comp_sum_kernel(Quot q, StepWs w) {
-  // one block per component: thread-strided partial sums over its incident
-  // entries in edge order, then a fixed-order block tree (deterministic)
+// K5a + K5b in one launch (solver.py:108-111): blocks [0, pair_blocks) sum
+// the conductance of each component pair over its run in edge order (a warp
+// per pair, lane-strided + fixed xor tree), the others the diagonal and
+// A^T W b of each component over its incident edges in edge order (a block
+// per component); both reduction orders are independent of the grid.
+__global__ void __launch_bounds__(256) sums_kernel(Quot q, StepWs w, const int32_t* __restrict__ nU_dev,
+                                                   int pair_blocks) {
   __shared__ double red[32];
-  for (int c = blockIdx.x; c < q.C; c += gridDim.x) {
+  if (int(blockIdx.x) < pair_blocks) {
+    const int U = nU_dev[0];
+    const int lane = threadIdx.x & 31;
+    const int warps = (pair_blocks * blockDim.x) >> 5;
+    for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += warps) {
+      double sum = 0.0;
+      for (int j = q.pstart[u] + lane; j < q.pstart[u + 1]; j += 32) {
+        const int e = q.order[j];
+        sum += w.wa[e] + w.wb[e];
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) w.S[u] = sum;
+    }
+    return;
+  }
+  const int nb = gridDim.x - pair_blocks;
+  for (int c = blockIdx.x - pair_blocks; c < q.C; c += nb) {
     double d = 0.0, r = 0.0;
     for (int j = q.cstart[c] + threadIdx.x; j < q.cstart[c + 1]; j += blockDim.x) {
       const int ent = q.cent[j];
@@ -752,13 +753,26 @@ __global__ void chunk_sum_kernel(const double* __restrict__ part, const int32_t*
   out[maps[j]] = e;
 }
 
+// K7a + the per-map energy + the deferred shift in one launch: a map's
+// kEChunks blocks write their partial energies; the last to finish (a
+// per-map arrival counter) sums them in chunk order (as chunk_sum_kernel);
+// each block also adds its share of the map's scales to zshift.
 __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const double* __restrict__ s,
                                                        double* __restrict__ residual,
                                                        double* __restrict__ weights,
-                                                       double* __restrict__ part) {
+                                                       double* __restrict__ part,
+                                                       double* __restrict__ energy_out,
+                                                       int32_t* __restrict__ arrivals,
+                                                       double* __restrict__ zshift) {
   __shared__ double red[32];
+  __shared__ bool last;
   const int m = w.mp.active[blockIdx.y];
   if (!map_live(w.mp, m)) return;
+  if (zshift) {  // zshift[c] += s[c] over this block's share of the map's components
+    const int cf = w.mp.first[m], cn = w.mp.count[m];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cn; j += gridDim.x * blockDim.x)
+      zshift[cf + j] += s[cf + j];
+  }
   int c0, c1;
   chunk_range(q.estart[m], q.estart[m + 1], c0, c1);
   double en = 0.0;
@@ -773,7 +787,19 @@ __global__ void __launch_bounds__(256) residual_kernel(Quot q, StepWs w, const d
     en += ra * (w.wa[e] * ra) + rb * (w.wb[e] * rb);
   }
   en = block_sum(en, red);
-  if (threadIdx.x == 0) part[blockIdx.y * kEChunks + blockIdx.x] = en;
+  if (threadIdx.x == 0) {
+    part[blockIdx.y * kEChunks + blockIdx.x] = en;
+    __threadfence();
+    last = atomicAdd(arrivals + blockIdx.y, 1) == kEChunks - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double e = 0.0;
+    for (int c = 0; c < kEChunks; ++c) e += __ldcg(part + blockIdx.y * kEChunks + c);
+    energy_out[m] = e;
+    arrivals[blockIdx.y] = 0;  // ready for the next call on this workspace
+  }
 }
 
 // K7b: z[valid] += s[label] on the active maps' pixels (pipeline.py:181-182)
@@ -797,19 +823,6 @@ __global__ void apply_kernel(double* __restrict__ z, const int32_t* __restrict__
     for (int u = 0; u < U; ++u)
       if (l[u] >= 0) z[base + j0 + u * stride] += s[l[u]];
   }
-}
-
-// deferred scales: zshift[c] += s[c] over the components of the active maps
-__global__ void shift_accumulate_kernel(double* __restrict__ zshift, const double* __restrict__ s,
-                                        const int32_t* __restrict__ first,
-                                        const int32_t* __restrict__ count,
-                                        const int32_t* __restrict__ active,
-                                        const int32_t* __restrict__ live) {
-  const int m = active[blockIdx.y];
-  if (live && !live[m]) return;
-  const int c0 = first[m], n = count[m];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    zshift[c0 + j] += s[c0 + j];
 }
 
 // zshift[label] = 0 for every labelled pixel of the listed maps (after the
@@ -1241,8 +1254,11 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     NI_COUNT_LAUNCH(), weights_kernel<4, 1><<<wblocks, 256, 0, s>>>(
                            q, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, wp, w);
   NI_LAUNCH_CHECK();
-  NI_COUNT_LAUNCH(), pair_sum_kernel<<<blocks_for(32 * int64_t(K)), 256, 0, s>>>(q, w, q.nU);
-  NI_COUNT_LAUNCH(), comp_sum_kernel<<<int(std::min<int64_t>(C, int64_t(kSMs) * 8)), 256, 0, s>>>(q, w);
+  {
+    const int pb = blocks_for(32 * int64_t(K));
+    const int cb = int(std::min<int64_t>(C, int64_t(kSMs) * 8));
+    NI_COUNT_LAUNCH(), sums_kernel<<<pb + cb, 256, 0, s>>>(q, w, q.nU, pb);
+  }
   NI_LAUNCH_CHECK();
   // remove the roundoff null-space component of A^T W b; maps
   // of <= kWarpMaxComps components do it in their CG warp
@@ -1286,16 +1302,12 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
     NI_CUDA_TRY(cudaLaunchCooperativeKernel((void*)scale_cg_kernel, dim3(g), dim3(kCgThreads), args,
                                             0, s));
   }
-  NI_COUNT_LAUNCH(), residual_kernel<<<dim3(kEChunks, nact), 256, 0, s>>>(q, w, scales, residual,
-                                                                          weights, w.epart);
-  NI_COUNT_LAUNCH(), chunk_sum_kernel<<<div_up(nact, 64), 64, 0, s>>>(w.epart, w.mp.active, nact,
-                                                                     energy_out, live);
+  NI_CUDA_TRY(cudaMemsetAsync(w.arrivals, 0, sizeof(int32_t) * nact, s));
+  NI_COUNT_LAUNCH(), residual_kernel<<<dim3(kEChunks, nact), 256, 0, s>>>(
+                         q, w, scales, residual, weights, w.epart, energy_out, w.arrivals, zshift);
   NI_LAUNCH_CHECK();
   const int64_t per_map = int64_t(H) * W;
-  if (zshift) {  // deferred: zshift[c] += s[c] for the active maps' components
-    NI_COUNT_LAUNCH(), shift_accumulate_kernel<<<dim3(div_up(C, 256 * nact) + 1, nact), 256, 0, s>>>(
-                           zshift, scales, w.mp.first, w.mp.count, w.mp.active, live);
-  } else {
+  if (!zshift) {
     const int bx = int(std::max<int64_t>(
         1, std::min<int64_t>((per_map + 1023) / 1024, int64_t(kSMs) * 16 / nact + 1)));
     NI_COUNT_LAUNCH(), apply_kernel<<<dim3(bx, nact), 256, 0, s>>>(z, labels, scales,
@@ -1388,7 +1400,7 @@ __device__ void fused_iteration(
   }
   __syncthreads();
   // K5a: pair conductances (the map's pairs are a contiguous run of the
-  // (min, max)-sorted pair list); a warp per pair, as pair_sum_kernel
+  // (min, max)-sorted pair list); a warp per pair, as sums_kernel
   const int U = q.nU[0];
   const int u0 = lower_bound_i32(q.pp, U, c0), u1 = lower_bound_i32(q.pp, U, c1);
   for (int u = u0 + wid; u < u1; u += nw) {

@@ -60,7 +60,8 @@ def test_host_only_entry_points(lib):
     assert _lib.size_query(lib.ni_merge_workspace_size, 100, 10, 2) > 0
     assert _lib.size_query(lib.ni_gauge_workspace_size, 3, 16, 16) > 0
     # argument validation happens before any device work
-    st = lib.ni_coefficients(None, None, None, 1, 4, 4, 8, 1, None, None, None, None, None, None)
+    st = lib.ni_coefficients(None, None, None, 1, 4, 4, 8, 1, None, None, None, None, None, None,
+                             None)
     assert st == _lib.NI_ERR_INVALID_ARG
     assert "connectivity=4" in _lib.last_error()
     with pytest.raises(ValueError):
