@@ -2498,9 +2498,14 @@ int compact_level(Level& L, int32_t* counters, cudaStream_t st) {
 }
 
 // Events of the calling thread, created once per device (not per call).
+// V-cycles are enqueued kLag ahead of the last one whose outcome (active
+// units, processed pixels) the host has read: per V-cycle a pinned slot and
+// an event, kRing of them in a ring.
+constexpr int kLag = 2, kRing = 4;
 struct EventPool {
   int dev = -1;
-  cudaEvent_t ev[7];
+  cudaEvent_t ev[2 + 5 * kRing + kRing];  // loop; per ring slot: 5 stage marks; slot done
+  int32_t* host = nullptr;                 // pinned [kRing][4]
 };
 thread_local EventPool g_events;
 
@@ -2512,6 +2517,9 @@ int thread_events(cudaEvent_t** out) {
       for (cudaEvent_t e : g_events.ev) cudaEventDestroy(e);
     g_events.dev = -1;
     for (cudaEvent_t& e : g_events.ev) NI_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDefault));
+    if (!g_events.host)
+      NI_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&g_events.host),
+                                sizeof(int32_t) * 4 * kRing, cudaHostAllocPortable));
     g_events.dev = dev;
   }
   *out = g_events.ev;
@@ -2838,8 +2846,39 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   NI_TRY(make_tma_maps(tm, g, f));
   NI_CUDA_TRY(cudaEventRecord(e0, st));
   if (NA > 0) {
-    while (true) {
-      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[2], st));
+    int32_t* hslot = g_events.host;
+    // outcome of V-cycle j: nact = 0 means every unit is done; V-cycles
+    // enqueued after it find nothing to do (tiles and unknowns of finished
+    // units are skipped)
+    auto settle = [&](int j, bool& fin) -> int {
+      const int r = j % kRing;
+      NI_CUDA_TRY(cudaEventSynchronize(ev[2 + 5 * kRing + r]));
+      const int32_t* hv = hslot + 4 * r;
+      if (prof) {
+        unsigned long long pxd;
+        memcpy(&pxd, hv + 2, sizeof(pxd));
+        px_vcycles += (long long)pxd;
+        for (int k = 0; k < 4; ++k) {
+          float t = 0.f;
+          NI_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 + 5 * r + k], ev[2 + 5 * r + k + 1]));
+          stage_ms[k] += t;
+        }
+      }
+      fin = hv[0] == 0;
+      return NI_OK;
+    };
+    int done_at = -1;  // the V-cycle after which no unit was active
+    for (int it = 0;; ++it) {
+      if (it >= kLag) {
+        bool fin = false;
+        NI_TRY(settle(it - kLag, fin));
+        if (fin) {
+          done_at = it - kLag;
+          break;
+        }
+      }
+      cudaEvent_t* evs = ev + 2 + 5 * (it % kRing);
+      if (prof) NI_CUDA_TRY(cudaEventRecord(evs[0], st));
 #if NI_MG_V2
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_a2_kernel<8><<<NA, NT, kPassA2Smem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_a2_kernel<4><<<NA, NT, kPassA2Smem, st>>>(fa, tm);
@@ -2849,7 +2888,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
 #endif
       fa.par ^= 1;  // pass B and the next pass A read the r / s pass A wrote
       NI_LAUNCH_CHECK();
-      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[3], st));
+      if (prof) NI_CUDA_TRY(cudaEventRecord(evs[1], st));
       for (int l = 1; l < L; ++l) {
         const Level& C = lev[l];
         const Level& N = lev[l + 1];
@@ -2880,7 +2919,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
 #undef NI_MG_UP
         NI_LAUNCH_CHECK();
       }
-      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[4], st));
+      if (prof) NI_CUDA_TRY(cudaEventRecord(evs[2], st));
 #if NI_MG_V2 && NI_MG_B_V2
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b2_kernel<8><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
       else NI_COUNT_LAUNCH(), pass_b2_kernel<4><<<NA, NT, kPassB2Smem, st>>>(fa, tm);
@@ -2889,28 +2928,23 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
       else NI_COUNT_LAUNCH(), pass_b_kernel<4><<<NA, NT, kPassBSmem, st>>>(fa, tm);
 #endif
       NI_LAUNCH_CHECK();
-      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[5], st));
+      if (prof) NI_CUDA_TRY(cudaEventRecord(evs[3], st));
       // counters [6] active units, [8..9] processed unit pixels (u64)
       NI_CUDA_TRY(cudaMemsetAsync(f.counters + 6, 0, 4 * sizeof(int32_t), st));
       NI_COUNT_LAUNCH(), scalar_kernel<<<grid_for(int64_t(NU) * 32), 256, 0, st>>>(sa);
       NI_LAUNCH_CHECK();
-      if (prof) NI_CUDA_TRY(cudaEventRecord(ev[6], st));
-      ++vcycles;
-      int32_t hv[4] = {0, 0, 0, 0};
-      NI_CUDA_TRY(cudaMemcpyAsync(hv, f.counters + 6, sizeof(hv), cudaMemcpyDeviceToHost, st));
-      NI_CUDA_TRY(cudaStreamSynchronize(st));
-      if (prof) {
-        unsigned long long pxd;
-        memcpy(&pxd, hv + 2, sizeof(pxd));
-        px_vcycles += (long long)pxd;
-        for (int k = 0; k < 4; ++k) {
-          float t = 0.f;
-          NI_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 + k], ev[3 + k]));
-          stage_ms[k] += t;
-        }
-      }
-      if (hv[0] == 0) break;
+      if (prof) NI_CUDA_TRY(cudaEventRecord(evs[4], st));
+      NI_CUDA_TRY(cudaMemcpyAsync(hslot + 4 * (it % kRing), f.counters + 6, 4 * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, st));
+      NI_CUDA_TRY(cudaEventRecord(ev[2 + 5 * kRing + it % kRing], st));
     }
+    // the V-cycles still in flight after done_at are no-ops; settle them so
+    // the ring and the profile are consistent
+    for (int j = done_at + 1; j < done_at + 1 + kLag; ++j) {
+      bool fin = false;
+      NI_TRY(settle(j, fin));
+    }
+    vcycles = done_at + 1;
   }
   NI_CUDA_TRY(cudaEventRecord(e1, st));
   // ---- output: x minus its per-unit mean
