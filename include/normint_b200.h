@@ -312,6 +312,15 @@ int ni_gauge_workspace_size(int B, int H, int W, size_t* bytes);
 int ni_gauge(double* z, const uint8_t* valid, int B, int H, int W, double target,
              double* depth_out, void* workspace, size_t workspace_bytes, ni_stream_t stream);
 
+/* Serving read-back (run_pipeline_stream; the reference returns its depth in
+ * host memory, pipeline.py:240-248): copy `bytes` from device memory `src` to
+ * PINNED host memory `host_dst` with a `ctas`-CTA kernel storing through the
+ * mapped (UVA) address instead of a copy engine, so the read-back of one batch
+ * does not hold the device->host copy queue that the next batch's small
+ * control reads use.  NI_ERR_INVALID_ARG if host_dst is not pinned or the two
+ * pointers differ in 16-byte alignment. */
+int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, int ctas, ni_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,18 +45,29 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     s_tp[tid] = (va + 1.0 - cy) / fy;
     s_hp[tid] = (0.5 * (va + (va + 1.0)) - cy) / fy;
   }
-  // per-map edge / degenerate-edge counts of this tile's rows (maps m0 ..),
-  // accumulated in shared memory, one global atomic per map and counter
-  __shared__ unsigned long long s_cnt[CROWS][2];
+  // per-map edge / degenerate-edge counts of this tile's rows (maps m0 ..):
+  // a warp (one row) reduces its lanes' counts, lane 0 adds them to a 32-bit
+  // shared counter (<= 4096 per tile), one global atomic per map and counter.
+  // (Per-thread 64-bit shared atomics were a CAS loop under contention that
+  // cost more than the coefficients themselves.)
+  __shared__ unsigned s_cnt[CROWS][2];
   const int m0 = row0 / H;
-  if (tid < CROWS) s_cnt[tid][0] = s_cnt[tid][1] = 0ull;
+  if (tid < CROWS) s_cnt[tid][0] = s_cnt[tid][1] = 0u;
   __syncthreads();
   long long ndegen = 0;
   ColRays cr;
-  for (int ry = threadIdx.y; ry < CROWS && u < W; ry += CTHR_Y) {
+  const bool in_cols = u < W;
+  for (int ry = threadIdx.y; ry < CROWS; ry += CTHR_Y) {
     const int row = row0 + ry;
-    if (row >= rows) break;
+    if (row >= rows) break;  // uniform over the warp (one row)
     const int m = row / H;
+    if (!in_cols) {
+      if (map_counts) {  // the warp's reduction needs every lane
+        __reduce_add_sync(0xffffffffu, 0u);
+        __reduce_add_sync(0xffffffffu, 0u);
+      }
+      continue;
+    }
     const int vloc = row - m * H;
     const int64_t i = int64_t(row) * W + u;
     const double fx = intr[4 * m + 0], fy = intr[4 * m + 1];
@@ -129,10 +140,14 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     }
     gamma[i] = g;
     eflags[i] = flags;
-    if (map_counts && flags) {
+    if (map_counts) {
       const unsigned nex = __popc(flags & 0xfu), nok = __popc(flags >> 4);
-      atomicAdd(&s_cnt[m - m0][0], (unsigned long long)nex);
-      if (nex != nok) atomicAdd(&s_cnt[m - m0][1], (unsigned long long)(nex - nok));
+      const unsigned wex = __reduce_add_sync(0xffffffffu, nex);
+      const unsigned wdg = __reduce_add_sync(0xffffffffu, nex - nok);
+      if (threadIdx.x == 0) {
+        if (wex) atomicAdd(&s_cnt[m - m0][0], wex);
+        if (wdg) atomicAdd(&s_cnt[m - m0][1], wdg);
+      }
     }
 #pragma unroll
     for (int k = 0; k < KF; ++k) {
@@ -148,8 +163,10 @@ __global__ void __launch_bounds__(CCOLS * CTHR_Y) coefficients_kernel(
     __syncthreads();
     if (tid < CROWS) {
       const int m = m0 + tid;
-      if (s_cnt[tid][0]) atomicAdd((unsigned long long*)&map_counts[2 * m], s_cnt[tid][0]);
-      if (s_cnt[tid][1]) atomicAdd((unsigned long long*)&map_counts[2 * m + 1], s_cnt[tid][1]);
+      if (s_cnt[tid][0])
+        atomicAdd((unsigned long long*)&map_counts[2 * m], (unsigned long long)s_cnt[tid][0]);
+      if (s_cnt[tid][1])
+        atomicAdd((unsigned long long*)&map_counts[2 * m + 1], (unsigned long long)s_cnt[tid][1]);
     }
   }
 }

@@ -84,3 +84,71 @@ extern "C" int ni_fill_mg_last_profile(double* ms4, long long* px_vcycles) {
   if (px_vcycles) *px_vcycles = r.mg_px_vcycles;
   return NI_OK;
 }
+
+// ---- read-back through the SMs (serving stream, pipeline.py's
+// run_pipeline_stream): a device -> pinned-host copy done by a small kernel
+// storing into mapped host memory instead of by a copy engine.  A copy-engine
+// read-back of a whole batch (~0.5 GB, ~10 ms) holds the device->host queue,
+// so every small control read of the next batch's pipeline (.cpu() of counts
+// and flags) waits behind it; the kernel's posted PCIe writes leave that queue
+// free.  Each thread moves 16-byte vectors, 4 in flight.
+namespace ni {
+__global__ void __launch_bounds__(512) d2h_mapped_kernel(const uint4* __restrict__ src,
+                                                         uint4* __restrict__ dst, int64_t n16) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                d = __ldcs(src + i + 3 * stride);
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = __ldcs(src + i);
+}
+__global__ void d2h_mapped_tail_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                       int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+}  // namespace ni
+
+extern "C" int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, int ctas,
+                               ni_stream_t stream) {
+  NI_CHECK_ARG(src && host_dst, "null pointer");
+  NI_CHECK_ARG(ctas > 0 && ctas <= 4096, "ctas must be in 1..4096");
+  if (bytes == 0) return NI_OK;
+  void* dptr = nullptr;
+  // pinned host memory (cudaHostAlloc / cudaHostRegister) is mapped under UVA
+  if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
+    cudaGetLastError();
+    ni::set_error("ni_copy_to_host: destination is not pinned (mapped) host memory");
+    return NI_ERR_INVALID_ARG;
+  }
+  NI_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == (reinterpret_cast<uintptr_t>(dptr) & 15),
+               "source and destination must share their 16-byte alignment");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(src) & 15;
+  size_t head = mis ? (16 - mis) : 0;
+  if (head > bytes) head = bytes;
+  const auto* s8 = static_cast<const uint8_t*>(src);
+  auto* d8 = static_cast<uint8_t*>(dptr);
+  if (head) {
+    NI_COUNT_LAUNCH(), ni::d2h_mapped_tail_kernel<<<1, 16, 0, s>>>(s8, d8, int64_t(head));
+    NI_LAUNCH_CHECK();
+  }
+  const int64_t n16 = int64_t((bytes - head) / 16);
+  if (n16) {
+    NI_COUNT_LAUNCH(), ni::d2h_mapped_kernel<<<ctas, 512, 0, s>>>(
+        reinterpret_cast<const uint4*>(s8 + head), reinterpret_cast<uint4*>(d8 + head), n16);
+    NI_LAUNCH_CHECK();
+  }
+  const size_t done = head + size_t(n16) * 16;
+  if (done < bytes) {
+    NI_COUNT_LAUNCH(), ni::d2h_mapped_tail_kernel<<<1, 16, 0, s>>>(s8 + done, d8 + done,
+                                                                  int64_t(bytes - done));
+    NI_LAUNCH_CHECK();
+  }
+  return NI_OK;
+}

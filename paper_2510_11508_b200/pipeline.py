@@ -760,6 +760,9 @@ def run_pipeline_batch(
     return out
 
 
+_D2H_CTAS = 16  # read-back kernel CTAs (512 threads each; PCIe-bound); 0: copy engine
+
+
 def run_pipeline_stream(
     batches,
     intrinsics,
@@ -787,7 +790,14 @@ def run_pipeline_stream(
     dev = _device(device)
     comp = torch.cuda.current_stream(dev)
     h2d = torch.cuda.Stream(dev)  # uploads and read-backs on separate streams: the
-    d2h = torch.cuda.Stream(dev)  # link is full duplex, so they overlap each other too
+    # link is full duplex, so they overlap each other too.  The read-back is a
+    # small SM kernel storing into mapped pinned memory (ni_copy_to_host), not a
+    # copy-engine transfer: a ~10 ms copy-engine read-back would hold the
+    # device->host queue that every small control read (.cpu()) of the next
+    # batch's pipeline waits in.  High priority: its few CTAs are scheduled
+    # ahead of the compute grids' pending CTAs.
+    d2h = torch.cuda.Stream(dev, priority=-1)
+    lib = _lib.load()
     it = iter(batches)
 
     def upload():
@@ -803,6 +813,15 @@ def run_pipeline_stream(
         return n_d, m_d, ready
 
     nxt = upload()
+    try:
+        yield from _stream_loop(nxt, upload, comp, d2h, lib, dev, intrinsics, theta_c, settings,
+                                weights, connectivity, model, gauge_depth)
+    finally:  # a consumer that stops early: the read-back kernel may still write `out`
+        d2h.synchronize()
+
+
+def _stream_loop(nxt, upload, comp, d2h, lib, dev, intrinsics, theta_c, settings, weights,
+                 connectivity, model, gauge_depth):
     pending = None
     while nxt is not None:
         n_d, m_d, ready = nxt
@@ -818,9 +837,23 @@ def run_pipeline_stream(
                           dtype=torch.float64, pin_memory=True)
         with torch.cuda.stream(d2h):
             d2h.wait_event(done)
-            for i, r in enumerate(res):
-                r.log_depth.values_t.record_stream(d2h)
-                out[i].copy_(r.log_depth.values_t, non_blocking=True)
+            hw = out.shape[1]
+            vals = [r.log_depth.values_t for r in res]
+            base = vals[0].data_ptr()
+            whole = all(v.is_contiguous() and v.data_ptr() == base + 8 * hw * i
+                        for i, v in enumerate(vals))  # the batch's z: one copy
+            for i, v in enumerate(vals):
+                v.record_stream(d2h)
+                if not _D2H_CTAS:  # copy-engine read-back (the A/B baseline)
+                    out[i].copy_(v, non_blocking=True)
+                    continue
+                if whole and i:
+                    continue
+                nbytes = 8 * hw * (len(vals) if whole else 1)
+                _lib.check(lib.ni_copy_to_host(C.c_void_p(v.data_ptr()),
+                                               C.c_void_p(out[i].data_ptr()), nbytes,
+                                               _D2H_CTAS, C.c_void_p(d2h.cuda_stream)),
+                           "read-back")
             fetched = torch.cuda.Event()
             fetched.record(d2h)
         if pending is not None:

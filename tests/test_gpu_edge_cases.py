@@ -180,3 +180,32 @@ def test_stream_matches_batch():
             assert a.iterations == b.iterations
             assert np.array_equal(a.log_depth.values, b.log_depth.values)
             assert np.array_equal(host[i].numpy(), a.log_depth.values_t.cpu().numpy())
+
+
+def test_copy_to_host_kernel_ragged_and_errors():
+    """ni_copy_to_host (the serving read-back through mapped pinned memory):
+    exact bytes for lengths / offsets that exercise the unaligned head and the
+    tail, nothing written past the range, and a loud error for pageable or
+    misaligned destinations."""
+    import ctypes as C
+
+    from paper_2510_11508_b200 import _lib
+
+    lib = _lib.load()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    src = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device="cuda")
+    for off, n in ((0, 1 << 20), (3, 1000), (16, 17), (5, 7), (0, 0), (1, (1 << 20) - 1)):
+        dst = torch.full((1 << 20,), 0xAB, dtype=torch.uint8).pin_memory()
+        _lib.check(lib.ni_copy_to_host(C.c_void_p(src.data_ptr() + off),
+                                       C.c_void_p(dst.data_ptr() + off), n, 7, s), "copy")
+        torch.cuda.synchronize()
+        want = torch.full((1 << 20,), 0xAB, dtype=torch.uint8)
+        want[off:off + n] = src[off:off + n].cpu()
+        assert torch.equal(dst, want), (off, n)
+    pageable = torch.empty(1024, dtype=torch.uint8)
+    assert lib.ni_copy_to_host(C.c_void_p(src.data_ptr()), C.c_void_p(pageable.data_ptr()),
+                               1024, 4, s) != 0
+    assert b"pinned" in lib.ni_last_error()
+    dst = torch.empty(1024, dtype=torch.uint8).pin_memory()
+    assert lib.ni_copy_to_host(C.c_void_p(src.data_ptr() + 1), C.c_void_p(dst.data_ptr()),
+                               64, 4, s) != 0
