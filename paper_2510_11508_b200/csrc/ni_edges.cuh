@@ -28,14 +28,16 @@ struct WeightArgs {
 // (b = a + offset_k), at log-depth state z.  Invalid edges get 0.
 // Log-depth at pixel x: z[x], plus the pixel's component shift when the
 // caller defers the scale application (zs != nullptr: z_eff = z + zs[label]).
-__device__ __forceinline__ double z_at(const double* __restrict__ z, const double* __restrict__ zs,
+// (zs is not __restrict__: the fused scale loop advances the shifts inside the
+// kernel that reads them, so they must not take the non-coherent load path)
+__device__ __forceinline__ double z_at(const double* __restrict__ z, const double* zs,
                                        const int32_t* __restrict__ labels, int64_t x) {
   return zs ? z[x] + zs[labels[x]] : z[x];
 }
 
 template <int CONN, int MODEL>
 __device__ __forceinline__ void edge_weights_at(const double* __restrict__ z,
-                                                const double* __restrict__ zs,
+                                                const double* zs,
                                                 const int32_t* __restrict__ zlab,
                                                 const double* __restrict__ omega_a,
                                                 const double* __restrict__ omega_b,

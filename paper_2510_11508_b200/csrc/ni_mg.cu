@@ -1370,8 +1370,12 @@ __global__ void __launch_bounds__(NT) pass_a_kernel(const __grid_constant__ Fine
 
 // Pass B: prolongation + post-smoothing -> u = M r; w = A u; per-slot dots
 // (r,u), (w,u), (r,r), sum u, sum r, sum w.
+// 54 KB: four CTAs per SM.  The per-slot staging of multi-unit tiles (w values
+// and slots of the tile's pixels) reuses the dinv and x2 boxes, which are dead
+// once x3 is computed.
 constexpr size_t kPassBSmem = 4 * size_t(al128(BOX2 * 4)) + size_t(al128(S3 * BH1 * 4)) +
-                              size_t(al128(BWM * BH1)) + size_t(TPX) * 4 + size_t(TPX) * 2 + 128;
+                              size_t(al128(BWM * BH1)) + 128;
+static_assert(TPX * 4 <= BOX2 * 4 && TPX * 2 <= BOX2 * 4, "pass B staging must fit the dead boxes");
 
 template <int CONN>
 __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ FineArgs a,
@@ -1384,9 +1388,9 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
   float* sX2 = sH + al128(BOX2 * 4) / 4;  // par0 lands here, then x2 replaces it
   float* sX3 = sX2 + al128(BOX2 * 4) / 4;
   uint8_t* sM = reinterpret_cast<uint8_t*>(sX3 + al128(S3 * BH1 * 4) / 4);
-  float* sWv = reinterpret_cast<float*>(sM + al128(BWM * BH1));
-  uint16_t* sSl = reinterpret_cast<uint16_t*>(sWv + TPX);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sSl + TPX);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sM + al128(BWM * BH1));
+  float* sWv = sD;                                  // after the x3 barrier: dinv is dead
+  uint16_t* sSl = reinterpret_cast<uint16_t*>(sX2);  // ... and so is x2
   __shared__ double sred[NT / 32][NPART];
   const int t = a.tiles[blockIdx.x];
   if (tile_done(a, t)) return;

@@ -23,6 +23,7 @@
 // bit-identical and independent of which other maps share the batch.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <vector>
 
@@ -266,20 +267,29 @@ struct Maps {
 
 __device__ __forceinline__ bool map_live(const Maps& mp, int m) { return !mp.live || mp.live[m]; }
 
+// The three tables are one block of the workspace so that a call uploads
+// them with ONE host->device copy (a pageable copy costs the stream ~10 us, and
+// behind a bulk upload of the serving stream far more; the outer loop makes
+// one call per iteration).
 static void carve_maps(Carver& c, Maps& mp, int B) {
   mp.B = B;
-  mp.first = c.take<int32_t>(B + 1);
-  mp.count = c.take<int32_t>(B + 1);
-  mp.active = c.take<int32_t>(B + 1);
+  mp.first = c.take<int32_t>(3 * size_t(B + 1));
+  mp.count = mp.first ? mp.first + (B + 1) : nullptr;
+  mp.active = mp.first ? mp.first + 2 * (B + 1) : nullptr;
 }
 
 static int upload_maps(Maps& mp, const int32_t* first, const int32_t* count, const int32_t* active,
                        int nact, cudaStream_t s) {
   mp.nact = nact;
-  NI_CUDA_TRY(cudaMemcpyAsync(mp.first, first, sizeof(int32_t) * (mp.B + 1), cudaMemcpyHostToDevice, s));
-  NI_CUDA_TRY(cudaMemcpyAsync(mp.count, count, sizeof(int32_t) * mp.B, cudaMemcpyHostToDevice, s));
-  if (nact > 0)
-    NI_CUDA_TRY(cudaMemcpyAsync(mp.active, active, sizeof(int32_t) * nact, cudaMemcpyHostToDevice, s));
+  const int B1 = mp.B + 1;
+  static thread_local std::vector<int32_t> pack;
+  pack.assign(3 * size_t(B1), 0);
+  std::copy(first, first + B1, pack.begin());
+  std::copy(count, count + mp.B, pack.begin() + B1);
+  if (nact > 0) std::copy(active, active + nact, pack.begin() + 2 * B1);
+  // pageable source: the driver stages it before the call returns
+  NI_CUDA_TRY(cudaMemcpyAsync(mp.first, pack.data(), sizeof(int32_t) * (2 * B1 + nact),
+                              cudaMemcpyHostToDevice, s));
   return NI_OK;
 }
 
@@ -356,6 +366,79 @@ __global__ void weights_kernel(Quot q, const double* __restrict__ z,
   }
 }
 
+// Strided segmented sums with the loads of kSumDepth consecutive steps in
+// flight: a thread's gather chain (index -> operands) is two dependent L2
+// round trips per step, so a serial loop is latency-bound (measured: a
+// 1,500-edge pair cost one warp ~28 us).  The additions run in the same order
+// as the plain loop, so the sums are bit-identical to it.  The operand arrays
+// are not __restrict__: the fused kernel writes them earlier in the same
+// launch, so they must not go through the non-coherent load path.
+constexpr int kSumDepth = 8;
+
+// sum of wa[e] + wb[e] over e = order[j], j = j0 + lane, + stride, ... < j1
+__device__ __forceinline__ double run_pair_sum(const int32_t* __restrict__ order,
+                                               const double* wa, const double* wb, int j,
+                                               int j1, int stride) {
+  double sum = 0.0;
+  for (; j + (kSumDepth - 1) * stride < j1; j += kSumDepth * stride) {
+    int e[kSumDepth];
+    double a[kSumDepth], b[kSumDepth];
+#pragma unroll
+    for (int k = 0; k < kSumDepth; ++k) e[k] = order[j + k * stride];
+#pragma unroll
+    for (int k = 0; k < kSumDepth; ++k) {
+      a[k] = wa[e[k]];
+      b[k] = wb[e[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < kSumDepth; ++k) sum += a[k] + b[k];
+  }
+  for (; j < j1; j += stride) {
+    const int e = order[j];
+    sum += wa[e] + wb[e];
+  }
+  return sum;
+}
+
+// diagonal d and right-hand side r of a component over its incident entries
+// cent[j], j = j0 + lane, + stride, ... < j1 (solver.py:108-111)
+__device__ __forceinline__ void run_comp_sum(const int32_t* __restrict__ cent,
+                                             const double* wa, const double* wb,
+                                             const double* ba, const double* bb, int j, int j1,
+                                             int stride, double& d, double& r) {
+  constexpr int D = kSumDepth / 2;
+  d = 0.0;
+  r = 0.0;
+  for (; j + (D - 1) * stride < j1; j += D * stride) {
+    int ent[D];
+    double va[D], vb[D], xa[D], xb[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) ent[k] = cent[j + k * stride];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int e = ent[k] >> 1;
+      va[k] = wa[e];
+      vb[k] = wb[e];
+      xa[k] = ba[e];
+      xb[k] = bb[e];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double t = va[k] * xa[k] - vb[k] * xb[k];
+      d += va[k] + vb[k];
+      r += (ent[k] & 1) ? -t : t;
+    }
+  }
+  for (; j < j1; j += stride) {
+    const int en = cent[j];
+    const int e = en >> 1;
+    const double a = wa[e], b = wb[e];
+    const double t = a * ba[e] - b * bb[e];
+    d += a + b;
+    r += (en & 1) ? -t : t;
+  }
+}
+
 // K5a + K5b in one launch (solver.py:108-111): blocks [0, pair_blocks) sum
 // the conductance of each component pair over its run in edge order (a warp
 // per pair, lane-strided + fixed xor tree), the others the diagonal and
@@ -369,11 +452,7 @@ __global__ void __launch_bounds__(256) sums_kernel(Quot q, StepWs w, const int32
     const int lane = threadIdx.x & 31;
     const int warps = (pair_blocks * blockDim.x) >> 5;
     for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += warps) {
-      double sum = 0.0;
-      for (int j = q.pstart[u] + lane; j < q.pstart[u + 1]; j += 32) {
-        const int e = q.order[j];
-        sum += w.wa[e] + w.wb[e];
-      }
+      double sum = run_pair_sum(q.order, w.wa, w.wb, q.pstart[u] + lane, q.pstart[u + 1], 32);
       sum = warp_sum(sum);
       if (lane == 0) w.S[u] = sum;
     }
@@ -381,15 +460,9 @@ __global__ void __launch_bounds__(256) sums_kernel(Quot q, StepWs w, const int32
   }
   const int nb = gridDim.x - pair_blocks;
   for (int c = blockIdx.x - pair_blocks; c < q.C; c += nb) {
-    double d = 0.0, r = 0.0;
-    for (int j = q.cstart[c] + threadIdx.x; j < q.cstart[c + 1]; j += blockDim.x) {
-      const int ent = q.cent[j];
-      const int e = ent >> 1;
-      const double wa = w.wa[e], wb = w.wb[e];
-      const double t = wa * w.ba[e] - wb * w.bb[e];
-      d += wa + wb;
-      r += (ent & 1) ? -t : t;
-    }
+    double d, r;
+    run_comp_sum(q.cent, w.wa, w.wb, w.ba, w.bb, q.cstart[c] + threadIdx.x, q.cstart[c + 1],
+                 blockDim.x, d, r);
     d = block_sum(d, red);
     r = block_sum(r, red);
     if (threadIdx.x == 0) {
@@ -1334,6 +1407,11 @@ constexpr int kFusedThreads = 512;
 #endif                                // the multi-kernel step spread over every SM
 constexpr int kFusedMaxEdges = NI_FUSED_MAX_EDGES;
 constexpr int kFusedMaxComps = 1024;
+#ifndef NI_FUSED_CLUSTER
+#define NI_FUSED_CLUSTER 8  // CTAs per map (a thread-block cluster; 8 is the portable maximum)
+#endif
+constexpr int kFusedCluster = NI_FUSED_CLUSTER;
+static_assert(kFusedCluster >= 1 && kFusedCluster <= 8, "portable cluster sizes only");
 
 struct DecideArgs {
   int t;  // 1-based iteration after this step
@@ -1362,16 +1440,20 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
 template <int CONN, int MODEL>
 __device__ void fused_iteration(
     int m, const Quot& q, const StepWs& w, const double* __restrict__ z,
-    const double* __restrict__ zs, const int32_t* __restrict__ zlab,
+    const double* zs, const int32_t* __restrict__ zlab,
     const double* __restrict__ omega_a, const double* __restrict__ omega_b,
     const double* __restrict__ gamma, const uint8_t* __restrict__ eflags, int H, int W,
     int64_t npix, const WeightArgs& wp, double rtol, int cg_max_iters, double* __restrict__ s,
     double* __restrict__ residual, double* __restrict__ weights, double* __restrict__ energy_out,
-    int32_t* __restrict__ ok_out, double* __restrict__ zshift, const DecideArgs& da, double* red) {
+    int32_t* __restrict__ ok_out, double* zshift, const DecideArgs& da, double* red) {
   __shared__ double s_cnd[32][32];  // small maps: entry j of lane's Laplacian row (<= 31)
   __shared__ int8_t s_col[32][32];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = int(cl.block_rank()), CL = int(cl.num_blocks());
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int gtid = rank * nt + tid, gnt = CL * nt;  // thread / warp of the map's cluster
+  const int gwid = rank * nw + wid, gnw = CL * nw;
   const int e0 = q.estart[m], e1 = q.estart[m + 1];
   const int c0 = w.mp.first[m], n = w.mp.count[m], c1 = c0 + n;
   // K4: weights and row right-hand sides (solver.py:253-278, 170-180); two
@@ -1385,7 +1467,7 @@ __device__ void fused_iteration(
   double* __restrict__ wba = w.ba;
   double* __restrict__ wbb = w.bb;
 #pragma unroll 2
-  for (int e = e0 + tid; e < e1; e += nt) {
+  for (int e = e0 + gtid; e < e1; e += gnt) {
     const int32_t a = qea[e], b = qeb[e], k = qek[e];
     double wa, wb;
     edge_weights_at<CONN, MODEL>(z, zs, zlab, omega_a, omega_b, gamma, eflags, H, W, npix, a, k,
@@ -1398,33 +1480,22 @@ __device__ void fused_iteration(
     wba[e] = oa - (za - zb);
     wbb[e] = ob - (zb - za);
   }
-  __syncthreads();
+  cl.sync();
   // K5a: pair conductances (the map's pairs are a contiguous run of the
   // (min, max)-sorted pair list); a warp per pair, as sums_kernel
   const int U = q.nU[0];
   const int u0 = lower_bound_i32(q.pp, U, c0), u1 = lower_bound_i32(q.pp, U, c1);
-  for (int u = u0 + wid; u < u1; u += nw) {
-    double sum = 0.0;
-    for (int j = q.pstart[u] + lane; j < q.pstart[u + 1]; j += 32) {
-      const int e = q.order[j];
-      sum += w.wa[e] + w.wb[e];
-    }
+  for (int u = u0 + gwid; u < u1; u += gnw) {
+    double sum = run_pair_sum(q.order, w.wa, w.wb, q.pstart[u] + lane, q.pstart[u + 1], 32);
     sum = warp_sum(sum);
     if (lane == 0) w.S[u] = sum;
   }
-  __syncthreads();
-  // K5b: diagonal and A^T W b per component: a warp per component,
-  // lane-strided over its incident entries in edge order
-  for (int c = c0 + wid; c < c1; c += nw) {
-    double d = 0.0, r = 0.0;
-    for (int j = q.cstart[c] + lane; j < q.cstart[c + 1]; j += 32) {
-      const int ent = q.cent[j];
-      const int e = ent >> 1;
-      const double wa = w.wa[e], wb = w.wb[e];
-      const double t = wa * w.ba[e] - wb * w.bb[e];
-      d += wa + wb;
-      r += (ent & 1) ? -t : t;
-    }
+  // K5b: diagonal and A^T W b per component: a warp per component (the
+  // cluster's warps in reverse, so pairs and components start on different
+  // ends), lane-strided over its incident entries in edge order
+  for (int c = c0 + (gnw - 1 - gwid); c < c1; c += gnw) {
+    double d, r;
+    run_comp_sum(q.cent, w.wa, w.wb, w.ba, w.bb, q.cstart[c] + lane, q.cstart[c + 1], 32, d, r);
     d = warp_sum(d);
     r = warp_sum(r);
     if (lane == 0) {
@@ -1432,8 +1503,10 @@ __device__ void fused_iteration(
       w.rhs[c] = r;
     }
   }
-  __syncthreads();  // every warp's diagonal / right-hand side is written
-  if (n <= 32) {
+  cl.sync();  // every warp's pair sum, diagonal and right-hand side is written
+  if (rank != 0) {
+    // the solve is the first CTA's
+  } else if (n <= 32) {
     // One warp, a lane per component: the parts (components joined by
     // S > 0) by label propagation, the roundoff null-space projection of the
     // right-hand side, and the CG.
@@ -1524,10 +1597,11 @@ __device__ void fused_iteration(
     }
     if (tid == 0) ok_out[m] = ok;
   }
-  __syncthreads();
-  // K7a: residual rows and the map's energy (solver.py:301-302)
+  cl.sync();
+  // K7a: residual rows and the map's energy (solver.py:301-302): a partial
+  // per CTA, summed in rank order by the first
   double en = 0.0;
-  for (int e = e0 + tid; e < e1; e += nt) {
+  for (int e = e0 + gtid; e < e1; e += gnt) {
     const double sa = s[q.pa[e]], sb = s[q.pb[e]];
     const double ra = sa - sb - w.ba[e];
     const double rb = sb - sa - w.bb[e];
@@ -1538,10 +1612,20 @@ __device__ void fused_iteration(
     en += ra * (w.wa[e] * ra) + rb * (w.wb[e] * rb);
   }
   en = block_sum(en, red);
-  // K7b: deferred z += s[label]
-  for (int c = c0 + tid; c < c1; c += nt) zshift[c] += s[c];
+  if (CL > 1) {
+    if (tid == 0) w.epart[int64_t(m) * kEChunks + rank] = en;
+    // K7b: deferred z += s[label]
+    for (int c = c0 + gtid; c < c1; c += gnt) zshift[c] += s[c];
+    cl.sync();
+    if (rank == 0 && tid == 0) {
+      en = 0.0;
+      for (int r = 0; r < CL; ++r) en += w.epart[int64_t(m) * kEChunks + r];
+    }
+  } else {
+    for (int c = c0 + tid; c < c1; c += nt) zshift[c] += s[c];
+  }
   // the convergence test of pipeline.py:66-83
-  if (tid == 0) {
+  if (rank == 0 && tid == 0) {
     energy_out[m] = en;
     const double ep = da.e_prev[m];
     const int t = da.t;
@@ -1558,23 +1642,26 @@ __device__ void fused_iteration(
       atomicSub(da.nlive, 1);
     }
   }
-  __syncthreads();
+  cl.sync();  // the live flag, the shifts and the scales before the next iteration
 }
 
 // k outer iterations of each map (a CTA per map, its loop entirely inside the
 // CTA: maps never interact), stopping at the map's convergence.
 template <int CONN, int MODEL>
 __global__ void __launch_bounds__(kFusedThreads) scale_fused_kernel(
-    Quot q, StepWs w, const double* __restrict__ z, const double* __restrict__ zs,
+    Quot q, StepWs w, const double* __restrict__ z, const double* zs,
     const int32_t* __restrict__ zlab, const double* __restrict__ omega_a,
     const double* __restrict__ omega_b, const double* __restrict__ gamma,
     const uint8_t* __restrict__ eflags, int H, int W, int64_t npix, WeightArgs wp, int t0,
     int k, int alignment_iters, double rtol, int cg_max_iters, double* __restrict__ s,
     double* __restrict__ residual, double* __restrict__ weights,
     double* __restrict__ energy_out, int32_t* __restrict__ ok_out,
-    double* __restrict__ zshift, DecideArgs da) {
+    double* zshift, DecideArgs da) {
+  // zs and zshift are the same array (the shifts are read by the weights and
+  // advanced at the end of every iteration): neither is __restrict__, so the
+  // reads stay on the coherent path
   __shared__ double red[32];
-  const int m = w.mp.active[blockIdx.x];
+  const int m = w.mp.active[blockIdx.x / cg::this_cluster().num_blocks()];
   for (int i = 0; i < k; ++i) {
     if (!da.live[m]) return;  // uniform: written by thread 0 before the previous barrier
     WeightArgs wi = wp;
@@ -1635,15 +1722,34 @@ extern "C" int ni_scale_step_fused(const void* quot_ws, size_t quot_bytes, int K
   DecideArgs da{t + 1, max_iters, alignment_iters, delta_e_max, e_prev, live, iters,
                 e_hist, ok_hist, hist_stride, nlive};
   const int64_t npix = int64_t(B) * H * W;
+  // a thread-block cluster per map: kFusedCluster CTAs on as many SMs share the
+  // map's edge loops and segmented sums, with cluster barriers between the
+  // stages (no grid barrier: maps never interact)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(nact) * kFusedCluster);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kFusedCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const double* zs_arg = zshift;
 #define NI_FUSED(CN, MD)                                                                       \
-  NI_COUNT_LAUNCH(), scale_fused_kernel<CN, MD><<<nact, kFusedThreads, 0, s>>>(                 \
-                         q, w, z, zshift, labels, omega_a, omega_b, gamma, eflags, H, W, npix, \
-                         wp, t, k_iters, alignment_iters, cg_tol, cg_max_iters, scales,        \
-                         residual, weights, energy_out, cg_ok_out, zshift, da)
+  launched = cudaLaunchKernelEx(&cfg, scale_fused_kernel<CN, MD>, q, w, z, zs_arg, labels,     \
+                                omega_a, omega_b, gamma, eflags, H, W, npix, wp, t, k_iters,   \
+                                alignment_iters, cg_tol, cg_max_iters, scales, residual,       \
+                                weights, energy_out, cg_ok_out, zshift, da)
+  cudaError_t launched;
+  NI_COUNT_LAUNCH();
   if (connectivity == 8) NI_FUSED(8, 0);
   else if (model == 0) NI_FUSED(4, 0);
   else NI_FUSED(4, 1);
 #undef NI_FUSED
+  NI_CUDA_TRY(launched);
   NI_LAUNCH_CHECK();
   return NI_OK;
 }

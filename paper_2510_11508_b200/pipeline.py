@@ -760,7 +760,11 @@ def run_pipeline_batch(
     return out
 
 
-_D2H_CTAS = 16  # read-back kernel CTAs (512 threads each; PCIe-bound); 0: copy engine
+_D2H_CTAS = 2  # read-back kernel CTAs (512 threads each); 0: copy engine.  Measured on the 64-map
+# C5 stream (scripts/e2e_ab.py): 1-3 CTAs 65.5-67 ms per step, 16 CTAs 71-74 ms (a wide read-back
+# kernel slows the concurrent compute kernels), copy engine 83 ms; 2 CTAs still finish the
+# 537 MB well inside one step.
+_D2H_PRIORITY = -1  # stream priority of the read-back kernel
 
 
 def run_pipeline_stream(
@@ -796,7 +800,7 @@ def run_pipeline_stream(
     # device->host queue that every small control read (.cpu()) of the next
     # batch's pipeline waits in.  High priority: its few CTAs are scheduled
     # ahead of the compute grids' pending CTAs.
-    d2h = torch.cuda.Stream(dev, priority=-1)
+    d2h = torch.cuda.Stream(dev, priority=_D2H_PRIORITY)
     lib = _lib.load()
     it = iter(batches)
 

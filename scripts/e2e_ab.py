@@ -1,7 +1,8 @@
 """e2e stream A/B: ms per step of run_pipeline_stream over the 64-map C5 batch
-for several read-back CTA counts (0 = copy-engine read-back), interleaved.
+for several read-back CTA counts (0 = copy-engine read-back) and stream
+priorities, interleaved.
 
-    python scripts/e2e_ab.py [ctas ...]
+    python scripts/e2e_ab.py [ctas[:priority] ...]
 """
 import sys
 import time
@@ -13,7 +14,7 @@ sys.path.insert(0, ".")
 import paper_2510_11508_b200 as nb  # noqa: E402
 from paper_2510_11508_b200 import pipeline, scenes  # noqa: E402
 
-variants = [int(x) for x in sys.argv[1:]] or [32, 16]
+variants = [tuple(int(y) for y in (x.split(":") + ["-1"])[:2]) for x in sys.argv[1:]] or [(16, -1)]
 maps = [scenes.config5_map(i) for i in range(64)]
 n = torch.from_numpy(np.stack([m.normals for m in maps]).astype(np.float32)).pin_memory()
 k = torch.from_numpy(np.stack([m.mask for m in maps])).pin_memory()
@@ -28,11 +29,12 @@ def run(steps):
 
 
 run(3)
-for rep in range(2):
-    for v in variants:
+for rep in range(3):
+    for v, prio in variants:
         pipeline._D2H_CTAS = v
+        pipeline._D2H_PRIORITY = prio
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         run(10)
         torch.cuda.synchronize()
-        print(f"rep {rep} ctas {v}: {1e3 * (time.perf_counter() - t0) / 10:.2f} ms/step", flush=True)
+        print(f"rep {rep} ctas {v} priority {prio}: {1e3 * (time.perf_counter() - t0) / 10:.2f} ms/step", flush=True)

@@ -60,6 +60,16 @@ for s, e, name in iv[1:]:
 busy += cur_e - cur_s
 print(f"span {span / 1e3:.2f} ms, busy {busy / 1e3:.2f} ms, idle {(span - busy) / 1e3:.2f} ms, "
       f"{len(iv)} device events, {len(gaps)} gaps")
+# copies: how many, and how long they take (control reads / uploads queue behind
+# bulk transfers on the same link direction)
+import collections  # noqa: E402
+cp = collections.defaultdict(lambda: [0, 0.0])
+for s_, e_, name in iv:
+    if name.startswith("Mem"):
+        cp[name][0] += 1
+        cp[name][1] += e_ - s_
+for name, (cnt, tot_us) in sorted(cp.items(), key=lambda kv: -kv[1][1]):
+    print(f"{name:45s} {cnt:5d} x {tot_us / max(cnt, 1):8.1f} us = {tot_us / 1e3:7.2f} ms")
 gaps.sort(reverse=True)
 tot = sum(g[0] for g in gaps)
 print(f"gaps > 50 us: {sum(g[0] for g in gaps if g[0] > 50) / 1e3:.2f} ms; "
