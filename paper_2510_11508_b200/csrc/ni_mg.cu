@@ -1013,6 +1013,112 @@ __global__ void __launch_bounds__(256) up_kernel(int n, const int32_t* __restric
   }
 }
 
+// ---- the small levels in one launch
+//
+// Below a few thousand unknowns a level's kernels are pure launch latency
+// (~3 us each, four per level and V-cycle).  One 1024-thread CTA runs every
+// level from the first one with <= kTailMaxN unknowns down to the coarsest and
+// back up: the same per-unknown arithmetic as down_kernel / up_kernel (so the
+// result does not depend on which levels the tail covers: a batch and its
+// single maps stay bit-identical), block barriers instead of launches.
+// Unknowns of converged units are not skipped here (their values never reach a
+// live unit and stay finite).  The level arrays are written and re-read inside
+// the kernel, so nothing here is __restrict__ / read through the non-coherent
+// path.
+constexpr int kTailThreads = 1024;
+#ifndef NI_MG_TAIL_MAX
+#define NI_MG_TAIL_MAX 8192
+#endif
+constexpr int kTailMaxN = NI_MG_TAIL_MAX;
+constexpr int kTailMaxLevels = 16;
+
+struct TailLevel {
+  int n;
+  const Link8* lnk;
+  const float* dinv;
+  const int32_t* child;  // [4][n]
+  float *b, *x1, *x2, *e;
+};
+
+struct TailArgs {
+  int nlev;            // levels in the tail: lv[1..nlev] = levels T..L
+  int nu2;             // 2: two sweeps before / after the coarse correction
+  TailLevel lv[kTailMaxLevels + 1];  // lv[0] = level T - 1 (x2 and its pre-smoothed state only)
+  const float* xpre0;  // pre-smoothed state of level T - 1
+};
+
+__device__ __forceinline__ float tail_link_sum(const TailLevel& V, int i, float xi,
+                                               const float* x) {
+  float acc = 0.f;
+  const Link8 l = V.lnk[i];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (l.rel[k] == kNoLink) continue;
+    acc += __bfloat162float(l.c[k]) * (xi - x[i + l.rel[k]]);
+  }
+  return acc;
+}
+
+// xs + OM dinv (b - A xs) at unknown i (up_kernel's expression)
+__device__ __forceinline__ float tail_sweep(const TailLevel& V, int i, const float* xs) {
+  const float di = V.dinv[i];
+  float e = 0.f;
+  if (di != 0.f) {
+    const float xi = xs[i];
+    e = xi + OM * di * (V.b[i] - tail_link_sum(V, i, xi, xs));
+  }
+  return e;
+}
+
+__global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs a) {
+  const int tid = threadIdx.x;
+  for (int k = 1; k <= a.nlev; ++k) {  // down
+    const TailLevel& V = a.lv[k];
+    const float* xp = V.x1;
+    if (a.nu2 == 2) {
+      for (int i = tid; i < V.n; i += kTailThreads) V.e[i] = tail_sweep(V, i, V.x1);
+      __syncthreads();
+      xp = V.e;
+    }
+    if (k < a.nlev) {
+      const TailLevel& N = a.lv[k + 1];
+      for (int i = tid; i < N.n; i += kTailThreads) {
+        float sum = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int32_t c = N.child[int64_t(q) * N.n + i];
+          if (c < 0) continue;
+          const float xc = xp[c];
+          sum += V.b[c] - tail_link_sum(V, c, xc, xp);
+        }
+        N.b[i] = sum;
+        N.x1[i] = OM * N.dinv[i] * sum;
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = a.nlev; k >= 1; --k) {  // up
+    const TailLevel& V = a.lv[k];
+    const float* xs = k == a.nlev ? (a.nu2 == 2 ? V.e : V.x1) : V.x2;
+    if (a.nu2 == 2) {
+      for (int i = tid; i < V.n; i += kTailThreads) V.x1[i] = tail_sweep(V, i, xs);
+      __syncthreads();
+      xs = V.x1;
+    }
+    const TailLevel& P = a.lv[k - 1];
+    const float* xpc = k == 1 ? a.xpre0 : (a.nu2 == 2 ? P.e : P.x1);
+    for (int i = tid; i < V.n; i += kTailThreads) {
+      const float e = tail_sweep(V, i, xs);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int32_t c = V.child[int64_t(q) * V.n + i];
+        if (c >= 0) P.x2[c] = xpc[c] + OC * e;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- fine passes
 //
 // A CTA owns one 64 x 32 tile.  The planes it stencils are staged in shared
@@ -2848,6 +2954,107 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   TmaMaps tm;
   memset(&tm, 0, sizeof(tm));
   NI_TRY(make_tma_maps(tm, g, f));
+  // ---- the coarse part of one V-cycle (levels 1..L), between pass A (which
+  // leaves b and x1 = OM dinv b on level 1) and pass B (which prolongs e of
+  // level 1).  Levels >= 2 run kCoarseSweeps damped-Jacobi sweeps before and
+  // after their coarse correction instead of one: they hold 1/16, 1/64, ... of
+  // the pixels, so the extra sweeps are cheap, and the PCG needs a quarter
+  // fewer V-cycles (scripts/mg_blueprint.py, MG_NU=2 MG_NU_FROM=2: 12.5 -> 9.2;
+  // a third sweep gains nothing more).  Any number of sweeps keeps the
+  // preconditioner symmetric positive definite.  (A W-cycle over levels 2-3
+  // needed 8.0 but its two-visit operator 2M - MAM is indefinite wherever the
+  // 1.9x over-corrected M has an eigenvalue of AM above 2: on the 4096^2 map
+  // the PCG then broke down and left a 6e-3 error in the fill.)
+  int nu2 = 2;
+  {
+    const char* a = NI_ENV_ONCE("NI_MG_COARSE_SWEEPS");
+    if (a) nu2 = atoi(a) >= 2 ? 2 : 1;
+  }
+  // the pre-smoothed state of level l: x1 after one sweep, e (free on levels
+  // >= 2) after two
+  auto xpre = [&](int l) -> float* { return (l >= 2 && nu2 == 2) ? lev[l].e : lev[l].x1; };
+  auto launch_down = [&](int l) -> int {  // b, x1 of level l + 1 from level l
+    const Level& C = lev[l];
+    const Level& N = lev[l + 1];
+    if (C.cmp)
+      NI_COUNT_LAUNCH(), down_kernel<true><<<grid_for(N.n), 256, 0, st>>>(
+                             N.n, N.child, C.n, C.nbr, C.cond, C.lnk, xpre(l), C.b, N.dinv, N.b,
+                             N.x1, N.unit, ustatus);
+    else
+      NI_COUNT_LAUNCH(), down_kernel<false><<<grid_for(N.n), 256, 0, st>>>(
+                             N.n, N.child, C.n, C.nbr, C.cond, C.lnk, xpre(l), C.b, N.dinv, N.b,
+                             N.x1, N.unit, ustatus);
+    NI_LAUNCH_CHECK();
+    return NI_OK;
+  };
+  // one damped-Jacobi sweep of level l from xs: out = xs + OM dinv (b - A xs);
+  // scatter: hand x2 = xpre + OC out to the children instead of storing it
+  auto launch_sweep = [&](int l, const float* xs, float* out, bool scatter) -> int {
+    const Level& C = lev[l];
+#define NI_MG_UP(SC, CM, EOUT, CH, X1C, X2C, NC)                                               \
+  NI_COUNT_LAUNCH(), up_kernel<SC, CM><<<grid_for(C.n), 256, 0, st>>>(                           \
+                         C.n, C.nbr, C.cond, C.lnk, C.dinv, C.b, xs, EOUT, CH, X1C, X2C, NC, C.unit, \
+                         ustatus)
+    if (scatter) {
+      if (C.cmp) NI_MG_UP(true, true, nullptr, C.child, xpre(l - 1), lev[l - 1].x2, lev[l - 1].n);
+      else NI_MG_UP(true, false, nullptr, C.child, xpre(l - 1), lev[l - 1].x2, lev[l - 1].n);
+    } else {
+      if (C.cmp) NI_MG_UP(false, true, out, nullptr, nullptr, nullptr, 0);
+      else NI_MG_UP(false, false, out, nullptr, nullptr, nullptr, 0);
+    }
+#undef NI_MG_UP
+    NI_LAUNCH_CHECK();
+    return NI_OK;
+  };
+  // the first level of the single-launch tail (L + 1: none)
+  int T = L + 1;
+  TailArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  {
+    const char* a = NI_ENV_ONCE("NI_MG_TAIL");
+    const bool on = !a || atoi(a) != 0;
+    int t0 = 2;
+    while (t0 <= L && lev[t0].n > kTailMaxN) ++t0;
+    bool ok = on && t0 <= L && L - t0 + 1 <= kTailMaxLevels;
+    for (int l = t0; ok && l <= L; ++l) ok = lev[l].cmp;
+    if (ok) {
+      T = t0;
+      ta.nlev = L - T + 1;
+      ta.nu2 = nu2;
+      for (int l = T - 1; l <= L; ++l) {
+        TailLevel& V = ta.lv[l - (T - 1)];
+        V.n = lev[l].n;
+        V.lnk = lev[l].lnk;
+        V.dinv = lev[l].dinv;
+        V.child = lev[l].child;
+        V.b = lev[l].b;
+        V.x1 = lev[l].x1;
+        V.x2 = lev[l].x2;
+        V.e = lev[l].e;
+      }
+      ta.xpre0 = xpre(T - 1);
+    }
+  }
+  auto coarse_cycle = [&]() -> int {
+    for (int l = 1; l < T; ++l) {
+      if (l >= 2 && nu2 == 2) NI_TRY(launch_sweep(l, lev[l].x1, lev[l].e, false));  // second pre-sweep
+      if (l < L) NI_TRY(launch_down(l));
+    }
+    if (T <= L) {  // levels T..L and back, leaving x2 of level T - 1
+      NI_COUNT_LAUNCH(), tail_kernel<<<1, kTailThreads, 0, st>>>(ta);
+      NI_LAUNCH_CHECK();
+    }
+    for (int l = std::min(L, T - 1); l >= 2; --l) {
+      const float* xs = l == L ? xpre(l) : lev[l].x2;
+      if (nu2 == 2) {  // first post-sweep into x1 (free once x2 exists)
+        NI_TRY(launch_sweep(l, xs, lev[l].x1, false));
+        xs = lev[l].x1;
+      }
+      NI_TRY(launch_sweep(l, xs, nullptr, true));
+    }
+    NI_TRY(launch_sweep(1, L == 1 ? lev[1].x1 : lev[1].x2, lev[1].e, false));
+    return NI_OK;
+  };
   NI_CUDA_TRY(cudaEventRecord(e0, st));
   if (NA > 0) {
     int32_t* hslot = g_events.host;
@@ -2893,36 +3100,7 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
       fa.par ^= 1;  // pass B and the next pass A read the r / s pass A wrote
       NI_LAUNCH_CHECK();
       if (prof) NI_CUDA_TRY(cudaEventRecord(evs[1], st));
-      for (int l = 1; l < L; ++l) {
-        const Level& C = lev[l];
-        const Level& N = lev[l + 1];
-        if (C.cmp)
-          NI_COUNT_LAUNCH(), down_kernel<true><<<grid_for(N.n), 256, 0, st>>>(
-                                 N.n, N.child, C.n, C.nbr, C.cond, C.lnk, C.x1, C.b, N.dinv, N.b,
-                                 N.x1, N.unit, ustatus);
-        else
-          NI_COUNT_LAUNCH(), down_kernel<false><<<grid_for(N.n), 256, 0, st>>>(
-                                 N.n, N.child, C.n, C.nbr, C.cond, C.lnk, C.x1, C.b, N.dinv, N.b,
-                                 N.x1, N.unit, ustatus);
-        NI_LAUNCH_CHECK();
-      }
-      for (int l = L; l >= 1; --l) {
-        const Level& C = lev[l];
-        const float* xs = l == L ? C.x1 : C.x2;
-#define NI_MG_UP(SC, CM, EOUT, CH, X1C, X2C, NC)                                               \
-  NI_COUNT_LAUNCH(), up_kernel<SC, CM><<<grid_for(C.n), 256, 0, st>>>(                           \
-                         C.n, C.nbr, C.cond, C.lnk, C.dinv, C.b, xs, EOUT, CH, X1C, X2C, NC, C.unit, \
-                         ustatus)
-        if (l >= 2) {
-          if (C.cmp) NI_MG_UP(true, true, nullptr, C.child, lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
-          else NI_MG_UP(true, false, nullptr, C.child, lev[l - 1].x1, lev[l - 1].x2, lev[l - 1].n);
-        } else {
-          if (C.cmp) NI_MG_UP(false, true, C.e, nullptr, nullptr, nullptr, 0);
-          else NI_MG_UP(false, false, C.e, nullptr, nullptr, nullptr, 0);
-        }
-#undef NI_MG_UP
-        NI_LAUNCH_CHECK();
-      }
+      NI_TRY(coarse_cycle());
       if (prof) NI_CUDA_TRY(cudaEventRecord(evs[2], st));
 #if NI_MG_V2 && NI_MG_B_V2
       if (connectivity == 8) NI_COUNT_LAUNCH(), pass_b2_kernel<8><<<NA, NT, kPassB2Smem, st>>>(fa, tm);

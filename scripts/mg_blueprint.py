@@ -93,13 +93,17 @@ def apply_A(lev, x):
 
 OVERCORRECT = float(__import__("os").environ.get("MG_OC", "1.0"))  # coarse-correction scale
 NU_COARSE = int(__import__("os").environ.get("MG_NU", "1"))  # smoothing sweeps below level 0
+NU_FROM = int(__import__("os").environ.get("MG_NU_FROM", "1"))  # ... on levels >= this
+GAMMA = int(__import__("os").environ.get("MG_GAMMA", "1"))  # cycle index (2: W-cycle) ...
+GAMMA_FROM = int(__import__("os").environ.get("MG_GAMMA_FROM", "1"))  # ... for recursions into levels >= this
+GAMMA_TO = int(__import__("os").environ.get("MG_GAMMA_TO", "99"))  # ... and <= this
 
 
 def vcycle(levels, parents, b, l=0, omega=0.8, coarse_sweeps=20):
     lev = levels[l]
     d = lev["cond"].sum(1)
     dinv = np.where(d > 0, 1.0 / np.where(d > 0, d, 1.0), 0.0)
-    nu = 1 if l == 0 else NU_COARSE
+    nu = NU_COARSE if l >= NU_FROM else 1
     x = omega * dinv * b
     if l == len(levels) - 1:
         for _ in range(coarse_sweeps - 1):
@@ -109,7 +113,12 @@ def vcycle(levels, parents, b, l=0, omega=0.8, coarse_sweeps=20):
         x = x + omega * dinv * (b - apply_A(lev, x))
     r = b - apply_A(lev, x)
     bc = np.bincount(parents[l], weights=r, minlength=len(levels[l + 1]["lab"]))
-    x = x + OVERCORRECT * vcycle(levels, parents, bc, l + 1, omega, coarse_sweeps)[parents[l]]
+    ec = vcycle(levels, parents, bc, l + 1, omega, coarse_sweeps)
+    if GAMMA > 1 and GAMMA_FROM <= l + 1 <= GAMMA_TO and l + 1 < len(levels) - 1:
+        for _ in range(GAMMA - 1):  # second visit on the coarse residual (symmetric: 2M - MAM)
+            ec = ec + vcycle(levels, parents, bc - apply_A(levels[l + 1], ec), l + 1, omega,
+                             coarse_sweeps)
+    x = x + OVERCORRECT * ec[parents[l]]
     for _ in range(nu):
         x = x + omega * dinv * (b - apply_A(lev, x))
     return x
@@ -164,6 +173,10 @@ if __name__ == "__main__":
         levels.append(c)
     print("unknowns per level:", [len(l_["lab"]) for l_ in levels])
     x, iters = pcg_per_component(levels, parents, b, comp, coarse_sweeps=sweeps)
+    print("MG-PCG iterations per component: max", int(iters.max()), "px-weighted mean",
+          round(float((iters[comp]).mean()), 2))
+    if __import__("os").environ.get("MG_NOCG"):
+        sys.exit(0)
     # the same components with scipy-semantics CG (the current GPU fill)
     cg_it = []
     for c in np.argsort(-np.bincount(comp))[:8]:
