@@ -587,16 +587,34 @@ __device__ __forceinline__ double warp_cg(int lane, bool own, int deg, int jmax,
   const double atol = rtol * bnrm;
   double rho_prev = 0.0;
   ok = 0;
+  // the first four row entries in registers: their shuffles of p are
+  // independent, so they issue back to back instead of one shared-memory
+  // round trip + shuffle per entry (the iteration is one long latency chain)
+  int col4[4];
+  double cnd4[4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    col4[jj] = jj < deg ? int(s_col[jj][lane]) : lane;
+    cnd4[jj] = jj < deg ? s_cnd[jj][lane] : 0.0;
+  }
   for (int it = 0; it < maxiter; ++it) {
+    const double rho = rr;
+    // (the division is issued beside the square root of the stop test)
+    const double beta = it == 0 ? 0.0 : rho / rho_prev;
     if (sqrt(rr) < atol) {
       ok = 1;
       break;
     }
-    const double rho = rr;
-    const double beta = it == 0 ? 0.0 : rho / rho_prev;
     pv = r + beta * pv;
     double aq = dg * pv;
-    for (int jj = 0; jj < jmax; ++jj) {
+    double pn4[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (jj < jmax) pn4[jj] = __shfl_sync(0xffffffffu, pv, col4[jj]);  // jmax is warp-uniform
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (jj < deg) aq -= cnd4[jj] * pn4[jj];
+    for (int jj = 4; jj < jmax; ++jj) {
       const bool has = jj < deg;
       const double pn = __shfl_sync(0xffffffffu, pv, has ? int(s_col[jj][lane]) : lane);
       if (has) aq -= s_cnd[jj][lane] * pn;
@@ -1755,7 +1773,8 @@ extern "C" int ni_scale_step_fused(const void* quot_ws, size_t quot_bytes, int K
 }
 
 extern "C" int ni_scale_fused_limits(int* max_edges, int* max_comps) {
-  if (max_edges) *max_edges = kFusedMaxEdges;
+  const char* ov = NI_ENV_ONCE("NI_FUSED_MAX_EDGES");  // measurement knob
+  if (max_edges) *max_edges = ov ? atoi(ov) : kFusedMaxEdges;
   if (max_comps) *max_comps = kFusedMaxComps;
   return NI_OK;
 }
