@@ -86,8 +86,8 @@ constexpr int NPART = 6;  // per-slot partials: (r,u) (w,u) (r,r) sum u, sum r, 
 #define NI_MG_OMEGA 0.8f
 #endif
 #ifndef NI_MG_OC
-#define NI_MG_OC 1.9f
-#endif
+#define NI_MG_OC 2.0f  // with two sweeps on levels >= 2 (blueprint, three C5 maps: 1.9 9.0-9.4
+#endif                 // iterations per pixel, 2.0 8.2-8.5, 2.1 9.5; GPU C5 step 51.8 -> 50.0 ms)
 constexpr float OM = NI_MG_OMEGA;  // damped-Jacobi weight
 constexpr float OC = NI_MG_OC;     // coarse-correction scale
 
@@ -1564,29 +1564,28 @@ __global__ void __launch_bounds__(NT) pass_b_kernel(const __grid_constant__ Fine
     if (e < BOX2) sX2[e] = OM * sD[e] * sR[e] + OC * ev[q];
   }
   __syncthreads();
-  // post-smoothing on the tile + 1-pixel ring: x3 = x2 + OM dinv (r - A x2)
-  for (int ry = wid; ry < BH1; ry += NT / 32) {
+  // post-smoothing on the tile + 1-pixel ring: x3 = x2 + OM dinv (r - A x2).
+  // The 66 x 34 ring is walked as a flat list (a row-per-warp mapping spent a
+  // third of the stencil's instructions on the two lanes of the 65th / 66th
+  // column: the pass is issue-bound)
+  for (int e = threadIdx.x; e < S3 * BH1; e += NT) {
+    const int ry = e / S3, rx = e - ry * S3;  // pixel (ry - 1, rx - 1) of the tile
+    const int c2 = (ry + 1) * BW + rx - 1 + CX;
+    const uint8_t mk = sM[ry * BWM + rx - 1 + CXM];
+    float v = 0.f;
+    if (mk) {
+      v = sX2[c2];
+      const float hi = sH[c2];
+      float acc = 0.f;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int rx = lane + 32 * k;  // pixel (ry - 1, rx - 1) of the tile
-      if (rx >= TX + 2) continue;
-      const int c2 = (ry + 1) * BW + rx - 1 + CX;
-      const uint8_t mk = sM[ry * BWM + rx - 1 + CXM];
-      float v = 0.f;
-      if (mk) {
-        v = sX2[c2];
-        const float hi = sH[c2];
-        float acc = 0.f;
-#pragma unroll
-        for (int bit = 0; bit < 8; ++bit) {
-          if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
-          const int jn = c2 + nb_off<CONN>(bit, BW);
-          acc += (hi + sH[jn]) * (v - sX2[jn]);
-        }
-        v += OM * sD[c2] * (sR[c2] - acc);
+      for (int bit = 0; bit < 8; ++bit) {
+        if ((bit & 3) >= KF || !((mk >> bit) & 1)) continue;
+        const int jn = c2 + nb_off<CONN>(bit, BW);
+        acc += (hi + sH[jn]) * (v - sX2[jn]);
       }
-      sX3[ry * S3 + rx] = v;
+      v += OM * sD[c2] * (sR[c2] - acc);
     }
+    sX3[e] = v;
   }
   __syncthreads();
   // u = x3, w = A u on the tile; per-thread partial dots for the tile's

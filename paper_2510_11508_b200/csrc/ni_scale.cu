@@ -1422,7 +1422,8 @@ extern "C" int ni_scale_step(const void* quot_ws, size_t quot_bytes, int K, int 
 constexpr int kFusedThreads = 512;
 #ifndef NI_FUSED_MAX_EDGES
 #define NI_FUSED_MAX_EDGES (1 << 14)  // measured: 64 C5 maps (~50 k edges each) run faster as
-#endif                                // the multi-kernel step spread over every SM
+#endif                                // the multi-kernel step spread over every SM (51.9 ms per
+                                      // step against 53.5 ms with a cluster per map)
 constexpr int kFusedMaxEdges = NI_FUSED_MAX_EDGES;
 constexpr int kFusedMaxComps = 1024;
 #ifndef NI_FUSED_CLUSTER
