@@ -2703,6 +2703,35 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
   else NI_MG_PREP(4, 1);
 #undef NI_MG_PREP
   NI_LAUNCH_CHECK();
+  // Host-only set-up of the fine passes (opt-in shared-memory sizes once per
+  // process, the 16 tensor maps of this call's planes: ~0.3 ms of driver
+  // calls), done here while the GPU runs prep_kernel instead of between the
+  // hierarchy build and the first pass A.
+  {
+    static std::atomic<bool> attrs_set{false};
+    if (!attrs_set.load(std::memory_order_acquire)) {
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassBSmem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassBSmem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassASmem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassASmem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassB2Smem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassB2Smem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassA2Smem)));
+      NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kPassA2Smem)));
+      attrs_set.store(true, std::memory_order_release);
+    }
+  }
+  TmaMaps tm;
+  memset(&tm, 0, sizeof(tm));
+  NI_TRY(make_tma_maps(tm, g, f));
   int32_t hc[16];
   NI_CUDA_TRY(cudaMemcpyAsync(hc, f.counters, sizeof(hc), cudaMemcpyDeviceToHost, st));
   NI_CUDA_TRY(cudaStreamSynchronize(st));
@@ -2934,25 +2963,6 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
     sa.trace_unit = tr ? atoi(tr) : -1;
   }
   int vcycles = 0;
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassBSmem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassBSmem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassASmem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassASmem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassB2Smem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_b2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassB2Smem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassA2Smem)));
-  NI_CUDA_TRY(cudaFuncSetAttribute(pass_a2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kPassA2Smem)));
-  TmaMaps tm;
-  memset(&tm, 0, sizeof(tm));
-  NI_TRY(make_tma_maps(tm, g, f));
   // ---- the coarse part of one V-cycle (levels 1..L), between pass A (which
   // leaves b and x1 = OM dinv b on level 1) and pass B (which prolongs e of
   // level 1).  Levels >= 2 run kCoarseSweeps damped-Jacobi sweeps before and

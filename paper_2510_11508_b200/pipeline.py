@@ -524,7 +524,11 @@ class _DeviceLoop:
         self.wall = _ms(start) / max(t - self.t0, 1)
         return t
 
-    def collect(self, loop, active, t, e_prev, energies, records, warnings, iters) -> list:
+    def collect(self, loop, active, t, e_prev, energies, records, warnings, iters):
+        """Read the chunk's outcome back.  Returns (still, finish): the maps still
+        in the loop, and a callable that writes the chunk's records -- ~0.5 ms of
+        host work for 64 maps x 37 iterations, which the caller runs after it has
+        enqueued the GPU work that does not depend on it."""
         t0 = self.t0
         host = torch.cat([self.e_hist[:, t0:t].reshape(-1),
                           self.ok_hist[:, t0:t].reshape(-1).to(torch.float64),
@@ -539,20 +543,26 @@ class _DeviceLoop:
         still = []
         for m in active:
             m = int(m)
-            last = int(conv[m]) if not live[m] else t
-            for tt in range(t0 + 1, last + 1):
-                e_t = float(eh[m, tt - 1 - t0])
-                if not oh[m, tt - 1 - t0]:
-                    warnings[m].append(f"iteration {tt - 1}: cg hit iteration cap")
-                energies[m].append(e_t)
-                records[m].append({"t": tt, "E_t": e_t, "component_count": int(loop.count[m]),
-                                   "merge_performed": False, "wall_ms": self.wall})
             e_prev[m] = float(ep[m])
             if live[m]:
                 still.append(m)
             else:
-                iters[m] = last
-        return still
+                iters[m] = int(conv[m])
+        wall, counts = self.wall, [int(c) for c in loop.count]
+
+        def finish():
+            for m in active:
+                m = int(m)
+                last = int(conv[m]) if not live[m] else t
+                for tt in range(t0 + 1, last + 1):
+                    e_t = float(eh[m, tt - 1 - t0])
+                    if not oh[m, tt - 1 - t0]:
+                        warnings[m].append(f"iteration {tt - 1}: cg hit iteration cap")
+                    energies[m].append(e_t)
+                    records[m].append({"t": tt, "E_t": e_t, "component_count": counts[m],
+                                       "merge_performed": False, "wall_ms": wall})
+
+        return still, finish
 
     def sync_prev(self, e_prev: np.ndarray):
         self.e_prev.copy_(torch.from_numpy(np.ascontiguousarray(e_prev, dtype=np.float64)))
@@ -666,6 +676,7 @@ def run_pipeline_batch(
     version = np.zeros(B, dtype=np.int64)
     hasher = None
     chunk = _DeviceLoop(g, settings)
+    deferred = []
     t = 0
     while len(active):
         # iterations that cannot merge run back to back with the convergence
@@ -674,8 +685,13 @@ def run_pipeline_batch(
         if k >= 2:
             chunk.sync_prev(e_prev)
             t = chunk.run(loop, z, t, k, active)
-            still = chunk.collect(loop, active, t, e_prev, energies, records, warnings, iters)
+            still, finish = chunk.collect(loop, active, t, e_prev, energies, records, warnings,
+                                          iters)
             active = np.array(still, dtype=np.int32)
+            if len(active):
+                finish()
+            else:  # the loop is over: the records wait until the gauge is enqueued
+                deferred.append(finish)
             continue
         it_start = time.perf_counter()
         residual, wts = loop.step(z, t, active)
@@ -748,6 +764,8 @@ def run_pipeline_batch(
     ws = _ws(_lib.size_query(lib.ni_gauge_workspace_size, g.B, g.H, g.W), g.dev)
     _lib.check(lib.ni_gauge(_ptr(z), _ptr(valid), g.B, g.H, g.W, C.c_double(target), C.c_void_p(0),
                             _ptr(ws), ws.numel(), g.s()), "gauge")
+    for finish in deferred:
+        finish()
     out = []
     for m in range(B):
         sl = slice(m * g.hw, (m + 1) * g.hw)
