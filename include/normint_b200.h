@@ -321,6 +321,12 @@ int ni_gauge(double* z, const uint8_t* valid, int B, int H, int W, double target
  * pointers differ in 16-byte alignment. */
 int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, int ctas, ni_stream_t stream);
 
+/* The upload twin of ni_copy_to_host: `ctas` CTAs read pinned (mapped) host
+ * memory and store `bytes` bytes into device memory `dst` on `stream`
+ * (run_pipeline_stream's upload of the next batch; no reference counterpart).
+ * Same argument rules. */
+int ni_copy_from_host(void* dst, const void* host_src, size_t bytes, int ctas, ni_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

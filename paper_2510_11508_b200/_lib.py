@@ -82,6 +82,7 @@ SIGNATURES = {
     "ni_gauge_workspace_size": ([_I, _I, _I, _PSZ], _I),
     "ni_gauge": ([_P, _P, _I, _I, _I, _D, _P, _P, _SZ, _P], _I),
     "ni_copy_to_host": ([_P, _P, _SZ, _I, _P], _I),
+    "ni_copy_from_host": ([_P, _P, _SZ, _I, _P], _I),
 }
 
 _lib = None

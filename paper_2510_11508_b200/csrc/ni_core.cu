@@ -114,26 +114,30 @@ __global__ void d2h_mapped_tail_kernel(const uint8_t* __restrict__ src, uint8_t*
 }
 }  // namespace ni
 
-extern "C" int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, int ctas,
-                               ni_stream_t stream) {
-  NI_CHECK_ARG(src && host_dst, "null pointer");
-  NI_CHECK_ARG(ctas > 0 && ctas <= 4096, "ctas must be in 1..4096");
-  if (bytes == 0) return NI_OK;
-  void* dptr = nullptr;
-  // pinned host memory (cudaHostAlloc / cudaHostRegister) is mapped under UVA
-  if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
-    cudaGetLastError();
-    ni::set_error("ni_copy_to_host: destination is not pinned (mapped) host memory");
+// one implementation for both directions: `host` is the pinned (mapped) side
+static int mapped_copy(const void* dev, void* host, size_t bytes, int ctas, ni_stream_t stream,
+                       bool to_host, const char* who) {
+  if (!dev || !host) {
+    ni::set_error("invalid argument: null pointer");
     return NI_ERR_INVALID_ARG;
   }
-  NI_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == (reinterpret_cast<uintptr_t>(dptr) & 15),
+  NI_CHECK_ARG(ctas > 0 && ctas <= 4096, "ctas must be in 1..4096");
+  if (bytes == 0) return NI_OK;
+  void* hptr = nullptr;
+  // pinned host memory (cudaHostAlloc / cudaHostRegister) is mapped under UVA
+  if (cudaHostGetDevicePointer(&hptr, host, 0) != cudaSuccess || !hptr) {
+    cudaGetLastError();
+    ni::set_error("%s: the host buffer is not pinned (mapped) host memory", who);
+    return NI_ERR_INVALID_ARG;
+  }
+  NI_CHECK_ARG((reinterpret_cast<uintptr_t>(dev) & 15) == (reinterpret_cast<uintptr_t>(hptr) & 15),
                "source and destination must share their 16-byte alignment");
   cudaStream_t s = (cudaStream_t)stream;
-  const uintptr_t mis = reinterpret_cast<uintptr_t>(src) & 15;
+  const auto* s8 = static_cast<const uint8_t*>(to_host ? dev : hptr);
+  auto* d8 = static_cast<uint8_t*>(to_host ? hptr : const_cast<void*>(dev));
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(s8) & 15;
   size_t head = mis ? (16 - mis) : 0;
   if (head > bytes) head = bytes;
-  const auto* s8 = static_cast<const uint8_t*>(src);
-  auto* d8 = static_cast<uint8_t*>(dptr);
   if (head) {
     NI_COUNT_LAUNCH(), ni::d2h_mapped_tail_kernel<<<1, 16, 0, s>>>(s8, d8, int64_t(head));
     NI_LAUNCH_CHECK();
@@ -151,4 +155,18 @@ extern "C" int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, in
     NI_LAUNCH_CHECK();
   }
   return NI_OK;
+}
+
+extern "C" int ni_copy_to_host(const void* src, void* host_dst, size_t bytes, int ctas,
+                               ni_stream_t stream) {
+  return mapped_copy(src, host_dst, bytes, ctas, stream, true, "ni_copy_to_host");
+}
+
+// The upload twin: a small kernel reads mapped pinned host memory and stores
+// into device memory (serving stream: the next batch's normals + mask while the
+// current batch computes).
+extern "C" int ni_copy_from_host(void* dst, const void* host_src, size_t bytes, int ctas,
+                                 ni_stream_t stream) {
+  return mapped_copy(dst, const_cast<void*>(host_src), bytes, ctas, stream, false,
+                     "ni_copy_from_host");
 }

@@ -792,6 +792,8 @@ _D2H_CTAS = 2  # read-back kernel CTAs (512 threads each); 0: copy engine.  Meas
 # kernel slows the concurrent compute kernels), copy engine 83 ms; 2 CTAs still finish the
 # 537 MB well inside one step.
 _D2H_PRIORITY = -1  # stream priority of the read-back kernel
+_D2H_CTAS_LAST = 16  # the stream's last batch: nothing computes beside its read-back
+_H2D_CTAS = 0  # upload kernel CTAs (ni_copy_from_host); 0: copy engine
 
 
 def run_pipeline_stream(
@@ -837,8 +839,19 @@ def run_pipeline_stream(
         except StopIteration:
             return None
         with torch.cuda.stream(h2d):
-            n_d = n_h.to(dev, non_blocking=True)
-            m_d = m_h.to(dev, non_blocking=True)
+            if _H2D_CTAS and all(t.is_pinned() and t.is_contiguous() for t in (n_h, m_h)):
+                # upload by a small SM kernel reading the mapped pinned buffers
+                # (ni_copy_from_host), like the read-back
+                n_d = torch.empty(n_h.shape, dtype=n_h.dtype, device=dev)
+                m_d = torch.empty(m_h.shape, dtype=m_h.dtype, device=dev)
+                for d_t, h_t in ((n_d, n_h), (m_d, m_h)):
+                    _lib.check(lib.ni_copy_from_host(
+                        C.c_void_p(d_t.data_ptr()), C.c_void_p(h_t.data_ptr()),
+                        h_t.numel() * h_t.element_size(), _H2D_CTAS,
+                        C.c_void_p(h2d.cuda_stream)), "upload")
+            else:
+                n_d = n_h.to(dev, non_blocking=True)
+                m_d = m_h.to(dev, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(h2d)
         return n_d, m_d, ready
@@ -881,9 +894,10 @@ def _stream_loop(nxt, upload, comp, d2h, lib, dev, intrinsics, theta_c, settings
                 if whole and i:
                     continue
                 nbytes = 8 * hw * (len(vals) if whole else 1)
+                ctas = _D2H_CTAS if nxt is not None else max(_D2H_CTAS, _D2H_CTAS_LAST)
                 _lib.check(lib.ni_copy_to_host(C.c_void_p(v.data_ptr()),
                                                C.c_void_p(out[i].data_ptr()), nbytes,
-                                               _D2H_CTAS, C.c_void_p(d2h.cuda_stream)),
+                                               ctas, C.c_void_p(d2h.cuda_stream)),
                            "read-back")
             fetched = torch.cuda.Event()
             fetched.record(d2h)
