@@ -209,3 +209,46 @@ def test_copy_to_host_kernel_ragged_and_errors():
     dst = torch.empty(1024, dtype=torch.uint8).pin_memory()
     assert lib.ni_copy_to_host(C.c_void_p(src.data_ptr() + 1), C.c_void_p(dst.data_ptr()),
                                64, 4, s) != 0
+
+
+def test_copy_from_host_kernel_and_stream_upload():
+    """ni_copy_from_host (the upload twin of ni_copy_to_host): exact bytes for
+    ragged ranges, a loud error for a pageable source, and a serving stream
+    that uploads with it returns the copy-engine stream's results bit for bit."""
+    import ctypes as C
+
+    import paper_2510_11508_b200 as nb
+    from paper_2510_11508_b200 import _lib, pipeline, scenes
+
+    lib = _lib.load()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    src = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8).pin_memory()
+    for off, n in ((0, 1 << 20), (3, 1000), (16, 17), (5, 7), (0, 0)):
+        dst = torch.full((1 << 20,), 0xAB, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.ni_copy_from_host(C.c_void_p(dst.data_ptr() + off),
+                                         C.c_void_p(src.data_ptr() + off), n, 5, s), "copy")
+        torch.cuda.synchronize()
+        want = torch.full((1 << 20,), 0xAB, dtype=torch.uint8)
+        want[off:off + n] = src[off:off + n]
+        assert torch.equal(dst.cpu(), want), (off, n)
+    pageable = torch.empty(1024, dtype=torch.uint8)
+    dst = torch.empty(1024, dtype=torch.uint8, device="cuda")
+    assert lib.ni_copy_from_host(C.c_void_p(dst.data_ptr()), C.c_void_p(pageable.data_ptr()),
+                                 1024, 4, s) != 0
+    assert b"pinned" in lib.ni_last_error()
+
+    maps = [scenes.config3(40 + i, size=48, cells=5) for i in range(3)]
+    n = torch.from_numpy(np.stack([m.normals for m in maps]).astype(np.float32)).pin_memory()
+    k = torch.from_numpy(np.stack([m.mask for m in maps])).pin_memory()
+    intr = [nb.CameraIntrinsics(*m.intrinsics()) for m in maps]
+    theta = float(np.deg2rad(3.5))
+    outs = {}
+    for ctas in (0, 2):
+        pipeline._H2D_CTAS = ctas
+        try:
+            outs[ctas] = [h.clone() for _, h in nb.run_pipeline_stream(((n, k) for _ in range(2)),
+                                                                       intr, theta)]
+        finally:
+            pipeline._H2D_CTAS = 0
+    for a, b in zip(outs[0], outs[2]):
+        assert torch.equal(a, b)
