@@ -3042,6 +3042,13 @@ extern "C" int ni_fill_mg(const int32_t* labels, int count, const double* omega_
         V.e = lev[l].e;
       }
       ta.xpre0 = xpre(T - 1);
+      // the tail does not skip the unknowns of units that never become active
+      // (zero right-hand side): give them defined values (b, x1, x2, e are
+      // carved back to back)
+      for (int l = T; l <= L; ++l)
+        NI_CUDA_TRY(cudaMemsetAsync(lev[l].b, 0,
+                                    size_t(reinterpret_cast<char*>(lev[l].e + lev[l].n + 1) -
+                                           reinterpret_cast<char*>(lev[l].b)), st));
     }
   }
   auto coarse_cycle = [&]() -> int {
