@@ -66,33 +66,71 @@ __global__ void __launch_bounds__(256) select_hist_kernel(const double* __restri
   }
 }
 
-__global__ void select_pick_kernel(unsigned int* __restrict__ hist, SelState* __restrict__ st,
-                                   int shift, int B) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= B) return;
+// A warp per map: lane l owns bins 8 l .. 8 l + 7 of each histogram; the bin
+// that holds the k-th element is found from a shuffle scan of the lane sums
+// (the same bin and remainder as a serial walk over the 256 bins, which as a
+// thread per map cost ~60 us per pass).
+__global__ void __launch_bounds__(128) select_pick_kernel(unsigned int* __restrict__ hist,
+                                                          SelState* __restrict__ st, int shift,
+                                                          int B) {
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (m >= B) return;  // warp-uniform
   SelState s = st[m];
   unsigned int* h = hist + size_t(m) * 512;
+  unsigned int bins[2][8];
+#pragma unroll
+  for (int sel = 0; sel < 2; ++sel)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bins[sel][j] = h[sel * 256 + lane * 8 + j];
   if (shift == 56) {
     long long n = 0;
-    for (int d = 0; d < 256; ++d) n += h[d];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) n += bins[0][j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
     s.n = n;
     s.k[0] = n > 0 ? (n - 1) / 2 : 0;
     s.k[1] = n / 2;
     s.prefix[0] = s.prefix[1] = 0;
   }
+#pragma unroll
   for (int sel = 0; sel < 2; ++sel) {
+    long long lsum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) lsum += bins[sel][j];
+    long long incl = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long up = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += up;
+    }
+    const long long excl = incl - lsum;
+    const unsigned found = __ballot_sync(0xffffffffu, incl > s.k[sel]);
+    // the serial walk stops at bin 255 at the latest
+    const int fl = found ? __ffs(found) - 1 : 31;
     long long acc = 0;
     int d = 0;
-    for (; d < 255; ++d) {
-      const long long c = h[sel * 256 + d];
-      if (acc + c > s.k[sel]) break;
-      acc += c;
+    if (lane == fl) {
+      acc = excl;
+      int j = 0;
+      for (; j < 7; ++j) {
+        const long long c = bins[sel][j];
+        if (acc + c > s.k[sel]) break;
+        acc += c;
+      }
+      d = lane * 8 + j;  // in the found lane the walk stops by j = 7: incl > k
     }
+    acc = __shfl_sync(0xffffffffu, acc, fl);
+    d = __shfl_sync(0xffffffffu, d, fl);
     s.k[sel] -= acc;
     s.prefix[sel] |= (unsigned long long)d << shift;
   }
-  for (int t = 0; t < 512; ++t) h[t] = 0;
-  st[m] = s;
+#pragma unroll
+  for (int sel = 0; sel < 2; ++sel)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[sel * 256 + lane * 8 + j] = 0;
+  if (lane == 0) st[m] = s;
 }
 
 __global__ void gauge_apply_kernel(double* __restrict__ z, const uint8_t* __restrict__ valid,
@@ -147,7 +185,7 @@ extern "C" int ni_gauge(double* z, const uint8_t* valid, int B, int H, int W, do
   if (bx < 1) bx = 1;
   for (int shift = 56; shift >= 0; shift -= 8) {
     NI_COUNT_LAUNCH(), select_hist_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, shift, st, hist);
-    NI_COUNT_LAUNCH(), select_pick_kernel<<<div_up(B, 64), 64, 0, s>>>(hist, st, shift, B);
+    NI_COUNT_LAUNCH(), select_pick_kernel<<<div_up(B, 4), 128, 0, s>>>(hist, st, shift, B);
   }
   NI_LAUNCH_CHECK();
   NI_COUNT_LAUNCH(), gauge_apply_kernel<<<dim3(bx, B), 256, 0, s>>>(z, valid, per_map, st, target, depth_out, med);

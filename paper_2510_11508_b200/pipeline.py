@@ -256,17 +256,28 @@ def _pair_energy(g: _Grid, co, x: torch.Tensor, wts) -> torch.Tensor:
     return out
 
 
+def _fill_mg_buffers(g: _Grid, count: int):
+    """Output and workspace buffers of ni_fill_mg.  run_pipeline_batch makes
+    them while the coefficients kernel still runs (before its first host
+    read-back), so the allocations are off the GPU's critical path."""
+    z = devmem.empty(g.npix, torch.float64, g.dev)
+    iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
+    nbytes = _lib.size_query(g.lib.ni_fill_mg_workspace_size, g.B, g.H, g.W, g.conn, count)
+    return z, iters, status, nbytes, _ws(nbytes, g.dev)
+
+
 def _fill_mg(g: _Grid, labels, count, co, settings: SolveSettings):
     """The fill at z = 0 (solver.py:195-239) as one batched multigrid-
     preconditioned CG over every solve unit of the batch (ni_fill_mg)."""
     lib = g.lib
     omega_a, omega_b, gamma, eflags = co
-    z = devmem.empty(g.npix, torch.float64, g.dev)
-    iters = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
-    status = torch.zeros(max(count, 1), dtype=torch.int32, device=g.dev)
-    nbytes = _lib.size_query(lib.ni_fill_mg_workspace_size, g.B, g.H, g.W, g.conn, count)
-    for _ in range(3):  # the hierarchy's size depends on the data: retry with what it needs
-        ws = _ws(nbytes, g.dev)
+    pre = getattr(g, "fill_buffers", None)
+    g.fill_buffers = None
+    z, iters, status, nbytes, ws0 = pre if pre is not None else _fill_mg_buffers(g, count)
+    for attempt in range(3):  # the hierarchy's size depends on the data: retry with what it needs
+        ws = ws0 if attempt == 0 else _ws(nbytes, g.dev)
+        ws0 = None
         need = C.c_size_t(0)
         st = lib.ni_fill_mg(_ptr(labels), count, _ptr(omega_a), _ptr(omega_b), _ptr(gamma),
                             _ptr(eflags), g.B, g.H, g.W, g.conn, g.model,
@@ -632,6 +643,8 @@ def run_pipeline_batch(
 
     t0 = time.perf_counter()
     co = _coefficients(g, intr)
+    if _FILL_SOLVER != "cg" and not settings.refill_reweighted:
+        g.fill_buffers = _fill_mg_buffers(g, int(first[B]))  # while the kernel runs
     degen = int(g.stats[5].item())
     coef_ms = _ms(t0)
     for m in range(B):

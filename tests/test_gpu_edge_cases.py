@@ -252,3 +252,33 @@ def test_copy_from_host_kernel_and_stream_upload():
             pipeline._H2D_CTAS = 0
     for a, b in zip(outs[0], outs[2]):
         assert torch.equal(a, b)
+
+
+def test_tail_kernel_matches_per_level_launches():
+    """The single-launch tail of the multigrid fill (the small levels in one
+    CTA) computes exactly what the per-level kernels compute: the same run
+    with NI_MG_TAIL=0 (a process-wide knob, hence the subprocesses) gives a
+    bit-identical log-depth."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import hashlib, numpy as np, paper_2510_11508_b200 as nb\n"
+        "from paper_2510_11508_b200 import scenes\n"
+        "sc = scenes.config4(3, size=160, cells=9)\n"
+        "r = nb.run_pipeline(nb.NormalMap.create(sc.normals, sc.mask),\n"
+        "                    nb.CameraIntrinsics(*sc.intrinsics()), float(np.deg2rad(3.5)),\n"
+        "                    nb.SolveSettings(freq_merging=5))\n"
+        "print('DIGEST', hashlib.sha256(r.log_depth.values.tobytes()).hexdigest(),\n"
+        "      hashlib.sha256(r.filled.values.tobytes()).hexdigest(), r.iterations,\n"
+        "      r.fill_report['mg']['levels'])\n")
+    digests = []
+    for tail in ("1", "0"):
+        env = dict(os.environ, NI_MG_TAIL=tail)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                             text=True, timeout=280)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digests.append([ln for ln in out.stdout.splitlines() if ln.startswith("DIGEST")][0])
+    assert digests[0] == digests[1], digests
+    assert int(digests[0].split()[-1]) >= 3  # the case has levels for the tail to cover
