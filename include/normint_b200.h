@@ -241,10 +241,11 @@ int ni_loop_decide(const double* energy, const int32_t* cg_ok, const int32_t* ac
 
 /* k_iters outer iterations (0-based t .. t + k_iters - 1) for maps with
  * small quotients (<= max_edges inter edges and <= max_comps components,
- * ni_scale_fused_limits), one CTA per map of active[0..nact) (HOST list), in
- * a single launch: each iteration is ni_scale_step with deferred scales
- * (zshift) followed by ni_loop_decide; a map's CTA stops at its convergence.
- * Same arguments and outputs as those calls.  Asynchronous. */
+ * ni_scale_fused_limits), one thread-block cluster (8 CTAs) per map of
+ * active[0..nact) (HOST list), in a single launch: each iteration is
+ * ni_scale_step with deferred scales (zshift) followed by ni_loop_decide; a
+ * map's cluster stops at its convergence.  Same arguments and outputs as
+ * those calls.  Asynchronous. */
 int ni_scale_step_fused(const void* quot_ws, size_t quot_bytes, int K, int count, int B,
                         const int32_t* map_first, const int32_t* map_count,
                         const int32_t* active, int nact, const int32_t* labels,

@@ -819,6 +819,7 @@ _D2H_CTAS = 2  # read-back kernel CTAs (512 threads each); 0: copy engine.  Meas
 _D2H_PRIORITY = -1  # stream priority of the read-back kernel
 _D2H_CTAS_LAST = 16  # the stream's last batch: nothing computes beside its read-back
 _H2D_CTAS = 0  # upload kernel CTAs (ni_copy_from_host); 0: copy engine
+_PIN_ALLOC_MS: list = []  # host time of the last pinned read-back allocations
 
 
 def run_pipeline_stream(
@@ -902,8 +903,11 @@ def _stream_loop(nxt, upload, comp, d2h, lib, dev, intrinsics, theta_c, settings
                                  settings, weights, connectivity, model, gauge_depth)
         done = torch.cuda.Event()
         done.record(comp)
+        t_alloc = time.perf_counter()
         out = torch.empty((len(res), res[0].log_depth.height * res[0].log_depth.width),
                           dtype=torch.float64, pin_memory=True)
+        _PIN_ALLOC_MS.append(_ms(t_alloc))  # diagnostic (scripts/e2e_outlier.py)
+        del _PIN_ALLOC_MS[:-64]
         with torch.cuda.stream(d2h):
             d2h.wait_event(done)
             hw = out.shape[1]
