@@ -293,14 +293,21 @@ def run_ours(args, rank, world, local_rank):
             return [nb.run_pipeline(nm, intr[0], theta, settings)]
         return nb.run_pipeline_batch(nm, intr, theta, settings)
 
+    gaps = []  # host time between the stream's yields (diagnostic: where a slow run lost its time)
+
     def run_e2e(k):
         """k steps through the serving API: every step copies its pinned host
         inputs to the device and reads every map's log-depth back into pinned
         host memory; run_pipeline_stream overlaps the next step's upload and
         the previous step's read-back with the current step's compute."""
+        gaps.clear()
+        t = time.perf_counter()
         for _ in nb.run_pipeline_stream(((n_pin, m_pin) for _ in range(k)), intr, theta,
                                         settings, device=dev):
-            pass  # each step's log-depth is already in pinned host memory
+            # each step's log-depth is already in pinned host memory
+            t2 = time.perf_counter()
+            gaps.append(round(1e3 * (t2 - t), 1))
+            t = t2
 
     def barrier():
         if world > 1:
@@ -328,6 +335,13 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
+    # What a serving process does after start-up: move the interpreter's
+    # long-lived objects (torch, numpy, the generated scenes) out of the
+    # collector's reach, so a full collection inside a step walks only that
+    # step's records instead of pausing the host thread for ~35 ms.
+    import gc
+    gc.collect()
+    gc.freeze()
 
     fills = []
     iters = []
@@ -348,7 +362,13 @@ def run_ours(args, rank, world, local_rank):
     run_e2e(3)  # warms the pinned-host and device caching allocators
     torch.cuda.synchronize()
     e2e_steps = max(2, min(2 * args.steps, 20))  # a serving stream: its two ends amortised
+    from paper_2510_11508_b200 import pipeline as _pl
+    allocs0 = torch.cuda.memory_stats(dev).get("num_device_alloc", 0)
+    _pl._PIN_ALLOC_MS.clear()
     e2e_ms = timed(lambda: run_e2e(e2e_steps), 1, lambda r: None) / e2e_steps
+    e2e_diag = {"device_allocs": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0)
+                                     - allocs0),
+                "pinned_alloc_ms_max": round(max(_pl._PIN_ALLOC_MS or [0.0]), 2)}
 
     from paper_2510_11508_b200.shard import gather_stats, whole_job
     stats = gather_stats(valid_local, ms, max(iters), B, dev)
@@ -378,6 +398,7 @@ def run_ours(args, rank, world, local_rank):
             "data": "synthetic (seeded generators, paper_2510_11508_b200/scenes.py)",
             "config": {
                 **workload_config(args, world, merge_freq),
+                "host": "gc.freeze() after the warm-up steps",
                 "maps_per_rank": B,
                 "valid_px_total": valid_total,
                 "per_rank": [{"maps": int(r["maps"]), "valid_px": int(r["valid_px"]),
@@ -386,7 +407,7 @@ def run_ours(args, rank, world, local_rank):
             },
             "e2e": {"value": round(valid_total / (e2e_ms * 1e-3), 1), "unit": "valid_px/s",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps, "yield_gaps_ms": list(gaps), **e2e_diag,
                     "api": "run_pipeline_stream over pinned host batches: each step uploads its "
                            "normals + mask and reads every map's log-depth back; the next "
                            "step's upload and the previous step's read-back overlap the "

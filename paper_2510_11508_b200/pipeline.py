@@ -820,6 +820,7 @@ _D2H_PRIORITY = -1  # stream priority of the read-back kernel
 _D2H_CTAS_LAST = 16  # the stream's last batch: nothing computes beside its read-back
 _H2D_CTAS = 0  # upload kernel CTAs (ni_copy_from_host); 0: copy engine
 _PIN_ALLOC_MS: list = []  # host time of the last pinned read-back allocations
+_STREAMS: dict = {}  # (device, read-back priority) -> (upload stream, read-back stream)
 
 
 def run_pipeline_stream(
@@ -848,39 +849,65 @@ def run_pipeline_stream(
     """
     dev = _device(device)
     comp = torch.cuda.current_stream(dev)
-    h2d = torch.cuda.Stream(dev)  # uploads and read-backs on separate streams: the
+    # The two copy streams are made once per device: torch's caching allocator
+    # pools blocks per stream, so fresh streams per call would re-allocate the
+    # 0.9 GB upload buffers with cudaMalloc every time (measured: the first
+    # batch of some streams took 60-300 ms longer) and strand the old ones.
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _D2H_PRIORITY)
+    if key not in _STREAMS:
+        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev, priority=_D2H_PRIORITY))
+    h2d, d2h = _STREAMS[key]
+    # uploads and read-backs on separate streams: the
     # link is full duplex, so they overlap each other too.  The read-back is a
     # small SM kernel storing into mapped pinned memory (ni_copy_to_host), not a
     # copy-engine transfer: a ~10 ms copy-engine read-back would hold the
     # device->host queue that every small control read (.cpu()) of the next
     # batch's pipeline waits in.  High priority: its few CTAs are scheduled
     # ahead of the compute grids' pending CTAs.
-    d2h = torch.cuda.Stream(dev, priority=_D2H_PRIORITY)
     lib = _lib.load()
     it = iter(batches)
+
+    # Two pairs of upload buffers, used in turn: NormalMap.create has consumed a
+    # pair (and synchronised) before the batch computes, so the next-but-one
+    # upload can overwrite it.  Allocating the buffers per batch instead left
+    # their reuse to the caching allocator's cross-stream bookkeeping, which
+    # sometimes had to cudaMalloc 0.9 GB in the middle of the stream (one bench
+    # run in five lost 80-200 ms there).
+    ring = [None, None]
+    count = [0]
 
     def upload():
         try:
             n_h, m_h = next(it)
         except StopIteration:
             return None
+        i = count[0] % 2
+        count[0] += 1
+        slot = ring[i]
         with torch.cuda.stream(h2d):
-            if _H2D_CTAS and all(t.is_pinned() and t.is_contiguous() for t in (n_h, m_h)):
+            if (slot is None or slot[0].shape != n_h.shape or slot[0].dtype != n_h.dtype
+                    or slot[1].shape != m_h.shape or slot[1].dtype != m_h.dtype):
+                slot = [torch.empty(n_h.shape, dtype=n_h.dtype, device=dev),
+                        torch.empty(m_h.shape, dtype=m_h.dtype, device=dev), None]
+                ring[i] = slot
+            elif slot[2] is not None:
+                h2d.wait_event(slot[2])  # the batch that used this pair has been ingested
+            n_d, m_d = slot[0], slot[1]
+            if (_H2D_CTAS and not n_h.is_cuda
+                    and all(t.is_pinned() and t.is_contiguous() for t in (n_h, m_h))):
                 # upload by a small SM kernel reading the mapped pinned buffers
                 # (ni_copy_from_host), like the read-back
-                n_d = torch.empty(n_h.shape, dtype=n_h.dtype, device=dev)
-                m_d = torch.empty(m_h.shape, dtype=m_h.dtype, device=dev)
                 for d_t, h_t in ((n_d, n_h), (m_d, m_h)):
                     _lib.check(lib.ni_copy_from_host(
                         C.c_void_p(d_t.data_ptr()), C.c_void_p(h_t.data_ptr()),
                         h_t.numel() * h_t.element_size(), _H2D_CTAS,
                         C.c_void_p(h2d.cuda_stream)), "upload")
             else:
-                n_d = n_h.to(dev, non_blocking=True)
-                m_d = m_h.to(dev, non_blocking=True)
+                n_d.copy_(n_h, non_blocking=True)
+                m_d.copy_(m_h, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(h2d)
-        return n_d, m_d, ready
+        return n_d, m_d, ready, slot
 
     nxt = upload()
     try:
@@ -894,13 +921,15 @@ def _stream_loop(nxt, upload, comp, d2h, lib, dev, intrinsics, theta_c, settings
                  connectivity, model, gauge_depth):
     pending = None
     while nxt is not None:
-        n_d, m_d, ready = nxt
+        n_d, m_d, ready, slot = nxt
         comp.wait_event(ready)
-        n_d.record_stream(comp)
-        m_d.record_stream(comp)
         nxt = upload()  # prefetch the next batch while this one computes
-        res = run_pipeline_batch(NormalMap.create(n_d, m_d, device=dev), intrinsics, theta_c,
-                                 settings, weights, connectivity, model, gauge_depth)
+        nmap = NormalMap.create(n_d, m_d, device=dev)
+        slot[2] = torch.cuda.Event()  # the upload pair is free again
+        slot[2].record(comp)
+        res = run_pipeline_batch(nmap, intrinsics, theta_c, settings, weights, connectivity,
+                                 model, gauge_depth)
+        del nmap
         done = torch.cuda.Event()
         done.record(comp)
         t_alloc = time.perf_counter()

@@ -2,7 +2,7 @@
 of 10 steps, ms per step, the largest pinned read-back allocation and the GC
 activity.
 
-    python scripts/e2e_outlier.py [runs] [nogc]
+    python scripts/e2e_outlier.py [runs] [nogc|freeze]
 """
 import gc
 import sys
@@ -37,6 +37,7 @@ def _gc_cb(phase, info):
 
 gc.callbacks.append(_gc_cb)
 NOGC = len(sys.argv) > 2 and sys.argv[2] == "nogc"
+FREEZE = len(sys.argv) > 2 and sys.argv[2] == "freeze"
 
 
 def run(steps):
@@ -50,6 +51,9 @@ def run(steps):
 
 
 run(3)
+if FREEZE:
+    gc.collect()
+    gc.freeze()
 for r in range(runs):
     torch.cuda.synchronize()
     g0 = sum(s["collections"] for s in gc.get_stats())
