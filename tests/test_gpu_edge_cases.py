@@ -282,3 +282,22 @@ def test_tail_kernel_matches_per_level_launches():
         digests.append([ln for ln in out.stdout.splitlines() if ln.startswith("DIGEST")][0])
     assert digests[0] == digests[1], digests
     assert int(digests[0].split()[-1]) >= 3  # the case has levels for the tail to cover
+
+
+def test_paired_weighted_fill_batch_vs_oracle():
+    """A batch of >= 10 maps puts two components into one item of the weighted
+    CG (ni_fill's paired mode, default mailbox depth): the refill pass of such
+    a batch is compared with the oracle map by map (labels, outer iterations,
+    merged partition, depth) -- not only with the unpaired GPU path."""
+    maps = [scenes.config3(70 + i, size=56, cells=6) for i in range(12)]
+    theta = float(np.deg2rad(3.5))
+    st = nb.SolveSettings(freq_merging=5, refill_reweighted=True)
+    nm = nb.NormalMap.create(np.stack([m.normals for m in maps]), np.stack([m.mask for m in maps]))
+    res = nb.run_pipeline_batch(nm, [nb.CameraIntrinsics(*m.intrinsics()) for m in maps], theta, st)
+    for m, r in zip(maps, res):
+        ref = O.run_pipeline(m.normals.astype(np.float64), m.mask, m.intrinsics(), theta,
+                             O.Settings(freq_merging=5, refill_reweighted=True))
+        assert np.array_equal(r.partition0.labels, ref.labels0)
+        assert r.iterations == ref.iterations
+        assert np.array_equal(r.partition.labels, ref.labels)
+        assert_depth_close(r.log_depth.values, ref.log_depth, m.mask, m.intrinsics()[0])
