@@ -301,3 +301,23 @@ def test_paired_weighted_fill_batch_vs_oracle():
         assert r.iterations == ref.iterations
         assert np.array_equal(r.partition.labels, ref.labels)
         assert_depth_close(r.log_depth.values, ref.log_depth, m.mask, m.intrinsics()[0])
+
+
+def test_theta_none_above_the_block_cg_limit():
+    """theta_c = None on a map with more than 8192 valid pixels: every pixel is
+    a component (graph.py:153-155), so the scale system has > 8192 unknowns
+    and its CG takes the cooperative multi-block path; a few outer iterations
+    against the oracle (labels, energies, depth)."""
+    sc = scenes.config3(9, size=128, cells=8)
+    assert int(sc.mask.sum()) > 8192
+    st = nb.SolveSettings(max_iters=4)
+    r = nb.run_pipeline(nb.NormalMap.create(sc.normals, sc.mask),
+                        nb.CameraIntrinsics(*sc.intrinsics()), None, st)
+    ref = O.run_pipeline(sc.normals.astype(np.float64), sc.mask, sc.intrinsics(), None,
+                         O.Settings(max_iters=4))
+    assert r.partition0.component_count == int(sc.mask.sum()) == ref.count0
+    assert np.array_equal(r.partition0.labels, ref.labels0)
+    assert r.iterations == ref.iterations
+    np.testing.assert_allclose(r.energies, ref.energies, rtol=2e-3, atol=1e-9)
+    assert len(r.warnings) == len(ref.warnings)
+    assert_depth_close(r.log_depth.values, ref.log_depth, sc.mask, sc.intrinsics()[0])
