@@ -20,7 +20,7 @@
 // A tightly converged solve stays within ~1e-7 of scipy's iterate, five
 // orders of magnitude inside the parity bound (scripts/
 // solver_tolerance_study.py); the CG needs ~1,000-2,600 sweeps per component
-// of a 1024^2 map, the MG-PCG ~20 V-cycles.
+// of a 1024^2 map, the MG-PCG 9-14 V-cycles.
 //
 // Hierarchy (built once per call, all maps at once).  Level 0 is the pixel
 // grid.  A level-l unknown is a (2^l x 2^l block, unit) aggregate: the
@@ -35,8 +35,11 @@
 //
 // V-cycle (symmetric, so plain PCG applies): damped Jacobi from zero
 // (omega = 0.8), residual, restriction (sum over children), recursion,
-// prolongation scaled by 1.6 (over-correction, the standard fix for
-// piecewise-constant prolongation), one damped-Jacobi post-sweep.
+// prolongation scaled by 2.0 (over-correction, the standard fix for
+// piecewise-constant prolongation), damped-Jacobi post-smoothing; one sweep
+// before and after the coarse correction on levels 0 and 1, two on the
+// (cheap) levels >= 2; the levels below ~8,000 unknowns run in one
+// single-CTA launch (tail_kernel).
 //
 // PCG in the Chronopoulos-Gear form: one fine "down" pass (vector updates
 // p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s fused with the
